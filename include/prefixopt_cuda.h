@@ -1,0 +1,161 @@
+/*
+ * prefixopt_cuda.h — C ABI of the B200 (sm_100a) GGR reorder + PHC path.
+ *
+ * This is the drop-in boundary for the reference's hot path
+ * (`prefixopt::ggr`, `phc`, `hit`, `sort_rows_fixed_order`, `compute_stats`,
+ * `fixed_order_by_hitcount_stats`, `fixed_order_by_stats`). The reference has
+ * no FFI of its own (it is a header-only C++20 library); the
+ * entry points below are what a binding for that API needs: plain pointers
+ * and sizes, no C++ or torch types. The C++ headers under proj/include/
+ * prefixopt/ and the Python package paper_2403_05821_b200 both sit on top
+ * of these functions.
+ *
+ * Conventions
+ *   - A table is a row-major grid of byte strings: cell (r, f) is
+ *     arena[offsets[r*m+f] .. offsets[r*m+f+1]). Arena/offsets live on the
+ *     host or on the current CUDA device (po_table.location). Host inputs are
+ *     copied to the device inside the call.
+ *   - Every function returns PO_OK or an error code; po_last_error() returns
+ *     the message for the calling thread. Error codes mirror the reference's
+ *     exception taxonomy (errors.hpp:10-42) so a wrapper can rethrow the same
+ *     class.
+ *   - `stream` is a cudaStream_t (NULL = legacy default stream). Calls are
+ *     synchronous with respect to the host: outputs are valid on return.
+ *   - Calls are re-entrant across host threads; each call owns its scratch.
+ */
+#ifndef PREFIXOPT_CUDA_H
+#define PREFIXOPT_CUDA_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (errors.hpp:10-42) ----------------------------------- */
+#define PO_OK 0
+#define PO_ERR_ERROR 1        /* prefixopt::error (also CUDA failures)      */
+#define PO_ERR_SCHEMA 2       /* prefixopt::schema_error                    */
+#define PO_ERR_STRUCTURAL 3   /* prefixopt::structural_error                */
+#define PO_ERR_DOMAIN 4       /* prefixopt::domain_error                    */
+#define PO_ERR_SIZE 5         /* prefixopt::size_error                      */
+#define PO_ERR_IO 6           /* prefixopt::io_error                        */
+#define PO_ERR_OUT_OF_RANGE 7 /* std::out_of_range (Table::cell .at())      */
+#define PO_ERR_INVALID_ARG 8  /* bad ABI usage (null pointers, bad enum)    */
+
+/* ---- enums (tokenizer.hpp:40-96, scoring.hpp:20, ggr.hpp:25-29) -------- */
+#define PO_LOC_HOST 0
+#define PO_LOC_DEVICE 1
+
+#define PO_TOK_CHAR 0   /* CharTokenizer::count  (tokenizer.hpp:44)        */
+#define PO_TOK_WORD 1   /* WordTokenizer::count  (tokenizer.hpp:64-73)     */
+#define PO_TOK_CUSTOM 2 /* lengths supplied in po_table.cell_lens          */
+
+#define PO_SCORE_VALUE 0    /* SegmentScoring::value_only                  */
+#define PO_SCORE_FRAGMENT 1 /* SegmentScoring::full_fragment               */
+
+#define PO_STATS_WEIGHTED 0 /* cardinality_weighted_squared (default)      */
+#define PO_STATS_SQUARED 1  /* squared_length                              */
+#define PO_STATS_LENFREQ 2  /* length_frequency                            */
+
+/* Table view. Replaces prefixopt::Table (table.hpp:24-104) at the boundary. */
+typedef struct po_table {
+  uint64_t n_rows;
+  uint32_t n_fields;
+  uint32_t location;               /* PO_LOC_* of arena / offsets / cell_lens */
+  const char* const* field_names;  /* host, n_fields entries                  */
+  const uint64_t* field_name_lens; /* host, byte length of each name          */
+  const uint8_t* arena;            /* cell bytes                               */
+  const uint64_t* offsets;         /* n_rows*n_fields + 1, row-major           */
+  const uint64_t* cell_lens;       /* PO_TOK_CUSTOM only: per-cell segment
+                                      length (tok.count of the value, or of the
+                                      fragment in full_fragment mode), else NULL */
+} po_table;
+
+/* GgrConfig (ggr.hpp:48-54). */
+typedef struct po_ggr_config {
+  uint64_t row_recursion_depth;     /* default 4      */
+  uint64_t column_recursion_depth;  /* default 2      */
+  uint64_t hitcount_stop_threshold; /* default 100000 */
+  int32_t use_fds;                  /* default 1      */
+  int32_t stats_variant;            /* PO_STATS_*     */
+} po_ggr_config;
+
+/* FunctionalDependencySet (fd.hpp:21-26) with names already resolved to
+ * field indices by the caller (Table::require_field, ggr.hpp:158). */
+typedef struct po_fd_groups {
+  uint32_t n_groups;
+  const uint32_t* group_offsets; /* n_groups + 1 */
+  const int32_t* members;        /* field indices */
+} po_fd_groups;
+
+/* SolveStats (solve_result.hpp:9-14). */
+typedef struct po_solve_stats {
+  uint64_t recursive_calls;
+  uint64_t candidates_examined;
+  uint64_t max_depth;
+  double wall_ms;
+} po_solve_stats;
+
+/* ---- entry points ------------------------------------------------------ */
+
+/* prefixopt::ggr (ggr.hpp:367-394). Emits the schedule (row ids in request
+ * order, and a full field permutation per request: n_rows*n_fields ints),
+ * its PHC and the solver counters. Outputs live at `out_location`. */
+int po_ggr(const po_table* t, const po_fd_groups* fds, const po_ggr_config* cfg,
+           int32_t tokenizer, int32_t scoring, uint32_t out_location,
+           uint64_t* out_row_ids, int32_t* out_field_orders, uint64_t* out_phc,
+           po_solve_stats* out_stats, void* stream);
+
+/* prefixopt::phc (objective.hpp:94-99) over an arbitrary schedule: entry i is
+ * row row_ids[i] rendered with fields order_fields[order_offsets[i] ..
+ * order_offsets[i+1]). Schedule arrays live at `sched_location`. */
+int po_phc(const po_table* t, int32_t tokenizer, int32_t scoring, uint64_t n_entries,
+           const uint64_t* row_ids, const uint64_t* order_offsets,
+           const int32_t* order_fields, uint32_t sched_location, uint64_t* out_phc,
+           void* stream);
+
+/* prefixopt::hit (objective.hpp:70-91): score of request r against r-1.
+ * r >= n_entries -> PO_ERR_DOMAIN. */
+int po_hit(const po_table* t, int32_t tokenizer, int32_t scoring, uint64_t n_entries,
+           const uint64_t* row_ids, const uint64_t* order_offsets,
+           const int32_t* order_fields, uint32_t sched_location, uint64_t r,
+           uint64_t* out_hit, void* stream);
+
+/* prefixopt::sort_rows_fixed_order (objective.hpp:154-171). `field_order`
+ * (host) must be a permutation of the schema, else PO_ERR_SCHEMA. Writes the
+ * n_rows row ids in request order at out_location. */
+int po_sort_rows_fixed_order(const po_table* t, const int32_t* field_order,
+                             uint32_t out_location, uint64_t* out_row_ids, void* stream);
+
+/* prefixopt::compute_stats (stats.hpp:25-45): per field the exact number of
+ * distinct raw values and the sum of segment lengths (host outputs). The
+ * caller forms avg_len = double(total_len) / n_rows. */
+int po_compute_stats(const po_table* t, int32_t tokenizer, int32_t scoring,
+                     uint64_t* out_cardinality, uint64_t* out_total_len, void* stream);
+
+/* prefixopt::fixed_order_by_hitcount_stats (ggr.hpp:59-84) and
+ * fixed_order_by_stats (objective.hpp:176-188): host-only IEEE-double
+ * ranking of fields from (total_rows, cardinality[], avg_len[]). */
+int po_fixed_order_by_hitcount_stats(uint32_t n_fields, uint64_t total_rows,
+                                     const uint64_t* cardinality, const double* avg_len,
+                                     int32_t variant, int32_t* out_order);
+int po_fixed_order_by_stats(uint32_t n_fields, uint64_t total_rows,
+                            const uint64_t* cardinality, const double* avg_len,
+                            int32_t* out_order);
+
+/* Thread-local message of the last failing call on this thread. */
+const char* po_last_error(void);
+
+/* Library/device info: compiled arch string, e.g. "sm_100a". */
+const char* po_build_info(void);
+
+/* Number of CUDA kernels this library launched in this process (counter
+ * incremented at each launch site; used by bench.py's gpu_launches). */
+uint64_t po_kernel_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PREFIXOPT_CUDA_H */

@@ -1,0 +1,124 @@
+"""ORACLE — TEST INFRASTRUCTURE ONLY.
+
+Python bindings of the CPU checkers (oracle/oracle.h):
+  kind="port"       oracle/libggr_oracle.so   the CPU restatement
+  kind="reference"  oracle/_ref/libggr_ref.so the reference headers compiled
+                                              from /root/reference
+Used by tests/, __graft_entry__.smoke() and bench.py's CPU-baseline /
+--impl reference legs. The product package never imports this module.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from pathlib import Path
+
+import numpy as np
+
+from paper_2403_05821_b200._abi import FdView, _bind, po_ggr_config, po_solve_stats
+from paper_2403_05821_b200.api import (GgrConfig, RequestSchedule, SegmentScoring, SolveResult,
+                                       SolveStats, _cell_lens, _fd_indices)
+from paper_2403_05821_b200.errors import raise_for
+
+ORACLE_DIR = Path(__file__).resolve().parent
+PATHS = {
+    "port": ORACLE_DIR / "libggr_oracle.so",
+    "reference": ORACLE_DIR / "_ref" / "libggr_ref.so",
+}
+PREFIX = {"port": "oracle_", "reference": "ref_"}
+
+
+class OracleLib:
+    def __init__(self, kind: str):
+        path = PATHS[kind]
+        if not path.exists():
+            raise FileNotFoundError(
+                f"{path} not built (make -C oracle{' ref' if kind == 'reference' else ''})")
+        self.kind = kind
+        self.path = path
+        L = C.CDLL(str(path))
+        p = PREFIX[kind]
+        vp = C.c_void_p
+        self._ggr = _bind(L, p + "ggr", C.c_int, [vp, vp, vp, C.c_int32, C.c_int32, vp, vp, vp, vp])
+        self._phc = _bind(L, p + "phc", C.c_int, [vp, C.c_int32, C.c_int32, C.c_uint64, vp, vp, vp, vp])
+        self._sort = _bind(L, p + "sort_rows_fixed_order", C.c_int, [vp, vp, vp])
+        self._stats = _bind(L, p + "compute_stats", C.c_int, [vp, C.c_int32, C.c_int32, vp, vp])
+        self._fohs = _bind(L, p + "fixed_order_by_hitcount_stats", C.c_int,
+                           [C.c_uint32, C.c_uint64, vp, vp, C.c_int32, vp])
+        self._err = _bind(L, p + "last_error", C.c_char_p, [])
+
+    def _check(self, code):
+        if code:
+            raise_for(code, (self._err() or b"").decode("utf-8", "replace"))
+
+    # same call shapes as paper_2403_05821_b200.api
+    def ggr(self, t, fds=None, cfg: GgrConfig | None = None, tok=None,
+            scoring=SegmentScoring.value_only) -> SolveResult:
+        from paper_2403_05821_b200.api import char_tokenizer
+        cfg = cfg or GgrConfig()
+        tok = tok or char_tokenizer()
+        n, m = t.row_count(), t.field_count()
+        fdv = FdView(_fd_indices(t, fds, cfg))
+        view = t.view(cell_lens=_cell_lens(t, tok, scoring))
+        rows = np.empty(max(n, 1), dtype=np.uint64)
+        orders = np.empty(max(n * m, 1), dtype=np.int32)
+        score = C.c_uint64(0)
+        st = po_solve_stats()
+        c = cfg.abi()
+        self._check(self._ggr(view.ref(), fdv.ref(), C.byref(c), tok.kind, int(scoring),
+                              rows.ctypes.data, orders.ctypes.data, C.byref(score), C.byref(st)))
+        sched = RequestSchedule.full(rows[:n], orders[:n * m].reshape(n, m))
+        return SolveResult(int(score.value), sched,
+                           SolveStats(st.recursive_calls, st.candidates_examined, st.max_depth,
+                                      st.wall_ms))
+
+    def phc(self, s, t, tok=None, scoring=SegmentScoring.value_only) -> int:
+        from paper_2403_05821_b200.api import char_tokenizer
+        tok = tok or char_tokenizer()
+        if not isinstance(s, RequestSchedule):
+            s = RequestSchedule.from_entries(s)
+        view = t.view(cell_lens=_cell_lens(t, tok, scoring))
+        out = C.c_uint64(0)
+        flds = s.order_fields if s.order_fields.size else np.zeros(1, np.int32)
+        self._check(self._phc(view.ref(), tok.kind, int(scoring), s.size(), s.row_ids.ctypes.data,
+                              s.order_offsets.ctypes.data, flds.ctypes.data, C.byref(out)))
+        return int(out.value)
+
+    def sort_rows_fixed_order(self, t, field_order) -> np.ndarray:
+        fo = np.array(list(field_order) or [0], dtype=np.int32)
+        rows = np.empty(max(t.row_count(), 1), dtype=np.uint64)
+        view = t.view()
+        self._check(self._sort(view.ref(), fo.ctypes.data, rows.ctypes.data))
+        return rows[:t.row_count()]
+
+    def compute_stats(self, t, tok=None, scoring=SegmentScoring.value_only):
+        from paper_2403_05821_b200.api import char_tokenizer
+        tok = tok or char_tokenizer()
+        m = t.field_count()
+        card = np.zeros(max(m, 1), dtype=np.uint64)
+        tot = np.zeros(max(m, 1), dtype=np.uint64)
+        view = t.view(cell_lens=_cell_lens(t, tok, scoring))
+        self._check(self._stats(view.ref(), tok.kind, int(scoring), card.ctypes.data,
+                                tot.ctypes.data))
+        return card[:m], tot[:m]
+
+    def fixed_order_by_hitcount_stats(self, total_rows, card, avg, variant=0):
+        m = len(card)
+        c = np.array(list(card) or [0], dtype=np.uint64)
+        a = np.array(list(avg) or [0.0], dtype=np.float64)
+        out = np.zeros(max(m, 1), dtype=np.int32)
+        self._check(self._fohs(m, total_rows, c.ctypes.data, a.ctypes.data, variant,
+                               out.ctypes.data))
+        return out[:m].tolist()
+
+
+_LIBS: dict = {}
+
+
+def oracle(kind: str = "port") -> OracleLib:
+    if kind not in _LIBS:
+        _LIBS[kind] = OracleLib(kind)
+    return _LIBS[kind]
+
+
+def available(kind: str) -> bool:
+    return PATHS[kind].exists()

@@ -1,0 +1,227 @@
+// ORACLE — TEST INFRASTRUCTURE ONLY.
+//
+// Exposes the UNMODIFIED reference implementation (the header-only library
+// under /root/reference/proj/include, compiled in place by oracle/Makefile)
+// through the oracle C interface with the `ref_` prefix. Nothing here
+// re-implements the algorithm: each entry point builds a prefixopt::Table
+// from the ABI view and calls the reference function named in its comment.
+// The output goes to oracle/_ref/ (git-ignored, shipped to the GPU box).
+
+#include <chrono>
+#include <stdexcept>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "prefixopt/ggr.hpp"
+#include "prefixopt/objective.hpp"
+#include "prefixopt/stats.hpp"
+
+#include "oracle.h"
+
+namespace {
+
+thread_local std::string g_err;
+
+prefixopt::Table to_table(const po_table* t) {
+  if (!t || t->location != PO_LOC_HOST) throw std::invalid_argument("ref shim needs host table");
+  std::vector<std::string> names;
+  for (uint32_t f = 0; f < t->n_fields; ++f)
+    names.emplace_back(t->field_names[f], t->field_name_lens[f]);
+  std::vector<std::vector<std::string>> rows(t->n_rows);
+  for (uint64_t r = 0; r < t->n_rows; ++r) {
+    rows[r].reserve(t->n_fields);
+    for (uint32_t f = 0; f < t->n_fields; ++f) {
+      uint64_t i = r * t->n_fields + f;
+      rows[r].emplace_back(reinterpret_cast<const char*>(t->arena) + t->offsets[i],
+                           t->offsets[i + 1] - t->offsets[i]);
+    }
+  }
+  return prefixopt::Table(std::move(names), std::move(rows));
+}
+
+// A deterministic tokenizer defined by the caller's per-cell lengths: maps
+// the exact text the reference passes to count() (the value, or the rendered
+// fragment in full_fragment mode) to its length.
+class TableTokenizer final : public prefixopt::Tokenizer {
+ public:
+  TableTokenizer(const po_table* t, const prefixopt::Table& tab, prefixopt::SegmentScoring s) {
+    for (uint64_t r = 0; r < tab.row_count(); ++r)
+      for (uint32_t f = 0; f < tab.field_count(); ++f) {
+        const std::string& v = tab.cell(r, f);
+        std::string key = s == prefixopt::SegmentScoring::value_only
+                              ? v
+                              : prefixopt::fragment_text(tab.field_name(f), v);
+        lens_[key] = t->cell_lens[r * t->n_fields + f];
+      }
+  }
+  std::string_view name() const override { return "custom"; }
+  std::vector<std::string_view> tokens(std::string_view) const override {
+    throw std::logic_error("not used on this path");
+  }
+  std::size_t count(std::string_view text) const override {
+    auto it = lens_.find(std::string(text));
+    if (it == lens_.end()) throw std::logic_error("custom tokenizer: unknown text");
+    return it->second;
+  }
+
+ private:
+  std::unordered_map<std::string, std::size_t> lens_;
+};
+
+struct Tok {
+  std::unique_ptr<TableTokenizer> custom;
+  const prefixopt::Tokenizer* tok = nullptr;
+};
+
+Tok make_tok(int kind, const po_table* t, const prefixopt::Table& tab,
+             prefixopt::SegmentScoring s) {
+  Tok out;
+  if (kind == PO_TOK_CHAR) out.tok = &prefixopt::char_tokenizer();
+  else if (kind == PO_TOK_WORD) out.tok = &prefixopt::word_tokenizer();
+  else {
+    out.custom = std::make_unique<TableTokenizer>(t, tab, s);
+    out.tok = out.custom.get();
+  }
+  return out;
+}
+
+prefixopt::SegmentScoring scoring_of(int s) {
+  return s == PO_SCORE_VALUE ? prefixopt::SegmentScoring::value_only
+                             : prefixopt::SegmentScoring::full_fragment;
+}
+
+prefixopt::StatsScoreVariant variant_of(int v) {
+  if (v == PO_STATS_SQUARED) return prefixopt::StatsScoreVariant::squared_length;
+  if (v == PO_STATS_LENFREQ) return prefixopt::StatsScoreVariant::length_frequency;
+  return prefixopt::StatsScoreVariant::cardinality_weighted_squared;
+}
+
+template <class F>
+int guarded(F&& fn) {
+  try {
+    fn();
+    return PO_OK;
+  } catch (const prefixopt::schema_error& e) {
+    g_err = e.what();
+    return PO_ERR_SCHEMA;
+  } catch (const prefixopt::domain_error& e) {
+    g_err = e.what();
+    return PO_ERR_DOMAIN;
+  } catch (const prefixopt::structural_error& e) {
+    g_err = e.what();
+    return PO_ERR_STRUCTURAL;
+  } catch (const prefixopt::size_error& e) {
+    g_err = e.what();
+    return PO_ERR_SIZE;
+  } catch (const prefixopt::error& e) {
+    g_err = e.what();
+    return PO_ERR_ERROR;
+  } catch (const std::out_of_range& e) {
+    g_err = e.what();
+    return PO_ERR_OUT_OF_RANGE;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return PO_ERR_ERROR;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+// prefixopt::ggr (ggr.hpp:367-394)
+int ref_ggr(const po_table* tv, const po_fd_groups* fds, const po_ggr_config* cfg, int32_t tok,
+            int32_t scoring, uint64_t* out_rows, int32_t* out_orders, uint64_t* out_phc,
+            po_solve_stats* out_stats) {
+  return guarded([&] {
+    prefixopt::Table t = to_table(tv);
+    auto sc = scoring_of(scoring);
+    Tok tk = make_tok(tok, tv, t, sc);
+    prefixopt::FunctionalDependencySet set;
+    if (fds)
+      for (uint32_t g = 0; g < fds->n_groups; ++g) {
+        std::vector<std::string> names;
+        for (uint32_t k = fds->group_offsets[g]; k < fds->group_offsets[g + 1]; ++k)
+          names.push_back(t.field_name(fds->members[k]));
+        set.groups.push_back(std::move(names));
+      }
+    prefixopt::GgrConfig c;
+    c.row_recursion_depth = cfg->row_recursion_depth;
+    c.column_recursion_depth = cfg->column_recursion_depth;
+    c.hitcount_stop_threshold = cfg->hitcount_stop_threshold;
+    c.use_fds = cfg->use_fds != 0;
+    c.stats_variant = variant_of(cfg->stats_variant);
+    prefixopt::SolveResult res = prefixopt::ggr(t, set, c, *tk.tok, sc);
+    uint32_t m = tv->n_fields;
+    for (size_t i = 0; i < res.schedule.entries.size(); ++i) {
+      const auto& e = res.schedule.entries[i];
+      out_rows[i] = e.row_id;
+      for (uint32_t p = 0; p < m; ++p)
+        out_orders[i * m + p] = p < e.field_order.size() ? e.field_order[p] : -1;
+    }
+    *out_phc = res.phc_score;
+    if (out_stats) {
+      out_stats->recursive_calls = res.stats.recursive_calls;
+      out_stats->candidates_examined = res.stats.candidates_examined;
+      out_stats->max_depth = res.stats.max_depth;
+      out_stats->wall_ms = res.stats.wall_ms;
+    }
+  });
+}
+
+// prefixopt::phc (objective.hpp:94-99)
+int ref_phc(const po_table* tv, int32_t tok, int32_t scoring, uint64_t n, const uint64_t* rows,
+            const uint64_t* offs, const int32_t* fields, uint64_t* out_phc) {
+  return guarded([&] {
+    prefixopt::Table t = to_table(tv);
+    auto sc = scoring_of(scoring);
+    Tok tk = make_tok(tok, tv, t, sc);
+    prefixopt::RequestSchedule s;
+    for (uint64_t i = 0; i < n; ++i)
+      s.entries.push_back({rows[i], std::vector<int>(fields + offs[i], fields + offs[i + 1])});
+    *out_phc = prefixopt::phc(s, t, *tk.tok, sc);
+  });
+}
+
+// prefixopt::sort_rows_fixed_order (objective.hpp:154-171)
+int ref_sort_rows_fixed_order(const po_table* tv, const int32_t* order, uint64_t* out_rows) {
+  return guarded([&] {
+    prefixopt::Table t = to_table(tv);
+    std::vector<int> o(order, order + tv->n_fields);
+    prefixopt::RequestSchedule s = prefixopt::sort_rows_fixed_order(t, o);
+    for (size_t i = 0; i < s.entries.size(); ++i) out_rows[i] = s.entries[i].row_id;
+  });
+}
+
+// prefixopt::compute_stats (stats.hpp:25-45); total_len is recovered from
+// avg_len * n, which is exact for the integer sums the tests use (< 2^53).
+int ref_compute_stats(const po_table* tv, int32_t tok, int32_t scoring, uint64_t* out_card,
+                      uint64_t* out_total) {
+  return guarded([&] {
+    prefixopt::Table t = to_table(tv);
+    auto sc = scoring_of(scoring);
+    Tok tk = make_tok(tok, tv, t, sc);
+    prefixopt::ColumnStats st = prefixopt::compute_stats(t, *tk.tok, sc);
+    for (size_t f = 0; f < st.fields.size(); ++f) {
+      out_card[f] = st.fields[f].cardinality;
+      out_total[f] = static_cast<uint64_t>(st.fields[f].avg_len * double(t.row_count()) + 0.5);
+    }
+  });
+}
+
+// prefixopt::fixed_order_by_hitcount_stats (ggr.hpp:59-84)
+int ref_fixed_order_by_hitcount_stats(uint32_t m, uint64_t total_rows, const uint64_t* card,
+                                      const double* avg, int32_t variant, int32_t* out) {
+  return guarded([&] {
+    prefixopt::ColumnStats st;
+    st.total_rows = total_rows;
+    for (uint32_t f = 0; f < m; ++f) st.fields.push_back({"f" + std::to_string(f), card[f], avg[f]});
+    std::vector<int> o = prefixopt::fixed_order_by_hitcount_stats(st, variant_of(variant));
+    std::copy(o.begin(), o.end(), out);
+  });
+}
+
+const char* ref_last_error(void) { return g_err.c_str(); }
+
+}  // extern "C"

@@ -1,0 +1,257 @@
+// extern "C" entry points of libprefixopt_cuda.so (include/prefixopt_cuda.h).
+// Each call runs synchronously on the caller's stream; exceptions become
+// PO_ERR_* codes with a thread-local message.
+
+#include <chrono>
+#include <cstdlib>
+#include <cstring>
+#include <numeric>
+
+#include "internal.cuh"
+
+namespace po {
+
+std::atomic<uint64_t> g_launches{0};
+
+namespace {
+
+thread_local std::string g_err;
+
+template <class F>
+int guarded(F&& fn) {
+  try {
+    fn();
+    return PO_OK;
+  } catch (const Error& e) {
+    g_err = e.what();
+    return e.code;
+  } catch (const std::bad_alloc& e) {
+    g_err = std::string("host allocation failed: ") + e.what();
+    return PO_ERR_ERROR;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return PO_ERR_ERROR;
+  }
+}
+
+void check_modes(int tok, int scoring) {
+  if (tok < PO_TOK_CHAR || tok > PO_TOK_CUSTOM) fail(PO_ERR_INVALID_ARG, "unknown tokenizer kind");
+  if (scoring != PO_SCORE_VALUE && scoring != PO_SCORE_FRAGMENT)
+    fail(PO_ERR_INVALID_ARG, "unknown scoring mode");
+}
+
+uint32_t debug_hash_bits() {
+  const char* v = std::getenv("PO_DEBUG_HASH_BITS");
+  if (!v || !*v) return 64;
+  int b = std::atoi(v);
+  return (b <= 0 || b > 64) ? 64u : uint32_t(b);
+}
+
+struct Prepared {
+  DeviceTable t;
+  Encoded e;
+};
+
+void prepare(const po_table* tv, int tok, int scoring, cudaStream_t s, Prepared& p) {
+  check_modes(tok, scoring);
+  make_device_table(tv, tok, s, p.t);
+  encode(p.t, tok, scoring, s, p.e, debug_hash_bits());
+}
+
+__global__ void k_u32_to_u64(const uint32_t* a, uint64_t n, uint64_t* b) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
+       i += uint64_t(gridDim.x) * blockDim.x)
+    b[i] = a[i];
+}
+
+// Copies a device u32 row array to the caller's u64 buffer (host or device).
+void deliver_rows(const uint32_t* d_rows32, uint64_t n, uint32_t loc, uint64_t* out,
+                  cudaStream_t s) {
+  if (n == 0) return;
+  if (loc == PO_LOC_DEVICE) {
+    PO_LAUNCH(k_u32_to_u64, grid_for(n, 256), 256, 0, s, d_rows32, n, out);
+  } else {
+    DevBuf<uint64_t> tmp(n, s);
+    PO_LAUNCH(k_u32_to_u64, grid_for(n, 256), 256, 0, s, d_rows32, n, tmp.get());
+    tmp.download(out, n);
+  }
+}
+
+template <class T>
+const T* stage(const T* p, uint64_t count, uint32_t loc, DevBuf<T>& own, cudaStream_t s) {
+  if (loc == PO_LOC_DEVICE || count == 0) return p;
+  own.alloc(count, s);
+  own.upload(p, count);
+  return own.get();
+}
+
+uint64_t phc_call(const po_table* tv, int tok, int scoring, uint64_t n_entries,
+                  const uint64_t* rows, const uint64_t* offs, const int32_t* fields, uint32_t loc,
+                  cudaStream_t s, uint64_t first, uint64_t last_plus_one) {
+  if (loc != PO_LOC_HOST && loc != PO_LOC_DEVICE) fail(PO_ERR_INVALID_ARG, "bad schedule location");
+  if (n_entries && (!rows || !offs)) fail(PO_ERR_INVALID_ARG, "null schedule arrays");
+  Prepared p;
+  prepare(tv, tok, scoring, s, p);
+  uint64_t nfields = 0;
+  if (n_entries) {
+    if (loc == PO_LOC_HOST) nfields = offs[n_entries];
+    else {
+      PO_CUDA(cudaMemcpyAsync(&nfields, offs + n_entries, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+      sync(s);
+    }
+  }
+  DevBuf<uint64_t> own_rows, own_offs;
+  DevBuf<int32_t> own_fields;
+  const uint64_t* d_rows = stage(rows, n_entries, loc, own_rows, s);
+  const uint64_t* d_offs = stage(offs, n_entries + 1, loc, own_offs, s);
+  const int32_t* d_fields = stage(fields, nfields, loc, own_fields, s);
+  return phc_device(p.e, last_plus_one, d_rows, nullptr, d_offs, d_fields, s, first);
+}
+
+}  // namespace
+
+}  // namespace po
+
+using namespace po;
+
+extern "C" {
+
+int po_ggr(const po_table* t, const po_fd_groups* fds, const po_ggr_config* cfg, int32_t tok,
+           int32_t scoring, uint32_t out_location, uint64_t* out_row_ids,
+           int32_t* out_field_orders, uint64_t* out_phc, po_solve_stats* out_stats,
+           void* stream) {
+  return guarded([&] {
+    auto t0 = std::chrono::steady_clock::now();
+    if (!cfg || !out_phc) fail(PO_ERR_INVALID_ARG, "null config or output");
+    if (out_location != PO_LOC_HOST && out_location != PO_LOC_DEVICE)
+      fail(PO_ERR_INVALID_ARG, "bad output location");
+    if (cfg->stats_variant < 0 || cfg->stats_variant > 2)
+      fail(PO_ERR_INVALID_ARG, "unknown stats variant");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    std::vector<std::vector<int>> groups;
+    if (fds && cfg->use_fds)
+      for (uint32_t g = 0; g < fds->n_groups; ++g)
+        groups.emplace_back(fds->members + fds->group_offsets[g],
+                            fds->members + fds->group_offsets[g + 1]);
+    Prepared p;
+    prepare(t, tok, scoring, s, p);
+    const uint64_t n = p.e.n, m = p.e.m;
+    DevBuf<uint32_t> rows(n, s);
+    int32_t* d_orders = nullptr;
+    DevBuf<int32_t> own_orders;
+    if (out_location == PO_LOC_DEVICE) d_orders = out_field_orders;
+    else {
+      own_orders.alloc(n * m, s);
+      d_orders = own_orders.get();
+    }
+    GgrOutput go;
+    ggr_device(p.e, groups, *cfg, rows.get(), d_orders, go, s);
+    deliver_rows(rows.get(), n, out_location, out_row_ids, s);
+    if (out_location == PO_LOC_HOST) own_orders.download(out_field_orders, n * m);
+    sync(s);
+    *out_phc = go.phc;
+    if (out_stats) {
+      *out_stats = go.stats;
+      out_stats->wall_ms =
+          std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    }
+  });
+}
+
+int po_phc(const po_table* t, int32_t tok, int32_t scoring, uint64_t n_entries,
+           const uint64_t* row_ids, const uint64_t* order_offsets, const int32_t* order_fields,
+           uint32_t sched_location, uint64_t* out_phc, void* stream) {
+  return guarded([&] {
+    if (!out_phc) fail(PO_ERR_INVALID_ARG, "null output");
+    *out_phc = phc_call(t, tok, scoring, n_entries, row_ids, order_offsets, order_fields,
+                        sched_location, static_cast<cudaStream_t>(stream), 1, n_entries);
+  });
+}
+
+int po_hit(const po_table* t, int32_t tok, int32_t scoring, uint64_t n_entries,
+           const uint64_t* row_ids, const uint64_t* order_offsets, const int32_t* order_fields,
+           uint32_t sched_location, uint64_t r, uint64_t* out_hit, void* stream) {
+  return guarded([&] {
+    if (!out_hit) fail(PO_ERR_INVALID_ARG, "null output");
+    if (r >= n_entries)  // objective.hpp:73-75
+      fail(PO_ERR_DOMAIN, "hit: request index " + std::to_string(r) +
+                              " out of range for schedule of " + std::to_string(n_entries));
+    *out_hit = r == 0 ? 0
+                      : phc_call(t, tok, scoring, n_entries, row_ids, order_offsets, order_fields,
+                                 sched_location, static_cast<cudaStream_t>(stream), r, r + 1);
+  });
+}
+
+int po_sort_rows_fixed_order(const po_table* t, const int32_t* field_order, uint32_t out_location,
+                             uint64_t* out_row_ids, void* stream) {
+  return guarded([&] {
+    if (!t) fail(PO_ERR_INVALID_ARG, "null table");
+    const uint32_t m = t->n_fields;
+    // validate_field_permutation (objective.hpp:140-149)
+    std::vector<char> seen(m, 0);
+    std::vector<int> order(m);
+    for (uint32_t i = 0; i < m; ++i) {
+      int f = field_order[i];
+      if (f < 0 || uint32_t(f) >= m || seen[f])
+        fail(PO_ERR_SCHEMA, "field order is not a permutation of the schema");
+      seen[f] = 1;
+      order[i] = f;
+    }
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    Prepared p;
+    prepare(t, PO_TOK_CHAR, PO_SCORE_VALUE, s, p);
+    const uint64_t n = p.e.n;
+    DevBuf<uint32_t> perm(n, s);
+    if (m == 0) {
+      std::vector<uint32_t> id(n);
+      std::iota(id.begin(), id.end(), 0u);
+      perm.upload(id.data(), n);
+    } else {
+      sort_all_rows(p.e, order, perm.get(), s);
+    }
+    deliver_rows(perm.get(), n, out_location, out_row_ids, s);
+    sync(s);
+  });
+}
+
+int po_compute_stats(const po_table* t, int32_t tok, int32_t scoring, uint64_t* out_card,
+                     uint64_t* out_total, void* stream) {
+  return guarded([&] {
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    Prepared p;
+    prepare(t, tok, scoring, s, p);
+    for (uint32_t f = 0; f < p.e.m; ++f) {
+      out_card[f] = p.e.card[f];
+      out_total[f] = p.e.total_len[f];
+    }
+  });
+}
+
+int po_fixed_order_by_hitcount_stats(uint32_t m, uint64_t total_rows, const uint64_t* card,
+                                     const double* avg, int32_t variant, int32_t* out) {
+  return guarded([&] {
+    if (variant < 0 || variant > 2) fail(PO_ERR_INVALID_ARG, "unknown stats variant");
+    std::vector<uint64_t> c(card, card + m);
+    std::vector<double> a(avg, avg + m);
+    std::vector<int> o = hitcount_order(total_rows, c, a, variant);
+    std::copy(o.begin(), o.end(), out);
+  });
+}
+
+int po_fixed_order_by_stats(uint32_t m, uint64_t total_rows, const uint64_t* card,
+                            const double* avg, int32_t* out) {
+  return guarded([&] {
+    std::vector<uint64_t> c(card, card + m);
+    std::vector<double> a(avg, avg + m);
+    std::vector<int> o = stats_order(total_rows, c, a);
+    std::copy(o.begin(), o.end(), out);
+  });
+}
+
+const char* po_last_error(void) { return g_err.c_str(); }
+
+const char* po_build_info(void) { return "prefixopt-b200 sm_100a"; }
+
+uint64_t po_kernel_launch_count(void) { return g_launches.load(); }
+
+}  // extern "C"

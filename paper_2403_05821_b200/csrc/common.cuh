@@ -1,0 +1,213 @@
+// Shared device/host helpers for the sm_100a GGR + PHC path.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstring>
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/prefixopt_cuda.h"
+
+namespace po {
+
+// ---------------------------------------------------------------------------
+// errors: mapped to PO_ERR_* at the ABI boundary (abi.cu)
+// ---------------------------------------------------------------------------
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+[[noreturn]] inline void fail(int code, const std::string& msg) { throw Error(code, msg); }
+
+inline void cuda_check(cudaError_t e, const char* what, const char* file, int line) {
+  if (e != cudaSuccess)
+    fail(PO_ERR_ERROR, std::string("CUDA error in ") + what + " (" + file + ":" +
+                           std::to_string(line) + "): " + cudaGetErrorString(e));
+}
+#define PO_CUDA(x) ::po::cuda_check((x), #x, __FILE__, __LINE__)
+
+extern std::atomic<uint64_t> g_launches;
+
+// Every kernel of this library is launched through PO_LAUNCH so bench.py can
+// report how many of OUR kernels ran (po_kernel_launch_count).
+#define PO_LAUNCH(kernel, grid, block, smem, stream, ...)                    \
+  do {                                                                       \
+    if ((grid) > 0) {                                                        \
+      kernel<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__);            \
+      ::po::g_launches.fetch_add(1, std::memory_order_relaxed);              \
+      PO_CUDA(cudaGetLastError());                                           \
+    }                                                                        \
+  } while (0)
+
+constexpr int kSMs = 148;  // B200: 2 dies x 74 SMs
+
+inline unsigned grid_for(uint64_t work, unsigned block, unsigned max_waves = 16) {
+  uint64_t g = (work + block - 1) / block;
+  uint64_t cap = uint64_t(kSMs) * max_waves * (1024 / block);
+  if (g > cap) g = cap;
+  return unsigned(g);
+}
+
+// ---------------------------------------------------------------------------
+// stream-ordered device buffer (cudaMallocAsync on the call's stream)
+// ---------------------------------------------------------------------------
+template <class T>
+class DevBuf {
+ public:
+  DevBuf() = default;
+  DevBuf(size_t n, cudaStream_t s) { alloc(n, s); }
+  ~DevBuf() { release(); }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept { *this = std::move(o); }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    if (this != &o) {
+      release();
+      p_ = o.p_;
+      n_ = o.n_;
+      s_ = o.s_;
+      o.p_ = nullptr;
+      o.n_ = 0;
+    }
+    return *this;
+  }
+  void alloc(size_t n, cudaStream_t s) {
+    release();
+    s_ = s;
+    n_ = n;
+    if (n) PO_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p_), n * sizeof(T) + 64, s));
+  }
+  void zero() {
+    if (n_) PO_CUDA(cudaMemsetAsync(p_, 0, n_ * sizeof(T), s_));
+  }
+  void fill_bytes(int v) {
+    if (n_) PO_CUDA(cudaMemsetAsync(p_, v, n_ * sizeof(T), s_));
+  }
+  void release() {
+    if (p_) cudaFreeAsync(p_, s_);
+    p_ = nullptr;
+    n_ = 0;
+  }
+  T* get() const { return p_; }
+  size_t size() const { return n_; }
+  void upload(const T* h, size_t n) {
+    if (n) PO_CUDA(cudaMemcpyAsync(p_, h, n * sizeof(T), cudaMemcpyHostToDevice, s_));
+  }
+  void download(T* h, size_t n) const {
+    if (n) PO_CUDA(cudaMemcpyAsync(h, p_, n * sizeof(T), cudaMemcpyDeviceToHost, s_));
+  }
+
+ private:
+  T* p_ = nullptr;
+  size_t n_ = 0;
+  cudaStream_t s_ = nullptr;
+};
+
+template <class T>
+DevBuf<T> to_device(const std::vector<T>& v, cudaStream_t s) {
+  DevBuf<T> d(v.size(), s);
+  d.upload(v.data(), v.size());
+  return d;
+}
+
+inline void sync(cudaStream_t s) { PO_CUDA(cudaStreamSynchronize(s)); }
+
+inline int bits_for(uint64_t max_value) {  // bits to hold values 0..max_value
+  int b = 0;
+  while (b < 64 && (max_value >> b)) ++b;
+  return b == 0 ? 1 : b;
+}
+
+// ---------------------------------------------------------------------------
+// device helpers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t ld_relaxed_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ uint64_t rotl64(uint64_t x, int r) { return (x << r) | (x >> (64 - r)); }
+
+__device__ __forceinline__ uint64_t fmix64(uint64_t k) {
+  k ^= k >> 33;
+  k *= 0xff51afd7ed558ccdULL;
+  k ^= k >> 33;
+  k *= 0xc4ceb9fe1a85ec53ULL;
+  k ^= k >> 33;
+  return k;
+}
+
+// Sequential reader of an arbitrarily aligned byte string as little-endian
+// 8-byte words, using only 8-byte-aligned loads that never start at or past
+// `limit` (the end of the arena), so no load leaves the allocation.
+struct WordReader {
+  const uint64_t* p;
+  const uint64_t* lim;  // first aligned word that starts at/after the arena end
+  uint32_t sh;
+  uint64_t cur;
+  __device__ __forceinline__ WordReader(const uint8_t* a, const uint8_t* limit) {
+    uintptr_t ad = reinterpret_cast<uintptr_t>(a);
+    p = reinterpret_cast<const uint64_t*>(ad & ~uintptr_t(7));
+    lim = reinterpret_cast<const uint64_t*>((reinterpret_cast<uintptr_t>(limit) + 7) & ~uintptr_t(7));
+    sh = uint32_t(ad & 7) * 8;
+    cur = p < lim ? __ldg(p) : 0;
+  }
+  __device__ __forceinline__ uint64_t next() {
+    const uint64_t* q = p + 1;
+    uint64_t nxt = q < lim ? __ldg(q) : 0;
+    uint64_t w = sh ? ((cur >> sh) | (nxt << (64 - sh))) : cur;
+    cur = nxt;
+    p = q;
+    return w;
+  }
+};
+
+__device__ __forceinline__ uint64_t mask_low_bytes(uint64_t w, uint32_t nbytes) {
+  return nbytes >= 8 ? w : (w & ((uint64_t(1) << (8 * nbytes)) - 1));
+}
+
+// 64-bit hash of a cell's bytes (value identity for the dictionary; exact
+// equality is always verified on the bytes, so quality only affects speed).
+__device__ __forceinline__ uint64_t hash_bytes(const uint8_t* a, uint64_t len, const uint8_t* limit) {
+  uint64_t h = 0x9E3779B97F4A7C15ULL ^ (len * 0xC2B2AE3D27D4EB4FULL);
+  if (len) {
+    WordReader rd(a, limit);
+    uint64_t left = len;
+    while (left) {
+      uint64_t w = rd.next();
+      uint32_t take = left >= 8 ? 8u : uint32_t(left);
+      w = mask_low_bytes(w, take);
+      h ^= w * 0xbf58476d1ce4e5b9ULL;
+      h = rotl64(h, 27) * 0x94d049bb133111ebULL + 0x52dce729ULL;
+      left -= take;
+    }
+  }
+  h = fmix64(h);
+  return h ? h : 1;  // 0 marks an empty slot
+}
+
+__device__ __forceinline__ bool bytes_equal(const uint8_t* a, const uint8_t* b, uint64_t len,
+                                            const uint8_t* limit) {
+  if (a == b || len == 0) return true;
+  WordReader ra(a, limit), rb(b, limit);
+  uint64_t left = len;
+  while (left) {
+    uint32_t take = left >= 8 ? 8u : uint32_t(left);
+    uint64_t wa = mask_low_bytes(ra.next(), take);
+    uint64_t wb = mask_low_bytes(rb.next(), take);
+    if (wa != wb) return false;
+    left -= take;
+  }
+  return true;
+}
+
+typedef unsigned __int128 u128;
+
+}  // namespace po

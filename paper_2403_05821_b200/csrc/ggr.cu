@@ -1,0 +1,884 @@
+// Greedy Group Recursion on the GPU (ggr.hpp:135-394), level-synchronous.
+//
+// The reference recursion (recurse, ggr.hpp:207-314) is processed one tree
+// level at a time. Every live node owns a value-group histogram ("table")
+// keyed by (column, vid) with the group's row count and one partner-length
+// sum per distinct FD partner of the column:
+//   * the root table is dense (index colbase[c] + vid) and comes free from
+//     the dictionary counts (K2);
+//   * a split's rest child inherits its parent's table and subtracts the
+//     block rows (decremental histogram: hist(rest) = hist(parent) -
+//     hist(block), exact integer arithmetic);
+//   * a split's block child gets a fresh hashed table aggregated from its
+//     own rows only.
+// Per level: K5 argmax_seg (exact u128 rational argmax with the reference's
+// total tie order) over every scanning node's table, a host decision per
+// node (early stop / split, ggr.hpp:276-301), K6 split (relabel rows), K4
+// group_hist aggregation of block rows, and K7 leaf_stats for every node that
+// falls back. After the last level the leaves are laid out in DFS order
+// (block before rest, ggr.hpp:303-313) and one K8 multikey row sort orders
+// every leaf's rows at once; K10 emits the schedule and K9 scores it. The
+// whole-table statistics fallback competes last (ggr.hpp:379-387).
+
+#include <cub/cub.cuh>
+#include <cooperative_groups.h>
+
+#include <algorithm>
+#include <chrono>
+#include <memory>
+#include <numeric>
+
+#include "internal.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace po {
+
+namespace {
+
+// ---------------------------------------------------------------------------
+// tables
+// ---------------------------------------------------------------------------
+struct TDesc {
+  unsigned long long* keys;  // hashed: (c+1)<<32 | vid, 0 = empty; null for dense
+  uint32_t* cnt;
+  unsigned long long* psum;  // cap * K
+  uint64_t cap;
+  uint32_t dense;
+  uint32_t pad;
+};
+
+struct HTable {
+  bool dense = false;
+  uint64_t cap = 0;
+  DevBuf<unsigned long long> keys;
+  DevBuf<uint32_t> cnt;
+  DevBuf<unsigned long long> psum;
+  TDesc desc() const {
+    return TDesc{keys.get(), cnt.get(), psum.get(), cap, dense ? 1u : 0u, 0u};
+  }
+};
+
+__device__ __forceinline__ uint64_t tkey_hash(unsigned long long k) { return fmix64(k); }
+
+__device__ __forceinline__ uint64_t tbl_insert(const TDesc& t, unsigned long long key) {
+  uint64_t s = tkey_hash(key) & (t.cap - 1);
+  for (;;) {
+    unsigned long long k = t.keys[s];
+    if (k == key) return s;
+    if (k == 0) {
+      unsigned long long prev = atomicCAS(&t.keys[s], 0ull, key);
+      if (prev == 0 || prev == key) return s;
+    }
+    s = (s + 1) & (t.cap - 1);
+  }
+}
+
+__device__ __forceinline__ uint64_t tbl_find(const TDesc& t, unsigned long long key) {
+  uint64_t s = tkey_hash(key) & (t.cap - 1);
+  for (;;) {
+    unsigned long long k = t.keys[s];
+    if (k == key || k == 0) return s;  // 0 cannot happen for a present key
+    s = (s + 1) & (t.cap - 1);
+  }
+}
+
+__device__ __forceinline__ uint32_t col_of_dense(const uint64_t* colbase, uint32_t m, uint64_t e) {
+  uint32_t lo = 0, hi = m;  // largest c with colbase[c] <= e
+  while (hi - lo > 1) {
+    uint32_t mid = (lo + hi) >> 1;
+    if (colbase[mid] <= e) lo = mid;
+    else hi = mid;
+  }
+  return lo;
+}
+
+// Decodes table entry e into (column, vid); false when the slot is empty.
+__device__ __forceinline__ bool decode_entry(const TDesc& t, const uint64_t* colbase, uint32_t m,
+                                             uint64_t e, uint32_t& c, uint32_t& v) {
+  if (t.dense) {
+    c = col_of_dense(colbase, m, e);
+    v = uint32_t(e - colbase[c]);
+    return true;
+  }
+  unsigned long long k = t.keys[e];
+  if (!k) return false;
+  c = uint32_t(k >> 32) - 1;
+  v = uint32_t(k);
+  return true;
+}
+
+__device__ __forceinline__ bool mask_has(const uint32_t* mask, uint32_t c) {
+  return (mask[c >> 5] >> (c & 31)) & 1u;
+}
+
+// ---------------------------------------------------------------------------
+// K5 argmax_seg
+// ---------------------------------------------------------------------------
+struct Cand {
+  u128 numer;
+  uint64_t count;  // 0 = no candidate
+  uint32_t col;
+  uint32_t vid;
+};
+
+// Candidate::better_than (ggr.hpp:189-197): exact rational compare of
+// numer/count via u128 cross products (wrapping exactly like the reference),
+// then larger count, lower column, smaller value (vid == raw-byte rank).
+__device__ __forceinline__ bool beats(const Cand& a, const Cand& b) {
+  if (a.count == 0) return false;
+  if (b.count == 0) return true;
+  u128 l = a.numer * u128(b.count), r = b.numer * u128(a.count);
+  if (l != r) return l > r;
+  if (a.count != b.count) return a.count > b.count;
+  if (a.col != b.col) return a.col < b.col;
+  return a.vid < b.vid;
+}
+
+__device__ __forceinline__ Cand shfl_cand(const Cand& a, int delta) {
+  Cand o;
+  uint64_t lo = uint64_t(a.numer), hi = uint64_t(a.numer >> 64);
+  lo = __shfl_down_sync(0xffffffffu, lo, delta);
+  hi = __shfl_down_sync(0xffffffffu, hi, delta);
+  o.numer = (u128(hi) << 64) | lo;
+  o.count = __shfl_down_sync(0xffffffffu, a.count, delta);
+  o.col = __shfl_down_sync(0xffffffffu, a.col, delta);
+  o.vid = __shfl_down_sync(0xffffffffu, a.vid, delta);
+  return o;
+}
+
+struct ScanSlot {
+  TDesc t;
+  uint32_t mask_off;  // into level colmask words
+  uint32_t w_off;     // into level partner weights (m*K per slot)
+};
+
+struct WorkItem {
+  uint32_t slot;
+  uint32_t pad;
+  uint64_t lo, hi;
+};
+
+constexpr int kArgBlock = 256;
+
+__global__ void __launch_bounds__(kArgBlock) k_argmax(
+    const WorkItem* __restrict__ work, const ScanSlot* __restrict__ slots,
+    const uint32_t* __restrict__ masks, const uint32_t* __restrict__ weights,
+    const uint64_t* __restrict__ colbase, const uint64_t* __restrict__ vlen, uint32_t m,
+    uint32_t K, Cand* partial, unsigned long long* partial_cands) {
+  const WorkItem w = work[blockIdx.x];
+  const ScanSlot sl = slots[w.slot];
+  const uint32_t* mask = masks + sl.mask_off;
+  const uint32_t* wt = weights + sl.w_off;
+  Cand best;
+  best.numer = 0;
+  best.count = 0;
+  best.col = 0;
+  best.vid = 0;
+  unsigned long long ncand = 0;
+  for (uint64_t e = w.lo + threadIdx.x; e < w.hi; e += blockDim.x) {
+    uint32_t c, v;
+    if (!decode_entry(sl.t, colbase, m, e, c, v)) continue;
+    const uint32_t cnt = sl.t.cnt[e];
+    if (cnt == 0 || !mask_has(mask, c)) continue;
+    ++ncand;
+    const uint64_t vl = vlen[colbase[c] + v];
+    uint64_t ptot = 0;
+    for (uint32_t k = 0; k < K; ++k)
+      if (wt[c * K + k]) ptot += uint64_t(wt[c * K + k]) * sl.t.psum[e * K + k];
+    // hitcount numerator (ggr.hpp:261-266)
+    Cand cd;
+    cd.numer = (u128(vl) * vl * cnt + ptot) * u128(cnt - 1);
+    cd.count = cnt;
+    cd.col = c;
+    cd.vid = v;
+    if (beats(cd, best)) best = cd;
+  }
+  // block reduction (any order: beats is a total order)
+  for (int d = 16; d > 0; d >>= 1) {
+    Cand o = shfl_cand(best, d);
+    if (beats(o, best)) best = o;
+    ncand += __shfl_down_sync(0xffffffffu, ncand, d);
+  }
+  __shared__ Cand sb[kArgBlock / 32];
+  __shared__ unsigned long long sc[kArgBlock / 32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) {
+    sb[wid] = best;
+    sc[wid] = ncand;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    Cand b = sb[0];
+    unsigned long long n = sc[0];
+    for (int i = 1; i < kArgBlock / 32; ++i) {
+      if (beats(sb[i], b)) b = sb[i];
+      n += sc[i];
+    }
+    partial[blockIdx.x] = b;
+    partial_cands[blockIdx.x] = n;
+  }
+}
+
+__global__ void k_argmax_final(const Cand* partial, const unsigned long long* partial_cands,
+                               const uint32_t* slot_work_off, uint32_t nslots, Cand* out,
+                               unsigned long long* out_cands) {
+  for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < nslots; s += gridDim.x * blockDim.x) {
+    Cand b;
+    b.numer = 0;
+    b.count = 0;
+    b.col = 0;
+    b.vid = 0;
+    unsigned long long n = 0;
+    for (uint32_t i = slot_work_off[s]; i < slot_work_off[s + 1]; ++i) {
+      if (beats(partial[i], b)) b = partial[i];
+      n += partial_cands[i];
+    }
+    out[s] = b;
+    out_cands[s] = n;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K6 split: relabel rows of split nodes and collect block rows
+// ---------------------------------------------------------------------------
+struct SplitD {
+  TDesc tB;           // new table of the block child (keys null: not needed)
+  TDesc tP;           // parent table to decrement for the rest child (cnt null: not needed)
+  uint32_t mask_off;  // parent columns
+  uint32_t col, vid;
+  uint32_t block_id, rest_id;
+  uint32_t need_rows;
+};
+
+__global__ void k_relabel(uint32_t* node_of_row, uint64_t n, const int32_t* split_of_node,
+                          const SplitD* sp, const uint32_t* vid, uint32_t m, uint32_t* cursor,
+                          const uint64_t* seg_off, uint32_t* blockrows) {
+  const uint32_t lane = threadIdx.x & 31;
+  for (uint64_t base = blockIdx.x * uint64_t(blockDim.x); base < n;
+       base += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t r = base + threadIdx.x;
+    int32_t j = -1;
+    bool inb = false;
+    if (r < n) {
+      j = split_of_node[node_of_row[r]];
+      if (j >= 0) {
+        const SplitD& d = sp[j];
+        inb = vid[r * m + d.col] == d.vid;
+        node_of_row[r] = inb ? d.block_id : d.rest_id;
+        if (!d.need_rows) inb = false;
+      }
+    }
+    // warp-aggregated append of block rows to their split's segment
+    const unsigned active = __ballot_sync(0xffffffffu, inb);
+    if (inb) {
+      const unsigned peers = __match_any_sync(active, j);
+      const int leader = __ffs(peers) - 1;
+      uint32_t basepos = 0;
+      if (int(lane) == leader) basepos = atomicAdd(&cursor[j], uint32_t(__popc(peers)));
+      basepos = __shfl_sync(peers, basepos, leader);
+      const uint32_t rank = __popc(peers & ((1u << lane) - 1));
+      blockrows[seg_off[j] + basepos + rank] = uint32_t(r);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K4 group_hist: block-row aggregation into the block child's table and
+// decrement of the parent's table (inherited by the rest child)
+// ---------------------------------------------------------------------------
+__global__ void k_aggregate(const uint32_t* blockrows, uint64_t total_rows, const uint64_t* seg_off,
+                            uint32_t nsplit, const SplitD* sp, const uint32_t* masks,
+                            const uint32_t* vid, const uint64_t* vlen, const uint64_t* colbase,
+                            uint32_t m, uint32_t K, const int32_t* dpart, const uint32_t* npart) {
+  const uint64_t total = total_rows * m;
+  for (uint64_t t = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; t < total;
+       t += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t q = t / m;
+    const uint32_t c = uint32_t(t - q * m);
+    // split owning block row q
+    uint32_t lo = 0, hi = nsplit;
+    while (hi - lo > 1) {
+      uint32_t mid = (lo + hi) >> 1;
+      if (seg_off[mid] <= q) lo = mid;
+      else hi = mid;
+    }
+    const SplitD& d = sp[lo];
+    if (!mask_has(masks + d.mask_off, c)) continue;
+    const uint64_t r = blockrows[q];
+    const uint32_t v = vid[r * m + c];
+    const unsigned long long key = (uint64_t(c + 1) << 32) | v;
+    if (d.tB.keys) {
+      const uint64_t s = tbl_insert(d.tB, key);
+      atomicAdd(&d.tB.cnt[s], 1u);
+      for (uint32_t k = 0; k < npart[c]; ++k) {
+        const int32_t p = dpart[c * K + k];
+        atomicAdd(&d.tB.psum[s * K + k],
+                  (unsigned long long)vlen[colbase[p] + vid[r * m + p]]);
+      }
+    }
+    if (d.tP.cnt) {
+      const uint64_t s = d.tP.dense ? colbase[c] + v : tbl_find(d.tP, key);
+      atomicSub(&d.tP.cnt[s], 1u);
+      for (uint32_t k = 0; k < npart[c]; ++k) {
+        const int32_t p = dpart[c * K + k];
+        atomicAdd(&d.tP.psum[s * K + k],
+                  (unsigned long long)(0ull - vlen[colbase[p] + vid[r * m + p]]));
+      }
+    }
+  }
+}
+
+// Root partner sums: psum[colbase[c]+vid(r,c)][k] += len(r, partner k of c).
+__global__ void k_root_psum(const uint32_t* vid, uint64_t n, uint32_t m, uint32_t K,
+                            const int32_t* dpart, const uint32_t* npart, const uint64_t* vlen,
+                            const uint64_t* colbase, unsigned long long* psum) {
+  const uint64_t total = n * m;
+  for (uint64_t t = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; t < total;
+       t += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t r = t / m;
+    const uint32_t c = uint32_t(t - r * m);
+    const uint32_t np = npart[c];
+    if (!np) continue;
+    const uint64_t e = colbase[c] + vid[t];
+    for (uint32_t k = 0; k < np; ++k) {
+      const int32_t p = dpart[c * K + k];
+      atomicAdd(&psum[e * K + k], (unsigned long long)vlen[colbase[p] + vid[r * m + p]]);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K7 leaf_stats: per (leaf, column) distinct count and length sum
+// ---------------------------------------------------------------------------
+__global__ void k_leaf_stats(const WorkItem* work, const ScanSlot* slots, const uint32_t* masks,
+                             const uint64_t* colbase, const uint64_t* vlen, uint32_t m,
+                             unsigned long long* card, unsigned long long* tot) {
+  const WorkItem w = work[blockIdx.x];
+  const ScanSlot sl = slots[w.slot];
+  const uint32_t* mask = masks + sl.mask_off;
+  for (uint64_t e = w.lo + threadIdx.x; e < w.hi; e += blockDim.x) {
+    uint32_t c, v;
+    if (!decode_entry(sl.t, colbase, m, e, c, v)) continue;
+    const uint32_t cnt = sl.t.cnt[e];
+    if (cnt == 0 || !mask_has(mask, c)) continue;
+    atomicAdd(&card[uint64_t(w.slot) * m + c], 1ull);
+    atomicAdd(&tot[uint64_t(w.slot) * m + c], (unsigned long long)(uint64_t(cnt) * vlen[colbase[c] + v]));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// layout + emit
+// ---------------------------------------------------------------------------
+__global__ void k_row_leaf(const uint32_t* node_of_row, uint64_t n, const uint32_t* node_leaf,
+                           const uint32_t* leaf_off, uint32_t* row_leaf, uint32_t* grp) {
+  for (uint64_t r = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; r < n;
+       r += uint64_t(gridDim.x) * blockDim.x) {
+    const uint32_t l = node_leaf[node_of_row[r]];
+    row_leaf[r] = l;
+    grp[r] = leaf_off[l];
+  }
+}
+
+__global__ void k_emit(const uint32_t* pos, uint64_t n, uint32_t m, const uint32_t* row_leaf,
+                       const int32_t* leaf_orders, uint32_t* rows_out, int32_t* orders_out) {
+  for (uint64_t r = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; r < n;
+       r += uint64_t(gridDim.x) * blockDim.x) {
+    const uint32_t p = pos[r];
+    rows_out[p] = uint32_t(r);
+    const int32_t* src = leaf_orders + uint64_t(row_leaf[r]) * m;
+    int32_t* dst = orders_out + uint64_t(p) * m;
+    for (uint32_t f = 0; f < m; ++f) dst[f] = src[f];
+  }
+}
+
+__global__ void k_tile_order(const int32_t* order, uint64_t n, uint32_t m, int32_t* out) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n * m;
+       i += uint64_t(gridDim.x) * blockDim.x)
+    out[i] = order[i % m];
+}
+
+__global__ void k_iota_u32(uint32_t* a, uint64_t n) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
+       i += uint64_t(gridDim.x) * blockDim.x)
+    a[i] = uint32_t(i);
+}
+
+// ---------------------------------------------------------------------------
+// host-side tree
+// ---------------------------------------------------------------------------
+enum Kind { SCAN, EMPTY, ROWID, SINGLE, RAW1, FALLBACK, SPLIT };
+
+struct Node {
+  uint64_t size = 0;
+  std::vector<int> cols;  // ascending schema order (ggr.hpp:177, 292-296)
+  uint64_t rd = 0, cd = 0, depth = 0;
+  int kind = SCAN;
+  std::shared_ptr<HTable> table;
+  std::vector<int> block_cols;  // SPLIT: [best.col] + active partners
+  int block_child = -1, rest_child = -1;
+  std::vector<int> leaf_order;  // FALLBACK: stats-ranked order
+};
+
+int classify(const Node& nd, const po_ggr_config& cfg) {
+  // base cases then depth gate, in the reference's order (ggr.hpp:213-234)
+  if (nd.size == 0) return EMPTY;
+  if (nd.cols.empty()) return ROWID;
+  if (nd.size == 1) return SINGLE;
+  if (nd.cols.size() == 1) return RAW1;
+  if (nd.rd > cfg.row_recursion_depth || nd.cd > cfg.column_recursion_depth) return FALLBACK;
+  return SCAN;
+}
+
+constexpr uint64_t kWorkChunk = 8192;
+
+struct Level {
+  std::vector<ScanSlot> slots;
+  std::vector<uint32_t> masks;
+  std::vector<uint32_t> weights;
+  std::vector<WorkItem> work;
+  std::vector<uint32_t> slot_work_off{0};
+};
+
+}  // namespace
+
+void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups,
+                const po_ggr_config& cfg, uint32_t* d_rows, int32_t* d_orders, GgrOutput& out,
+                cudaStream_t s) {
+  const uint64_t n = e.n;
+  const uint32_t m = e.m;
+  out = GgrOutput{};
+  out.stats.recursive_calls = 1;  // the root call (ggr.hpp:210)
+  if (n == 0) return;
+  if (m == 0) {  // every row, ascending, no fields (ggr.hpp:214-219)
+    PO_LAUNCH(k_iota_u32, grid_for(n, 256), 256, 0, s, d_rows, n);
+    return;
+  }
+
+  // FD partners (ggr.hpp:154-164): per field, the other members of every
+  // group holding it, each group's members in ascending order.
+  std::vector<std::vector<int>> partners(m);
+  if (cfg.use_fds) {
+    for (const auto& g : fd_groups) {
+      std::vector<int> mem = g;
+      for (int f : mem)
+        if (f < 0 || f >= int(m)) fail(PO_ERR_SCHEMA, "FD group names a field outside the schema");
+      std::sort(mem.begin(), mem.end());
+      for (int f : mem)
+        for (int o : mem)
+          if (o != f) partners[f].push_back(o);
+    }
+  }
+  uint32_t K = 0;
+  std::vector<std::vector<int>> dpart(m);
+  for (uint32_t c = 0; c < m; ++c) {
+    std::vector<int> u = partners[c];
+    std::sort(u.begin(), u.end());
+    if (std::adjacent_find(u.begin(), u.end()) != u.end())
+      fail(PO_ERR_SCHEMA,
+           "FD groups repeat a field pair (a field would appear twice in a field order); "
+           "groups must not share two members");
+    dpart[c] = u;
+    K = std::max<uint32_t>(K, uint32_t(u.size()));
+  }
+  std::vector<int32_t> h_dpart(std::max<size_t>(1, size_t(m) * K), 0);
+  std::vector<uint32_t> h_npart(m, 0);
+  for (uint32_t c = 0; c < m; ++c) {
+    h_npart[c] = uint32_t(dpart[c].size());
+    for (size_t k = 0; k < dpart[c].size(); ++k) h_dpart[c * K + k] = dpart[c][k];
+  }
+  auto d_dpart = to_device(h_dpart, s);
+  auto d_npart = to_device(h_npart, s);
+  const uint32_t W = (m + 31) / 32;
+  const uint64_t* colbase = e.d_colbase.get();
+  const uint64_t* vlen = e.vlen.get();
+
+  // Tree state.
+  std::vector<Node> nodes;
+  nodes.reserve(1024);
+  {
+    Node root;
+    root.size = n;
+    root.cols.resize(m);
+    std::iota(root.cols.begin(), root.cols.end(), 0);
+    root.kind = classify(root, cfg);
+    nodes.push_back(std::move(root));
+  }
+  DevBuf<uint32_t> node_of_row(n, s);
+  node_of_row.zero();
+  std::vector<int32_t> h_split_of_node;
+  DevBuf<int32_t> split_of_node;
+  auto ensure_split_map = [&](size_t need) {
+    if (split_of_node.size() >= need) return;
+    size_t cap = std::max<size_t>(1024, split_of_node.size());
+    while (cap < need) cap *= 2;
+    DevBuf<int32_t> nb(cap, s);
+    nb.fill_bytes(0xFF);
+    if (split_of_node.size())
+      PO_CUDA(cudaMemcpyAsync(nb.get(), split_of_node.get(), split_of_node.size() * sizeof(int32_t),
+                              cudaMemcpyDeviceToDevice, s));
+    split_of_node = std::move(nb);
+  };
+  ensure_split_map(1024);
+
+  auto col_mask = [&](const std::vector<int>& cols, std::vector<uint32_t>& dst) {
+    uint32_t off = uint32_t(dst.size());
+    dst.resize(dst.size() + W, 0);
+    for (int c : cols) dst[off + (uint32_t(c) >> 5)] |= 1u << (uint32_t(c) & 31);
+    return off;
+  };
+
+  // Root table: dense over all distinct values.
+  if (nodes[0].kind == SCAN || nodes[0].kind == FALLBACK) {
+    auto t = std::make_shared<HTable>();
+    t->dense = true;
+    t->cap = e.D;
+    t->cnt.alloc(e.D, s);
+    PO_CUDA(cudaMemcpyAsync(t->cnt.get(), e.count.get(), e.D * sizeof(uint32_t),
+                            cudaMemcpyDeviceToDevice, s));
+    if (K) {
+      t->psum.alloc(e.D * K, s);
+      t->psum.zero();
+      PO_LAUNCH(k_root_psum, grid_for(n * m, 256), 256, 0, s, e.vid.get(), n, m, K, d_dpart.get(),
+                d_npart.get(), vlen, colbase, t->psum.get());
+    }
+    nodes[0].table = t;
+  }
+
+  // Leaf statistics for nodes that fall back (FALLBACK kind with a table).
+  auto run_leaf_stats = [&](const std::vector<int>& leaves) {
+    if (leaves.empty()) return;
+    Level L;
+    for (size_t i = 0; i < leaves.size(); ++i) {
+      const Node& nd = nodes[leaves[i]];
+      ScanSlot sl;
+      sl.t = nd.table->desc();
+      sl.mask_off = col_mask(nd.cols, L.masks);
+      sl.w_off = 0;
+      L.slots.push_back(sl);
+      for (uint64_t lo = 0; lo < nd.table->cap; lo += kWorkChunk)
+        L.work.push_back(WorkItem{uint32_t(i), 0, lo, std::min(nd.table->cap, lo + kWorkChunk)});
+    }
+    auto d_slots = to_device(L.slots, s);
+    auto d_masks = to_device(L.masks, s);
+    auto d_work = to_device(L.work, s);
+    DevBuf<unsigned long long> card(leaves.size() * m, s), tot(leaves.size() * m, s);
+    card.zero();
+    tot.zero();
+    PO_LAUNCH(k_leaf_stats, unsigned(L.work.size()), 256, 0, s, d_work.get(), d_slots.get(),
+              d_masks.get(), colbase, vlen, m, card.get(), tot.get());
+    std::vector<unsigned long long> hc(leaves.size() * m), ht(leaves.size() * m);
+    card.download(hc.data(), hc.size());
+    tot.download(ht.data(), ht.size());
+    sync(s);
+    for (size_t i = 0; i < leaves.size(); ++i) {
+      Node& nd = nodes[leaves[i]];
+      std::vector<uint64_t> cc(nd.cols.size());
+      std::vector<double> avg(nd.cols.size());
+      for (size_t k = 0; k < nd.cols.size(); ++k) {
+        cc[k] = hc[i * m + nd.cols[k]];
+        avg[k] = static_cast<double>(ht[i * m + nd.cols[k]]) / static_cast<double>(nd.size);
+      }
+      // fallback (ggr.hpp:319-338): local stats -> stats-ranked order
+      std::vector<int> local = hitcount_order(nd.size, cc, avg, cfg.stats_variant);
+      nd.leaf_order.clear();
+      for (int li : local) nd.leaf_order.push_back(nd.cols[li]);
+      nd.table.reset();
+    }
+  };
+
+  std::vector<int> frontier;
+  if (nodes[0].kind == SCAN) frontier.push_back(0);
+  else if (nodes[0].kind == FALLBACK) run_leaf_stats({0});
+
+  while (!frontier.empty()) {
+    // ---- K5: argmax over every scanning node of this level ----
+    Level L;
+    for (size_t i = 0; i < frontier.size(); ++i) {
+      const Node& nd = nodes[frontier[i]];
+      ScanSlot sl;
+      sl.t = nd.table->desc();
+      sl.mask_off = col_mask(nd.cols, L.masks);
+      sl.w_off = uint32_t(L.weights.size());
+      L.weights.resize(L.weights.size() + size_t(m) * std::max<uint32_t>(K, 1), 0);
+      std::vector<char> act(m, 0);
+      for (int c : nd.cols) act[c] = 1;
+      for (uint32_t c = 0; c < m; ++c)
+        for (size_t k = 0; k < dpart[c].size(); ++k)
+          if (act[dpart[c][k]]) L.weights[sl.w_off + c * K + k] = 1;
+      L.slots.push_back(sl);
+      for (uint64_t lo = 0; lo < nd.table->cap; lo += kWorkChunk)
+        L.work.push_back(WorkItem{uint32_t(i), 0, lo, std::min(nd.table->cap, lo + kWorkChunk)});
+      L.slot_work_off.push_back(uint32_t(L.work.size()));
+    }
+    const uint32_t nslots = uint32_t(L.slots.size());
+    auto d_slots = to_device(L.slots, s);
+    auto d_masks = to_device(L.masks, s);
+    if (L.weights.empty()) L.weights.push_back(0);
+    auto d_w = to_device(L.weights, s);
+    auto d_work = to_device(L.work, s);
+    auto d_swo = to_device(L.slot_work_off, s);
+    DevBuf<Cand> partial(std::max<size_t>(1, L.work.size()), s);
+    DevBuf<unsigned long long> pcands(std::max<size_t>(1, L.work.size()), s);
+    DevBuf<Cand> best(nslots, s);
+    DevBuf<unsigned long long> ncand(nslots, s);
+    PO_LAUNCH(k_argmax, unsigned(L.work.size()), kArgBlock, 0, s, d_work.get(), d_slots.get(),
+              d_masks.get(), d_w.get(), colbase, vlen, m, K, partial.get(), pcands.get());
+    PO_LAUNCH(k_argmax_final, grid_for(nslots, 128), 128, 0, s, partial.get(), pcands.get(),
+              d_swo.get(), nslots, best.get(), ncand.get());
+    std::vector<Cand> hbest(nslots);
+    std::vector<unsigned long long> hn(nslots);
+    best.download(hbest.data(), nslots);
+    ncand.download(hn.data(), nslots);
+    sync(s);
+
+    // ---- host decisions (ggr.hpp:276-301) ----
+    std::vector<int> stopped, new_fallback, next;
+    struct SplitH {
+      int node;
+      SplitD d;
+    };
+    std::vector<SplitH> splits;
+    std::vector<uint32_t> split_masks;
+    for (uint32_t i = 0; i < nslots; ++i) {
+      const int id = frontier[i];
+      out.stats.candidates_examined += hn[i];
+      const Cand& b = hbest[i];
+      if (b.count == 0 || b.numer == 0 ||
+          b.numer < u128(cfg.hitcount_stop_threshold) * u128(b.count)) {
+        nodes[id].kind = FALLBACK;
+        stopped.push_back(id);
+        continue;
+      }
+      Node& P = nodes[id];
+      P.kind = SPLIT;
+      std::vector<char> act(m, 0);
+      for (int c : P.cols) act[c] = 1;
+      P.block_cols = {int(b.col)};
+      for (int o : partners[b.col])
+        if (act[o]) P.block_cols.push_back(o);
+      Node B, R;
+      B.size = b.count;
+      for (int c : P.cols)
+        if (std::find(P.block_cols.begin(), P.block_cols.end(), c) == P.block_cols.end())
+          B.cols.push_back(c);
+      B.rd = P.rd;
+      B.cd = P.cd + 1;
+      B.depth = P.depth + 1;
+      R.size = P.size - b.count;
+      R.cols = P.cols;
+      R.rd = P.rd + 1;
+      R.cd = P.cd;
+      R.depth = P.depth + 1;
+      B.kind = classify(B, cfg);
+      R.kind = classify(R, cfg);
+      out.stats.recursive_calls += 2;
+      out.stats.max_depth = std::max<uint64_t>(out.stats.max_depth, P.depth + 1);
+      const bool needB = B.kind == SCAN || B.kind == FALLBACK;
+      const bool needR = R.kind == SCAN || R.kind == FALLBACK;
+      SplitD d{};
+      d.mask_off = col_mask(P.cols, split_masks);
+      d.col = b.col;
+      d.vid = b.vid;
+      if (needB) {
+        // entries <= sum over the parent's columns of min(card, |B|)
+        uint64_t bound = 0;
+        for (int c : P.cols) bound += std::min<uint64_t>(e.card[c], B.size);
+        uint64_t cap = 64;
+        while (cap < 2 * bound) cap <<= 1;
+        auto t = std::make_shared<HTable>();
+        t->cap = cap;
+        t->keys.alloc(cap, s);
+        t->keys.zero();
+        t->cnt.alloc(cap, s);
+        t->cnt.zero();
+        if (K) {
+          t->psum.alloc(cap * K, s);
+          t->psum.zero();
+        }
+        B.table = t;
+        d.tB = t->desc();
+      }
+      if (needR) {
+        R.table = P.table;
+        d.tP = P.table->desc();
+      }
+      d.need_rows = (needB || needR) ? 1u : 0u;
+      P.table.reset();
+      const int bid = int(nodes.size());
+      P.block_child = bid;
+      P.rest_child = bid + 1;
+      d.block_id = uint32_t(bid);
+      d.rest_id = uint32_t(bid + 1);
+      splits.push_back({id, d});
+      nodes.push_back(std::move(B));
+      nodes.push_back(std::move(R));
+      for (int ch : {bid, bid + 1}) {
+        if (nodes[ch].kind == SCAN) next.push_back(ch);
+        else if (nodes[ch].kind == FALLBACK) new_fallback.push_back(ch);
+      }
+    }
+
+    // ---- K6 split + K4 aggregation ----
+    if (!splits.empty()) {
+      const uint32_t ns = uint32_t(splits.size());
+      ensure_split_map(nodes.size());
+      std::vector<SplitD> hsp(ns);
+      std::vector<uint64_t> seg(ns + 1, 0);
+      for (uint32_t j = 0; j < ns; ++j) {
+        hsp[j] = splits[j].d;
+        seg[j + 1] = seg[j] + (hsp[j].need_rows ? nodes[hsp[j].block_id].size : 0);
+        int32_t jj = int32_t(j);
+        PO_CUDA(cudaMemcpyAsync(split_of_node.get() + splits[j].node, &jj, sizeof(int32_t),
+                                cudaMemcpyHostToDevice, s));
+      }
+      auto d_sp = to_device(hsp, s);
+      auto d_seg = to_device(seg, s);
+      auto d_smask = to_device(split_masks, s);
+      DevBuf<uint32_t> cursor(ns, s);
+      cursor.zero();
+      DevBuf<uint32_t> blockrows(std::max<uint64_t>(1, seg[ns]), s);
+      PO_LAUNCH(k_relabel, grid_for(n, 256), 256, 0, s, node_of_row.get(), n,
+                split_of_node.get(), d_sp.get(), e.vid.get(), m, cursor.get(), d_seg.get(),
+                blockrows.get());
+      if (seg[ns])
+        PO_LAUNCH(k_aggregate, grid_for(seg[ns] * m, 256), 256, 0, s, blockrows.get(), seg[ns],
+                  d_seg.get(), ns, d_sp.get(), d_smask.get(), e.vid.get(), vlen, colbase, m, K,
+                  d_dpart.get(), d_npart.get());
+      // unmark split nodes (host buffer must outlive the async copies: sync)
+      std::vector<int32_t> minus1(1, -1);
+      for (uint32_t j = 0; j < ns; ++j)
+        PO_CUDA(cudaMemcpyAsync(split_of_node.get() + splits[j].node, minus1.data(),
+                                sizeof(int32_t), cudaMemcpyHostToDevice, s));
+      sync(s);
+    }
+
+    // ---- K7: statistics of every node that falls back at this level ----
+    std::vector<int> leaves = stopped;
+    leaves.insert(leaves.end(), new_fallback.begin(), new_fallback.end());
+    run_leaf_stats(leaves);
+    frontier.swap(next);
+  }
+
+  // ---- layout: leaves in DFS order, block subtree first ----
+  std::vector<int> leaf_nodes;
+  std::vector<std::vector<int>> leaf_full_order;
+  std::vector<uint32_t> node_leaf(nodes.size(), 0);
+  {
+    struct Frame {
+      int id;
+      std::vector<int> prefix;
+    };
+    std::vector<Frame> stack;
+    stack.push_back({0, {}});
+    while (!stack.empty()) {
+      Frame f = std::move(stack.back());
+      stack.pop_back();
+      const Node& nd = nodes[f.id];
+      if (nd.kind == SPLIT) {
+        std::vector<int> bp = f.prefix;
+        bp.insert(bp.end(), nd.block_cols.begin(), nd.block_cols.end());
+        stack.push_back({nd.rest_child, f.prefix});  // popped after the block subtree
+        stack.push_back({nd.block_child, std::move(bp)});
+        continue;
+      }
+      if (nd.kind == EMPTY) continue;
+      std::vector<int> full = f.prefix;
+      if (nd.kind == FALLBACK) full.insert(full.end(), nd.leaf_order.begin(), nd.leaf_order.end());
+      else full.insert(full.end(), nd.cols.begin(), nd.cols.end());
+      if (full.size() != m) fail(PO_ERR_ERROR, "internal: leaf field order is not a permutation");
+      node_leaf[f.id] = uint32_t(leaf_nodes.size());
+      leaf_nodes.push_back(f.id);
+      leaf_full_order.push_back(std::move(full));
+    }
+  }
+  const uint32_t nleaves = uint32_t(leaf_nodes.size());
+  std::vector<uint32_t> leaf_off(nleaves, 0), leaf_chunk_off(nleaves), leaf_nchunks(nleaves);
+  std::vector<uint32_t> chunk_key_off, chunk_nkeys;
+  std::vector<int32_t> key_field, h_leaf_orders(size_t(nleaves) * m);
+  std::vector<uint8_t> key_kind, key_bits;
+  uint64_t off = 0;
+  for (uint32_t l = 0; l < nleaves; ++l) {
+    const Node& nd = nodes[leaf_nodes[l]];
+    leaf_off[l] = uint32_t(off);
+    off += nd.size;
+    std::copy(leaf_full_order[l].begin(), leaf_full_order[l].end(),
+              h_leaf_orders.begin() + size_t(l) * m);
+    // sort keys of the leaf
+    std::vector<std::pair<int, uint8_t>> keys;  // (field, kind)
+    if (nd.kind == RAW1) keys.push_back({nd.cols[0], 0});  // raw bytes (ggr.hpp:221-231)
+    else if (nd.kind == FALLBACK)                          // fragment keys (ggr.hpp:340-350)
+      for (int f : nd.leaf_order) keys.push_back({f, 1});
+    leaf_chunk_off[l] = uint32_t(chunk_nkeys.size());
+    int used = 64;
+    for (auto [f, kind] : keys) {
+      int b = bits_for(e.card[f] ? e.card[f] - 1 : 0);
+      if (used + b > 64) {
+        chunk_key_off.push_back(uint32_t(key_field.size()));
+        chunk_nkeys.push_back(0);
+        used = 0;
+      }
+      key_field.push_back(f);
+      key_kind.push_back(kind);
+      key_bits.push_back(uint8_t(b));
+      chunk_nkeys.back()++;
+      used += b;
+    }
+    leaf_nchunks[l] = uint32_t(chunk_nkeys.size()) - leaf_chunk_off[l];
+  }
+  if (off != n) fail(PO_ERR_ERROR, "internal: leaves do not cover the table");
+  if (chunk_nkeys.empty()) {
+    chunk_key_off.push_back(0);
+    chunk_nkeys.push_back(0);
+    key_field.push_back(0);
+    key_kind.push_back(0);
+    key_bits.push_back(1);
+  }
+  auto d_node_leaf = to_device(node_leaf, s);
+  auto d_leaf_off = to_device(leaf_off, s);
+  auto d_lco = to_device(leaf_chunk_off, s), d_lnc = to_device(leaf_nchunks, s);
+  auto d_cko = to_device(chunk_key_off, s), d_cnk = to_device(chunk_nkeys, s);
+  auto d_kf = to_device(key_field, s);
+  auto d_kk = to_device(key_kind, s), d_kb = to_device(key_bits, s);
+  auto d_leaf_orders = to_device(h_leaf_orders, s);
+  DevBuf<uint32_t> row_leaf(n, s), grp(n, s), pos(n, s);
+  PO_LAUNCH(k_row_leaf, grid_for(n, 256), 256, 0, s, node_of_row.get(), n, d_node_leaf.get(),
+            d_leaf_off.get(), row_leaf.get(), grp.get());
+  RefineKey RK;
+  RK.kind = 2;
+  RK.m = m;
+  RK.vid = e.vid.get();
+  RK.esc_rank = e.esc_rank.get();
+  RK.colbase = colbase;
+  RK.row_leaf = row_leaf.get();
+  RK.leaf_chunk_off = d_lco.get();
+  RK.leaf_nchunks = d_lnc.get();
+  RK.chunk_key_off = d_cko.get();
+  RK.chunk_nkeys = d_cnk.get();
+  RK.key_field = d_kf.get();
+  RK.key_kind = d_kk.get();
+  RK.key_bits = d_kb.get();
+  refine_sort(uint32_t(n), grp.get(), uint32_t(n), RK, pos.get(), s);
+  PO_LAUNCH(k_emit, grid_for(n, 256), 256, 0, s, pos.get(), n, m, row_leaf.get(),
+            d_leaf_orders.get(), d_rows, d_orders);
+  out.phc = phc_device(e, n, nullptr, d_rows, nullptr, d_orders, s);
+
+  // ---- whole-table fallback competition (ggr.hpp:379-387) ----
+  std::vector<double> avg(m);
+  for (uint32_t c = 0; c < m; ++c)
+    avg[c] = static_cast<double>(e.total_len[c]) / static_cast<double>(n);
+  std::vector<int> fb_order = hitcount_order(n, e.card, avg, cfg.stats_variant);
+  DevBuf<uint32_t> fb_perm(n, s);
+  sort_all_rows(e, fb_order, fb_perm.get(), s);
+  std::vector<int32_t> fo(fb_order.begin(), fb_order.end());
+  auto d_fo = to_device(fo, s);
+  const uint64_t fb_phc = phc_device(e, n, nullptr, fb_perm.get(), nullptr, d_fo.get(), s, 1, true);
+  if (fb_phc > out.phc) {
+    PO_CUDA(cudaMemcpyAsync(d_rows, fb_perm.get(), n * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
+    PO_LAUNCH(k_tile_order, grid_for(n * m, 256), 256, 0, s, d_fo.get(), n, m, d_orders);
+    out.phc = fb_phc;
+  }
+  sync(s);
+}
+
+}  // namespace po

@@ -1,0 +1,124 @@
+// Internal interfaces between the translation units of libprefixopt_cuda.so.
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+namespace po {
+
+// Device view of the caller's table (arena/offsets already in HBM).
+struct DeviceTable {
+  uint64_t n = 0;
+  uint32_t m = 0;
+  std::vector<std::string> names;  // host
+  const uint8_t* arena = nullptr;  // device
+  uint64_t arena_bytes = 0;
+  const uint64_t* offsets = nullptr;  // device, n*m+1
+  const uint64_t* cell_lens = nullptr;  // device or null (custom tokenizer)
+  // owned copies when the caller passed host buffers
+  DevBuf<uint8_t> own_arena;
+  DevBuf<uint64_t> own_offsets;
+  DevBuf<uint64_t> own_lens;
+};
+
+// Builds a DeviceTable from the ABI view, copying host buffers to HBM.
+void make_device_table(const po_table* t, int tok, cudaStream_t s, DeviceTable& out);
+
+// Exact dictionary encoding of every column (K1 cell_scan + K2 dict_encode +
+// K3 rank_sort). After encode():
+//   vid[r*m+c]           rank of cell (r,c)'s value among the distinct values
+//                        of column c in raw-byte order (== dense value id)
+//   card[c], colbase[c]  distinct count and prefix sum (host + device)
+//   the per-distinct arrays below are indexed by colbase[c] + vid:
+//   vlen                 segment length of the value (tokenizer + scoring)
+//   count                occurrences of the value in column c
+//   esc_rank             rank of the value in the escaped fragment-key order
+//                        (json_escape(v) followed by '"', scoring.hpp:33-69)
+struct Encoded {
+  uint64_t n = 0;
+  uint32_t m = 0;
+  uint64_t D = 0;  // total distinct values
+  std::vector<uint64_t> card, colbase;  // host (colbase has m+1 entries)
+  DevBuf<uint64_t> d_colbase;
+  DevBuf<uint32_t> vid;       // n*m
+  DevBuf<uint64_t> vlen;      // D
+  DevBuf<uint32_t> count;     // D
+  DevBuf<uint32_t> esc_rank;  // D
+  DevBuf<uint32_t> rep_row;   // D: a row holding the value
+  std::vector<uint64_t> total_len;  // host, per column: sum of segment lengths (stats.hpp:38)
+};
+
+void encode(const DeviceTable& t, int tok, int scoring, cudaStream_t s, Encoded& e,
+            uint32_t hash_bits_debug = 64);
+
+// Segmented refinement sort (rank_sort / multikey_sort engine).
+// Items [0, n_items) start in groups whose ids are their final start
+// positions (grp_init[i]); each round sorts the unresolved items of every
+// group by the next 63-bit key chunk (stable, so the initial item order breaks
+// all remaining ties) and splits groups on chunk changes. An item is resolved
+// when its run has one member or its key reports `terminal`.
+// out_pos[item] receives the item's final position.
+struct RefineKey {
+  int kind = 0;  // 0 = string (raw order), 1 = string (escaped order), 2 = row keys
+  // string keys
+  const uint8_t* arena = nullptr;
+  uint64_t arena_bytes = 0;
+  const uint64_t* offsets = nullptr;
+  const uint32_t* item_cell_row = nullptr;  // item -> row of the cell holding the string
+  const uint32_t* item_col = nullptr;       // item -> column
+  uint32_t m = 0;
+  // row keys
+  const uint32_t* vid = nullptr;
+  const uint32_t* esc_rank = nullptr;
+  const uint64_t* colbase = nullptr;
+  const uint32_t* row_leaf = nullptr;      // row -> leaf index
+  const uint32_t* leaf_chunk_off = nullptr;  // leaf -> first chunk descriptor
+  const uint32_t* leaf_nchunks = nullptr;
+  const uint32_t* chunk_key_off = nullptr;   // chunk -> first key
+  const uint32_t* chunk_nkeys = nullptr;
+  const int32_t* key_field = nullptr;
+  const uint8_t* key_kind = nullptr;  // 0 raw (vid), 1 escaped (esc_rank)
+  const uint8_t* key_bits = nullptr;
+};
+
+void refine_sort(uint32_t n_items, const uint32_t* d_grp_init, uint32_t grp_max,
+                 const RefineKey& key, uint32_t* d_out_pos, cudaStream_t s,
+                 uint32_t* rounds_out = nullptr);
+
+// PHC (K9 phc_lcp): sum over entries i>=1 of hit(i) (objective.hpp:70-99).
+// Schedule on device: rows[i] (u64 or u32), field orders either full
+// (offsets == null, order i at fields[i*m]), CSR, or one order of m fields
+// shared by every entry (uniform_order).
+uint64_t phc_device(const Encoded& e, uint64_t n_entries, const uint64_t* rows64,
+                    const uint32_t* rows32, const uint64_t* order_offsets,
+                    const int32_t* fields, cudaStream_t s, uint64_t first_entry = 1,
+                    bool uniform_order = false);
+
+__global__ void k_invert(const uint32_t* pos, uint64_t n, uint32_t* perm);
+
+// Stats-ranked field order (ggr.hpp:59-84) — host IEEE double, no FMA.
+std::vector<int> hitcount_order(uint64_t total_rows, const std::vector<uint64_t>& card,
+                                const std::vector<double>& avg, int variant);
+std::vector<int> stats_order(uint64_t total_rows, const std::vector<uint64_t>& card,
+                             const std::vector<double>& avg);
+
+// Whole-table sort of all rows by escaped keys in one field order
+// (sort_rows_fixed_order, objective.hpp:154-171). d_perm[pos] = row.
+void sort_all_rows(const Encoded& e, const std::vector<int>& order, uint32_t* d_perm,
+                   cudaStream_t s);
+
+struct GgrOutput {
+  uint64_t phc = 0;
+  po_solve_stats stats{};
+};
+
+// GGR (ggr.hpp:144-394) on an encoded table. Writes the emitted schedule to
+// d_rows (u32, n) and d_orders (i32, n*m) on the device.
+void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups,
+                const po_ggr_config& cfg, uint32_t* d_rows, int32_t* d_orders, GgrOutput& out,
+                cudaStream_t s);
+
+}  // namespace po

@@ -1,0 +1,162 @@
+"""GPU parity: the CUDA path (libprefixopt_cuda.so through the C ABI) must be
+bit-exact with the reference — row permutation, per-row field orders, PHC and
+the three SolveStats counters — on the reference-generated golden vectors and,
+differentially, against the oracle restatement on seeded random tables."""
+import os
+import random
+
+import numpy as np
+import pytest
+
+import paper_2403_05821_b200 as po
+from golden_cases import check_result, load_cases, same_result
+from oracle.pyoracle import oracle
+from tables import (ALPHABETS, distinct_first_table, fd_covered_table, group_per_field_table,
+                    random_table, skewed_table)
+
+pytestmark = pytest.mark.gpu
+CASES = load_cases()
+TOKS = [po.char_tokenizer(), po.word_tokenizer()]
+SCS = [po.SegmentScoring.value_only, po.SegmentScoring.full_fragment]
+
+
+@pytest.mark.parametrize("case", CASES, ids=[c[0] for c in CASES])
+def test_ggr_matches_reference_golden(case):
+    name, t, fds, cfg, tok, sc, exp = case
+    check_result(po.ggr(t, fds, cfg, tok, sc), exp, name)
+
+
+def test_quickstart_known_answer():
+    case = next(c for c in CASES if c[0] == "movie_reviews_quickstart")
+    assert po.ggr(*case[1:6]).phc_score == 254072
+
+
+def test_structured_families_closed_form():
+    # test_solver_greedy.cpp:109-124
+    for n in (2, 4, 7, 10):
+        t = distinct_first_table(n, 3)
+        r = po.ggr(t, None, po.exact_config())
+        assert r.phc_score == 2 * (n - 1)
+        assert po.phc(r.schedule, t) == r.phc_score
+    for x in (2, 3):
+        assert po.ggr(group_per_field_table(x, 3), None, po.exact_config()).phc_score == 3 * (x - 1)
+
+
+def test_random_tables_vs_oracle():
+    rng = random.Random(1234)
+    P = oracle("port")
+    for trial in range(400):
+        alpha = ALPHABETS[rng.choice(list(ALPHABETS))]
+        t = random_table(rng, 12, 5, alpha, max_len=4, min_len=0, min_rows=0)
+        m = t.field_count()
+        fds = None
+        if m >= 2 and rng.random() < 0.35:
+            fds = [[f"f{i}" for i in rng.sample(range(m), rng.randint(2, m))]]
+        cfg = rng.choice([po.GgrConfig(), po.exact_config(), po.GgrConfig(1, 1, 0),
+                          po.GgrConfig(0, 0, 3), po.GgrConfig(2, 1, 1, True, po.StatsScoreVariant(rng.randint(0, 2)))])
+        tok, sc = rng.choice(TOKS), rng.choice(SCS)
+        a = po.ggr(t, fds, cfg, tok, sc)
+        b = P.ggr(t, fds, cfg, tok, sc)
+        assert same_result(a, b), (trial, t.row_count(), m, cfg, tok.name, sc, fds)
+
+
+def test_fd_covered_tables_vs_oracle():
+    rng = random.Random(53)
+    P = oracle("port")
+    for _ in range(60):
+        t = fd_covered_table(rng, 10, 4)
+        fds = [t.field_names]
+        assert same_result(po.ggr(t, fds, po.exact_config()), P.ggr(t, fds, po.exact_config()))
+
+
+@pytest.mark.parametrize("cfg", [po.GgrConfig(), po.exact_config(),
+                                 po.GgrConfig(hitcount_stop_threshold=50)])
+def test_skewed_medium_tables_vs_oracle(cfg):
+    rng = random.Random(99)
+    P = oracle("port")
+    for n in (300, 2000):
+        t = skewed_table(rng, n, [3, 40, 200, n], [6, 12, 20, 10])
+        for tok in TOKS:
+            a = po.ggr(t, [["col1", "col2"]], cfg, tok)
+            b = P.ggr(t, [["col1", "col2"]], cfg, tok)
+            assert same_result(a, b), (n, cfg, tok.name)
+
+
+def test_hash_collisions_are_resolved_on_bytes(monkeypatch):
+    # force 3-bit hashes: every column has colliding distinct values, so the
+    # dictionary must separate them by byte comparison
+    monkeypatch.setenv("PO_DEBUG_HASH_BITS", "3")
+    rng = random.Random(5)
+    P = oracle("port")
+    for trial in range(40):
+        t = random_table(rng, 30, 4, ALPHABETS["all"], max_len=5, min_len=0)
+        cfg = rng.choice([po.GgrConfig(), po.exact_config()])
+        assert same_result(po.ggr(t, None, cfg), P.ggr(t, None, cfg)), trial
+
+
+def test_phc_hit_random_schedules_vs_oracle():
+    rng = random.Random(42)
+    P = oracle("port")
+    for trial in range(200):
+        t = random_table(rng, 8, 4, ALPHABETS["esc"], max_len=3, min_len=0)
+        n, m = t.row_count(), t.field_count()
+        entries = [(r, rng.sample(range(m), rng.randint(0, m))) for r in rng.sample(range(n), n)]
+        s = po.RequestSchedule.from_entries(entries)
+        for tok in TOKS:
+            for sc in SCS:
+                assert po.phc(s, t, tok, sc) == P.phc(s, t, tok, sc)
+        if n:
+            r = rng.randrange(n)
+            prev = P.phc(po.RequestSchedule.from_entries(entries[max(r - 1, 0):r + 1]), t) if r else 0
+            assert po.hit(s, r, t) == prev
+
+
+def test_sort_rows_fixed_order_and_stats_vs_oracle():
+    rng = random.Random(3)
+    P = oracle("port")
+    for trial in range(150):
+        t = random_table(rng, 10, 4, ALPHABETS[rng.choice(list(ALPHABETS))], max_len=4, min_len=0)
+        m = t.field_count()
+        order = list(range(m))
+        rng.shuffle(order)
+        s = po.sort_rows_fixed_order(t, order)
+        assert s.row_ids.tolist() == P.sort_rows_fixed_order(t, order).tolist()
+        for tok in TOKS:
+            for sc in SCS:
+                st = po.compute_stats(t, tok, sc)
+                card, tot = P.compute_stats(t, tok, sc)
+                assert [f.cardinality for f in st.fields] == card.tolist()
+                n = t.row_count()
+                assert [f.avg_len for f in st.fields] == [float(x) / n for x in tot.tolist()]
+
+
+def test_error_behaviour():
+    t = po.Table(["A", "B"], [["1", "2"]])
+    with pytest.raises(po.SchemaError):
+        po.sort_rows_fixed_order(t, [0])
+    with pytest.raises(po.SchemaError):
+        po.sort_rows_fixed_order(t, [0, 0])
+    s = po.RequestSchedule.from_entries([(0, [0])])
+    with pytest.raises(po.DomainError):
+        po.hit(s, 1, t)
+    bad = po.RequestSchedule.from_entries([(0, [0]), (5, [0])])
+    with pytest.raises(IndexError):
+        po.phc(bad, t)
+    with pytest.raises(po.SchemaError):
+        po.ggr(t, [["A", "nope"]], po.GgrConfig())
+    # unknown FD names are ignored when use_fds is false (ggr.hpp:155)
+    po.ggr(t, [["A", "nope"]], po.GgrConfig(use_fds=False))
+
+
+def test_degenerate_tables():
+    assert po.ggr(po.Table(["a"], []), None).schedule.size() == 0
+    r = po.ggr(po.Table(["a", "b"], [["1", "2"]]), None)
+    assert r.phc_score == 0 and r.schedule.entries[0].field_order == [0, 1]
+    r = po.ggr(po.Table([], [[], [], []]), None)
+    assert r.schedule.row_ids.tolist() == [0, 1, 2]
+
+
+def test_launches_counted():
+    before = po._abi.cuda_lib().kernel_launch_count()
+    po.ggr(distinct_first_table(5, 3), None)
+    assert po._abi.cuda_lib().kernel_launch_count() > before

@@ -1,0 +1,62 @@
+"""CPU: pin the oracle restatement (oracle/ggr_oracle.cpp) against the
+reference — the committed reference-generated golden vectors always, and the
+reference library itself (oracle/_ref) when it is built in this container."""
+import random
+
+import pytest
+
+from golden_cases import check_result, load_cases, same_result
+from oracle.pyoracle import available, oracle
+from paper_2403_05821_b200 import GgrConfig, SegmentScoring, char_tokenizer, exact_config, word_tokenizer
+from tables import ALPHABETS, random_table
+
+CASES = load_cases()
+
+
+@pytest.mark.parametrize("case", CASES, ids=[c[0] for c in CASES])
+def test_oracle_matches_reference_golden(case):
+    name, t, fds, cfg, tok, sc, exp = case
+    check_result(oracle("port").ggr(t, fds, cfg, tok, sc), exp, name)
+
+
+def test_quickstart_known_answer():
+    # demos/quickstart.cpp on movie_reviews.csv, threshold 0: ggr PHC 254,072
+    case = next(c for c in CASES if c[0] == "movie_reviews_quickstart")
+    assert case[-1]["phc"] == 254072
+    assert oracle("port").ggr(*case[1:6]).phc_score == 254072
+
+
+@pytest.mark.skipif(not available("reference"), reason="oracle/_ref not built here")
+def test_oracle_matches_reference_random():
+    P, R = oracle("port"), oracle("reference")
+    rng = random.Random(7)
+    for trial in range(600):
+        alpha = ALPHABETS[rng.choice(list(ALPHABETS))]
+        t = random_table(rng, 10, 4, alpha, max_len=4, min_len=0)
+        m = t.field_count()
+        fds = None
+        if m >= 2 and rng.random() < 0.4:
+            fds = [[f"f{i}" for i in rng.sample(range(m), rng.randint(2, m))]]
+        cfg = rng.choice([GgrConfig(), exact_config(), GgrConfig(1, 1, 0), GgrConfig(0, 0, 3)])
+        tok = rng.choice([char_tokenizer(), word_tokenizer()])
+        sc = rng.choice([SegmentScoring.value_only, SegmentScoring.full_fragment])
+        assert same_result(P.ggr(t, fds, cfg, tok, sc), R.ggr(t, fds, cfg, tok, sc)), trial
+
+
+@pytest.mark.skipif(not available("reference"), reason="oracle/_ref not built here")
+def test_oracle_phc_sort_stats_match_reference():
+    P, R = oracle("port"), oracle("reference")
+    rng = random.Random(11)
+    for trial in range(200):
+        t = random_table(rng, 8, 4, ALPHABETS["esc"], max_len=3, min_len=0)
+        n, m = t.row_count(), t.field_count()
+        order = list(range(m))
+        rng.shuffle(order)
+        assert P.sort_rows_fixed_order(t, order).tolist() == R.sort_rows_fixed_order(t, order).tolist()
+        for tok in (char_tokenizer(), word_tokenizer()):
+            for sc in (SegmentScoring.value_only, SegmentScoring.full_fragment):
+                pc, pt = P.compute_stats(t, tok, sc)
+                rc, rt = R.compute_stats(t, tok, sc)
+                assert pc.tolist() == rc.tolist() and pt.tolist() == rt.tolist()
+                entries = [(r, rng.sample(range(m), rng.randint(0, m))) for r in rng.sample(range(n), n)]
+                assert P.phc(entries, t, tok, sc) == R.phc(entries, t, tok, sc)
