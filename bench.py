@@ -1,0 +1,353 @@
+#!/usr/bin/env python
+"""Benchmark: rows/s reordered + PHC-scored by prefixopt::ggr on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--impl ours|reference]
+
+A step is one full `ggr()` (GgrConfig defaults: dictionary encoding, greedy
+group recursion, leaf fallbacks, whole-table fallback competition and the
+PHC of the emitted schedule) over one synthetic table of BASELINE config C2
+(Amazon-products shape, 1M rows x 6 columns, ~0.75 GB of cell bytes; the
+configuration BASELINE.json's metric is quoted on). Inputs (0.75 GB) are
+larger than L2 (126 MB), so no explicit flush is needed between steps.
+
+  value   whole-job rows/s with the table resident in HBM (device buffers)
+  e2e     the same call through the C ABI with pinned HOST buffers: the
+          arena+offsets H2D copy and the schedule D2H copy are inside every
+          step
+Under torchrun (N>1) every rank runs an independent replica on its own copy
+of the table (row-sharded multi-GPU GGR is not built yet): scaling "weak",
+value = N * rows / max-over-ranks time.
+
+--impl reference times the reference C++ implementation (oracle/_ref, the
+unmodified prefixopt headers compiled from /root/reference; the CPU port in
+oracle/ when _ref is absent) on the host cores, one bounded row-prefix sample
+of the same table per step.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+import numpy as np  # noqa: E402
+
+METRIC = "rows/sec reordered+PHC-scored (1/2/4/8 B200) & HBM roofline %, vs CPU ref"
+UNIT = "rows/s"
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-i", str(self.gpu), "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                out, _ = self.proc.communicate()
+            self.lines = [l for l in out.splitlines() if l.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in getattr(self, "lines", []):
+            f = [x.strip() for x in l.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = max(mx, float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_reference_rows_per_s(table, fds, sample_rows: int, kind: str):
+    """Reference prefixopt::ggr on the first `sample_rows` rows; rows/s from the
+    reference's own SolveStats.wall_ms (excludes building its Table)."""
+    from oracle.pyoracle import available, oracle
+    from paper_2403_05821_b200 import GgrConfig, Table
+    if kind == "reference" and not available("reference"):
+        kind = "port"
+    m = table.field_count()
+    n = min(sample_rows, table.row_count())
+    offs = table.offsets[: n * m + 1].copy()
+    sub = Table.from_arena(table.field_names, table.arena[: int(offs[-1]) or 1], offs, n)
+    res = oracle(kind).ggr(sub, fds, GgrConfig())
+    secs = res.stats.wall_ms / 1e3
+    return n / secs, secs, kind, n, res
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    from paper_2403_05821_b200 import gen
+    cfg_id = args.config
+    sample = args.ref_rows
+    table = gen.generate(cfg_id, n_rows=sample)
+    fds = gen.fds(cfg_id)
+    for _ in range(args.warmup):
+        cpu_reference_rows_per_s(table, fds, sample, "reference")
+    rates, secs_total, kind = [], 0.0, "reference"
+    for _ in range(args.steps):
+        r, secs, kind, n, _res = cpu_reference_rows_per_s(table, fds, sample, "reference")
+        rates.append(r)
+        secs_total += secs
+    value = args.steps * sample / secs_total
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * secs_total / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+        "config": {"workload": gen.CONFIGS[cfg_id].name, "rows_per_step": sample,
+                   "sample": f"first {sample} rows of {gen.CONFIGS[cfg_id].name}",
+                   "parallelism": "single-thread CPU (the reference has no threads)"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": kind,
+                         "sample": f"first {sample} rows of {gen.CONFIGS[cfg_id].name}, "
+                                   "GgrConfig defaults, wall time from SolveStats.wall_ms"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args):
+    import torch
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2403_05821_b200 as po
+    from paper_2403_05821_b200 import gen
+    from paper_2403_05821_b200._abi import PO_LOC_DEVICE, PO_LOC_HOST, cuda_lib
+
+    lib = cuda_lib()
+    cfg_id = args.config
+    t0 = time.time()
+    table = gen.generate(cfg_id, n_rows=args.rows)
+    n, m = table.row_count(), table.field_count()
+    cell_bytes = table.cell_bytes
+    log(f"[rank {rank}] generated {gen.CONFIGS[cfg_id].name}: {n} rows, {cell_bytes/1e9:.3f} GB "
+        f"in {time.time()-t0:.1f}s")
+    fds = gen.fds(cfg_id)
+    fd_idx = [[table.require_field(x) for x in g] for g in fds]
+    cfg = po.GgrConfig()
+    stream = torch.cuda.current_stream()
+    sp = stream.cuda_stream
+
+    d_arena = torch.from_numpy(table.arena).to("cuda")
+    d_offs = torch.from_numpy(table.offsets.view(np.int64)).to("cuda")
+    dview = table.view(PO_LOC_DEVICE, arena=d_arena, offsets=d_offs)
+    d_rows = torch.empty(n, dtype=torch.int64, device="cuda")
+    d_orders = torch.empty(n * m, dtype=torch.int32, device="cuda")
+
+    def step_device():
+        return po.ggr_into(dview, fd_idx, cfg, 0, 0, PO_LOC_DEVICE, d_rows, d_orders, sp)
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        import torch.distributed as dist
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(max(args.warmup, 0)):
+        phc, st = step_device()
+    barrier()
+    l0 = lib.kernel_launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            phc, st = step_device()
+        ev1.record(stream)
+        barrier()
+    launches = (lib.kernel_launch_count() - l0) // max(args.steps, 1)
+    ms = ev0.elapsed_time(ev1) / args.steps
+    ms = max_over_ranks(ms)
+    value = world * n / (ms / 1e3)
+    log(f"[rank {rank}] device-resident: {ms:.3f} ms/step, phc={phc}, stats={st}")
+
+    # per-kernel CUDA-event profile of the same step (separate pass)
+    lib.profile_enable(1)
+    lib.profile_report()
+    for _ in range(args.prof_steps):
+        step_device()
+    torch.cuda.synchronize()
+    prof = lib.profile_report()
+    lib.profile_enable(0)
+    prof_steps = max(args.prof_steps, 1)
+    kern = sorted(((v[1] / prof_steps, k, v[0] / prof_steps) for k, v in prof.items()),
+                  reverse=True)
+    total_kernel_ms = sum(x[0] for x in kern)
+    for ms_k, k, cnt in kern[:12]:
+        log(f"   {k:28s} {ms_k:8.3f} ms/step  {cnt:6.1f} launches  "
+            f"({100*ms_k/max(total_kernel_ms,1e-9):5.1f}% of kernel time)")
+
+    # roofline of the dominant byte-streaming kernel: k_dict_insert reads every
+    # cell byte + its offset pair once: algorithmic bytes = S + 8*(n*m+1) + 4*n*m
+    peak, peak_kind = peaks()
+    dom = "k_dict_insert"
+    dom_ms = prof.get(dom, (1, 0.0))[1] / max(prof.get(dom, (1, 0.0))[0], 1)
+    dom_bytes = cell_bytes + 8 * (n * m + 1) + 4 * n * m
+    achieved = dom_bytes / (dom_ms / 1e3) / 1e9 if dom_ms > 0 else 0.0
+    # whole-pipeline figure on SURVEY.md §8d's B_alg = S_row + 8m + 4 + m per row
+    b_alg = cell_bytes + n * (8 * m + 4 + m)
+
+    # e2e: pinned host inputs and outputs through the C ABI every step
+    h_arena = torch.from_numpy(table.arena).pin_memory()
+    h_offs = torch.from_numpy(table.offsets.view(np.int64)).pin_memory()
+    hview = table.view(PO_LOC_HOST, arena=h_arena, offsets=h_offs)
+    h_rows = torch.empty(n, dtype=torch.int64).pin_memory()
+    h_orders = torch.empty(n * m, dtype=torch.int32).pin_memory()
+
+    def step_e2e():
+        return po.ggr_into(hview, fd_idx, cfg, 0, 0, PO_LOC_HOST, h_rows, h_orders, sp)
+
+    for _ in range(max(1, args.warmup // 2)):
+        step_e2e()
+    barrier()
+    t_e = time.perf_counter()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        phc_e2e, _st = step_e2e()
+    e1.record(stream)
+    barrier()
+    ms_e2e = max_over_ranks(e0.elapsed_time(e1) / args.steps)
+    wall_e2e = (time.perf_counter() - t_e) * 1e3 / args.steps
+    h2d = int(table.arena.nbytes + table.offsets.nbytes)
+    d2h = int(n * 8 + n * m * 4 + 8)
+    if phc_e2e != phc:
+        raise RuntimeError(f"e2e PHC {phc_e2e} != device-resident PHC {phc}")
+
+    cpu = None
+    if rank == 0 and not args.no_cpu:
+        try:
+            rate, secs, kind, ns, res = cpu_reference_rows_per_s(table, fds, args.cpu_rows,
+                                                                 "reference")
+            cpu = {"value": rate, "unit": UNIT, "cores": 1, "kind": kind,
+                   "sample": f"first {ns} rows of {gen.CONFIGS[cfg_id].name}, GgrConfig "
+                             f"defaults, {secs:.1f} s single-threaded (SolveStats.wall_ms)"}
+            log(f"[rank 0] CPU reference ({kind}) on {ns} rows: {secs:.2f}s -> {rate:.0f} rows/s")
+        except Exception as ex:  # pragma: no cover
+            log(f"[rank 0] CPU baseline failed: {ex}")
+
+    clocks = clk.summary()
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+            "data": "synthetic",
+            "config": {"workload": gen.CONFIGS[cfg_id].name, "rows": n, "fields": m,
+                       "cell_bytes": cell_bytes, "ggr_config": "defaults (4/2/100000, fds on)",
+                       "tokenizer": "char", "scoring": "value_only",
+                       "l2": "inputs (arena+offsets) larger than the 126 MB L2; no flush",
+                       "parallelism": "single GPU" if world == 1 else f"{world} independent replicas"},
+            "phc": int(phc),
+            "solve_stats": {"recursive_calls": st.recursive_calls,
+                            "candidates_examined": st.candidates_examined,
+                            "max_depth": st.max_depth},
+            "e2e": {"value": world * n / (ms_e2e / 1e3), "unit": UNIT,
+                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "ms_per_step": ms_e2e, "host_wall_ms_per_step": wall_e2e},
+            "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
+                         "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+                         "algorithmic_bytes_per_launch": dom_bytes,
+                         "kernel_ms": dom_ms, "peak_source": peak_kind,
+                         "pipeline_b_alg_frac": (b_alg / (ms / 1e3) / 1e9) / peak},
+            "kernels_ms_per_step": {k: round(v, 4) for v, k, _ in kern[:16]},
+            "cpu_baseline": cpu,
+            "gpu_launches": int(launches),
+            "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--rows", type=int, default=None)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--cpu-rows", type=int, default=300_000)
+    ap.add_argument("--ref-rows", type=int, default=50_000)
+    ap.add_argument("--prof-steps", type=int, default=3)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        log("warning: --warmup < 3 violates the timing rules")
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

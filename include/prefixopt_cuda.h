@@ -154,6 +154,12 @@ const char* po_build_info(void);
  * incremented at each launch site; used by bench.py's gpu_launches). */
 uint64_t po_kernel_launch_count(void);
 
+/* Per-kernel CUDA-event timing on the launching stream. po_profile_report
+ * drains the recorded launches and writes "name count total_ms" lines into
+ * buf (NUL-terminated, truncated to cap); returns the full length + 1. */
+void po_profile_enable(int enable);
+uint64_t po_profile_report(char* buf, uint64_t cap);
+
 #ifdef __cplusplus
 }
 #endif

@@ -164,6 +164,18 @@ class CudaLib:
         self.last_error = _bind(L, "po_last_error", C.c_char_p, [])
         self.build_info = _bind(L, "po_build_info", C.c_char_p, [])
         self.kernel_launch_count = _bind(L, "po_kernel_launch_count", C.c_uint64, [])
+        self.profile_enable = _bind(L, "po_profile_enable", None, [C.c_int])
+        self._profile_report = _bind(L, "po_profile_report", C.c_uint64, [C.c_char_p, C.c_uint64])
+
+    def profile_report(self) -> dict:
+        """{kernel name: (launches, total ms)} since the last report."""
+        buf = C.create_string_buffer(1 << 16)
+        self._profile_report(buf, len(buf))
+        out = {}
+        for line in buf.value.decode().splitlines():
+            name, cnt, ms = line.rsplit(" ", 2)
+            out[name] = (int(cnt), float(ms))
+        return out
 
     def check(self, code: int) -> None:
         if code:

@@ -18,6 +18,8 @@ REPO = PKG.parent
 CSRC = PKG / "csrc"
 BUILD = REPO / "build" / "cuda"
 OUT = PKG / "libprefixopt_cuda.so"
+GEN_OUT = PKG / "libpogen.so"
+CXX = os.environ.get("CXX", shutil.which("g++") or "g++")
 SOURCES = ["abi.cu", "encode.cu", "refine.cu", "phc.cu", "ggr.cu"]
 
 NVCC = os.environ.get("NVCC", shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc")
@@ -57,6 +59,10 @@ def build(verbose: bool = False, force: bool = False) -> Path:
         list(ex.map(run, jobs))
     if force or jobs or _stale(OUT, objs):
         run([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", str(OUT), *map(str, objs)])
+    gen_src = CSRC / "gen.cpp"
+    if force or _stale(GEN_OUT, [gen_src]):
+        run([CXX, "-std=c++17", "-O3", "-fPIC", "-shared", "-pthread", "-o", str(GEN_OUT),
+             str(gen_src)])
     return OUT
 
 

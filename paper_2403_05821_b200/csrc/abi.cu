@@ -5,6 +5,8 @@
 #include <chrono>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <numeric>
 
 #include "internal.cuh"
@@ -12,8 +14,76 @@
 namespace po {
 
 std::atomic<uint64_t> g_launches{0};
+std::atomic<int> g_profile{0};
 
 namespace {
+
+struct ProfRec {
+  const char* name;
+  cudaEvent_t a, b;
+};
+std::mutex g_prof_mu;
+std::vector<ProfRec> g_prof_pending;
+std::vector<cudaEvent_t> g_prof_free;
+std::map<std::string, std::pair<uint64_t, double>> g_prof_acc;  // name -> (count, ms)
+
+cudaEvent_t prof_event() {
+  if (!g_prof_free.empty()) {
+    cudaEvent_t e = g_prof_free.back();
+    g_prof_free.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  PO_CUDA(cudaEventCreate(&e));
+  return e;
+}
+
+void prof_drain() {  // caller holds g_prof_mu
+  for (auto& r : g_prof_pending) {
+    float ms = 0;
+    PO_CUDA(cudaEventSynchronize(r.b));
+    PO_CUDA(cudaEventElapsedTime(&ms, r.a, r.b));
+    auto& acc = g_prof_acc[r.name];
+    acc.first += 1;
+    acc.second += ms;
+    g_prof_free.push_back(r.a);
+    g_prof_free.push_back(r.b);
+  }
+  g_prof_pending.clear();
+}
+
+}  // namespace
+
+void profile_begin(const char* name, cudaStream_t s, void** token) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  if (g_prof_pending.size() > 4096) prof_drain();
+  ProfRec r{name, prof_event(), prof_event()};
+  PO_CUDA(cudaEventRecord(r.a, s));
+  g_prof_pending.push_back(r);
+  *token = reinterpret_cast<void*>(g_prof_pending.size());
+}
+
+void profile_end(void* token, cudaStream_t s) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  size_t i = reinterpret_cast<size_t>(token) - 1;
+  if (i < g_prof_pending.size()) PO_CUDA(cudaEventRecord(g_prof_pending[i].b, s));
+}
+
+namespace {
+
+// Keep freed stream-ordered allocations cached in the device pool between
+// calls instead of returning them to the driver at every synchronisation.
+void init_pool_once() {
+  static thread_local int done_dev = -1;
+  int dev = 0;
+  PO_CUDA(cudaGetDevice(&dev));
+  if (done_dev == dev) return;
+  cudaMemPool_t pool;
+  PO_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+  uint64_t thr = ~uint64_t(0);
+  PO_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+  done_dev = dev;
+}
 
 thread_local std::string g_err;
 
@@ -54,6 +124,7 @@ struct Prepared {
 
 void prepare(const po_table* tv, int tok, int scoring, cudaStream_t s, Prepared& p) {
   check_modes(tok, scoring);
+  init_pool_once();
   make_device_table(tv, tok, s, p.t);
   encode(p.t, tok, scoring, s, p.e, debug_hash_bits());
 }
@@ -253,5 +324,36 @@ const char* po_last_error(void) { return g_err.c_str(); }
 const char* po_build_info(void) { return "prefixopt-b200 sm_100a"; }
 
 uint64_t po_kernel_launch_count(void) { return g_launches.load(); }
+
+void po_profile_enable(int enable) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  if (!enable) {
+    try {
+      prof_drain();
+    } catch (...) {
+    }
+  }
+  g_profile.store(enable ? 1 : 0);
+}
+
+uint64_t po_profile_report(char* buf, uint64_t cap) {
+  std::string out;
+  {
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    try {
+      prof_drain();
+    } catch (...) {
+    }
+    for (auto& [name, v] : g_prof_acc)
+      out += name + " " + std::to_string(v.first) + " " + std::to_string(v.second) + "\n";
+    g_prof_acc.clear();
+  }
+  if (buf && cap) {
+    size_t k = std::min<size_t>(cap - 1, out.size());
+    std::memcpy(buf, out.data(), k);
+    buf[k] = 0;
+  }
+  return out.size() + 1;
+}
 
 }  // extern "C"

@@ -33,15 +33,25 @@ inline void cuda_check(cudaError_t e, const char* what, const char* file, int li
 #define PO_CUDA(x) ::po::cuda_check((x), #x, __FILE__, __LINE__)
 
 extern std::atomic<uint64_t> g_launches;
+extern std::atomic<int> g_profile;
+
+// Per-kernel CUDA-event timing (po_profile_enable / po_profile_report):
+// events recorded on the launching stream around each launch.
+void profile_begin(const char* name, cudaStream_t s, void** token);
+void profile_end(void* token, cudaStream_t s);
 
 // Every kernel of this library is launched through PO_LAUNCH so bench.py can
-// report how many of OUR kernels ran (po_kernel_launch_count).
+// report how many of OUR kernels ran (po_kernel_launch_count) and time them.
 #define PO_LAUNCH(kernel, grid, block, smem, stream, ...)                    \
   do {                                                                       \
     if ((grid) > 0) {                                                        \
+      void* po_tok_ = nullptr;                                               \
+      if (::po::g_profile.load(std::memory_order_relaxed))                   \
+        ::po::profile_begin(#kernel, (stream), &po_tok_);                    \
       kernel<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__);            \
       ::po::g_launches.fetch_add(1, std::memory_order_relaxed);              \
       PO_CUDA(cudaGetLastError());                                           \
+      if (po_tok_) ::po::profile_end(po_tok_, (stream));                     \
     }                                                                        \
   } while (0)
 

@@ -1,0 +1,23 @@
+"""The reference's own C++ tests (proj/tests/*.cpp in /root/reference),
+compiled against the drop-in headers in proj/include and linked with
+libprefixopt_cuda.so (proj/tests/Makefile), must pass on the GPU."""
+import subprocess
+from pathlib import Path
+
+import pytest
+
+BIN = Path(__file__).resolve().parent.parent / "proj" / "tests" / "bin"
+TESTS = ["test_objective", "test_solver_greedy", "test_solver_exact", "acceptance"]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", TESTS)
+def test_reference_cpp_suite_against_dropin(name):
+    exe = BIN / name
+    if not exe.exists():
+        pytest.skip(f"{exe} not built (make -C proj/tests needs /root/reference at build time)")
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=900)
+    print(r.stdout[-4000:], r.stderr[-4000:])
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    if name == "acceptance":
+        assert "[FAIL]" not in r.stdout
