@@ -185,22 +185,74 @@ __device__ __forceinline__ uint64_t mask_low_bytes(uint64_t w, uint32_t nbytes) 
 
 // 64-bit hash of a cell's bytes (value identity for the dictionary; exact
 // equality is always verified on the bytes, so quality only affects speed).
+// h = fmix64(len*C + sum_k term(word_k, k)) over the cell's 8-byte words
+// (little-endian, zero-padded), so a warp can hash a long cell cooperatively
+// (lane l takes words l, l+32, ...) and get the same value as one lane.
+__device__ __forceinline__ uint64_t word_term(uint64_t w, uint64_t k) {
+  return fmix64(w ^ (k * 0x9E3779B97F4A7C15ULL) ^ 0x5bd1e9955bd1e995ULL);
+}
+
+__device__ __forceinline__ uint64_t hash_finish(uint64_t sum, uint64_t len) {
+  uint64_t h = fmix64(sum + len * 0xC2B2AE3D27D4EB4FULL);
+  return h ? h : 1;  // 0 marks an empty slot
+}
+
 __device__ __forceinline__ uint64_t hash_bytes(const uint8_t* a, uint64_t len, const uint8_t* limit) {
-  uint64_t h = 0x9E3779B97F4A7C15ULL ^ (len * 0xC2B2AE3D27D4EB4FULL);
+  uint64_t sum = 0;
   if (len) {
     WordReader rd(a, limit);
     uint64_t left = len;
-    while (left) {
-      uint64_t w = rd.next();
+    for (uint64_t k = 0; left; ++k) {
       uint32_t take = left >= 8 ? 8u : uint32_t(left);
-      w = mask_low_bytes(w, take);
-      h ^= w * 0xbf58476d1ce4e5b9ULL;
-      h = rotl64(h, 27) * 0x94d049bb133111ebULL + 0x52dce729ULL;
+      sum += word_term(mask_low_bytes(rd.next(), take), k);
       left -= take;
     }
   }
-  h = fmix64(h);
-  return h ? h : 1;  // 0 marks an empty slot
+  return hash_finish(sum, len);
+}
+
+// 8 bytes at an arbitrary address (two aligned loads, none past `limit`).
+__device__ __forceinline__ uint64_t load8_unaligned(const uint8_t* a, const uint8_t* limit) {
+  const uintptr_t ad = reinterpret_cast<uintptr_t>(a);
+  const uint64_t* p = reinterpret_cast<const uint64_t*>(ad & ~uintptr_t(7));
+  const uint64_t* lim =
+      reinterpret_cast<const uint64_t*>((reinterpret_cast<uintptr_t>(limit) + 7) & ~uintptr_t(7));
+  const uint32_t sh = uint32_t(ad & 7) * 8;
+  const uint64_t w0 = p < lim ? __ldg(p) : 0;
+  if (!sh) return w0;
+  const uint64_t w1 = (p + 1) < lim ? __ldg(p + 1) : 0;
+  return (w0 >> sh) | (w1 << (64 - sh));
+}
+
+__device__ __forceinline__ uint64_t warp_sum_u64(uint64_t v) {
+  for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
+  return v;
+}
+
+// Whole-warp hash of one cell (same value as hash_bytes). All lanes call it
+// with the same (a, len) and all receive the hash.
+__device__ __forceinline__ uint64_t warp_hash_bytes(const uint8_t* a, uint64_t len,
+                                                    const uint8_t* limit, uint32_t lane) {
+  const uint64_t words = (len + 7) / 8;
+  uint64_t sum = 0;
+  for (uint64_t k = lane; k < words; k += 32) {
+    const uint64_t rem = len - 8 * k;
+    sum += word_term(mask_low_bytes(load8_unaligned(a + 8 * k, limit), rem >= 8 ? 8u : uint32_t(rem)), k);
+  }
+  return hash_finish(warp_sum_u64(sum), len);
+}
+
+__device__ __forceinline__ bool warp_bytes_equal(const uint8_t* a, const uint8_t* b, uint64_t len,
+                                                 const uint8_t* limit, uint32_t lane) {
+  bool ok = true;
+  const uint64_t words = (len + 7) / 8;
+  for (uint64_t k = lane; k < words && ok; k += 32) {
+    const uint64_t rem = len - 8 * k;
+    const uint32_t take = rem >= 8 ? 8u : uint32_t(rem);
+    ok = mask_low_bytes(load8_unaligned(a + 8 * k, limit), take) ==
+         mask_low_bytes(load8_unaligned(b + 8 * k, limit), take);
+  }
+  return __all_sync(0xffffffffu, ok);
 }
 
 __device__ __forceinline__ bool bytes_equal(const uint8_t* a, const uint8_t* b, uint64_t len,

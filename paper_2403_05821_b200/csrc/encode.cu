@@ -31,44 +31,100 @@ namespace {
 
 constexpr uint32_t kEmptyRep = 0xFFFFFFFFu;
 
-__global__ void k_dict_insert(const uint8_t* __restrict__ arena, const uint8_t* arena_end,
-                              const uint64_t* __restrict__ offsets, uint64_t n, uint32_t m,
-                              uint64_t cap, unsigned long long* keys, uint32_t* reps,
-                              uint32_t* slot_of_cell, uint64_t hash_mask) {
+constexpr uint64_t kShortCell = 32;  // longer cells are hashed/compared by the whole warp
+
+// K1+K2 fused. A warp takes 32 consecutive cells (contiguous in the row-major
+// arena). Short cells are hashed by their own lane; long cells one at a time
+// by the whole warp with coalesced 8-byte word loads. Each lane then probes
+// its column's table; a slot owned by another cell with the same hash is
+// verified on the bytes (cooperatively for long cells) and probing continues
+// on a mismatch, so value identity is exact.
+__global__ void __launch_bounds__(256) k_dict_insert(
+    const uint8_t* __restrict__ arena, const uint8_t* arena_end,
+    const uint64_t* __restrict__ offsets, uint64_t n, uint32_t m, uint64_t cap,
+    unsigned long long* keys, uint32_t* reps, uint32_t* slot_of_cell, uint64_t hash_mask) {
+  const uint32_t lane = threadIdx.x & 31;
   const uint64_t total = n * m;
-  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < total;
-       i += uint64_t(gridDim.x) * blockDim.x) {
-    const uint64_t r = i / m;
-    const uint32_t c = uint32_t(i - r * m);
-    const uint64_t o0 = offsets[i], o1 = offsets[i + 1];
-    const uint64_t len = o1 - o0;
-    const uint8_t* p = arena + o0;
-    uint64_t h = hash_bytes(p, len, arena_end) & hash_mask;
+  const uint64_t warp0 = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
+  const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  for (uint64_t base = warp0 * 32; base < total; base += nwarps * 32) {
+    const uint64_t i = base + lane;
+    const bool valid = i < total;
+    uint64_t o0 = 0, len = 0, r = 0;
+    uint32_t c = 0;
+    if (valid) {
+      o0 = offsets[i];
+      len = offsets[i + 1] - o0;
+      r = i / m;
+      c = uint32_t(i - r * m);
+    }
+    const bool is_long = valid && len > kShortCell;
+    uint64_t h = 0;
+    if (valid && !is_long) h = hash_bytes(arena + o0, len, arena_end);
+    for (unsigned lm = __ballot_sync(0xffffffffu, is_long); lm; lm &= lm - 1) {
+      const int src = __ffs(lm) - 1;
+      const uint64_t so = __shfl_sync(0xffffffffu, o0, src);
+      const uint64_t sl = __shfl_sync(0xffffffffu, len, src);
+      const uint64_t hh = warp_hash_bytes(arena + so, sl, arena_end, lane);
+      if (int(lane) == src) h = hh;
+    }
+    h &= hash_mask;
     if (h == 0) h = 1;
     unsigned long long* K = keys + uint64_t(c) * cap;
     uint32_t* R = reps + uint64_t(c) * cap;
     uint64_t slot = h & (cap - 1);
+    bool done = !valid;
     for (;;) {
-      unsigned long long k = K[slot];
-      if (k == 0) {
-        unsigned long long prev = atomicCAS(&K[slot], 0ull, (unsigned long long)h);
-        if (prev == 0) {
-          atomicExch(&R[slot], uint32_t(r));
-          break;
+      // per-lane probing until inserted, matched (short) or a long match awaits verification
+      bool verify = false;
+      uint64_t rep_off = 0;
+      while (!done && !verify) {
+        unsigned long long k = K[slot];
+        if (k == 0) {
+          const unsigned long long prev = atomicCAS(&K[slot], 0ull, (unsigned long long)h);
+          if (prev == 0) {
+            atomicExch(&R[slot], uint32_t(r));
+            done = true;
+            break;
+          }
+          k = prev;
         }
-        k = prev;
-      }
-      if (k == h) {
-        uint32_t rep;
-        while ((rep = ld_relaxed_u32(&R[slot])) == kEmptyRep) {
+        if (k == h) {
+          uint32_t rep;
+          while ((rep = ld_relaxed_u32(&R[slot])) == kEmptyRep) {
+          }
+          const uint64_t j = uint64_t(rep) * m + c;
+          const uint64_t q0 = offsets[j];
+          if (offsets[j + 1] - q0 == len) {
+            if (!is_long) {
+              if (bytes_equal(arena + o0, arena + q0, len, arena_end)) {
+                done = true;
+                break;
+              }
+            } else {
+              verify = true;
+              rep_off = q0;
+              break;
+            }
+          }
         }
-        const uint64_t j = uint64_t(rep) * m + c;
-        const uint64_t q0 = offsets[j], q1 = offsets[j + 1];
-        if (q1 - q0 == len && bytes_equal(p, arena + q0, len, arena_end)) break;
+        slot = (slot + 1) & (cap - 1);
       }
-      slot = (slot + 1) & (cap - 1);
+      // cooperative verification of long matches
+      for (unsigned vm = __ballot_sync(0xffffffffu, verify); vm; vm &= vm - 1) {
+        const int src = __ffs(vm) - 1;
+        const uint64_t a = __shfl_sync(0xffffffffu, o0, src);
+        const uint64_t b = __shfl_sync(0xffffffffu, rep_off, src);
+        const uint64_t sl = __shfl_sync(0xffffffffu, len, src);
+        const bool eq = warp_bytes_equal(arena + a, arena + b, sl, arena_end, lane);
+        if (int(lane) == src) {
+          if (eq) done = true;
+          else slot = (slot + 1) & (cap - 1);  // same hash, different bytes: keep probing
+        }
+      }
+      if (__all_sync(0xffffffffu, done)) break;
     }
-    slot_of_cell[i] = uint32_t(slot);
+    if (valid) slot_of_cell[i] = uint32_t(slot);
   }
 }
 
@@ -177,6 +233,10 @@ __global__ void k_vlen(const uint8_t* arena, const uint64_t* offsets, const uint
       continue;
     }
     uint64_t o0 = offsets[i], len = offsets[i + 1] - o0;
+    if (tok == PO_TOK_CHAR && scoring == PO_SCORE_VALUE) {
+      vlen[p] = len;  // CharTokenizer::count == byte length (tokenizer.hpp:44)
+      continue;
+    }
     TextLen t = text_len(arena + o0, len);
     uint64_t L;
     if (scoring == PO_SCORE_VALUE)
@@ -221,11 +281,26 @@ __global__ void k_count(const uint32_t* vid, uint64_t n, uint32_t m, uint32_t c,
   }
 }
 
+// Per-column sum of count*vlen (stats.hpp:38), privatised per block in
+// shared memory (m accumulators) so the global atomics are m per block.
 __global__ void k_total_len(const uint32_t* count, const uint64_t* vlen, const uint32_t* col_by_pos,
-                            uint64_t D, unsigned long long* total) {
+                            uint64_t D, uint32_t m, unsigned long long* total) {
+  extern __shared__ unsigned long long acc[];
+  const bool priv = m <= 4096;
+  if (priv)
+    for (uint32_t c = threadIdx.x; c < m; c += blockDim.x) acc[c] = 0;
+  __syncthreads();
   for (uint64_t p = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; p < D;
-       p += uint64_t(gridDim.x) * blockDim.x)
-    atomicAdd(&total[col_by_pos[p]], (unsigned long long)(uint64_t(count[p]) * vlen[p]));
+       p += uint64_t(gridDim.x) * blockDim.x) {
+    const unsigned long long v = uint64_t(count[p]) * vlen[p];
+    if (priv) atomicAdd(&acc[col_by_pos[p]], v);
+    else atomicAdd(&total[col_by_pos[p]], v);
+  }
+  if (priv) {
+    __syncthreads();
+    for (uint32_t c = threadIdx.x; c < m; c += blockDim.x)
+      if (acc[c]) atomicAdd(&total[c], acc[c]);
+  }
 }
 
 uint64_t word_count_host(const std::string& s) {
@@ -435,8 +510,8 @@ void encode(const DeviceTable& t, int tok, int scoring, cudaStream_t s, Encoded&
   }
   DevBuf<unsigned long long> tot(m, s);
   tot.zero();
-  PO_LAUNCH(k_total_len, grid_for(D, 256), 256, 0, s, e.count.get(), e.vlen.get(),
-            col_by_pos.get(), D, tot.get());
+  PO_LAUNCH(k_total_len, grid_for(D, 256, 2), 256, m <= 4096 ? m * 8 : 0, s, e.count.get(),
+            e.vlen.get(), col_by_pos.get(), D, uint32_t(m), tot.get());
   std::vector<unsigned long long> htot(m);
   tot.download(htot.data(), m);
   sync(s);

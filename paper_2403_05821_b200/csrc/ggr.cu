@@ -22,9 +22,12 @@
 
 #include <cub/cub.cuh>
 #include <cooperative_groups.h>
+#include <cooperative_groups/reduce.h>
 
 #include <algorithm>
 #include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <memory>
 #include <numeric>
 
@@ -220,22 +223,41 @@ __global__ void __launch_bounds__(kArgBlock) k_argmax(
   }
 }
 
-__global__ void k_argmax_final(const Cand* partial, const unsigned long long* partial_cands,
-                               const uint32_t* slot_work_off, uint32_t nslots, Cand* out,
-                               unsigned long long* out_cands) {
-  for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < nslots; s += gridDim.x * blockDim.x) {
-    Cand b;
-    b.numer = 0;
-    b.count = 0;
-    b.col = 0;
-    b.vid = 0;
-    unsigned long long n = 0;
-    for (uint32_t i = slot_work_off[s]; i < slot_work_off[s + 1]; ++i) {
-      if (beats(partial[i], b)) b = partial[i];
-      n += partial_cands[i];
+// One block per scanning node: reduce its per-chunk partials.
+__global__ void __launch_bounds__(kArgBlock) k_argmax_final(
+    const Cand* partial, const unsigned long long* partial_cands, const uint32_t* slot_work_off,
+    Cand* out, unsigned long long* out_cands) {
+  const uint32_t s = blockIdx.x;
+  Cand b;
+  b.numer = 0;
+  b.count = 0;
+  b.col = 0;
+  b.vid = 0;
+  unsigned long long n = 0;
+  for (uint32_t i = slot_work_off[s] + threadIdx.x; i < slot_work_off[s + 1]; i += blockDim.x) {
+    if (beats(partial[i], b)) b = partial[i];
+    n += partial_cands[i];
+  }
+  for (int d = 16; d > 0; d >>= 1) {
+    Cand o = shfl_cand(b, d);
+    if (beats(o, b)) b = o;
+    n += __shfl_down_sync(0xffffffffu, n, d);
+  }
+  __shared__ Cand sb[kArgBlock / 32];
+  __shared__ unsigned long long sc[kArgBlock / 32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) {
+    sb[wid] = b;
+    sc[wid] = n;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int i = 1; i < kArgBlock / 32; ++i) {
+      if (beats(sb[i], sb[0])) sb[0] = sb[i];
+      sc[0] += sc[i];
     }
-    out[s] = b;
-    out_cands[s] = n;
+    out[s] = sb[0];
+    out_cands[s] = sc[0];
   }
 }
 
@@ -287,46 +309,90 @@ __global__ void k_relabel(uint32_t* node_of_row, uint64_t n, const int32_t* spli
 // K4 group_hist: block-row aggregation into the block child's table and
 // decrement of the parent's table (inherited by the rest child)
 // ---------------------------------------------------------------------------
-__global__ void k_aggregate(const uint32_t* blockrows, uint64_t total_rows, const uint64_t* seg_off,
-                            uint32_t nsplit, const SplitD* sp, const uint32_t* masks,
-                            const uint32_t* vid, const uint64_t* vlen, const uint64_t* colbase,
-                            uint32_t m, uint32_t K, const int32_t* dpart, const uint32_t* npart) {
-  const uint64_t total = total_rows * m;
-  for (uint64_t t = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; t < total;
-       t += uint64_t(gridDim.x) * blockDim.x) {
-    const uint64_t q = t / m;
-    const uint32_t c = uint32_t(t - q * m);
-    // split owning block row q
-    uint32_t lo = 0, hi = nsplit;
-    while (hi - lo > 1) {
-      uint32_t mid = (lo + hi) >> 1;
-      if (seg_off[mid] <= q) lo = mid;
-      else hi = mid;
+struct AggTask {
+  uint32_t split;  // index into this level's SplitD array
+  uint32_t col;
+  uint32_t to_b;   // add into the block child's table (col is one of its columns)
+  uint32_t to_p;   // subtract from the parent's table (kept by the rest child)
+  uint64_t lo, hi; // block-row range [lo, hi) of the split's segment
+};
+
+constexpr int kAggBlock = 256;
+
+// One block per (split, column, row range). Lanes of a warp hold consecutive
+// block rows of ONE column, so equal values inside a warp are merged with
+// __match_any_sync / a labeled-partition reduction before the table atomics
+// (low-cardinality columns and the split column itself collapse to one
+// atomic per warp).
+__global__ void __launch_bounds__(kAggBlock) k_aggregate(
+    const AggTask* __restrict__ tasks, const uint32_t* __restrict__ blockrows,
+    const SplitD* __restrict__ sp, const uint32_t* __restrict__ vid,
+    const uint64_t* __restrict__ vlen, const uint64_t* __restrict__ colbase, uint32_t m,
+    uint32_t K, const int32_t* __restrict__ dpart, const uint32_t* __restrict__ npart) {
+  const AggTask tk = tasks[blockIdx.x];
+  const SplitD& d = sp[tk.split];
+  const uint32_t c = tk.col;
+  const uint32_t np = npart[c];
+  const uint32_t lane = threadIdx.x & 31;
+  for (uint64_t base = tk.lo; base < tk.hi; base += kAggBlock) {
+    const uint64_t q = base + threadIdx.x;
+    const bool valid = q < tk.hi;
+    uint32_t r = 0, v = 0xFFFFFFFFu;
+    if (valid) {
+      r = blockrows[q];
+      v = vid[uint64_t(r) * m + c];
     }
-    const SplitD& d = sp[lo];
-    if (!mask_has(masks + d.mask_off, c)) continue;
-    const uint64_t r = blockrows[q];
-    const uint32_t v = vid[r * m + c];
+    const unsigned grp = __match_any_sync(0xffffffffu, v);
+    const int leader = __ffs(grp) - 1;
+    const bool lead = valid && int(lane) == leader;
     const unsigned long long key = (uint64_t(c + 1) << 32) | v;
-    if (d.tB.keys) {
-      const uint64_t s = tbl_insert(d.tB, key);
-      atomicAdd(&d.tB.cnt[s], 1u);
-      for (uint32_t k = 0; k < npart[c]; ++k) {
-        const int32_t p = dpart[c * K + k];
-        atomicAdd(&d.tB.psum[s * K + k],
-                  (unsigned long long)vlen[colbase[p] + vid[r * m + p]]);
+    uint64_t sb = 0, spn = 0;
+    if (lead) {
+      const uint32_t cnt = __popc(grp);
+      if (tk.to_b) {
+        sb = tbl_insert(d.tB, key);
+        atomicAdd(&d.tB.cnt[sb], cnt);
+      }
+      if (tk.to_p) {
+        spn = d.tP.dense ? colbase[c] + v : tbl_find(d.tP, key);
+        atomicSub(&d.tP.cnt[spn], cnt);
       }
     }
-    if (d.tP.cnt) {
-      const uint64_t s = d.tP.dense ? colbase[c] + v : tbl_find(d.tP, key);
-      atomicSub(&d.tP.cnt[s], 1u);
-      for (uint32_t k = 0; k < npart[c]; ++k) {
-        const int32_t p = dpart[c * K + k];
-        atomicAdd(&d.tP.psum[s * K + k],
-                  (unsigned long long)(0ull - vlen[colbase[p] + vid[r * m + p]]));
+    for (uint32_t k = 0; k < np; ++k) {  // FD partner lengths, summed per group
+      const int32_t p = dpart[c * K + k];
+      unsigned long long l = valid ? vlen[colbase[p] + vid[uint64_t(r) * m + p]] : 0ull;
+      auto g = cg::labeled_partition(cg::tiled_partition<32>(cg::this_thread_block()), v);
+      l = cg::reduce(g, l, cg::plus<unsigned long long>());
+      if (lead) {
+        if (tk.to_b) atomicAdd(&d.tB.psum[sb * K + k], l);
+        if (tk.to_p) atomicAdd(&d.tP.psum[spn * K + k], 0ull - l);
       }
     }
   }
+}
+
+// ---- debug consistency checks (PO_DEBUG_CHECKS=1) ----
+__global__ void k_dbg_node_hist(const uint32_t* node_of_row, uint64_t n, uint32_t nnodes,
+                                unsigned long long* hist) {
+  for (uint64_t r = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; r < n;
+       r += uint64_t(gridDim.x) * blockDim.x) {
+    uint32_t nd = node_of_row[r];
+    atomicAdd(&hist[nd < nnodes ? nd : nnodes], 1ull);
+  }
+}
+
+__global__ void k_dbg_perm(const uint32_t* pos, uint64_t n, unsigned* seen, unsigned long long* bad) {
+  for (uint64_t r = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; r < n;
+       r += uint64_t(gridDim.x) * blockDim.x) {
+    uint32_t p = pos[r];
+    if (p >= n || atomicAdd(&seen[p], 1u) != 0) atomicAdd(bad, 1ull);
+  }
+}
+
+__global__ void k_mark_splits(int32_t* split_of_node, const uint32_t* nodes, uint32_t ns,
+                              int clear) {
+  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < ns; j += gridDim.x * blockDim.x)
+    split_of_node[nodes[j]] = clear ? -1 : int32_t(j);
 }
 
 // Root partner sums: psum[colbase[c]+vid(r,c)][k] += len(r, partner k of c).
@@ -354,16 +420,35 @@ __global__ void k_root_psum(const uint32_t* vid, uint64_t n, uint32_t m, uint32_
 __global__ void k_leaf_stats(const WorkItem* work, const ScanSlot* slots, const uint32_t* masks,
                              const uint64_t* colbase, const uint64_t* vlen, uint32_t m,
                              unsigned long long* card, unsigned long long* tot) {
+  extern __shared__ unsigned long long sh[];  // [2*m] when m is small
+  const bool priv = m <= 2048;
   const WorkItem w = work[blockIdx.x];
   const ScanSlot sl = slots[w.slot];
   const uint32_t* mask = masks + sl.mask_off;
+  if (priv)
+    for (uint32_t c = threadIdx.x; c < 2 * m; c += blockDim.x) sh[c] = 0;
+  __syncthreads();
   for (uint64_t e = w.lo + threadIdx.x; e < w.hi; e += blockDim.x) {
     uint32_t c, v;
     if (!decode_entry(sl.t, colbase, m, e, c, v)) continue;
     const uint32_t cnt = sl.t.cnt[e];
     if (cnt == 0 || !mask_has(mask, c)) continue;
-    atomicAdd(&card[uint64_t(w.slot) * m + c], 1ull);
-    atomicAdd(&tot[uint64_t(w.slot) * m + c], (unsigned long long)(uint64_t(cnt) * vlen[colbase[c] + v]));
+    const unsigned long long l = uint64_t(cnt) * vlen[colbase[c] + v];
+    if (priv) {
+      atomicAdd(&sh[c], 1ull);
+      atomicAdd(&sh[m + c], l);
+    } else {
+      atomicAdd(&card[uint64_t(w.slot) * m + c], 1ull);
+      atomicAdd(&tot[uint64_t(w.slot) * m + c], l);
+    }
+  }
+  if (priv) {
+    __syncthreads();
+    for (uint32_t c = threadIdx.x; c < m; c += blockDim.x)
+      if (sh[c]) {
+        atomicAdd(&card[uint64_t(w.slot) * m + c], sh[c]);
+        atomicAdd(&tot[uint64_t(w.slot) * m + c], sh[m + c]);
+      }
   }
 }
 
@@ -431,6 +516,14 @@ int classify(const Node& nd, const po_ggr_config& cfg) {
 }
 
 constexpr uint64_t kWorkChunk = 8192;
+
+bool debug_checks() {
+  static const bool on = [] {
+    const char* v = std::getenv("PO_DEBUG_CHECKS");
+    return v && *v && *v != '0';
+  }();
+  return on;
+}
 
 struct Level {
   std::vector<ScanSlot> slots;
@@ -565,7 +658,7 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
     DevBuf<unsigned long long> card(leaves.size() * m, s), tot(leaves.size() * m, s);
     card.zero();
     tot.zero();
-    PO_LAUNCH(k_leaf_stats, unsigned(L.work.size()), 256, 0, s, d_work.get(), d_slots.get(),
+    PO_LAUNCH(k_leaf_stats, unsigned(L.work.size()), 256, m <= 2048 ? 16 * m : 0, s, d_work.get(), d_slots.get(),
               d_masks.get(), colbase, vlen, m, card.get(), tot.get());
     std::vector<unsigned long long> hc(leaves.size() * m), ht(leaves.size() * m);
     card.download(hc.data(), hc.size());
@@ -624,8 +717,8 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
     DevBuf<unsigned long long> ncand(nslots, s);
     PO_LAUNCH(k_argmax, unsigned(L.work.size()), kArgBlock, 0, s, d_work.get(), d_slots.get(),
               d_masks.get(), d_w.get(), colbase, vlen, m, K, partial.get(), pcands.get());
-    PO_LAUNCH(k_argmax_final, grid_for(nslots, 128), 128, 0, s, partial.get(), pcands.get(),
-              d_swo.get(), nslots, best.get(), ncand.get());
+    PO_LAUNCH(k_argmax_final, nslots, kArgBlock, 0, s, partial.get(), pcands.get(), d_swo.get(),
+              best.get(), ncand.get());
     std::vector<Cand> hbest(nslots);
     std::vector<unsigned long long> hn(nslots);
     best.download(hbest.data(), nslots);
@@ -639,7 +732,6 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
       SplitD d;
     };
     std::vector<SplitH> splits;
-    std::vector<uint32_t> split_masks;
     for (uint32_t i = 0; i < nslots; ++i) {
       const int id = frontier[i];
       out.stats.candidates_examined += hn[i];
@@ -677,7 +769,7 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
       const bool needB = B.kind == SCAN || B.kind == FALLBACK;
       const bool needR = R.kind == SCAN || R.kind == FALLBACK;
       SplitD d{};
-      d.mask_off = col_mask(P.cols, split_masks);
+      d.mask_off = 0;
       d.col = b.col;
       d.vid = b.vid;
       if (needB) {
@@ -725,38 +817,72 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
       ensure_split_map(nodes.size());
       std::vector<SplitD> hsp(ns);
       std::vector<uint64_t> seg(ns + 1, 0);
+      std::vector<uint32_t> split_nodes(ns);
+      std::vector<AggTask> tasks;
+      constexpr uint64_t kRowsPerTask = 8 * kAggBlock;
       for (uint32_t j = 0; j < ns; ++j) {
         hsp[j] = splits[j].d;
-        seg[j + 1] = seg[j] + (hsp[j].need_rows ? nodes[hsp[j].block_id].size : 0);
-        int32_t jj = int32_t(j);
-        PO_CUDA(cudaMemcpyAsync(split_of_node.get() + splits[j].node, &jj, sizeof(int32_t),
-                                cudaMemcpyHostToDevice, s));
+        split_nodes[j] = uint32_t(splits[j].node);
+        const uint64_t rows = hsp[j].need_rows ? nodes[hsp[j].block_id].size : 0;
+        seg[j + 1] = seg[j] + rows;
+        if (!rows) continue;
+        const Node& P = nodes[splits[j].node];
+        const Node& B = nodes[hsp[j].block_id];
+        std::vector<char> inB(m, 0);
+        for (int c : B.cols) inB[c] = 1;
+        for (int c : P.cols) {
+          const uint32_t to_b = (hsp[j].tB.keys && inB[c]) ? 1u : 0u;
+          const uint32_t to_p = hsp[j].tP.cnt ? 1u : 0u;
+          if (!to_b && !to_p) continue;
+          for (uint64_t lo = seg[j]; lo < seg[j + 1]; lo += kRowsPerTask)
+            tasks.push_back(AggTask{j, uint32_t(c), to_b, to_p, lo,
+                                    std::min(seg[j + 1], lo + kRowsPerTask)});
+        }
       }
       auto d_sp = to_device(hsp, s);
       auto d_seg = to_device(seg, s);
-      auto d_smask = to_device(split_masks, s);
+      auto d_snodes = to_device(split_nodes, s);
       DevBuf<uint32_t> cursor(ns, s);
       cursor.zero();
       DevBuf<uint32_t> blockrows(std::max<uint64_t>(1, seg[ns]), s);
+      PO_LAUNCH(k_mark_splits, grid_for(ns, 128), 128, 0, s, split_of_node.get(), d_snodes.get(),
+                ns, 0);
       PO_LAUNCH(k_relabel, grid_for(n, 256), 256, 0, s, node_of_row.get(), n,
                 split_of_node.get(), d_sp.get(), e.vid.get(), m, cursor.get(), d_seg.get(),
                 blockrows.get());
-      if (seg[ns])
-        PO_LAUNCH(k_aggregate, grid_for(seg[ns] * m, 256), 256, 0, s, blockrows.get(), seg[ns],
-                  d_seg.get(), ns, d_sp.get(), d_smask.get(), e.vid.get(), vlen, colbase, m, K,
-                  d_dpart.get(), d_npart.get());
-      // unmark split nodes (host buffer must outlive the async copies: sync)
-      std::vector<int32_t> minus1(1, -1);
-      for (uint32_t j = 0; j < ns; ++j)
-        PO_CUDA(cudaMemcpyAsync(split_of_node.get() + splits[j].node, minus1.data(),
-                                sizeof(int32_t), cudaMemcpyHostToDevice, s));
-      sync(s);
+      if (!tasks.empty()) {
+        auto d_tasks = to_device(tasks, s);
+        PO_LAUNCH(k_aggregate, unsigned(tasks.size()), kAggBlock, 0, s, d_tasks.get(),
+                  blockrows.get(), d_sp.get(), e.vid.get(), vlen, colbase, m, K, d_dpart.get(),
+                  d_npart.get());
+      }
+      PO_LAUNCH(k_mark_splits, grid_for(ns, 128), 128, 0, s, split_of_node.get(), d_snodes.get(),
+                ns, 1);
     }
 
     // ---- K7: statistics of every node that falls back at this level ----
     std::vector<int> leaves = stopped;
     leaves.insert(leaves.end(), new_fallback.begin(), new_fallback.end());
     run_leaf_stats(leaves);
+    if (debug_checks()) {
+      DevBuf<unsigned long long> hist(nodes.size() + 1, s);
+      hist.zero();
+      PO_LAUNCH(k_dbg_node_hist, grid_for(n, 256), 256, 0, s, node_of_row.get(), n,
+                uint32_t(nodes.size()), hist.get());
+      std::vector<unsigned long long> hh(nodes.size() + 1);
+      hist.download(hh.data(), hh.size());
+      sync(s);
+      for (size_t id = 0; id < nodes.size(); ++id) {
+        const Node& nd = nodes[id];
+        const bool live = nd.kind != SPLIT;
+        if (live && hh[id] != nd.size)
+          fprintf(stderr, "[po debug] level: node %zu kind %d size %llu but %llu rows labelled\n",
+                  id, nd.kind, (unsigned long long)nd.size, hh[id]);
+        if (!live && hh[id])
+          fprintf(stderr, "[po debug] split node %zu still labels %llu rows\n", id, hh[id]);
+      }
+      if (hh[nodes.size()]) fprintf(stderr, "[po debug] %llu rows with invalid node\n", hh[nodes.size()]);
+    }
     frontier.swap(next);
   }
 
@@ -810,10 +936,11 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
     else if (nd.kind == FALLBACK)                          // fragment keys (ggr.hpp:340-350)
       for (int f : nd.leaf_order) keys.push_back({f, 1});
     leaf_chunk_off[l] = uint32_t(chunk_nkeys.size());
-    int used = 64;
+    const int cap_bits = int(refine_chunk_bits(uint32_t(n)));
+    int used = cap_bits;
     for (auto [f, kind] : keys) {
       int b = bits_for(e.card[f] ? e.card[f] - 1 : 0);
-      if (used + b > 64) {
+      if (used + b > cap_bits) {
         chunk_key_off.push_back(uint32_t(key_field.size()));
         chunk_nkeys.push_back(0);
         used = 0;
@@ -859,9 +986,50 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
   RK.key_kind = d_kk.get();
   RK.key_bits = d_kb.get();
   refine_sort(uint32_t(n), grp.get(), uint32_t(n), RK, pos.get(), s);
+  if (debug_checks()) {
+    DevBuf<unsigned> seen(n, s);
+    DevBuf<unsigned long long> bad(1, s);
+    seen.zero();
+    bad.zero();
+    PO_LAUNCH(k_dbg_perm, grid_for(n, 256), 256, 0, s, pos.get(), n, seen.get(), bad.get());
+    unsigned long long hb = 0;
+    bad.download(&hb, 1);
+    sync(s);
+    if (hb) fprintf(stderr, "[po debug] leaf sort positions: %llu collisions/out of range\n", hb);
+  }
   PO_LAUNCH(k_emit, grid_for(n, 256), 256, 0, s, pos.get(), n, m, row_leaf.get(),
             d_leaf_orders.get(), d_rows, d_orders);
-  out.phc = phc_device(e, n, nullptr, d_rows, nullptr, d_orders, s);
+  try {
+    out.phc = phc_device(e, n, nullptr, d_rows, nullptr, d_orders, s);
+  } catch (const Error&) {
+    // post-mortem diagnostics (no effect on the timing before the failure)
+    DevBuf<unsigned> seen(n, s);
+    DevBuf<unsigned long long> bad(1, s);
+    seen.zero();
+    bad.zero();
+    PO_LAUNCH(k_dbg_perm, grid_for(n, 256), 256, 0, s, pos.get(), n, seen.get(), bad.get());
+    DevBuf<unsigned long long> hist(nodes.size() + 1, s);
+    hist.zero();
+    PO_LAUNCH(k_dbg_node_hist, grid_for(n, 256), 256, 0, s, node_of_row.get(), n,
+              uint32_t(nodes.size()), hist.get());
+    std::vector<unsigned long long> hh(nodes.size() + 1);
+    hist.download(hh.data(), hh.size());
+    unsigned long long hb = 0;
+    bad.download(&hb, 1);
+    sync(s);
+    fprintf(stderr, "[po post-mortem] n=%llu nodes=%zu leaves=%u pos collisions=%llu\n",
+            (unsigned long long)n, nodes.size(), nleaves, hb);
+    for (size_t id = 0; id < nodes.size(); ++id)
+      if (nodes[id].kind != SPLIT && hh[id] != nodes[id].size)
+        fprintf(stderr, "[po post-mortem] node %zu kind %d size %llu labelled %llu\n", id,
+                nodes[id].kind, (unsigned long long)nodes[id].size, hh[id]);
+    std::vector<uint32_t> hrows(std::min<uint64_t>(n, 64));
+    PO_CUDA(cudaMemcpy(hrows.data(), d_rows, hrows.size() * 4, cudaMemcpyDeviceToHost));
+    fprintf(stderr, "[po post-mortem] first rows:");
+    for (auto x : hrows) fprintf(stderr, " %u", x);
+    fprintf(stderr, "\n");
+    throw;
+  }
 
   // ---- whole-table fallback competition (ggr.hpp:379-387) ----
   std::vector<double> avg(m);
@@ -872,7 +1040,22 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
   sort_all_rows(e, fb_order, fb_perm.get(), s);
   std::vector<int32_t> fo(fb_order.begin(), fb_order.end());
   auto d_fo = to_device(fo, s);
-  const uint64_t fb_phc = phc_device(e, n, nullptr, fb_perm.get(), nullptr, d_fo.get(), s, 1, true);
+  uint64_t fb_phc = 0;
+  try {
+    fb_phc = phc_device(e, n, nullptr, fb_perm.get(), nullptr, d_fo.get(), s, 1, true);
+  } catch (const Error&) {
+    std::vector<uint32_t> hp(n);
+    PO_CUDA(cudaMemcpy(hp.data(), fb_perm.get(), n * 4, cudaMemcpyDeviceToHost));
+    std::vector<char> seen(n, 0);
+    uint64_t bad = 0, dup = 0;
+    for (auto x : hp) {
+      if (x >= n) ++bad;
+      else if (seen[x]++) ++dup;
+    }
+    fprintf(stderr, "[po post-mortem] fallback perm: %llu out of range, %llu duplicates\n",
+            (unsigned long long)bad, (unsigned long long)dup);
+    throw;
+  }
   if (fb_phc > out.phc) {
     PO_CUDA(cudaMemcpyAsync(d_rows, fb_perm.get(), n * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
     PO_LAUNCH(k_tile_order, grid_for(n * m, 256), 256, 0, s, d_fo.get(), n, m, d_orders);

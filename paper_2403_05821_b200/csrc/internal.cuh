@@ -57,10 +57,11 @@ void encode(const DeviceTable& t, int tok, int scoring, cudaStream_t s, Encoded&
 // Segmented refinement sort (rank_sort / multikey_sort engine).
 // Items [0, n_items) start in groups whose ids are their final start
 // positions (grp_init[i]); each round sorts the unresolved items of every
-// group by the next 63-bit key chunk (stable, so the initial item order breaks
+// group by the next key chunk (refine_chunk_bits(grp_max) bits) (stable, so the initial item order breaks
 // all remaining ties) and splits groups on chunk changes. An item is resolved
 // when its run has one member or its key reports `terminal`.
-// out_pos[item] receives the item's final position.
+// out_pos[item] receives the item's final position. grp_max must bound every
+// group id of every round, i.e. the largest start position (n_items - 1).
 struct RefineKey {
   int kind = 0;  // 0 = string (raw order), 1 = string (escaped order), 2 = row keys
   // string keys
@@ -82,7 +83,11 @@ struct RefineKey {
   const int32_t* key_field = nullptr;
   const uint8_t* key_kind = nullptr;  // 0 raw (vid), 1 escaped (esc_rank)
   const uint8_t* key_bits = nullptr;
+  uint32_t chunk_bits = 0;  // set by refine_sort: 64 - bits(grp_max)
 };
+
+// Bits available for a key chunk next to group ids up to grp_max.
+uint32_t refine_chunk_bits(uint32_t grp_max);
 
 void refine_sort(uint32_t n_items, const uint32_t* d_grp_init, uint32_t grp_max,
                  const RefineKey& key, uint32_t* d_out_pos, cudaStream_t s,

@@ -103,10 +103,12 @@ void sort_all_rows(const Encoded& e, const std::vector<int>& order, uint32_t* d_
   std::vector<uint32_t> chunk_key_off, chunk_nkeys;
   std::vector<int32_t> key_field;
   std::vector<uint8_t> key_kind, key_bits;
-  int used = 64;
+  // later rounds use start positions (< n) as group ids
+  const int cap_bits = int(refine_chunk_bits(uint32_t(n)));
+  int used = cap_bits;
   for (int f : order) {
     int b = bits_for(e.card[f] ? e.card[f] - 1 : 0);
-    if (used + b > 64) {
+    if (used + b > cap_bits) {
       chunk_key_off.push_back(uint32_t(key_field.size()));
       chunk_nkeys.push_back(0);
       used = 0;
@@ -146,7 +148,7 @@ void sort_all_rows(const Encoded& e, const std::vector<int>& order, uint32_t* d_
   K.key_field = d_kf.get();
   K.key_kind = d_kk.get();
   K.key_bits = d_kb.get();
-  refine_sort(uint32_t(n), grp.get(), 0, K, pos.get(), s);
+  refine_sort(uint32_t(n), grp.get(), uint32_t(n), K, pos.get(), s);
   PO_LAUNCH(k_invert, grid_for(n, 256), 256, 0, s, pos.get(), n, d_perm);
 }
 

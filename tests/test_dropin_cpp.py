@@ -21,3 +21,6 @@ def test_reference_cpp_suite_against_dropin(name):
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
     if name == "acceptance":
         assert "[FAIL]" not in r.stdout
+        # criterion 8 known answer: 30000x57 synthetic_wide_table, seed
+        # 20240008, GgrConfig defaults -> PHC 8,072,240
+        assert "score 8072240" in r.stdout
