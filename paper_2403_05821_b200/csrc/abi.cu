@@ -70,6 +70,44 @@ void profile_end(void* token, cudaStream_t s) {
 }
 
 namespace {
+thread_local std::vector<std::pair<std::string, double>> g_marks;
+thread_local std::chrono::steady_clock::time_point g_mark_t0;
+}  // namespace
+
+bool debug_timing() {
+  static const bool on = [] {
+    const char* v = std::getenv("PO_DEBUG_TIMING");
+    return v && *v && *v != '0';
+  }();
+  return on;
+}
+
+void timing_mark(const char* phase, cudaStream_t s) {
+  if (!debug_timing()) return;
+  sync(s);
+  auto now = std::chrono::steady_clock::now();
+  if (!g_marks.empty() || phase[0] == '<')
+    g_marks.push_back({phase, std::chrono::duration<double, std::milli>(now - g_mark_t0).count()});
+  g_mark_t0 = now;
+}
+
+void timing_report(const char* call) {
+  if (!debug_timing()) return;
+  std::map<std::string, double> agg;
+  std::vector<std::string> order;
+  double tot = 0;
+  for (auto& [k, v] : g_marks) {
+    if (!agg.count(k)) order.push_back(k);
+    agg[k] += v;
+    tot += v;
+  }
+  fprintf(stderr, "[po timing] %s total %.3f ms:", call, tot);
+  for (auto& k : order) fprintf(stderr, " %s=%.3f", k.c_str(), agg[k]);
+  fprintf(stderr, "\n");
+  g_marks.clear();
+}
+
+namespace {
 
 // Keep freed stream-ordered allocations cached in the device pool between
 // calls instead of returning them to the driver at every synchronisation.
@@ -126,6 +164,7 @@ void prepare(const po_table* tv, int tok, int scoring, cudaStream_t s, Prepared&
   check_modes(tok, scoring);
   init_pool_once();
   make_device_table(tv, tok, s, p.t);
+  timing_mark("table_h2d", s);
   encode(p.t, tok, scoring, s, p.e, debug_hash_bits());
 }
 
@@ -199,6 +238,7 @@ int po_ggr(const po_table* t, const po_fd_groups* fds, const po_ggr_config* cfg,
     if (cfg->stats_variant < 0 || cfg->stats_variant > 2)
       fail(PO_ERR_INVALID_ARG, "unknown stats variant");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
+    timing_mark("<start", s);
     std::vector<std::vector<int>> groups;
     if (fds && cfg->use_fds)
       for (uint32_t g = 0; g < fds->n_groups; ++g)
@@ -220,6 +260,8 @@ int po_ggr(const po_table* t, const po_fd_groups* fds, const po_ggr_config* cfg,
     deliver_rows(rows.get(), n, out_location, out_row_ids, s);
     if (out_location == PO_LOC_HOST) own_orders.download(out_field_orders, n * m);
     sync(s);
+    timing_mark("deliver", s);
+    timing_report("po_ggr");
     *out_phc = go.phc;
     if (out_stats) {
       *out_stats = go.stats;

@@ -40,6 +40,18 @@ extern std::atomic<int> g_profile;
 void profile_begin(const char* name, cudaStream_t s, void** token);
 void profile_end(void* token, cudaStream_t s);
 
+// Times a library call (CUB building blocks) like a kernel when profiling.
+struct ProfScope {
+  void* tok = nullptr;
+  cudaStream_t s;
+  ProfScope(const char* name, cudaStream_t st) : s(st) {
+    if (g_profile.load(std::memory_order_relaxed)) profile_begin(name, st, &tok);
+  }
+  ~ProfScope() {
+    if (tok) profile_end(tok, s);
+  }
+};
+
 // Every kernel of this library is launched through PO_LAUNCH so bench.py can
 // report how many of OUR kernels ran (po_kernel_launch_count) and time them.
 #define PO_LAUNCH(kernel, grid, block, smem, stream, ...)                    \
@@ -128,6 +140,12 @@ DevBuf<T> to_device(const std::vector<T>& v, cudaStream_t s) {
 
 inline void sync(cudaStream_t s) { PO_CUDA(cudaStreamSynchronize(s)); }
 
+// Host wall-time breakdown of one call (PO_DEBUG_TIMING=1): synchronises the
+// stream at every mark, so it perturbs the timing it reports; debug only.
+bool debug_timing();
+void timing_mark(const char* phase, cudaStream_t s);
+void timing_report(const char* call);
+
 inline int bits_for(uint64_t max_value) {  // bits to hold values 0..max_value
   int b = 0;
   while (b < 64 && (max_value >> b)) ++b;
@@ -140,6 +158,12 @@ inline int bits_for(uint64_t max_value) {  // bits to hold values 0..max_value
 __device__ __forceinline__ uint32_t ld_relaxed_u32(const uint32_t* p) {
   uint32_t v;
   asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
 
@@ -189,7 +213,8 @@ __device__ __forceinline__ uint64_t mask_low_bytes(uint64_t w, uint32_t nbytes) 
 // (little-endian, zero-padded), so a warp can hash a long cell cooperatively
 // (lane l takes words l, l+32, ...) and get the same value as one lane.
 __device__ __forceinline__ uint64_t word_term(uint64_t w, uint64_t k) {
-  return fmix64(w ^ (k * 0x9E3779B97F4A7C15ULL) ^ 0x5bd1e9955bd1e995ULL);
+  const uint64_t x = (w ^ (k * 0x9E3779B97F4A7C15ULL)) * 0xff51afd7ed558ccdULL;
+  return x ^ (x >> 32);
 }
 
 __device__ __forceinline__ uint64_t hash_finish(uint64_t sum, uint64_t len) {
@@ -268,6 +293,41 @@ __device__ __forceinline__ bool bytes_equal(const uint8_t* a, const uint8_t* b, 
     left -= take;
   }
   return true;
+}
+
+// ---- TMA bulk copy (cp.async.bulk) + mbarrier helpers (sm_90+/sm_100a) ----
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "WAIT%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// 1-D bulk copy global -> shared, completion counted on `bar` (bytes % 16 == 0,
+// both addresses 16-byte aligned).
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
 typedef unsigned __int128 u128;

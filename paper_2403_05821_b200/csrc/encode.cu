@@ -31,100 +31,386 @@ namespace {
 
 constexpr uint32_t kEmptyRep = 0xFFFFFFFFu;
 
-constexpr uint64_t kShortCell = 32;  // longer cells are hashed/compared by the whole warp
+// Reader of an arbitrarily aligned byte string as little-endian 8-byte words
+// from either shared memory (staged tile) or global memory, loading only
+// 8-byte-aligned words that start before `lim`.
+template <bool kShared>
+struct Words {
+  const uint64_t* p;
+  const uint64_t* lim;
+  uint32_t sh;
+  uint64_t cur;
+  __device__ __forceinline__ static uint64_t ld(const uint64_t* q) {
+    if constexpr (kShared) return *q;
+    else return __ldg(q);
+  }
+  __device__ __forceinline__ Words(const uint8_t* a, const uint8_t* limit) {
+    const uintptr_t ad = reinterpret_cast<uintptr_t>(a);
+    p = reinterpret_cast<const uint64_t*>(ad & ~uintptr_t(7));
+    lim = reinterpret_cast<const uint64_t*>((reinterpret_cast<uintptr_t>(limit) + 7) & ~uintptr_t(7));
+    sh = uint32_t(ad & 7) * 8;
+    cur = p < lim ? ld(p) : 0;
+  }
+  __device__ __forceinline__ uint64_t next() {
+    const uint64_t* q = p + 1;
+    const uint64_t nxt = q < lim ? ld(q) : 0;
+    const uint64_t w = sh ? ((cur >> sh) | (nxt << (64 - sh))) : cur;
+    cur = nxt;
+    p = q;
+    return w;
+  }
+};
 
-// K1+K2 fused. A warp takes 32 consecutive cells (contiguous in the row-major
-// arena). Short cells are hashed by their own lane; long cells one at a time
-// by the whole warp with coalesced 8-byte word loads. Each lane then probes
-// its column's table; a slot owned by another cell with the same hash is
-// verified on the bytes (cooperatively for long cells) and probing continues
-// on a mismatch, so value identity is exact.
-__global__ void __launch_bounds__(256) k_dict_insert(
+template <bool kShared>
+__device__ __forceinline__ uint64_t hash_cell(const uint8_t* a, uint64_t len, const uint8_t* limit) {
+  uint64_t sum = 0;
+  if (len) {
+    Words<kShared> rd(a, limit);
+    uint64_t k = 0;
+    for (; 8 * (k + 1) <= len; ++k) sum += word_term(rd.next(), k);
+    if (8 * k < len) sum += word_term(mask_low_bytes(rd.next(), uint32_t(len - 8 * k)), k);
+  }
+  return hash_finish(sum, len);
+}
+
+// Cell (shared or global) vs representative (global), 4 words per step so
+// several independent loads of the representative are in flight.
+template <bool kShared>
+__device__ __forceinline__ bool equal_cell_rep(const uint8_t* a, const uint8_t* a_lim,
+                                               const uint8_t* b, const uint8_t* b_lim,
+                                               uint64_t len) {
+  Words<kShared> ra(a, a_lim);
+  Words<false> rb(b, b_lim);
+  uint64_t left = len;
+  while (left >= 32) {
+    const uint64_t b0 = rb.next(), b1 = rb.next(), b2 = rb.next(), b3 = rb.next();
+    const uint64_t a0 = ra.next(), a1 = ra.next(), a2 = ra.next(), a3 = ra.next();
+    if ((a0 ^ b0) | (a1 ^ b1) | (a2 ^ b2) | (a3 ^ b3)) return false;
+    left -= 32;
+  }
+  while (left) {
+    const uint32_t take = left >= 8 ? 8u : uint32_t(left);
+    if (mask_low_bytes(ra.next(), take) != mask_low_bytes(rb.next(), take)) return false;
+    left -= take;
+  }
+  return true;
+}
+
+// Probe column c's table for the cell's value: claim an empty slot (the cell
+// becomes the representative) or find the slot whose representative has the
+// same bytes. Equal hashes with different bytes keep probing (exact).
+// Representative locator stored next to each claimed slot: arena offset
+// (high 40 bits) and byte length (low 24 bits; kLongRep = look it up).
+constexpr uint64_t kLongRep = 0xFFFFFF;
+__device__ __forceinline__ uint64_t pack_rep(uint64_t off, uint64_t len) {
+  return (off << 24) | (len < kLongRep ? len : kLongRep);
+}
+
+// Claims slot `slot` for the cell (representative) — publishes the locator
+// before the row (readers spin on the row with acquire semantics).
+__device__ __forceinline__ void publish_rep(uint32_t* R, unsigned long long* RO, uint64_t slot,
+                                            uint32_t row, uint64_t off, uint64_t len) {
+  RO[slot] = pack_rep(off, len);
+  __threadfence();
+  atomicExch(&R[slot], row);
+}
+
+__device__ __forceinline__ void read_rep(const uint32_t* R, const unsigned long long* RO,
+                                         uint64_t slot, uint32_t m, uint32_t c,
+                                         const uint64_t* __restrict__ offsets, uint64_t& off,
+                                         uint64_t& len) {
+  uint32_t rep;
+  while ((rep = ld_acquire_u32(&R[slot])) == kEmptyRep) {
+  }
+  const uint64_t pk = RO[slot];
+  off = pk >> 24;
+  len = pk & kLongRep;
+  if (len == kLongRep) {
+    const uint64_t j = uint64_t(rep) * m + c;
+    len = offsets[j + 1] - offsets[j];
+  }
+}
+
+// Probe column c's table for the cell's value: claim an empty slot (the cell
+// becomes the representative) or find the slot whose representative has the
+// same bytes. Equal hashes with different bytes keep probing (exact).
+template <bool kShared>
+__device__ __forceinline__ uint64_t probe_insert(unsigned long long* K, uint32_t* R,
+                                                 unsigned long long* RO, uint64_t cap, uint64_t h,
+                                                 uint64_t slot, uint32_t row, uint32_t c,
+                                                 uint32_t m, uint64_t o0, const uint8_t* cell,
+                                                 const uint8_t* cell_lim, uint64_t len,
+                                                 const uint8_t* arena, const uint8_t* arena_end,
+                                                 const uint64_t* __restrict__ offsets) {
+  for (;;) {
+    unsigned long long k = K[slot];
+    if (k == 0) {
+      const unsigned long long prev = atomicCAS(&K[slot], 0ull, (unsigned long long)h);
+      if (prev == 0) {
+        publish_rep(R, RO, slot, row, o0, len);
+        return slot;
+      }
+      k = prev;
+    }
+    if (k == h) {
+      uint64_t q0, ql;
+      read_rep(R, RO, slot, m, c, offsets, q0, ql);
+      if (ql == len && equal_cell_rep<kShared>(cell, cell_lim, arena + q0, arena_end, len))
+        return slot;
+    }
+    slot = (slot + 1) & (cap - 1);
+  }
+}
+
+// 8 bytes of a staged tile at byte offset `off` (two aligned shared loads).
+__device__ __forceinline__ uint64_t smem_word(const uint64_t* s64, uint32_t off) {
+  const uint32_t q = off >> 3, sh = (off & 7) * 8;
+  const uint64_t w0 = s64[q];
+  return sh ? ((w0 >> sh) | (s64[q + 1] << (64 - sh))) : w0;
+}
+
+constexpr uint32_t kDictBlock = 256;
+
+// ---------------------------------------------------------------------------
+// K1 cell_scan: tile-staged, load-balanced hashing of every cell.
+// A block takes a tile of up to 256 consecutive cells (contiguous bytes in the
+// row-major arena); one elected thread streams the tile's 16-byte-aligned
+// byte range into shared memory with a TMA bulk copy (double-buffered: the
+// next tile is in flight while this one is hashed). The tile's 8-byte words
+// (relative to each cell's start) are split evenly over the 256 threads
+// whatever the cell lengths; per-cell partial sums are folded in shared
+// memory. Output: the 64-bit hash of every cell. Tiles larger than a staging
+// buffer are hashed from global memory by one thread per cell (same hash).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kDictBlock) k_cell_hash(
     const uint8_t* __restrict__ arena, const uint8_t* arena_end,
-    const uint64_t* __restrict__ offsets, uint64_t n, uint32_t m, uint64_t cap,
-    unsigned long long* keys, uint32_t* reps, uint32_t* slot_of_cell, uint64_t hash_mask) {
+    const uint64_t* __restrict__ offsets, uint64_t total, uint32_t tile, uint32_t stage_bytes,
+    uint64_t hash_mask, unsigned long long* __restrict__ hashes) {
+  extern __shared__ __align__(128) uint8_t sbuf_all[];
+  typedef cub::BlockScan<uint32_t, kDictBlock> Scan;
+  __shared__ typename Scan::TempStorage scan_tmp;
+  __shared__ uint32_t s_wstart[kDictBlock + 1];
+  __shared__ uint32_t s_off[kDictBlock];
+  __shared__ uint32_t s_len[kDictBlock];
+  __shared__ unsigned long long s_hash[kDictBlock];
+  __shared__ __align__(8) uint64_t s_bar[2];
+  const uint32_t buf_bytes = (stage_bytes + 64 + 127) & ~127u;
+  const uint64_t ntiles = (total + tile - 1) / tile;
+  const uint32_t tid = threadIdx.x;
+  auto tile_range = [&](uint64_t t, uintptr_t& a0, uintptr_t& b1) {
+    const uint64_t j0 = t * tile;
+    const uint64_t j1 = j0 + tile < total ? j0 + tile : total;
+    a0 = reinterpret_cast<uintptr_t>(arena + offsets[j0]) & ~uintptr_t(15);
+    b1 = (reinterpret_cast<uintptr_t>(arena + offsets[j1]) + 15) & ~uintptr_t(15);
+  };
+  auto issue = [&](uint64_t t, int b) {
+    uintptr_t a0, b1;
+    tile_range(t, a0, b1);
+    if (b1 - a0 > stage_bytes) return;
+    fence_proxy_async_smem();
+    mbar_arrive_expect_tx(&s_bar[b], uint32_t(b1 - a0));
+    bulk_g2s(sbuf_all + b * buf_bytes, reinterpret_cast<const void*>(a0), uint32_t(b1 - a0),
+             &s_bar[b]);
+  };
+  if (tid == 0) {
+    mbar_init(&s_bar[0], 1);
+    mbar_init(&s_bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (tid == 0 && blockIdx.x < ntiles) issue(blockIdx.x, 0);
+  uint32_t uses[2] = {0u, 0u};
+  uint32_t kiter = 0;
+  for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++kiter) {
+    const int bsel = int(kiter & 1);
+    const uint64_t* s64 = reinterpret_cast<const uint64_t*>(sbuf_all + bsel * buf_bytes);
+    const uint64_t i0 = t * tile;
+    const uint32_t cnt = uint32_t(total - i0 < tile ? total - i0 : tile);
+    uintptr_t gA0, gB1;
+    tile_range(t, gA0, gB1);
+    const bool staged = gB1 - gA0 <= stage_bytes;
+    if (tid == 0 && t + gridDim.x < ntiles) issue(t + gridDim.x, bsel ^ 1);
+    const uint64_t i = i0 + tid;
+    const bool mine = tid < cnt;
+    const uint64_t o0 = mine ? offsets[i] : 0;
+    const uint64_t len = mine ? offsets[i + 1] - o0 : 0;
+    if (!staged) {
+      if (mine) {
+        uint64_t h = hash_cell<false>(arena + o0, len, arena_end) & hash_mask;
+        hashes[i] = h ? h : 1;
+      }
+      __syncthreads();
+      continue;
+    }
+    const uint32_t words = mine ? uint32_t((len + 7) / 8) : 0;
+    uint32_t wstart, total_words;
+    Scan(scan_tmp).ExclusiveSum(words, wstart, total_words);
+    s_wstart[tid] = wstart;
+    if (tid == 0) s_wstart[kDictBlock] = total_words;
+    s_off[tid] = mine ? uint32_t(reinterpret_cast<uintptr_t>(arena + o0) - gA0) : 0;
+    s_len[tid] = uint32_t(len);
+    s_hash[tid] = 0;
+    mbar_wait(&s_bar[bsel], uses[bsel] & 1u);
+    ++uses[bsel];
+    __syncthreads();
+    const uint32_t per = (total_words + kDictBlock - 1) / kDictBlock;
+    const uint32_t w0 = min(total_words, tid * per), w1 = min(total_words, w0 + per);
+    if (w0 < w1) {
+      uint32_t lo = 0, hi = kDictBlock;  // last cell with wstart <= w0
+      while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (s_wstart[mid] <= w0) lo = mid;
+        else hi = mid;
+      }
+      uint32_t cc = lo;
+      while (s_wstart[cc + 1] <= w0) ++cc;
+      uint32_t cend = s_wstart[cc + 1], cbase = s_wstart[cc], coff = s_off[cc], clen = s_len[cc];
+      unsigned long long part = 0;
+      for (uint32_t g = w0; g < w1; ++g) {
+        if (g >= cend) {
+          if (part) atomicAdd(&s_hash[cc], part);
+          part = 0;
+          do {
+            ++cc;
+          } while (g >= s_wstart[cc + 1]);
+          cend = s_wstart[cc + 1];
+          cbase = s_wstart[cc];
+          coff = s_off[cc];
+          clen = s_len[cc];
+        }
+        const uint32_t k = g - cbase;
+        uint64_t w = smem_word(s64, coff + 8 * k);
+        const uint32_t rem = clen - 8 * k;
+        if (rem < 8) w = mask_low_bytes(w, rem);
+        part += word_term(w, k);
+      }
+      if (part) atomicAdd(&s_hash[cc], part);
+    }
+    __syncthreads();
+    if (mine) {
+      const uint64_t h = hash_finish(s_hash[tid], len) & hash_mask;
+      hashes[i] = h ? h : 1;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K2a probe: one thread per cell, full occupancy, no barriers. The first
+// cell to reach an empty slot claims it and records itself as the value's
+// representative (row + arena locator); a cell meeting a slot with its hash
+// is tentatively that slot's value (verified on the bytes by K2b). Claims
+// and records become visible to K2b at the kernel boundary, so no fences or
+// spin-waits are needed here.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_dict_probe(
+    const unsigned long long* __restrict__ hashes, const uint64_t* __restrict__ offsets,
+    uint64_t total, uint32_t m, uint64_t cap, unsigned long long* keys, uint32_t* reps,
+    unsigned long long* repoffs, uint32_t* slot_of_cell) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < total;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t r = i / m;
+    const uint32_t c = uint32_t(i - r * m);
+    const unsigned long long h = hashes[i];
+    unsigned long long* K = keys + uint64_t(c) * cap;
+    uint64_t slot = h & (cap - 1);
+    for (;;) {
+      unsigned long long k = K[slot];
+      if (k == 0) {
+        const unsigned long long prev = atomicCAS(&K[slot], 0ull, h);
+        if (prev == 0) {
+          const uint64_t o0 = offsets[i];
+          reps[uint64_t(c) * cap + slot] = uint32_t(r);
+          repoffs[uint64_t(c) * cap + slot] = pack_rep(o0, offsets[i + 1] - o0);
+          break;
+        }
+        k = prev;
+      }
+      if (k == h) break;
+      slot = (slot + 1) & (cap - 1);
+    }
+    slot_of_cell[i] = uint32_t(slot);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K2b verify: every cell whose slot is owned by another row is compared
+// byte for byte with the representative (4 independent 8-byte loads per
+// step). A mismatch — two different strings with the same 64-bit hash —
+// flags the cell for K2c.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_dict_verify(
+    const uint8_t* __restrict__ arena, const uint8_t* arena_end,
+    const uint64_t* __restrict__ offsets, uint64_t total, uint32_t m, uint64_t cap,
+    const uint32_t* __restrict__ reps, const unsigned long long* __restrict__ repoffs,
+    const uint32_t* __restrict__ slot_of_cell, uint32_t* collided, uint32_t* n_collided) {
+  // A warp takes 32 consecutive cells. Cells up to 64 bytes are compared by
+  // their own lane; longer ones one at a time by the whole warp (lane l takes
+  // words l, l+32, ...: coalesced loads of both strings).
+  constexpr uint64_t kShort = 64;
   const uint32_t lane = threadIdx.x & 31;
-  const uint64_t total = n * m;
   const uint64_t warp0 = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
   const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
   for (uint64_t base = warp0 * 32; base < total; base += nwarps * 32) {
     const uint64_t i = base + lane;
-    const bool valid = i < total;
-    uint64_t o0 = 0, len = 0, r = 0;
-    uint32_t c = 0;
-    if (valid) {
-      o0 = offsets[i];
-      len = offsets[i + 1] - o0;
-      r = i / m;
-      c = uint32_t(i - r * m);
-    }
-    const bool is_long = valid && len > kShortCell;
-    uint64_t h = 0;
-    if (valid && !is_long) h = hash_bytes(arena + o0, len, arena_end);
-    for (unsigned lm = __ballot_sync(0xffffffffu, is_long); lm; lm &= lm - 1) {
-      const int src = __ffs(lm) - 1;
-      const uint64_t so = __shfl_sync(0xffffffffu, o0, src);
-      const uint64_t sl = __shfl_sync(0xffffffffu, len, src);
-      const uint64_t hh = warp_hash_bytes(arena + so, sl, arena_end, lane);
-      if (int(lane) == src) h = hh;
-    }
-    h &= hash_mask;
-    if (h == 0) h = 1;
-    unsigned long long* K = keys + uint64_t(c) * cap;
-    uint32_t* R = reps + uint64_t(c) * cap;
-    uint64_t slot = h & (cap - 1);
-    bool done = !valid;
-    for (;;) {
-      // per-lane probing until inserted, matched (short) or a long match awaits verification
-      bool verify = false;
-      uint64_t rep_off = 0;
-      while (!done && !verify) {
-        unsigned long long k = K[slot];
-        if (k == 0) {
-          const unsigned long long prev = atomicCAS(&K[slot], 0ull, (unsigned long long)h);
-          if (prev == 0) {
-            atomicExch(&R[slot], uint32_t(r));
-            done = true;
-            break;
-          }
-          k = prev;
-        }
-        if (k == h) {
-          uint32_t rep;
-          while ((rep = ld_relaxed_u32(&R[slot])) == kEmptyRep) {
-          }
+    bool need = false;
+    uint64_t o0 = 0, len = 0, q0 = 0;
+    if (i < total) {
+      const uint64_t r = i / m;
+      const uint32_t c = uint32_t(i - r * m);
+      const uint64_t sidx = uint64_t(c) * cap + slot_of_cell[i];
+      const uint32_t rep = reps[sidx];
+      if (rep != uint32_t(r)) {
+        o0 = offsets[i];
+        len = offsets[i + 1] - o0;
+        const uint64_t pk = repoffs[sidx];
+        q0 = pk >> 24;
+        uint64_t ql = pk & kLongRep;
+        if (ql == kLongRep) {
           const uint64_t j = uint64_t(rep) * m + c;
-          const uint64_t q0 = offsets[j];
-          if (offsets[j + 1] - q0 == len) {
-            if (!is_long) {
-              if (bytes_equal(arena + o0, arena + q0, len, arena_end)) {
-                done = true;
-                break;
-              }
-            } else {
-              verify = true;
-              rep_off = q0;
-              break;
-            }
-          }
+          ql = offsets[j + 1] - offsets[j];
         }
-        slot = (slot + 1) & (cap - 1);
+        if (ql != len) collided[atomicAdd(n_collided, 1u)] = uint32_t(i);
+        else need = len > 0;
       }
-      // cooperative verification of long matches
-      for (unsigned vm = __ballot_sync(0xffffffffu, verify); vm; vm &= vm - 1) {
-        const int src = __ffs(vm) - 1;
-        const uint64_t a = __shfl_sync(0xffffffffu, o0, src);
-        const uint64_t b = __shfl_sync(0xffffffffu, rep_off, src);
-        const uint64_t sl = __shfl_sync(0xffffffffu, len, src);
-        const bool eq = warp_bytes_equal(arena + a, arena + b, sl, arena_end, lane);
-        if (int(lane) == src) {
-          if (eq) done = true;
-          else slot = (slot + 1) & (cap - 1);  // same hash, different bytes: keep probing
-        }
-      }
-      if (__all_sync(0xffffffffu, done)) break;
     }
-    if (valid) slot_of_cell[i] = uint32_t(slot);
+    const bool lng = need && len > kShort;
+    if (need && !lng &&
+        !equal_cell_rep<false>(arena + o0, arena_end, arena + q0, arena_end, len))
+      collided[atomicAdd(n_collided, 1u)] = uint32_t(i);
+    for (unsigned lm = __ballot_sync(0xffffffffu, lng); lm; lm &= lm - 1) {
+      const int src = __ffs(lm) - 1;
+      const uint64_t a = __shfl_sync(0xffffffffu, o0, src);
+      const uint64_t b = __shfl_sync(0xffffffffu, q0, src);
+      const uint64_t l = __shfl_sync(0xffffffffu, len, src);
+      const bool eq = warp_bytes_equal(arena + a, arena + b, l, arena_end, lane);
+      if (int(lane) == src && !eq) collided[atomicAdd(n_collided, 1u)] = uint32_t(i);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K2c collision fix-up (rare path): a cell whose hash slot belongs to a
+// different string keeps probing past that slot with byte verification,
+// claiming or joining slots with the publish/acquire protocol (several
+// colliding cells of the same string may race here).
+// ---------------------------------------------------------------------------
+__global__ void k_dict_fixup(const uint8_t* __restrict__ arena, const uint8_t* arena_end,
+                             const uint64_t* __restrict__ offsets, uint32_t m, uint64_t cap,
+                             const unsigned long long* __restrict__ hashes,
+                             unsigned long long* keys, uint32_t* reps, unsigned long long* repoffs,
+                             const uint32_t* collided, uint32_t n_collided,
+                             uint32_t* slot_of_cell) {
+  for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < n_collided;
+       q += gridDim.x * blockDim.x) {
+    const uint64_t i = collided[q];
+    const uint64_t r = i / m;
+    const uint32_t c = uint32_t(i - r * m);
+    const uint64_t o0 = offsets[i], len = offsets[i + 1] - o0;
+    const uint64_t base = uint64_t(c) * cap;
+    const uint64_t slot = probe_insert<false>(
+        keys + base, reps + base, repoffs + base, cap, hashes[i], (slot_of_cell[i] + 1) & (cap - 1),
+        uint32_t(r), c, m, o0, arena + o0, arena_end, len, arena, arena_end, offsets);
+    slot_of_cell[i] = uint32_t(slot);
   }
 }
 
@@ -257,28 +543,41 @@ __global__ void k_vid(const uint32_t* slot_of_cell, const uint32_t* slot2vid, ui
   }
 }
 
-// Occurrence count per (column, vid): shared-memory privatised histogram for
-// low-cardinality columns, spread global atomics otherwise.
+// Occurrence count per (column, vid), all columns in one pass over the vid
+// matrix: low-cardinality columns are counted in a shared-memory histogram
+// (soff[c] = their bin offset, kSmemBins total), the others with spread
+// global atomics.
 constexpr uint32_t kSmemBins = 12288;
+constexpr uint32_t kLargeCol = 0xFFFFFFFFu;
 
-__global__ void k_count(const uint32_t* vid, uint64_t n, uint32_t m, uint32_t c, uint64_t card,
-                        uint64_t base, uint32_t* count) {
+__global__ void __launch_bounds__(512) k_count(const uint32_t* vid, uint64_t n, uint32_t m,
+                                               const uint32_t* soff, uint32_t nbins,
+                                               const uint64_t* colbase, uint32_t* count) {
   extern __shared__ uint32_t h[];
-  const bool priv = card <= kSmemBins;
-  if (priv)
-    for (uint32_t b = threadIdx.x; b < card; b += blockDim.x) h[b] = 0;
+  for (uint32_t b = threadIdx.x; b < nbins; b += blockDim.x) h[b] = 0;
   __syncthreads();
-  for (uint64_t r = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; r < n;
-       r += uint64_t(gridDim.x) * blockDim.x) {
-    uint32_t v = vid[r * m + c];
-    if (priv) atomicAdd(&h[v], 1u);
-    else atomicAdd(&count[base + v], 1u);
+  const uint64_t total = n * m;
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < total;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    const uint32_t c = uint32_t(i % m);
+    const uint32_t v = vid[i];
+    const uint32_t o = soff[c];
+    if (o != kLargeCol) atomicAdd(&h[o + v], 1u);
+    else atomicAdd(&count[colbase[c] + v], 1u);
   }
-  if (priv) {
-    __syncthreads();
-    for (uint32_t b = threadIdx.x; b < card; b += blockDim.x)
-      if (h[b]) atomicAdd(&count[base + b], h[b]);
-  }
+  __syncthreads();
+  // flush: the small column owning bin b is the one with the largest
+  // offset <= b (columns are few; linear scan)
+  for (uint32_t b = threadIdx.x; b < nbins; b += blockDim.x)
+    if (h[b]) {
+      uint32_t owner = 0, best = 0;
+      for (uint32_t cc = 0; cc < m; ++cc)
+        if (soff[cc] != kLargeCol && soff[cc] <= b && soff[cc] >= best) {
+          best = soff[cc];
+          owner = cc;
+        }
+      atomicAdd(&count[colbase[owner] + (b - soff[owner])], h[b]);
+    }
 }
 
 // Per-column sum of count*vlen (stats.hpp:38), privatised per block in
@@ -403,11 +702,45 @@ void encode(const DeviceTable& t, int tok, int scoring, cudaStream_t s, Encoded&
   keys.zero();
   DevBuf<uint32_t> reps(m * cap, s);
   reps.fill_bytes(0xFF);
+  DevBuf<unsigned long long> repoffs(m * cap, s);
   DevBuf<uint32_t> slot_of_cell(cells, s);
   uint64_t hmask = hash_bits_debug >= 64 ? ~uint64_t(0) : ((uint64_t(1) << hash_bits_debug) - 1);
-  PO_LAUNCH(k_dict_insert, grid_for(cells, 256), 256, 0, s, t.arena, arena_end, t.offsets, n,
-            uint32_t(m), cap, keys.get(), reps.get(), slot_of_cell.get(), hmask);
+  {
+    // K1: hash every cell (tile of cells per block sized so a typical tile's
+    // bytes use about half of a staging buffer)
+    const uint32_t stage = 24 * 1024;
+    const double avg = double(t.arena_bytes) / double(cells);
+    uint32_t tile = 256;
+    while (tile > 8 && avg * tile > stage * 0.6) tile >>= 1;
+    const uint32_t smem = 2 * ((stage + 64 + 127) & ~127u);
+    static bool attr_set = false;
+    if (!attr_set) {
+      PO_CUDA(cudaFuncSetAttribute(k_cell_hash, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   int(smem)));
+      attr_set = true;
+    }
+    const uint64_t ntiles = (cells + tile - 1) / tile;
+    DevBuf<unsigned long long> hashes(cells, s);
+    PO_LAUNCH(k_cell_hash, unsigned(std::min<uint64_t>(ntiles, uint64_t(kSMs) * 4)), kDictBlock,
+              smem, s, t.arena, arena_end, t.offsets, cells, tile, stage, hmask, hashes.get());
+    // K2a/K2b: probe + claim, then byte verification of every duplicate
+    PO_LAUNCH(k_dict_probe, grid_for(cells, 256, 32), 256, 0, s, hashes.get(), t.offsets, cells,
+              uint32_t(m), cap, keys.get(), reps.get(), repoffs.get(), slot_of_cell.get());
+    DevBuf<uint32_t> collided(cells, s), ncol(1, s);
+    ncol.zero();
+    PO_LAUNCH(k_dict_verify, grid_for(cells, 256, 32), 256, 0, s, t.arena, arena_end, t.offsets,
+              cells, uint32_t(m), cap, reps.get(), repoffs.get(), slot_of_cell.get(),
+              collided.get(), ncol.get());
+    uint32_t hcol = 0;
+    ncol.download(&hcol, 1);
+    sync(s);
+    if (hcol)  // K2c: exact resolution of 64-bit hash collisions
+      PO_LAUNCH(k_dict_fixup, grid_for(hcol, 128), 128, 0, s, t.arena, arena_end, t.offsets,
+                uint32_t(m), cap, hashes.get(), keys.get(), reps.get(), repoffs.get(),
+                collided.get(), hcol, slot_of_cell.get());
+  }
 
+  timing_mark("dict", s);
   // Distinct values per column (occupied slots), in column order.
   DevBuf<uint8_t> flags(cap, s);
   DevBuf<uint32_t> sel(cells, s);  // per distinct: slot within its column
@@ -420,8 +753,11 @@ void encode(const DeviceTable& t, int tok, int scoring, cudaStream_t s, Encoded&
   for (uint32_t c = 0; c < m; ++c) {
     PO_LAUNCH(k_occupied, grid_for(cap, 256), 256, 0, s, keys.get() + uint64_t(c) * cap, cap,
               flags.get());
-    PO_CUDA(cub::DeviceSelect::Flagged(tmp.get(), tmp_bytes, it, flags.get(),
-                                       sel.get() + e.colbase[c], nsel.get(), int(cap), s));
+    {
+      ProfScope ps("cub_select", s);
+      PO_CUDA(cub::DeviceSelect::Flagged(tmp.get(), tmp_bytes, it, flags.get(),
+                                         sel.get() + e.colbase[c], nsel.get(), int(cap), s));
+    }
     int k = 0;
     PO_CUDA(cudaMemcpyAsync(&k, nsel.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
     sync(s);
@@ -449,7 +785,9 @@ void encode(const DeviceTable& t, int tok, int scoring, cudaStream_t s, Encoded&
   rk.item_cell_row = d_row.get();
   rk.item_col = d_col.get();
   rk.m = uint32_t(m);
+  timing_mark("distinct", s);
   refine_sort(uint32_t(D), grp.get(), uint32_t(D), rk, raw_pos.get(), s);
+  timing_mark("rank_raw", s);
 
   DevBuf<uint32_t> slot2vid(m * cap, s), col_by_pos(D, s);
   e.rep_row.alloc(D, s);
@@ -468,6 +806,7 @@ void encode(const DeviceTable& t, int tok, int scoring, cudaStream_t s, Encoded&
   ek.item_col = col_by_pos.get();
   DevBuf<uint32_t> esc_pos(D, s);
   refine_sort(uint32_t(D), grp.get(), uint32_t(D), ek, esc_pos.get(), s);
+  timing_mark("rank_esc", s);
   e.esc_rank.alloc(D, s);
   PO_LAUNCH(k_esc_rank, grid_for(D, 256), 256, 0, s, esc_pos.get(), col_by_pos.get(),
             e.d_colbase.get(), D, e.esc_rank.get());
@@ -503,10 +842,17 @@ void encode(const DeviceTable& t, int tok, int scoring, cudaStream_t s, Encoded&
   slot2vid.release();
   e.count.alloc(D, s);
   e.count.zero();
-  for (uint32_t c = 0; c < m; ++c) {
-    size_t smem = e.card[c] <= kSmemBins ? e.card[c] * sizeof(uint32_t) : 0;
-    PO_LAUNCH(k_count, grid_for(n, 512, 4), 512, smem, s, e.vid.get(), n, uint32_t(m), c,
-              e.card[c], e.colbase[c], e.count.get());
+  {
+    std::vector<uint32_t> soff(m, kLargeCol);
+    uint32_t nbins = 0;
+    for (uint32_t c = 0; c < m; ++c)
+      if (nbins + e.card[c] <= kSmemBins) {
+        soff[c] = nbins;
+        nbins += uint32_t(e.card[c]);
+      }
+    auto d_soff = to_device(soff, s);
+    PO_LAUNCH(k_count, grid_for(cells, 512, 2), 512, nbins * sizeof(uint32_t), s, e.vid.get(), n,
+              uint32_t(m), d_soff.get(), nbins, e.d_colbase.get(), e.count.get());
   }
   DevBuf<unsigned long long> tot(m, s);
   tot.zero();
@@ -516,6 +862,7 @@ void encode(const DeviceTable& t, int tok, int scoring, cudaStream_t s, Encoded&
   tot.download(htot.data(), m);
   sync(s);
   for (uint32_t c = 0; c < m; ++c) e.total_len[c] = htot[c];
+  timing_mark("encode_tail", s);
 }
 
 }  // namespace po

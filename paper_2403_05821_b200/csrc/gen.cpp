@@ -234,10 +234,23 @@ const char* pogen_field_name(int config, int f) {
 // Generates rows [row_begin, row_begin + n_rows) of config `config`.
 // Pass 1 (arena == NULL): fills offsets (n_rows*m + 1, starting at 0) and
 // returns the arena size. Pass 2: writes the bytes. Returns -1 on bad config.
+long long pogen_generate_cols(int config, uint64_t seed, uint64_t row_begin, uint64_t n_rows,
+                              uint64_t colmask, uint64_t* offsets, uint8_t* arena, int n_threads);
+
 long long pogen_generate(int config, uint64_t seed, uint64_t row_begin, uint64_t n_rows,
                          uint64_t* offsets, uint8_t* arena, int n_threads) {
+  return pogen_generate_cols(config, seed, row_begin, n_rows, ~0ull, offsets, arena, n_threads);
+}
+
+// Same as pogen_generate restricted to the columns whose bit is set in
+// colmask (value ids still come from the full row, so FDs are preserved).
+long long pogen_generate_cols(int config, uint64_t seed, uint64_t row_begin, uint64_t n_rows,
+                              uint64_t colmask, uint64_t* offsets, uint8_t* arena, int n_threads) {
   Gen g(config, seed);
-  const int m = int(g.cfg.cols.size());
+  std::vector<int> sel;
+  for (int c = 0; c < int(g.cfg.cols.size()); ++c)
+    if ((colmask >> c) & 1) sel.push_back(c);
+  const int m = int(sel.size());
   if (m == 0) return -1;
   if (n_threads <= 0) n_threads = int(std::max(1u, std::thread::hardware_concurrency()));
   n_threads = int(std::min<uint64_t>(uint64_t(n_threads), std::max<uint64_t>(1, n_rows / 1024 + 1)));
@@ -249,9 +262,9 @@ long long pogen_generate(int config, uint64_t seed, uint64_t row_begin, uint64_t
       uint64_t lo = n_rows * t / n_threads, hi = n_rows * (t + 1) / n_threads;
       for (uint64_t i = lo; i < hi; ++i) {
         uint64_t r = g.source_row(row_begin + i);
-        for (int c = 0; c < m; ++c) {
-          g.text(c, g.value_id(c, r), s);
-          offsets[i * m + c + 1] = s.size();
+        for (int k = 0; k < m; ++k) {
+          g.text(sel[k], g.value_id(sel[k], r), s);
+          offsets[i * m + k + 1] = s.size();
         }
       }
     };
@@ -266,9 +279,9 @@ long long pogen_generate(int config, uint64_t seed, uint64_t row_begin, uint64_t
     uint64_t lo = n_rows * t / n_threads, hi = n_rows * (t + 1) / n_threads;
     for (uint64_t i = lo; i < hi; ++i) {
       uint64_t r = g.source_row(row_begin + i);
-      for (int c = 0; c < m; ++c) {
-        g.text(c, g.value_id(c, r), s);
-        std::memcpy(arena + offsets[i * m + c], s.data(), s.size());
+      for (int k = 0; k < m; ++k) {
+        g.text(sel[k], g.value_id(sel[k], r), s);
+        std::memcpy(arena + offsets[i * m + k], s.data(), s.size());
       }
     }
   };

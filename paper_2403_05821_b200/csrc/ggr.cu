@@ -158,9 +158,22 @@ struct ScanSlot {
 
 struct WorkItem {
   uint32_t slot;
-  uint32_t pad;
+  uint32_t col;  // dense tables: the one column of [lo, hi); hashed: kAnyCol
   uint64_t lo, hi;
 };
+
+constexpr uint32_t kAnyCol = 0xFFFFFFFFu;
+
+__device__ __forceinline__ bool decode_work(const WorkItem& w, const TDesc& t,
+                                            const uint64_t* colbase, uint32_t m, uint64_t e,
+                                            uint32_t& c, uint32_t& v) {
+  if (w.col != kAnyCol) {
+    c = w.col;
+    v = uint32_t(e - colbase[c]);
+    return true;
+  }
+  return decode_entry(t, colbase, m, e, c, v);
+}
 
 constexpr int kArgBlock = 256;
 
@@ -181,7 +194,7 @@ __global__ void __launch_bounds__(kArgBlock) k_argmax(
   unsigned long long ncand = 0;
   for (uint64_t e = w.lo + threadIdx.x; e < w.hi; e += blockDim.x) {
     uint32_t c, v;
-    if (!decode_entry(sl.t, colbase, m, e, c, v)) continue;
+    if (!decode_work(w, sl.t, colbase, m, e, c, v)) continue;
     const uint32_t cnt = sl.t.cnt[e];
     if (cnt == 0 || !mask_has(mask, c)) continue;
     ++ncand;
@@ -417,14 +430,35 @@ __global__ void k_root_psum(const uint32_t* vid, uint64_t n, uint32_t m, uint32_
 // ---------------------------------------------------------------------------
 // K7 leaf_stats: per (leaf, column) distinct count and length sum
 // ---------------------------------------------------------------------------
-__global__ void k_leaf_stats(const WorkItem* work, const ScanSlot* slots, const uint32_t* masks,
-                             const uint64_t* colbase, const uint64_t* vlen, uint32_t m,
-                             unsigned long long* card, unsigned long long* tot) {
-  extern __shared__ unsigned long long sh[];  // [2*m] when m is small
-  const bool priv = m <= 2048;
+__global__ void __launch_bounds__(256) k_leaf_stats(
+    const WorkItem* work, const ScanSlot* slots, const uint32_t* masks, const uint64_t* colbase,
+    const uint64_t* vlen, uint32_t m, unsigned long long* card, unsigned long long* tot) {
+  extern __shared__ unsigned long long sh[];  // [2*m] for hashed tables with small m
   const WorkItem w = work[blockIdx.x];
   const ScanSlot sl = slots[w.slot];
   const uint32_t* mask = masks + sl.mask_off;
+  if (w.col != kAnyCol) {
+    // dense table, one column: per-thread sums, one atomic pair per block
+    const uint32_t c = w.col;
+    unsigned long long k = 0, l = 0;
+    for (uint64_t e = w.lo + threadIdx.x; e < w.hi; e += blockDim.x) {
+      const uint32_t cnt = sl.t.cnt[e];
+      if (cnt) {
+        ++k;
+        l += uint64_t(cnt) * vlen[e];
+      }
+    }
+    typedef cub::BlockReduce<unsigned long long, 256> BR;
+    __shared__ typename BR::TempStorage t1, t2;
+    k = BR(t1).Sum(k);
+    l = BR(t2).Sum(l);
+    if (threadIdx.x == 0 && k) {
+      atomicAdd(&card[uint64_t(w.slot) * m + c], k);
+      atomicAdd(&tot[uint64_t(w.slot) * m + c], l);
+    }
+    return;
+  }
+  const bool priv = m <= 2048;
   if (priv)
     for (uint32_t c = threadIdx.x; c < 2 * m; c += blockDim.x) sh[c] = 0;
   __syncthreads();
@@ -614,6 +648,19 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
   };
   ensure_split_map(1024);
 
+  // Work items over a node's table: dense tables are cut at column
+  // boundaries (only the node's active columns), hashed ones in plain chunks.
+  auto add_work = [&](std::vector<WorkItem>& work, uint32_t slot, const HTable& t,
+                      const std::vector<int>& cols) {
+    if (t.dense) {
+      for (int c : cols)
+        for (uint64_t lo = e.colbase[c]; lo < e.colbase[c + 1]; lo += kWorkChunk)
+          work.push_back(WorkItem{slot, uint32_t(c), lo, std::min(e.colbase[c + 1], lo + kWorkChunk)});
+    } else {
+      for (uint64_t lo = 0; lo < t.cap; lo += kWorkChunk)
+        work.push_back(WorkItem{slot, kAnyCol, lo, std::min(t.cap, lo + kWorkChunk)});
+    }
+  };
   auto col_mask = [&](const std::vector<int>& cols, std::vector<uint32_t>& dst) {
     uint32_t off = uint32_t(dst.size());
     dst.resize(dst.size() + W, 0);
@@ -649,8 +696,7 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
       sl.mask_off = col_mask(nd.cols, L.masks);
       sl.w_off = 0;
       L.slots.push_back(sl);
-      for (uint64_t lo = 0; lo < nd.table->cap; lo += kWorkChunk)
-        L.work.push_back(WorkItem{uint32_t(i), 0, lo, std::min(nd.table->cap, lo + kWorkChunk)});
+      add_work(L.work, uint32_t(i), *nd.table, nd.cols);
     }
     auto d_slots = to_device(L.slots, s);
     auto d_masks = to_device(L.masks, s);
@@ -700,8 +746,7 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
         for (size_t k = 0; k < dpart[c].size(); ++k)
           if (act[dpart[c][k]]) L.weights[sl.w_off + c * K + k] = 1;
       L.slots.push_back(sl);
-      for (uint64_t lo = 0; lo < nd.table->cap; lo += kWorkChunk)
-        L.work.push_back(WorkItem{uint32_t(i), 0, lo, std::min(nd.table->cap, lo + kWorkChunk)});
+      add_work(L.work, uint32_t(i), *nd.table, nd.cols);
       L.slot_work_off.push_back(uint32_t(L.work.size()));
     }
     const uint32_t nslots = uint32_t(L.slots.size());
@@ -883,6 +928,7 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
       }
       if (hh[nodes.size()]) fprintf(stderr, "[po debug] %llu rows with invalid node\n", hh[nodes.size()]);
     }
+    timing_mark("levels", s);
     frontier.swap(next);
   }
 
@@ -985,7 +1031,9 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
   RK.key_field = d_kf.get();
   RK.key_kind = d_kk.get();
   RK.key_bits = d_kb.get();
+  timing_mark("layout", s);
   refine_sort(uint32_t(n), grp.get(), uint32_t(n), RK, pos.get(), s);
+  timing_mark("leaf_sort", s);
   if (debug_checks()) {
     DevBuf<unsigned> seen(n, s);
     DevBuf<unsigned long long> bad(1, s);
@@ -1031,6 +1079,7 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
     throw;
   }
 
+  timing_mark("emit_phc", s);
   // ---- whole-table fallback competition (ggr.hpp:379-387) ----
   std::vector<double> avg(m);
   for (uint32_t c = 0; c < m; ++c)
@@ -1038,6 +1087,7 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
   std::vector<int> fb_order = hitcount_order(n, e.card, avg, cfg.stats_variant);
   DevBuf<uint32_t> fb_perm(n, s);
   sort_all_rows(e, fb_order, fb_perm.get(), s);
+  timing_mark("fallback_sort", s);
   std::vector<int32_t> fo(fb_order.begin(), fb_order.end());
   auto d_fo = to_device(fo, s);
   uint64_t fb_phc = 0;
@@ -1056,6 +1106,7 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
             (unsigned long long)bad, (unsigned long long)dup);
     throw;
   }
+  timing_mark("fallback_phc", s);
   if (fb_phc > out.phc) {
     PO_CUDA(cudaMemcpyAsync(d_rows, fb_perm.get(), n * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
     PO_LAUNCH(k_tile_order, grid_for(n * m, 256), 256, 0, s, d_fo.get(), n, m, d_orders);

@@ -204,24 +204,33 @@ void refine_sort(uint32_t n_items, const uint32_t* d_grp_init, uint32_t grp_max,
     PO_LAUNCH(k_build_keys, grid_for(A, 256), 256, 0, s, items.get(), grp.get(), A, k, key,
               keys.get());
     size_t b = tb;
-    PO_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(), b, keys.get(), keys2.get(), items.get(),
-                                            items2.get(), A, 0, end_bit, s));
+    {
+      ProfScope ps("cub_radix_sort", s);
+      PO_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(), b, keys.get(), keys2.get(), items.get(),
+                                              items2.get(), A, 0, end_bit, s));
+    }
     PO_LAUNCH(k_marks, grid_for(A, 256), 256, 0, s, keys2.get(), A, key.chunk_bits, gmark.get(),
               rmark.get());
-    b = tb;
-    PO_CUDA(cub::DeviceScan::InclusiveScan(tmp.get(), b, gmark.get(), gstart.get(), cub::Max(),
-                                           A, s));
-    b = tb;
-    PO_CUDA(cub::DeviceScan::InclusiveScan(tmp.get(), b, rmark.get(), rstart.get(), cub::Max(),
-                                           A, s));
+    {
+      ProfScope ps("cub_scan", s);
+      b = tb;
+      PO_CUDA(cub::DeviceScan::InclusiveScan(tmp.get(), b, gmark.get(), gstart.get(), cub::Max(),
+                                             A, s));
+      b = tb;
+      PO_CUDA(cub::DeviceScan::InclusiveScan(tmp.get(), b, rmark.get(), rstart.get(), cub::Max(),
+                                             A, s));
+    }
     PO_LAUNCH(k_resolve, grid_for(A, 256), 256, 0, s, keys2.get(), items2.get(), gstart.get(),
               rstart.get(), A, k, key, d_out_pos, keep.get(), grp2.get());
-    b = tb;
-    PO_CUDA(cub::DeviceSelect::Flagged(tmp.get(), b, items2.get(), keep.get(), items.get(),
-                                       nsel.get(), A, s));
-    b = tb;
-    PO_CUDA(cub::DeviceSelect::Flagged(tmp.get(), b, grp2.get(), keep.get(), grp.get(),
-                                       nsel.get(), A, s));
+    {
+      ProfScope ps("cub_select", s);
+      b = tb;
+      PO_CUDA(cub::DeviceSelect::Flagged(tmp.get(), b, items2.get(), keep.get(), items.get(),
+                                         nsel.get(), A, s));
+      b = tb;
+      PO_CUDA(cub::DeviceSelect::Flagged(tmp.get(), b, grp2.get(), keep.get(), grp.get(),
+                                         nsel.get(), A, s));
+    }
     int na = 0;
     PO_CUDA(cudaMemcpyAsync(&na, nsel.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
     sync(s);
