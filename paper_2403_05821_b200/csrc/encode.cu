@@ -172,28 +172,23 @@ __device__ __forceinline__ uint64_t smem_word(const uint64_t* s64, uint32_t off)
 constexpr uint32_t kDictBlock = 256;
 
 // ---------------------------------------------------------------------------
-// K1 cell_scan: tile-staged, load-balanced hashing of every cell.
-// A block takes a tile of up to 256 consecutive cells (contiguous bytes in the
-// row-major arena); one elected thread streams the tile's 16-byte-aligned
-// byte range into shared memory with a TMA bulk copy (double-buffered: the
-// next tile is in flight while this one is hashed). The tile's 8-byte words
-// (relative to each cell's start) are split evenly over the 256 threads
-// whatever the cell lengths; per-cell partial sums are folded in shared
-// memory. Output: the 64-bit hash of every cell. Tiles larger than a staging
-// buffer are hashed from global memory by one thread per cell (same hash).
+// K1 cell_scan: tile-staged hashing of every cell.
+// A block takes a tile of whole rows (rows_per_tile * m <= 256 cells, one per
+// thread); one elected thread streams the tile's 16-byte-aligned byte range
+// into shared memory with a TMA bulk copy, double-buffered so the next tile
+// is in flight while this one is hashed. Threads take the tile's cells in
+// column-major order, so the 32 lanes of a warp hash cells of the same
+// column (similar lengths: little divergence) out of shared memory. Output:
+// the 64-bit hash of every cell. A tile larger than a staging buffer is
+// hashed from global memory (same hash).
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kDictBlock) k_cell_hash(
     const uint8_t* __restrict__ arena, const uint8_t* arena_end,
-    const uint64_t* __restrict__ offsets, uint64_t total, uint32_t tile, uint32_t stage_bytes,
-    uint64_t hash_mask, unsigned long long* __restrict__ hashes) {
+    const uint64_t* __restrict__ offsets, uint64_t total, uint32_t m, uint32_t rows_per_tile,
+    uint32_t stage_bytes, uint64_t hash_mask, unsigned long long* __restrict__ hashes) {
   extern __shared__ __align__(128) uint8_t sbuf_all[];
-  typedef cub::BlockScan<uint32_t, kDictBlock> Scan;
-  __shared__ typename Scan::TempStorage scan_tmp;
-  __shared__ uint32_t s_wstart[kDictBlock + 1];
-  __shared__ uint32_t s_off[kDictBlock];
-  __shared__ uint32_t s_len[kDictBlock];
-  __shared__ unsigned long long s_hash[kDictBlock];
   __shared__ __align__(8) uint64_t s_bar[2];
+  const uint32_t tile = rows_per_tile * m;  // cells per tile
   const uint32_t buf_bytes = (stage_bytes + 64 + 127) & ~127u;
   const uint64_t ntiles = (total + tile - 1) / tile;
   const uint32_t tid = threadIdx.x;
@@ -219,78 +214,46 @@ __global__ void __launch_bounds__(kDictBlock) k_cell_hash(
   }
   __syncthreads();
   if (tid == 0 && blockIdx.x < ntiles) issue(blockIdx.x, 0);
+  // column-major position of this thread inside a tile
+  const uint32_t col = tid / rows_per_tile, row = tid - col * rows_per_tile;
+  const bool active = tid < tile;
   uint32_t uses[2] = {0u, 0u};
   uint32_t kiter = 0;
   for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++kiter) {
     const int bsel = int(kiter & 1);
-    const uint64_t* s64 = reinterpret_cast<const uint64_t*>(sbuf_all + bsel * buf_bytes);
-    const uint64_t i0 = t * tile;
-    const uint32_t cnt = uint32_t(total - i0 < tile ? total - i0 : tile);
+    const uint8_t* sb = sbuf_all + bsel * buf_bytes;
     uintptr_t gA0, gB1;
     tile_range(t, gA0, gB1);
     const bool staged = gB1 - gA0 <= stage_bytes;
     if (tid == 0 && t + gridDim.x < ntiles) issue(t + gridDim.x, bsel ^ 1);
-    const uint64_t i = i0 + tid;
-    const bool mine = tid < cnt;
+    const uint64_t i = t * tile + uint64_t(row) * m + col;
+    const bool mine = active && i < total;
     const uint64_t o0 = mine ? offsets[i] : 0;
     const uint64_t len = mine ? offsets[i + 1] - o0 : 0;
-    if (!staged) {
+    if (staged) {
+      mbar_wait(&s_bar[bsel], uses[bsel] & 1u);
+      ++uses[bsel];
       if (mine) {
-        uint64_t h = hash_cell<false>(arena + o0, len, arena_end) & hash_mask;
+        const uint8_t* cell = sb + (reinterpret_cast<uintptr_t>(arena + o0) - gA0);
+        const uint64_t h = hash_cell<true>(cell, len, sb + (gB1 - gA0) + 16) & hash_mask;
         hashes[i] = h ? h : 1;
       }
-      __syncthreads();
-      continue;
-    }
-    const uint32_t words = mine ? uint32_t((len + 7) / 8) : 0;
-    uint32_t wstart, total_words;
-    Scan(scan_tmp).ExclusiveSum(words, wstart, total_words);
-    s_wstart[tid] = wstart;
-    if (tid == 0) s_wstart[kDictBlock] = total_words;
-    s_off[tid] = mine ? uint32_t(reinterpret_cast<uintptr_t>(arena + o0) - gA0) : 0;
-    s_len[tid] = uint32_t(len);
-    s_hash[tid] = 0;
-    mbar_wait(&s_bar[bsel], uses[bsel] & 1u);
-    ++uses[bsel];
-    __syncthreads();
-    const uint32_t per = (total_words + kDictBlock - 1) / kDictBlock;
-    const uint32_t w0 = min(total_words, tid * per), w1 = min(total_words, w0 + per);
-    if (w0 < w1) {
-      uint32_t lo = 0, hi = kDictBlock;  // last cell with wstart <= w0
-      while (hi - lo > 1) {
-        const uint32_t mid = (lo + hi) >> 1;
-        if (s_wstart[mid] <= w0) lo = mid;
-        else hi = mid;
-      }
-      uint32_t cc = lo;
-      while (s_wstart[cc + 1] <= w0) ++cc;
-      uint32_t cend = s_wstart[cc + 1], cbase = s_wstart[cc], coff = s_off[cc], clen = s_len[cc];
-      unsigned long long part = 0;
-      for (uint32_t g = w0; g < w1; ++g) {
-        if (g >= cend) {
-          if (part) atomicAdd(&s_hash[cc], part);
-          part = 0;
-          do {
-            ++cc;
-          } while (g >= s_wstart[cc + 1]);
-          cend = s_wstart[cc + 1];
-          cbase = s_wstart[cc];
-          coff = s_off[cc];
-          clen = s_len[cc];
-        }
-        const uint32_t k = g - cbase;
-        uint64_t w = smem_word(s64, coff + 8 * k);
-        const uint32_t rem = clen - 8 * k;
-        if (rem < 8) w = mask_low_bytes(w, rem);
-        part += word_term(w, k);
-      }
-      if (part) atomicAdd(&s_hash[cc], part);
-    }
-    __syncthreads();
-    if (mine) {
-      const uint64_t h = hash_finish(s_hash[tid], len) & hash_mask;
+    } else if (mine) {
+      const uint64_t h = hash_cell<false>(arena + o0, len, arena_end) & hash_mask;
       hashes[i] = h ? h : 1;
     }
+    __syncthreads();  // buffer bsel is refilled by the next-but-one issue
+  }
+}
+
+__global__ void k_cell_hash_global(const uint8_t* __restrict__ arena, const uint8_t* arena_end,
+                                   const uint64_t* __restrict__ offsets, uint64_t total,
+                                   uint64_t hash_mask, unsigned long long* __restrict__ hashes) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < total;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t o0 = offsets[i];
+    const uint64_t h = hash_cell<false>(arena + o0, offsets[i + 1] - o0, arena_end) & hash_mask;
+    hashes[i] = h ? h : 1;
   }
 }
 
@@ -420,13 +383,15 @@ __global__ void k_occupied(const unsigned long long* keys, uint64_t cap, uint8_t
     flags[i] = keys[i] != 0;
 }
 
-__global__ void k_distinct_info(const uint32_t* sel_slot, uint64_t cnt, uint64_t base, uint32_t c,
-                                uint64_t cap, const uint32_t* reps, uint32_t* d_col,
-                                uint32_t* d_row) {
+__global__ void k_distinct_info(const uint32_t* col_sel, uint64_t cnt, uint64_t base, uint32_t c,
+                                uint64_t cap, const uint32_t* reps, uint32_t* sel_slot,
+                                uint32_t* d_col, uint32_t* d_row) {
   for (uint64_t d = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; d < cnt;
        d += uint64_t(gridDim.x) * blockDim.x) {
+    const uint32_t slot = col_sel[d];
+    sel_slot[base + d] = slot;
     d_col[base + d] = c;
-    d_row[base + d] = reps[uint64_t(c) * cap + sel_slot[base + d]];
+    d_row[base + d] = reps[uint64_t(c) * cap + slot];
   }
 }
 
@@ -437,26 +402,22 @@ __global__ void k_grp_from_col(const uint32_t* col, const uint64_t* colbase, uin
     grp[d] = uint32_t(colbase[col[d]]);
 }
 
-// raw_pos[d] -> vid; scatter representative row / column into position order.
-__global__ void k_scatter_raw(const uint32_t* raw_pos, const uint32_t* d_col, const uint32_t* d_row,
+// raw_pos[d] -> vid; scatter representative row / column / escaped rank
+// into raw (vid) order.
+__global__ void k_scatter_raw(const uint32_t* raw_pos, const uint32_t* esc_pos,
+                              const uint32_t* d_col, const uint32_t* d_row,
                               const uint32_t* sel_slot, const uint64_t* colbase, uint64_t D,
                               uint64_t cap, uint32_t* slot2vid, uint32_t* row_by_pos,
-                              uint32_t* col_by_pos) {
+                              uint32_t* col_by_pos, uint32_t* esc_rank) {
   for (uint64_t d = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; d < D;
        d += uint64_t(gridDim.x) * blockDim.x) {
-    uint32_t p = raw_pos[d];
-    uint32_t c = d_col[d];
+    const uint32_t p = raw_pos[d];
+    const uint32_t c = d_col[d];
     slot2vid[uint64_t(c) * cap + sel_slot[d]] = uint32_t(p - colbase[c]);
     row_by_pos[p] = d_row[d];
     col_by_pos[p] = c;
+    esc_rank[p] = uint32_t(esc_pos[d] - colbase[c]);
   }
-}
-
-__global__ void k_esc_rank(const uint32_t* esc_pos, const uint32_t* col_by_pos,
-                           const uint64_t* colbase, uint64_t D, uint32_t* esc_rank) {
-  for (uint64_t p = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; p < D;
-       p += uint64_t(gridDim.x) * blockDim.x)
-    esc_rank[p] = uint32_t(esc_pos[p] - colbase[col_by_pos[p]]);
 }
 
 __device__ __forceinline__ bool is_ws(uint8_t c) {
@@ -706,12 +667,12 @@ void encode(const DeviceTable& t, int tok, int scoring, cudaStream_t s, Encoded&
   DevBuf<uint32_t> slot_of_cell(cells, s);
   uint64_t hmask = hash_bits_debug >= 64 ? ~uint64_t(0) : ((uint64_t(1) << hash_bits_debug) - 1);
   {
-    // K1: hash every cell (tile of cells per block sized so a typical tile's
-    // bytes use about half of a staging buffer)
-    const uint32_t stage = 24 * 1024;
-    const double avg = double(t.arena_bytes) / double(cells);
-    uint32_t tile = 256;
-    while (tile > 8 && avg * tile > stage * 0.6) tile >>= 1;
+    // K1: hash every cell. Tiles of whole rows sized so a typical tile uses
+    // about 60% of a staging buffer.
+    const uint32_t stage = 32 * 1024;
+    const double row_bytes = double(t.arena_bytes) / double(n);
+    uint32_t rows_per_tile = std::max<uint32_t>(1, kDictBlock / uint32_t(m));
+    while (rows_per_tile > 1 && row_bytes * rows_per_tile > stage * 0.6) rows_per_tile >>= 1;
     const uint32_t smem = 2 * ((stage + 64 + 127) & ~127u);
     static bool attr_set = false;
     if (!attr_set) {
@@ -719,10 +680,16 @@ void encode(const DeviceTable& t, int tok, int scoring, cudaStream_t s, Encoded&
                                    int(smem)));
       attr_set = true;
     }
-    const uint64_t ntiles = (cells + tile - 1) / tile;
     DevBuf<unsigned long long> hashes(cells, s);
-    PO_LAUNCH(k_cell_hash, unsigned(std::min<uint64_t>(ntiles, uint64_t(kSMs) * 4)), kDictBlock,
-              smem, s, t.arena, arena_end, t.offsets, cells, tile, stage, hmask, hashes.get());
+    if (m <= kDictBlock) {
+      const uint64_t ntiles = (cells + rows_per_tile * m - 1) / (rows_per_tile * m);
+      PO_LAUNCH(k_cell_hash, unsigned(std::min<uint64_t>(ntiles, uint64_t(kSMs) * 3)), kDictBlock,
+                smem, s, t.arena, arena_end, t.offsets, cells, uint32_t(m), rows_per_tile, stage,
+                hmask, hashes.get());
+    } else {  // very wide rows: one thread per cell straight from global memory
+      PO_LAUNCH(k_cell_hash_global, grid_for(cells, 256, 16), 256, 0, s, t.arena, arena_end,
+                t.offsets, cells, hmask, hashes.get());
+    }
     // K2a/K2b: probe + claim, then byte verification of every duplicate
     PO_LAUNCH(k_dict_probe, grid_for(cells, 256, 32), 256, 0, s, hashes.get(), t.offsets, cells,
               uint32_t(m), cap, keys.get(), reps.get(), repoffs.get(), slot_of_cell.get());
@@ -741,37 +708,45 @@ void encode(const DeviceTable& t, int tok, int scoring, cudaStream_t s, Encoded&
   }
 
   timing_mark("dict", s);
-  // Distinct values per column (occupied slots), in column order.
+  // Distinct values per column (occupied slots): every column is compacted
+  // into its own region of `stage` without host round trips, then one D2H of
+  // the m counts gives the cardinalities and the packed layout.
   DevBuf<uint8_t> flags(cap, s);
-  DevBuf<uint32_t> sel(cells, s);  // per distinct: slot within its column
-  DevBuf<int> nsel(1, s);
+  DevBuf<uint32_t> stage_sel(m * cap, s);
+  DevBuf<int> nsel(m, s);
   size_t tmp_bytes = 0;
   cub::CountingInputIterator<uint32_t> it(0);
-  PO_CUDA(cub::DeviceSelect::Flagged(nullptr, tmp_bytes, it, flags.get(), sel.get(), nsel.get(),
-                                     int(cap), s));
+  PO_CUDA(cub::DeviceSelect::Flagged(nullptr, tmp_bytes, it, flags.get(), stage_sel.get(),
+                                     nsel.get(), int(cap), s));
   DevBuf<uint8_t> tmp(tmp_bytes, s);
   for (uint32_t c = 0; c < m; ++c) {
     PO_LAUNCH(k_occupied, grid_for(cap, 256), 256, 0, s, keys.get() + uint64_t(c) * cap, cap,
               flags.get());
-    {
-      ProfScope ps("cub_select", s);
-      PO_CUDA(cub::DeviceSelect::Flagged(tmp.get(), tmp_bytes, it, flags.get(),
-                                         sel.get() + e.colbase[c], nsel.get(), int(cap), s));
-    }
-    int k = 0;
-    PO_CUDA(cudaMemcpyAsync(&k, nsel.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
+    ProfScope ps("cub_select", s);
+    PO_CUDA(cub::DeviceSelect::Flagged(tmp.get(), tmp_bytes, it, flags.get(),
+                                       stage_sel.get() + uint64_t(c) * cap, nsel.get() + c,
+                                       int(cap), s));
+  }
+  {
+    std::vector<int> hk(m);
+    nsel.download(hk.data(), m);  // pageable D2H: completes before returning
     sync(s);
-    e.card[c] = uint64_t(k);
-    e.colbase[c + 1] = e.colbase[c] + uint64_t(k);
+    for (uint32_t c = 0; c < m; ++c) {
+      e.card[c] = uint64_t(hk[c]);
+      e.colbase[c + 1] = e.colbase[c] + uint64_t(hk[c]);
+    }
   }
   e.D = e.colbase[m];
   const uint64_t D = e.D;
   e.d_colbase = to_device(e.colbase, s);
 
+  DevBuf<uint32_t> sel(D, s);  // per distinct (column order): slot within its column
   DevBuf<uint32_t> d_col(D, s), d_row(D, s);
   for (uint32_t c = 0; c < m; ++c)
-    PO_LAUNCH(k_distinct_info, grid_for(e.card[c], 256), 256, 0, s, sel.get(), e.card[c],
-              e.colbase[c], c, cap, reps.get(), d_col.get(), d_row.get());
+    PO_LAUNCH(k_distinct_info, grid_for(e.card[c], 256), 256, 0, s,
+              stage_sel.get() + uint64_t(c) * cap, e.card[c], e.colbase[c], c, cap, reps.get(),
+              sel.get(), d_col.get(), d_row.get());
+  stage_sel.release();
 
   // Raw-byte order of the distinct values of each column -> vid.
   DevBuf<uint32_t> grp(D, s), raw_pos(D, s);
@@ -786,30 +761,38 @@ void encode(const DeviceTable& t, int tok, int scoring, cudaStream_t s, Encoded&
   rk.item_col = d_col.get();
   rk.m = uint32_t(m);
   timing_mark("distinct", s);
-  refine_sort(uint32_t(D), grp.get(), uint32_t(D), rk, raw_pos.get(), s);
-  timing_mark("rank_raw", s);
+  // Escaped fragment-key order (json_escape(v) + '"') of the same items; both
+  // rank sorts advance in lockstep.
+  RefineKey ek = rk;
+  ek.kind = 1;
+  DevBuf<uint32_t> esc_pos(D, s);
+  {
+    // round 0 groups the distinct values by column index
+    std::vector<uint32_t> cb32(m);
+    for (uint32_t c = 0; c < m; ++c) cb32[c] = uint32_t(e.colbase[c]);
+    DevBuf<uint32_t> d_cb32 = to_device(cb32, s);
+    RefineJob jr, je;
+    jr.n_items = je.n_items = uint32_t(D);
+    jr.d_grp_init = je.d_grp_init = d_col.get();
+    jr.d_grp_start = je.d_grp_start = d_cb32.get();
+    jr.n_groups = je.n_groups = uint32_t(m);
+    jr.grp_max = je.grp_max = uint32_t(D);
+    jr.key = rk;
+    je.key = ek;
+    jr.d_out_pos = raw_pos.get();
+    je.d_out_pos = esc_pos.get();
+    refine_sort_multi({jr, je}, s);
+  }
+  timing_mark("rank_sorts", s);
 
   DevBuf<uint32_t> slot2vid(m * cap, s), col_by_pos(D, s);
   e.rep_row.alloc(D, s);
-  PO_LAUNCH(k_scatter_raw, grid_for(D, 256), 256, 0, s, raw_pos.get(), d_col.get(), d_row.get(),
-            sel.get(), e.d_colbase.get(), D, cap, slot2vid.get(), e.rep_row.get(),
-            col_by_pos.get());
+  e.esc_rank.alloc(D, s);
+  PO_LAUNCH(k_scatter_raw, grid_for(D, 256), 256, 0, s, raw_pos.get(), esc_pos.get(), d_col.get(),
+            d_row.get(), sel.get(), e.d_colbase.get(), D, cap, slot2vid.get(), e.rep_row.get(),
+            col_by_pos.get(), e.esc_rank.get());
   keys.release();
   flags.release();
-
-  // Escaped fragment-key order (json_escape(v) + '"') -> esc_rank.
-  PO_LAUNCH(k_grp_from_col, grid_for(D, 256), 256, 0, s, col_by_pos.get(), e.d_colbase.get(), D,
-            grp.get());
-  RefineKey ek = rk;
-  ek.kind = 1;
-  ek.item_cell_row = e.rep_row.get();
-  ek.item_col = col_by_pos.get();
-  DevBuf<uint32_t> esc_pos(D, s);
-  refine_sort(uint32_t(D), grp.get(), uint32_t(D), ek, esc_pos.get(), s);
-  timing_mark("rank_esc", s);
-  e.esc_rank.alloc(D, s);
-  PO_LAUNCH(k_esc_rank, grid_for(D, 256), 256, 0, s, esc_pos.get(), col_by_pos.get(),
-            e.d_colbase.get(), D, e.esc_rank.get());
 
   // Segment length per distinct value.
   std::vector<uint64_t> nchar(m), nword(m);

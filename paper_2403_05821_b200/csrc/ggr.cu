@@ -28,6 +28,7 @@
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <memory>
 #include <numeric>
 
@@ -567,6 +568,18 @@ struct Level {
   std::vector<uint32_t> slot_work_off{0};
 };
 
+// Per-level device upload: every small array of a level in one H2D copy.
+struct Pack {
+  std::vector<uint8_t> host;
+  template <class T>
+  size_t add(const std::vector<T>& v) {
+    size_t off = (host.size() + 15) & ~size_t(15);
+    host.resize(off + std::max<size_t>(1, v.size()) * sizeof(T), 0);
+    if (!v.empty()) std::memcpy(host.data() + off, v.data(), v.size() * sizeof(T));
+    return off;
+  }
+};
+
 }  // namespace
 
 void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups,
@@ -685,31 +698,18 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
     nodes[0].table = t;
   }
 
-  // Leaf statistics for nodes that fall back (FALLBACK kind with a table).
-  auto run_leaf_stats = [&](const std::vector<int>& leaves) {
-    if (leaves.empty()) return;
-    Level L;
-    for (size_t i = 0; i < leaves.size(); ++i) {
-      const Node& nd = nodes[leaves[i]];
-      ScanSlot sl;
-      sl.t = nd.table->desc();
-      sl.mask_off = col_mask(nd.cols, L.masks);
-      sl.w_off = 0;
-      L.slots.push_back(sl);
-      add_work(L.work, uint32_t(i), *nd.table, nd.cols);
-    }
-    auto d_slots = to_device(L.slots, s);
-    auto d_masks = to_device(L.masks, s);
-    auto d_work = to_device(L.work, s);
-    DevBuf<unsigned long long> card(leaves.size() * m, s), tot(leaves.size() * m, s);
-    card.zero();
-    tot.zero();
-    PO_LAUNCH(k_leaf_stats, unsigned(L.work.size()), 256, m <= 2048 ? 16 * m : 0, s, d_work.get(), d_slots.get(),
-              d_masks.get(), colbase, vlen, m, card.get(), tot.get());
-    std::vector<unsigned long long> hc(leaves.size() * m), ht(leaves.size() * m);
-    card.download(hc.data(), hc.size());
-    tot.download(ht.data(), ht.size());
-    sync(s);
+  DevBuf<uint8_t> pack_dev;
+  auto upload = [&](Pack& pk) -> uint8_t* {
+    pack_dev.alloc(pk.host.size(), s);
+    pack_dev.upload(pk.host.data(), pk.host.size());
+    return pack_dev.get();
+  };
+
+  // Leaf statistics -> stats-ranked field order of a fallback leaf
+  // (ggr.hpp:319-338). hc/ht: per (leaf slot, column) distinct count and
+  // length sum.
+  auto finish_leaves = [&](const std::vector<int>& leaves, const unsigned long long* hc,
+                           const unsigned long long* ht) {
     for (size_t i = 0; i < leaves.size(); ++i) {
       Node& nd = nodes[leaves[i]];
       std::vector<uint64_t> cc(nd.cols.size());
@@ -718,7 +718,6 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
         cc[k] = hc[i * m + nd.cols[k]];
         avg[k] = static_cast<double>(ht[i * m + nd.cols[k]]) / static_cast<double>(nd.size);
       }
-      // fallback (ggr.hpp:319-338): local stats -> stats-ranked order
       std::vector<int> local = hitcount_order(nd.size, cc, avg, cfg.stats_variant);
       nd.leaf_order.clear();
       for (int li : local) nd.leaf_order.push_back(nd.cols[li]);
@@ -726,18 +725,28 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
     }
   };
 
-  std::vector<int> frontier;
+  std::vector<int> frontier, pending;  // pending: fallback leaves awaiting stats
   if (nodes[0].kind == SCAN) frontier.push_back(0);
-  else if (nodes[0].kind == FALLBACK) run_leaf_stats({0});
+  else if (nodes[0].kind == FALLBACK) pending.push_back(0);
 
-  while (!frontier.empty()) {
-    // ---- K5: argmax over every scanning node of this level ----
-    Level L;
+  while (!frontier.empty() || !pending.empty()) {
+    // ---- one GPU pass per level: K5 argmax over the frontier, K7 leaf
+    // statistics of the leaves created by the previous level, one D2H ----
+    Level L, S;
+    std::vector<uint64_t> unique_groups(frontier.size(), 0);
     for (size_t i = 0; i < frontier.size(); ++i) {
       const Node& nd = nodes[frontier[i]];
       ScanSlot sl;
       sl.t = nd.table->desc();
-      sl.mask_off = col_mask(nd.cols, L.masks);
+      // Columns whose values are all distinct (card == n) hold one row per
+      // group in every node: their groups score 0 and can never be chosen
+      // over a positive score (ggr.hpp:263-266), so they are not scanned —
+      // their |node| groups are added to candidates_examined directly.
+      std::vector<int> scan_cols;
+      for (int c : nd.cols)
+        if (e.card[c] == n) unique_groups[i] += nd.size;
+        else scan_cols.push_back(c);
+      sl.mask_off = col_mask(scan_cols, L.masks);
       sl.w_off = uint32_t(L.weights.size());
       L.weights.resize(L.weights.size() + size_t(m) * std::max<uint32_t>(K, 1), 0);
       std::vector<char> act(m, 0);
@@ -746,32 +755,60 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
         for (size_t k = 0; k < dpart[c].size(); ++k)
           if (act[dpart[c][k]]) L.weights[sl.w_off + c * K + k] = 1;
       L.slots.push_back(sl);
-      add_work(L.work, uint32_t(i), *nd.table, nd.cols);
+      add_work(L.work, uint32_t(i), *nd.table, scan_cols);
       L.slot_work_off.push_back(uint32_t(L.work.size()));
     }
+    for (size_t i = 0; i < pending.size(); ++i) {
+      const Node& nd = nodes[pending[i]];
+      ScanSlot sl;
+      sl.t = nd.table->desc();
+      sl.mask_off = col_mask(nd.cols, S.masks);
+      sl.w_off = 0;
+      S.slots.push_back(sl);
+      add_work(S.work, uint32_t(i), *nd.table, nd.cols);
+    }
     const uint32_t nslots = uint32_t(L.slots.size());
-    auto d_slots = to_device(L.slots, s);
-    auto d_masks = to_device(L.masks, s);
-    if (L.weights.empty()) L.weights.push_back(0);
-    auto d_w = to_device(L.weights, s);
-    auto d_work = to_device(L.work, s);
-    auto d_swo = to_device(L.slot_work_off, s);
+    const size_t nleaf = pending.size();
+    Pack pk;
+    const size_t o_slots = pk.add(L.slots), o_masks = pk.add(L.masks), o_w = pk.add(L.weights);
+    const size_t o_work = pk.add(L.work), o_swo = pk.add(L.slot_work_off);
+    const size_t o_sslots = pk.add(S.slots), o_smasks = pk.add(S.masks), o_swork = pk.add(S.work);
+    uint8_t* dp = upload(pk);
     DevBuf<Cand> partial(std::max<size_t>(1, L.work.size()), s);
     DevBuf<unsigned long long> pcands(std::max<size_t>(1, L.work.size()), s);
-    DevBuf<Cand> best(nslots, s);
-    DevBuf<unsigned long long> ncand(nslots, s);
-    PO_LAUNCH(k_argmax, unsigned(L.work.size()), kArgBlock, 0, s, d_work.get(), d_slots.get(),
-              d_masks.get(), d_w.get(), colbase, vlen, m, K, partial.get(), pcands.get());
-    PO_LAUNCH(k_argmax_final, nslots, kArgBlock, 0, s, partial.get(), pcands.get(), d_swo.get(),
-              best.get(), ncand.get());
-    std::vector<Cand> hbest(nslots);
-    std::vector<unsigned long long> hn(nslots);
-    best.download(hbest.data(), nslots);
-    ncand.download(hn.data(), nslots);
+    // results: [best Cand x nslots][ncand u64 x nslots][card u64 x nleaf*m][tot u64 x nleaf*m]
+    const size_t res_bytes = nslots * (sizeof(Cand) + 8) + 2 * nleaf * m * 8;
+    DevBuf<uint8_t> res(std::max<size_t>(16, res_bytes), s);
+    Cand* d_best = reinterpret_cast<Cand*>(res.get());
+    auto* d_ncand = reinterpret_cast<unsigned long long*>(res.get() + nslots * sizeof(Cand));
+    auto* d_card = d_ncand + nslots;
+    auto* d_tot = d_card + nleaf * m;
+    if (nleaf) PO_CUDA(cudaMemsetAsync(d_card, 0, 2 * nleaf * m * 8, s));
+    if (nslots) {
+      PO_LAUNCH(k_argmax, unsigned(L.work.size()), kArgBlock, 0, s,
+                reinterpret_cast<WorkItem*>(dp + o_work), reinterpret_cast<ScanSlot*>(dp + o_slots),
+                reinterpret_cast<uint32_t*>(dp + o_masks), reinterpret_cast<uint32_t*>(dp + o_w),
+                colbase, vlen, m, K, partial.get(), pcands.get());
+      PO_LAUNCH(k_argmax_final, nslots, kArgBlock, 0, s, partial.get(), pcands.get(),
+                reinterpret_cast<uint32_t*>(dp + o_swo), d_best, d_ncand);
+    }
+    if (nleaf)
+      PO_LAUNCH(k_leaf_stats, unsigned(S.work.size()), 256, m <= 2048 ? 16 * m : 0, s,
+                reinterpret_cast<WorkItem*>(dp + o_swork), reinterpret_cast<ScanSlot*>(dp + o_sslots),
+                reinterpret_cast<uint32_t*>(dp + o_smasks), colbase, vlen, m, d_card, d_tot);
+    std::vector<uint8_t> hres(std::max<size_t>(16, res_bytes));
+    res.download(hres.data(), res_bytes);  // pageable D2H: returns when complete
     sync(s);
+    std::vector<Cand> hbest(nslots);
+    if (nslots) std::memcpy(hbest.data(), hres.data(), nslots * sizeof(Cand));
+    const unsigned long long* hn =
+        reinterpret_cast<const unsigned long long*>(hres.data() + nslots * sizeof(Cand));
+    finish_leaves(pending, hn + nslots, hn + nslots + nleaf * m);
+    pending.clear();
+    if (frontier.empty()) break;
 
     // ---- host decisions (ggr.hpp:276-301) ----
-    std::vector<int> stopped, new_fallback, next;
+    std::vector<int> next;
     struct SplitH {
       int node;
       SplitD d;
@@ -779,12 +816,12 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
     std::vector<SplitH> splits;
     for (uint32_t i = 0; i < nslots; ++i) {
       const int id = frontier[i];
-      out.stats.candidates_examined += hn[i];
+      out.stats.candidates_examined += hn[i] + unique_groups[i];
       const Cand& b = hbest[i];
       if (b.count == 0 || b.numer == 0 ||
           b.numer < u128(cfg.hitcount_stop_threshold) * u128(b.count)) {
-        nodes[id].kind = FALLBACK;
-        stopped.push_back(id);
+        nodes[id].kind = FALLBACK;  // early stop: statistics fallback
+        pending.push_back(id);
         continue;
       }
       Node& P = nodes[id];
@@ -822,7 +859,7 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
         uint64_t bound = 0;
         for (int c : P.cols) bound += std::min<uint64_t>(e.card[c], B.size);
         uint64_t cap = 64;
-        while (cap < 2 * bound) cap <<= 1;
+        while (cap < bound + bound / 2) cap <<= 1;
         auto t = std::make_shared<HTable>();
         t->cap = cap;
         t->keys.alloc(cap, s);
@@ -852,7 +889,7 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
       nodes.push_back(std::move(R));
       for (int ch : {bid, bid + 1}) {
         if (nodes[ch].kind == SCAN) next.push_back(ch);
-        else if (nodes[ch].kind == FALLBACK) new_fallback.push_back(ch);
+        else if (nodes[ch].kind == FALLBACK) pending.push_back(ch);
       }
     }
 
@@ -884,31 +921,25 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
                                     std::min(seg[j + 1], lo + kRowsPerTask)});
         }
       }
-      auto d_sp = to_device(hsp, s);
-      auto d_seg = to_device(seg, s);
-      auto d_snodes = to_device(split_nodes, s);
-      DevBuf<uint32_t> cursor(ns, s);
-      cursor.zero();
+      Pack sp;
+      const size_t o_sp = sp.add(hsp), o_seg = sp.add(seg), o_sn = sp.add(split_nodes);
+      const size_t o_tasks = sp.add(tasks);
+      const size_t o_cursor = sp.add(std::vector<uint32_t>(ns, 0u));
+      uint8_t* ds = upload(sp);
+      auto* d_sp = reinterpret_cast<SplitD*>(ds + o_sp);
+      auto* d_seg = reinterpret_cast<uint64_t*>(ds + o_seg);
+      auto* d_snodes = reinterpret_cast<uint32_t*>(ds + o_sn);
+      auto* d_cursor = reinterpret_cast<uint32_t*>(ds + o_cursor);
       DevBuf<uint32_t> blockrows(std::max<uint64_t>(1, seg[ns]), s);
-      PO_LAUNCH(k_mark_splits, grid_for(ns, 128), 128, 0, s, split_of_node.get(), d_snodes.get(),
-                ns, 0);
+      PO_LAUNCH(k_mark_splits, grid_for(ns, 128), 128, 0, s, split_of_node.get(), d_snodes, ns, 0);
       PO_LAUNCH(k_relabel, grid_for(n, 256), 256, 0, s, node_of_row.get(), n,
-                split_of_node.get(), d_sp.get(), e.vid.get(), m, cursor.get(), d_seg.get(),
-                blockrows.get());
-      if (!tasks.empty()) {
-        auto d_tasks = to_device(tasks, s);
-        PO_LAUNCH(k_aggregate, unsigned(tasks.size()), kAggBlock, 0, s, d_tasks.get(),
-                  blockrows.get(), d_sp.get(), e.vid.get(), vlen, colbase, m, K, d_dpart.get(),
-                  d_npart.get());
-      }
-      PO_LAUNCH(k_mark_splits, grid_for(ns, 128), 128, 0, s, split_of_node.get(), d_snodes.get(),
-                ns, 1);
+                split_of_node.get(), d_sp, e.vid.get(), m, d_cursor, d_seg, blockrows.get());
+      if (!tasks.empty())
+        PO_LAUNCH(k_aggregate, unsigned(tasks.size()), kAggBlock, 0, s,
+                  reinterpret_cast<AggTask*>(ds + o_tasks), blockrows.get(), d_sp, e.vid.get(),
+                  vlen, colbase, m, K, d_dpart.get(), d_npart.get());
+      PO_LAUNCH(k_mark_splits, grid_for(ns, 128), 128, 0, s, split_of_node.get(), d_snodes, ns, 1);
     }
-
-    // ---- K7: statistics of every node that falls back at this level ----
-    std::vector<int> leaves = stopped;
-    leaves.insert(leaves.end(), new_fallback.begin(), new_fallback.end());
-    run_leaf_stats(leaves);
     if (debug_checks()) {
       DevBuf<unsigned long long> hist(nodes.size() + 1, s);
       hist.zero();
@@ -931,6 +962,7 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
     timing_mark("levels", s);
     frontier.swap(next);
   }
+
 
   // ---- layout: leaves in DFS order, block subtree first ----
   std::vector<int> leaf_nodes;
@@ -966,9 +998,11 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
   }
   const uint32_t nleaves = uint32_t(leaf_nodes.size());
   std::vector<uint32_t> leaf_off(nleaves, 0), leaf_chunk_off(nleaves), leaf_nchunks(nleaves);
-  std::vector<uint32_t> chunk_key_off, chunk_nkeys;
-  std::vector<int32_t> key_field, h_leaf_orders(size_t(nleaves) * m);
-  std::vector<uint8_t> key_kind, key_bits;
+  std::vector<int32_t> h_leaf_orders(size_t(nleaves) * m);
+  KeySchedule ks;
+  // round 0 groups the rows by leaf index; later rounds by start position
+  const int cap0 = int(refine_chunk_bits(nleaves ? nleaves - 1 : 0));
+  const int cap = 64;  // rounds >= 1 sort inside groups: the chunk alone
   uint64_t off = 0;
   for (uint32_t l = 0; l < nleaves; ++l) {
     const Node& nd = nodes[leaf_nodes[l]];
@@ -978,35 +1012,19 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
               h_leaf_orders.begin() + size_t(l) * m);
     // sort keys of the leaf
     std::vector<std::pair<int, uint8_t>> keys;  // (field, kind)
-    if (nd.kind == RAW1) keys.push_back({nd.cols[0], 0});  // raw bytes (ggr.hpp:221-231)
-    else if (nd.kind == FALLBACK)                          // fragment keys (ggr.hpp:340-350)
-      for (int f : nd.leaf_order) keys.push_back({f, 1});
-    leaf_chunk_off[l] = uint32_t(chunk_nkeys.size());
-    const int cap_bits = int(refine_chunk_bits(uint32_t(n)));
-    int used = cap_bits;
-    for (auto [f, kind] : keys) {
-      int b = bits_for(e.card[f] ? e.card[f] - 1 : 0);
-      if (used + b > cap_bits) {
-        chunk_key_off.push_back(uint32_t(key_field.size()));
-        chunk_nkeys.push_back(0);
-        used = 0;
-      }
-      key_field.push_back(f);
-      key_kind.push_back(kind);
-      key_bits.push_back(uint8_t(b));
-      chunk_nkeys.back()++;
-      used += b;
-    }
-    leaf_nchunks[l] = uint32_t(chunk_nkeys.size()) - leaf_chunk_off[l];
+    if (nd.kind == RAW1) keys.push_back({nd.cols[0], uint8_t(0)});  // raw bytes (ggr.hpp:221-231)
+    else if (nd.kind == FALLBACK)  // fragment keys (ggr.hpp:340-350)
+      for (int f : nd.leaf_order) keys.push_back({f, uint8_t(1)});
+    leaf_chunk_off[l] = uint32_t(ks.chunk_nkeys.size());
+    leaf_nchunks[l] = ks.add_leaf(keys, e.card, cap0, cap);
   }
   if (off != n) fail(PO_ERR_ERROR, "internal: leaves do not cover the table");
-  if (chunk_nkeys.empty()) {
-    chunk_key_off.push_back(0);
-    chunk_nkeys.push_back(0);
-    key_field.push_back(0);
-    key_kind.push_back(0);
-    key_bits.push_back(1);
-  }
+  ks.pad();
+  const auto& chunk_key_off = ks.chunk_key_off;
+  const auto& chunk_nkeys = ks.chunk_nkeys;
+  const auto& key_field = ks.key_field;
+  const auto& key_kind = ks.key_kind;
+  const auto& key_bits = ks.key_bits;
   auto d_node_leaf = to_device(node_leaf, s);
   auto d_leaf_off = to_device(leaf_off, s);
   auto d_lco = to_device(leaf_chunk_off, s), d_lnc = to_device(leaf_nchunks, s);
@@ -1032,8 +1050,25 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
   RK.key_kind = d_kk.get();
   RK.key_bits = d_kb.get();
   timing_mark("layout", s);
-  refine_sort(uint32_t(n), grp.get(), uint32_t(n), RK, pos.get(), s);
-  timing_mark("leaf_sort", s);
+  // whole-table fallback order (ggr.hpp:379-381) from the dictionary stats;
+  // its row sort runs in lockstep with the leaf sort (every leaf at once)
+  std::vector<double> avg(m);
+  for (uint32_t c = 0; c < m; ++c)
+    avg[c] = static_cast<double>(e.total_len[c]) / static_cast<double>(n);
+  std::vector<int> fb_order = hitcount_order(n, e.card, avg, cfg.stats_variant);
+  FixedOrderSort fb_sort(e, fb_order, s);
+  RefineJob leaf_job;
+  leaf_job.n_items = uint32_t(n);
+  leaf_job.d_grp_init = row_leaf.get();  // round 0: leaf index
+  leaf_job.d_grp_start = d_leaf_off.get();
+  leaf_job.n_groups = nleaves;
+  leaf_job.grp_max = uint32_t(n);
+  leaf_job.key = RK;
+  leaf_job.d_out_pos = pos.get();
+  leaf_job.row_chunk_bits0 = ks.widest0;
+  leaf_job.row_chunk_bits = ks.widest;
+  refine_sort_multi({leaf_job, fb_sort.job()}, s);
+  timing_mark("leaf+fallback_sort", s);
   if (debug_checks()) {
     DevBuf<unsigned> seen(n, s);
     DevBuf<unsigned long long> bad(1, s);
@@ -1047,67 +1082,17 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
   }
   PO_LAUNCH(k_emit, grid_for(n, 256), 256, 0, s, pos.get(), n, m, row_leaf.get(),
             d_leaf_orders.get(), d_rows, d_orders);
-  try {
-    out.phc = phc_device(e, n, nullptr, d_rows, nullptr, d_orders, s);
-  } catch (const Error&) {
-    // post-mortem diagnostics (no effect on the timing before the failure)
-    DevBuf<unsigned> seen(n, s);
-    DevBuf<unsigned long long> bad(1, s);
-    seen.zero();
-    bad.zero();
-    PO_LAUNCH(k_dbg_perm, grid_for(n, 256), 256, 0, s, pos.get(), n, seen.get(), bad.get());
-    DevBuf<unsigned long long> hist(nodes.size() + 1, s);
-    hist.zero();
-    PO_LAUNCH(k_dbg_node_hist, grid_for(n, 256), 256, 0, s, node_of_row.get(), n,
-              uint32_t(nodes.size()), hist.get());
-    std::vector<unsigned long long> hh(nodes.size() + 1);
-    hist.download(hh.data(), hh.size());
-    unsigned long long hb = 0;
-    bad.download(&hb, 1);
-    sync(s);
-    fprintf(stderr, "[po post-mortem] n=%llu nodes=%zu leaves=%u pos collisions=%llu\n",
-            (unsigned long long)n, nodes.size(), nleaves, hb);
-    for (size_t id = 0; id < nodes.size(); ++id)
-      if (nodes[id].kind != SPLIT && hh[id] != nodes[id].size)
-        fprintf(stderr, "[po post-mortem] node %zu kind %d size %llu labelled %llu\n", id,
-                nodes[id].kind, (unsigned long long)nodes[id].size, hh[id]);
-    std::vector<uint32_t> hrows(std::min<uint64_t>(n, 64));
-    PO_CUDA(cudaMemcpy(hrows.data(), d_rows, hrows.size() * 4, cudaMemcpyDeviceToHost));
-    fprintf(stderr, "[po post-mortem] first rows:");
-    for (auto x : hrows) fprintf(stderr, " %u", x);
-    fprintf(stderr, "\n");
-    throw;
-  }
-
+  out.phc = phc_device(e, n, nullptr, d_rows, nullptr, d_orders, s);
   timing_mark("emit_phc", s);
+
   // ---- whole-table fallback competition (ggr.hpp:379-387) ----
-  std::vector<double> avg(m);
-  for (uint32_t c = 0; c < m; ++c)
-    avg[c] = static_cast<double>(e.total_len[c]) / static_cast<double>(n);
-  std::vector<int> fb_order = hitcount_order(n, e.card, avg, cfg.stats_variant);
   DevBuf<uint32_t> fb_perm(n, s);
-  sort_all_rows(e, fb_order, fb_perm.get(), s);
-  timing_mark("fallback_sort", s);
+  fb_sort.finish(fb_perm.get());
   std::vector<int32_t> fo(fb_order.begin(), fb_order.end());
   auto d_fo = to_device(fo, s);
-  uint64_t fb_phc = 0;
-  try {
-    fb_phc = phc_device(e, n, nullptr, fb_perm.get(), nullptr, d_fo.get(), s, 1, true);
-  } catch (const Error&) {
-    std::vector<uint32_t> hp(n);
-    PO_CUDA(cudaMemcpy(hp.data(), fb_perm.get(), n * 4, cudaMemcpyDeviceToHost));
-    std::vector<char> seen(n, 0);
-    uint64_t bad = 0, dup = 0;
-    for (auto x : hp) {
-      if (x >= n) ++bad;
-      else if (seen[x]++) ++dup;
-    }
-    fprintf(stderr, "[po post-mortem] fallback perm: %llu out of range, %llu duplicates\n",
-            (unsigned long long)bad, (unsigned long long)dup);
-    throw;
-  }
+  const uint64_t fb_phc = phc_device(e, n, nullptr, fb_perm.get(), nullptr, d_fo.get(), s, 1, true);
   timing_mark("fallback_phc", s);
-  if (fb_phc > out.phc) {
+  if (fb_phc > out.phc) {  // replace only when strictly better (ggr.hpp:383)
     PO_CUDA(cudaMemcpyAsync(d_rows, fb_perm.get(), n * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
     PO_LAUNCH(k_tile_order, grid_for(n * m, 256), 256, 0, s, d_fo.get(), n, m, d_orders);
     out.phc = fb_phc;

@@ -83,15 +83,77 @@ struct RefineKey {
   const int32_t* key_field = nullptr;
   const uint8_t* key_kind = nullptr;  // 0 raw (vid), 1 escaped (esc_rank)
   const uint8_t* key_bits = nullptr;
-  uint32_t chunk_bits = 0;  // set by refine_sort: 64 - bits(grp_max)
+  uint32_t chunk_bits = 0;       // set by refine_sort: 64 - bits(grp_max)
+  uint32_t nsym0 = 0, nsym = 0;  // set by refine_sort: string symbols in round 0 / later
 };
+
+struct RefineJob {
+  uint32_t n_items = 0;
+  // round-0 groups: d_grp_init[i] is a group index < n_groups whose start
+  // position is d_grp_start[index]; with d_grp_start == null it is the start
+  // position itself. grp_max bounds every start position (n_items - 1).
+  const uint32_t* d_grp_init = nullptr;
+  const uint32_t* d_grp_start = nullptr;
+  uint32_t n_groups = 0;
+  uint32_t grp_max = 0;
+  RefineKey key;
+  uint32_t* d_out_pos = nullptr;
+  uint32_t row_chunk_bits0 = 0;  // row keys: widest packed chunk of round 0 (0 = max)
+  uint32_t row_chunk_bits = 0;   // row keys: widest packed chunk of later rounds
+};
+
+// Host-side key schedule of row sorts: keys (field, kind, bits) packed into
+// chunks of at most cap0 bits (round 0) then cap bits (later rounds).
+struct KeySchedule {
+  std::vector<uint32_t> chunk_key_off, chunk_nkeys;
+  std::vector<int32_t> key_field;
+  std::vector<uint8_t> key_kind, key_bits;
+  uint32_t widest0 = 1, widest = 1;
+  // appends one leaf's chunks; returns its number of chunks
+  uint32_t add_leaf(const std::vector<std::pair<int, uint8_t>>& keys,
+                    const std::vector<uint64_t>& card, int cap0, int cap) {
+    const size_t first = chunk_nkeys.size();
+    bool open = false;
+    int used = 0, cur_cap = 0;
+    for (auto [f, kind] : keys) {
+      const int b = bits_for(card[f] ? card[f] - 1 : 0);
+      if (!open || used + b > cur_cap) {
+        cur_cap = chunk_nkeys.size() == first ? cap0 : cap;
+        chunk_key_off.push_back(uint32_t(key_field.size()));
+        chunk_nkeys.push_back(0);
+        used = 0;
+        open = true;
+      }
+      key_field.push_back(f);
+      key_kind.push_back(kind);
+      key_bits.push_back(uint8_t(b));
+      chunk_nkeys.back()++;
+      used += b;
+      if (chunk_nkeys.size() == first + 1) widest0 = std::max<uint32_t>(widest0, uint32_t(used));
+      else widest = std::max<uint32_t>(widest, uint32_t(used));
+    }
+    return uint32_t(chunk_nkeys.size() - first);
+  }
+  void pad() {  // keep device arrays non-empty
+    if (!chunk_nkeys.empty()) return;
+    chunk_key_off.push_back(0);
+    chunk_nkeys.push_back(0);
+    key_field.push_back(0);
+    key_kind.push_back(0);
+    key_bits.push_back(1);
+  }
+};
+
+// Several independent sorts advanced in lockstep: one host synchronisation
+// per round for all of them.
+void refine_sort_multi(const std::vector<RefineJob>& jobs, cudaStream_t s);
 
 // Bits available for a key chunk next to group ids up to grp_max.
 uint32_t refine_chunk_bits(uint32_t grp_max);
 
 void refine_sort(uint32_t n_items, const uint32_t* d_grp_init, uint32_t grp_max,
                  const RefineKey& key, uint32_t* d_out_pos, cudaStream_t s,
-                 uint32_t* rounds_out = nullptr);
+                 uint32_t row_chunk_bits = 0);
 
 // PHC (K9 phc_lcp): sum over entries i>=1 of hit(i) (objective.hpp:70-99).
 // Schedule on device: rows[i] (u64 or u32), field orders either full
@@ -114,6 +176,22 @@ std::vector<int> stats_order(uint64_t total_rows, const std::vector<uint64_t>& c
 // (sort_rows_fixed_order, objective.hpp:154-171). d_perm[pos] = row.
 void sort_all_rows(const Encoded& e, const std::vector<int>& order, uint32_t* d_perm,
                    cudaStream_t s);
+
+// The same sort as a refine job (to run in lockstep with other sorts).
+class FixedOrderSort {
+ public:
+  FixedOrderSort(const Encoded& e, const std::vector<int>& order, cudaStream_t s);
+  const RefineJob& job() const { return job_; }
+  void finish(uint32_t* d_perm);  // after the job ran: d_perm[pos] = row
+
+ private:
+  uint64_t n_ = 0;
+  cudaStream_t s_;
+  RefineJob job_;
+  DevBuf<uint32_t> lco_, lnc_, cko_, cnk_, row_leaf_, grp_, pos_, start_;
+  DevBuf<int32_t> kf_;
+  DevBuf<uint8_t> kk_, kb_;
+};
 
 struct GgrOutput {
   uint64_t phc = 0;

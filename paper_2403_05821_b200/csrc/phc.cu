@@ -95,61 +95,66 @@ uint64_t phc_device(const Encoded& e, uint64_t n_entries, const uint64_t* rows64
 }
 
 // Keys of a single leaf covering all rows (one field order, escaped ranks),
-// packed into 64-bit chunks.
-void sort_all_rows(const Encoded& e, const std::vector<int>& order, uint32_t* d_perm,
-                   cudaStream_t s) {
-  const uint64_t n = e.n;
-  if (n == 0) return;
-  std::vector<uint32_t> chunk_key_off, chunk_nkeys;
-  std::vector<int32_t> key_field;
-  std::vector<uint8_t> key_kind, key_bits;
-  // later rounds use start positions (< n) as group ids
-  const int cap_bits = int(refine_chunk_bits(uint32_t(n)));
-  int used = cap_bits;
-  for (int f : order) {
-    int b = bits_for(e.card[f] ? e.card[f] - 1 : 0);
-    if (used + b > cap_bits) {
-      chunk_key_off.push_back(uint32_t(key_field.size()));
-      chunk_nkeys.push_back(0);
-      used = 0;
-    }
-    key_field.push_back(f);
-    key_kind.push_back(1);
-    key_bits.push_back(uint8_t(b));
-    chunk_nkeys.back()++;
-    used += b;
-  }
-  std::vector<uint32_t> leaf_chunk_off{0}, leaf_nchunks{uint32_t(chunk_nkeys.size())};
-  if (chunk_nkeys.empty()) {  // keep device arrays non-empty
-    chunk_key_off.push_back(0);
-    chunk_nkeys.push_back(0);
-    key_field.push_back(0);
-    key_kind.push_back(1);
-    key_bits.push_back(1);
-  }
-  auto d_lco = to_device(leaf_chunk_off, s), d_lnc = to_device(leaf_nchunks, s);
-  auto d_cko = to_device(chunk_key_off, s), d_cnk = to_device(chunk_nkeys, s);
-  auto d_kf = to_device(key_field, s);
-  auto d_kk = to_device(key_kind, s), d_kb = to_device(key_bits, s);
-  DevBuf<uint32_t> row_leaf(n, s), grp(n, s), pos(n, s);
-  row_leaf.zero();
-  grp.zero();
-  RefineKey K;
+// packed into 64-bit chunks next to the group id.
+FixedOrderSort::FixedOrderSort(const Encoded& e, const std::vector<int>& order, cudaStream_t s)
+    : n_(e.n), s_(s) {
+  if (n_ == 0) return;
+  KeySchedule ks;
+  std::vector<std::pair<int, uint8_t>> keys;
+  for (int f : order) keys.push_back({f, uint8_t(1)});  // escaped ranks
+  // one round-0 group (index 0, start 0); later rounds: start positions < n
+  // rounds >= 1 sort inside groups: their chunks may use all 64 bits
+  const uint32_t nch = ks.add_leaf(keys, e.card, int(refine_chunk_bits(0)), 64);
+  ks.pad();
+  std::vector<uint32_t> leaf_chunk_off{0}, leaf_nchunks{nch};
+  lco_ = to_device(leaf_chunk_off, s);
+  lnc_ = to_device(leaf_nchunks, s);
+  cko_ = to_device(ks.chunk_key_off, s);
+  cnk_ = to_device(ks.chunk_nkeys, s);
+  kf_ = to_device(ks.key_field, s);
+  kk_ = to_device(ks.key_kind, s);
+  kb_ = to_device(ks.key_bits, s);
+  row_leaf_.alloc(n_, s);
+  grp_.alloc(n_, s);
+  pos_.alloc(n_, s);
+  start_.alloc(1, s);
+  row_leaf_.zero();
+  grp_.zero();
+  start_.zero();
+  job_.n_items = uint32_t(n_);
+  job_.d_grp_init = grp_.get();
+  job_.d_grp_start = start_.get();
+  job_.n_groups = 1;
+  job_.grp_max = uint32_t(n_);
+  job_.d_out_pos = pos_.get();
+  job_.row_chunk_bits0 = ks.widest0;
+  job_.row_chunk_bits = ks.widest;
+  RefineKey& K = job_.key;
   K.kind = 2;
   K.m = e.m;
   K.vid = e.vid.get();
   K.esc_rank = e.esc_rank.get();
   K.colbase = e.d_colbase.get();
-  K.row_leaf = row_leaf.get();
-  K.leaf_chunk_off = d_lco.get();
-  K.leaf_nchunks = d_lnc.get();
-  K.chunk_key_off = d_cko.get();
-  K.chunk_nkeys = d_cnk.get();
-  K.key_field = d_kf.get();
-  K.key_kind = d_kk.get();
-  K.key_bits = d_kb.get();
-  refine_sort(uint32_t(n), grp.get(), uint32_t(n), K, pos.get(), s);
-  PO_LAUNCH(k_invert, grid_for(n, 256), 256, 0, s, pos.get(), n, d_perm);
+  K.row_leaf = row_leaf_.get();
+  K.leaf_chunk_off = lco_.get();
+  K.leaf_nchunks = lnc_.get();
+  K.chunk_key_off = cko_.get();
+  K.chunk_nkeys = cnk_.get();
+  K.key_field = kf_.get();
+  K.key_kind = kk_.get();
+  K.key_bits = kb_.get();
+}
+
+void FixedOrderSort::finish(uint32_t* d_perm) {
+  if (n_) PO_LAUNCH(k_invert, grid_for(n_, 256), 256, 0, s_, pos_.get(), n_, d_perm);
+}
+
+void sort_all_rows(const Encoded& e, const std::vector<int>& order, uint32_t* d_perm,
+                   cudaStream_t s) {
+  FixedOrderSort fs(e, order, s);
+  if (e.n == 0) return;
+  refine_sort_multi({fs.job()}, s);
+  fs.finish(d_perm);
 }
 
 // fixed_order_by_hitcount_stats (ggr.hpp:59-84): host IEEE double; this

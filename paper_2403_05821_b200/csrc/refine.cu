@@ -4,14 +4,17 @@
 // and the raw single-column base case, ggr.hpp:221-231).
 //
 // MSD by key chunks: each round stable-radix-sorts the still-unresolved items
-// on one 64-bit word (group << chunk_bits | chunk) — group ids are final
-// start positions, so every group keeps a contiguous range of output slots —
-// then splits groups where the chunk changes. Most items resolve after one or
-// two rounds, so later rounds touch only the long shared prefixes.
+// on one 64-bit word (group << shift | chunk) and splits groups where the
+// chunk changes. Round 0 names groups by a small index (column, leaf) whose
+// start positions come from a table, so its chunk is as wide as possible;
+// later rounds name groups by their final start position. Most items resolve
+// in round 0, later rounds touch only the long shared prefixes.
 
 #include <cub/cub.cuh>
 
+#include <cstdio>
 #include <cstdlib>
+#include <memory>
 
 #include "internal.cuh"
 
@@ -27,20 +30,19 @@ __device__ __forceinline__ uint32_t end_code(const RefineKey& K) {
   return K.kind == 0 ? kRawEnd : c_esc_code[256];
 }
 
-// Chunk k of a string: nsym 9-bit symbols (bytes nsym*k .. nsym*k+nsym-1,
-// the end marker at position len, zero padding after). Raw order: end <
-// every byte (a prefix sorts first). Escaped order: the code of each byte is
-// the rank of its json_escape expansion and the end marker is the closing
-// '"' (0x22) of the fragment, so comparing code strings == comparing escaped
-// fragment keys (the expansions are prefix-free).
-__device__ __forceinline__ uint64_t string_chunk(const RefineKey& K, uint32_t item, uint32_t k) {
+// Symbols [base, base + nsym) of a string as 9-bit codes (the end marker at
+// position len, zero padding after). Raw order: end < every byte (a prefix
+// sorts first). Escaped order: the code of each byte is the rank of its
+// json_escape expansion and the end marker is the closing '"' (0x22) of the
+// fragment, so comparing code strings == comparing escaped fragment keys (the
+// expansions are prefix-free).
+__device__ __forceinline__ uint64_t string_chunk(const RefineKey& K, uint32_t item, uint64_t base,
+                                                 uint32_t nsym) {
   const uint64_t i = uint64_t(K.item_cell_row[item]) * K.m + K.item_col[item];
   const uint64_t o0 = K.offsets[i];
   const uint64_t len = K.offsets[i + 1] - o0;
   const uint8_t* p = K.arena + o0;
-  const uint32_t nsym = K.chunk_bits / 9;
   uint64_t chunk = 0;
-  const uint64_t base = uint64_t(k) * nsym;
   for (uint32_t j = 0; j < nsym; ++j) {
     const uint64_t pos = base + j;
     uint32_t code;
@@ -55,8 +57,7 @@ __device__ __forceinline__ uint64_t string_chunk(const RefineKey& K, uint32_t it
   return chunk;
 }
 
-__device__ __forceinline__ bool string_terminal(const RefineKey& K, uint64_t chunk) {
-  const uint32_t nsym = K.chunk_bits / 9;
+__device__ __forceinline__ bool string_terminal(const RefineKey& K, uint64_t chunk, uint32_t nsym) {
   const uint32_t e = end_code(K);
   for (uint32_t j = 0; j < nsym; ++j)
     if (((chunk >> (9 * j)) & 511u) == e) return true;
@@ -83,44 +84,109 @@ __device__ __forceinline__ bool row_terminal(const RefineKey& K, uint32_t row, u
   return k + 1 >= K.leaf_nchunks[K.row_leaf[row]];
 }
 
+// Per-round layout of a string key: round 0 takes nsym0 symbols, later
+// rounds nsym each.
+struct StrRound {
+  uint64_t base;
+  uint32_t nsym;
+};
+__device__ __forceinline__ StrRound str_round(const RefineKey& K, uint32_t k) {
+  if (k == 0) return {0, K.nsym0};
+  return {uint64_t(K.nsym0) + uint64_t(k - 1) * K.nsym, K.nsym};
+}
+
 __global__ void k_build_keys(const uint32_t* items, const uint32_t* grp, uint32_t A, uint32_t k,
-                             RefineKey K, uint64_t* keys) {
+                             uint32_t shift, RefineKey K, uint64_t* keys) {
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < A; i += gridDim.x * blockDim.x) {
-    const uint64_t chunk = K.kind == 2 ? row_chunk(K, items[i], k) : string_chunk(K, items[i], k);
-    keys[i] = (uint64_t(grp[i]) << K.chunk_bits) | chunk;
+    uint64_t chunk;
+    if (K.kind == 2) {
+      chunk = row_chunk(K, items[i], k);
+    } else {
+      const StrRound sr = str_round(K, k);
+      chunk = string_chunk(K, items[i], sr.base, sr.nsym);
+    }
+    keys[i] = shift < 64 ? ((uint64_t(grp[i]) << shift) | chunk) : chunk;
+  }
+}
+
+// Rounds >= 1 sort within segments (= groups): segment starts of the active
+// array, and the boundary markers from the segment flags + chunk changes.
+// flags over the previous round's item count (the compaction input size):
+// positions at or past the new count are cleared so the selection over the
+// old range only yields real segment starts.
+__global__ void k_seg_flags(const uint32_t* grp, const int* count, uint32_t old_count,
+                            uint8_t* flags) {
+  const uint32_t A = uint32_t(*count);
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < old_count;
+       i += gridDim.x * blockDim.x)
+    flags[i] = (i < A && (i == 0 || grp[i] != grp[i - 1])) ? 1 : 0;
+}
+
+__global__ void k_seg_end(uint32_t* seg_begin, const int* nseg, const int* count) {
+  seg_begin[*nseg] = uint32_t(*count);
+}
+
+__global__ void k_marks_seg(const uint64_t* keys, const uint8_t* flags, uint32_t A,
+                            uint32_t* gmark, uint32_t* rmark) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < A; i += gridDim.x * blockDim.x) {
+    const bool gb = flags[i] != 0;
+    const bool rb = gb || keys[i] != keys[i - 1];
+    gmark[i] = gb ? i : 0;
+    rmark[i] = rb ? i : 0;
   }
 }
 
 // Boundary markers for the two max-scans: start index of each item's group
 // and of its (group, chunk) run.
-__global__ void k_marks(const uint64_t* keys, uint32_t A, uint32_t chunk_bits, uint32_t* gmark,
+__global__ void k_marks(const uint64_t* keys, uint32_t A, uint32_t shift, uint32_t* gmark,
                         uint32_t* rmark) {
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < A; i += gridDim.x * blockDim.x) {
-    const bool gb = i == 0 || (keys[i] >> chunk_bits) != (keys[i - 1] >> chunk_bits);
+    const bool gb = i == 0 || (keys[i] >> shift) != (keys[i - 1] >> shift);
     const bool rb = i == 0 || keys[i] != keys[i - 1];
     gmark[i] = gb ? i : 0;
     rmark[i] = rb ? i : 0;
   }
 }
 
+// Resolved items get their final position; the others keep (new group start,
+// item) packed in one word for a single compaction. `start` maps round-0
+// group indices to start positions (null: the group id is the start).
 __global__ void k_resolve(const uint64_t* keys, const uint32_t* items, const uint32_t* gstart,
-                          const uint32_t* rstart, uint32_t A, uint32_t k, RefineKey K,
-                          uint32_t* out_pos, uint8_t* keep, uint32_t* next_grp) {
-  const uint64_t cmask = K.chunk_bits >= 64 ? ~0ull : ((1ull << K.chunk_bits) - 1);
+                          const uint32_t* rstart, uint32_t A, uint32_t k, uint32_t shift,
+                          const uint32_t* start, const uint32_t* seg_grp, RefineKey K,
+                          uint32_t* out_pos, uint8_t* keep, uint64_t* packed) {
+  const uint64_t cmask = shift >= 64 ? ~0ull : ((1ull << shift) - 1);
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < A; i += gridDim.x * blockDim.x) {
     const uint32_t item = items[i];
-    const uint32_t g = uint32_t(keys[i] >> K.chunk_bits);
+    uint32_t g;
+    if (seg_grp) {
+      g = seg_grp[i];  // segmented rounds: group start aligned with the active array
+    } else {
+      const uint32_t gid = uint32_t(keys[i] >> shift);
+      g = start ? start[gid] : gid;
+    }
     const uint32_t pos = g + (i - gstart[i]);
     const bool run_head = rstart[i] == i;
     const bool next_head = i + 1 >= A || rstart[i + 1] == i + 1;
-    const bool term = K.kind == 2 ? row_terminal(K, item, k) : string_terminal(K, keys[i] & cmask);
+    bool term;
+    if (K.kind == 2) term = row_terminal(K, item, k);
+    else term = string_terminal(K, keys[i] & cmask, str_round(K, k).nsym);
     if ((run_head && next_head) || term) {
       out_pos[item] = pos;
       keep[i] = 0;
     } else {
       keep[i] = 1;
     }
-    next_grp[i] = g + (rstart[i] - gstart[i]);
+    packed[i] = (uint64_t(g + (rstart[i] - gstart[i])) << 32) | item;
+  }
+}
+
+__global__ void k_unpack(const uint64_t* packed, const int* count, uint32_t* items, uint32_t* grp) {
+  const uint32_t A = uint32_t(*count);
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < A; i += gridDim.x * blockDim.x) {
+    const uint64_t v = packed[i];
+    items[i] = uint32_t(v);
+    grp[i] = uint32_t(v >> 32);
   }
 }
 
@@ -161,82 +227,199 @@ void ensure_esc_table() {
   g_esc_table_ready = true;
 }
 
+// One sort's device state across rounds.
+struct Job {
+  RefineJob spec;
+  RefineKey key;
+  uint32_t A = 0, k = 0;
+  uint32_t shift0 = 0, shift = 0;  // chunk bits of round 0 / of later rounds
+  int end_bit0 = 0, end_bit = 0;
+  size_t tb = 0;
+  DevBuf<uint32_t> items, items2, grp, gstart, rstart, gmark, rmark;
+  DevBuf<uint64_t> keys, keys2, pk, pk2;
+  DevBuf<uint8_t> keep, tmp, segflags;
+  DevBuf<uint32_t> seg_begin;
+  uint32_t nseg = 0;
+  size_t seg_tb = 0;
+  DevBuf<uint8_t> seg_tmp;
+};
+
 }  // namespace
 
 uint32_t refine_chunk_bits(uint32_t grp_max) { return 64u - uint32_t(bits_for(grp_max)); }
 
-void refine_sort(uint32_t n_items, const uint32_t* d_grp_init, uint32_t grp_max,
-                 const RefineKey& key_in, uint32_t* d_out_pos, cudaStream_t s,
-                 uint32_t* rounds_out) {
-  if (rounds_out) *rounds_out = 0;
-  if (n_items == 0) return;
-  RefineKey key = key_in;
-  key.chunk_bits = refine_chunk_bits(grp_max);
-  if (key.kind != 2 && key.chunk_bits < 9) fail(PO_ERR_SIZE, "too many distinct values to rank");
-  if (key.kind == 1) ensure_esc_table();
-
-  DevBuf<uint32_t> items(n_items, s), items2(n_items, s);
-  DevBuf<uint32_t> grp(n_items, s), grp2(n_items, s);
-  DevBuf<uint64_t> keys(n_items, s), keys2(n_items, s);
-  DevBuf<uint32_t> gstart(n_items, s), rstart(n_items, s);
-  DevBuf<uint32_t> gmark(n_items, s), rmark(n_items, s);
-  DevBuf<uint8_t> keep(n_items, s);
-  DevBuf<int> nsel(1, s);
-
-  PO_LAUNCH(k_iota, grid_for(n_items, 256), 256, 0, s, items.get(), n_items);
-  PO_CUDA(cudaMemcpyAsync(grp.get(), d_grp_init, n_items * sizeof(uint32_t),
-                          cudaMemcpyDeviceToDevice, s));
-
-  // temp storage sized for the largest round
-  size_t sort_bytes = 0, scan_bytes = 0, sel_bytes = 0;
-  PO_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, keys.get(), keys2.get(),
-                                          items.get(), items2.get(), n_items, 0, 64, s));
-  PO_CUDA(cub::DeviceScan::InclusiveScan(nullptr, scan_bytes, gmark.get(), gstart.get(),
-                                         cub::Max(), n_items, s));
-  PO_CUDA(cub::DeviceSelect::Flagged(nullptr, sel_bytes, items2.get(), keep.get(), items.get(),
-                                     nsel.get(), n_items, s));
-  const size_t tb = std::max(sort_bytes, std::max(scan_bytes, sel_bytes));
-  DevBuf<uint8_t> tmp(tb, s);
-  const int end_bit = int(key.chunk_bits) + bits_for(grp_max);
-
-  uint32_t A = n_items;
-  for (uint32_t k = 0; A > 0; ++k) {
-    PO_LAUNCH(k_build_keys, grid_for(A, 256), 256, 0, s, items.get(), grp.get(), A, k, key,
-              keys.get());
-    size_t b = tb;
-    {
-      ProfScope ps("cub_radix_sort", s);
-      PO_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(), b, keys.get(), keys2.get(), items.get(),
-                                              items2.get(), A, 0, end_bit, s));
+void refine_sort_multi(const std::vector<RefineJob>& specs, cudaStream_t s) {
+  std::vector<std::unique_ptr<Job>> jobs;
+  for (const RefineJob& sp : specs) {
+    if (sp.n_items == 0) continue;
+    auto j = std::make_unique<Job>();
+    j->spec = sp;
+    j->key = sp.key;
+    // group ids of round 0: indices < n_groups (with a start table) or start
+    // positions; later rounds: start positions <= grp_max
+    const uint32_t g0max = sp.d_grp_start ? (sp.n_groups ? sp.n_groups - 1 : 0) : sp.grp_max;
+    const uint32_t cb0 = refine_chunk_bits(g0max), cb = refine_chunk_bits(sp.grp_max);
+    // rounds >= 1 sort inside segments: the key is the chunk alone (64 bits)
+    (void)cb;
+    if (j->key.kind != 2) {
+      if (cb0 < 9) fail(PO_ERR_SIZE, "too many columns to rank");
+      j->key.nsym0 = cb0 / 9;
+      j->key.nsym = 7;
+      j->shift0 = 9 * j->key.nsym0;
+      j->shift = 64;
+    } else {
+      j->shift0 = std::min(sp.row_chunk_bits0 ? sp.row_chunk_bits0 : cb0, cb0);
+      j->shift = 64;
     }
-    PO_LAUNCH(k_marks, grid_for(A, 256), 256, 0, s, keys2.get(), A, key.chunk_bits, gmark.get(),
-              rmark.get());
-    {
-      ProfScope ps("cub_scan", s);
-      b = tb;
-      PO_CUDA(cub::DeviceScan::InclusiveScan(tmp.get(), b, gmark.get(), gstart.get(), cub::Max(),
-                                             A, s));
-      b = tb;
-      PO_CUDA(cub::DeviceScan::InclusiveScan(tmp.get(), b, rmark.get(), rstart.get(), cub::Max(),
-                                             A, s));
-    }
-    PO_LAUNCH(k_resolve, grid_for(A, 256), 256, 0, s, keys2.get(), items2.get(), gstart.get(),
-              rstart.get(), A, k, key, d_out_pos, keep.get(), grp2.get());
-    {
-      ProfScope ps("cub_select", s);
-      b = tb;
-      PO_CUDA(cub::DeviceSelect::Flagged(tmp.get(), b, items2.get(), keep.get(), items.get(),
-                                         nsel.get(), A, s));
-      b = tb;
-      PO_CUDA(cub::DeviceSelect::Flagged(tmp.get(), b, grp2.get(), keep.get(), grp.get(),
-                                         nsel.get(), A, s));
-    }
-    int na = 0;
-    PO_CUDA(cudaMemcpyAsync(&na, nsel.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
-    sync(s);
-    A = uint32_t(na);
-    if (rounds_out) ++*rounds_out;
+    j->key.chunk_bits = cb;
+    j->end_bit0 = int(j->shift0) + bits_for(g0max);
+    j->end_bit = 64;
+    if (j->key.kind == 1) ensure_esc_table();
+    const uint32_t n = sp.n_items;
+    j->items.alloc(n, s);
+    j->items2.alloc(n, s);
+    j->grp.alloc(n, s);
+    j->keys.alloc(n, s);
+    j->keys2.alloc(n, s);
+    j->pk.alloc(n, s);
+    j->pk2.alloc(n, s);
+    j->gstart.alloc(n, s);
+    j->rstart.alloc(n, s);
+    j->gmark.alloc(n, s);
+    j->rmark.alloc(n, s);
+    j->keep.alloc(n, s);
+    j->segflags.alloc(n, s);
+    j->seg_begin.alloc(n + 1, s);
+    PO_LAUNCH(k_iota, grid_for(n, 256), 256, 0, s, j->items.get(), n);
+    PO_CUDA(cudaMemcpyAsync(j->grp.get(), sp.d_grp_init, n * sizeof(uint32_t),
+                            cudaMemcpyDeviceToDevice, s));
+    size_t sort_bytes = 0, scan_bytes = 0, sel_bytes = 0;
+    int* nullcount = nullptr;
+    PO_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, j->keys.get(), j->keys2.get(),
+                                            j->items.get(), j->items2.get(), n, 0, 64, s));
+    PO_CUDA(cub::DeviceScan::InclusiveScan(nullptr, scan_bytes, j->gmark.get(), j->gstart.get(),
+                                           cub::Max(), n, s));
+    PO_CUDA(cub::DeviceSelect::Flagged(nullptr, sel_bytes, j->pk2.get(), j->keep.get(),
+                                       j->pk.get(), nullcount, n, s));
+    j->tb = std::max(sort_bytes, std::max(scan_bytes, sel_bytes));
+    j->tmp.alloc(j->tb, s);
+    j->A = n;
+    jobs.push_back(std::move(j));
   }
+  DevBuf<int> nsel(std::max<size_t>(1, 2 * jobs.size()), s);  // per job: active, segments
+  std::vector<int> hn(2 * jobs.size());
+  for (;;) {
+    bool any = false;
+    for (size_t q = 0; q < jobs.size(); ++q) {
+      Job& j = *jobs[q];
+      if (!j.A) continue;
+      any = true;
+      const uint32_t A = j.A;
+      const bool seg = j.k > 0;  // rounds >= 1: segmented sort inside groups
+      const uint32_t shift = seg ? 64u : j.shift0;
+      const uint32_t* start = seg ? nullptr : j.spec.d_grp_start;
+      PO_LAUNCH(k_build_keys, grid_for(A, 256), 256, 0, s, j.items.get(), j.grp.get(), A, j.k,
+                shift, j.key, j.keys.get());
+      size_t b = j.tb;
+      if (!seg) {
+        ProfScope ps("cub_radix_sort", s);
+        PO_CUDA(cub::DeviceRadixSort::SortPairs(j.tmp.get(), b, j.keys.get(), j.keys2.get(),
+                                                j.items.get(), j.items2.get(), A, 0, j.end_bit0, s));
+        PO_LAUNCH(k_marks, grid_for(A, 256), 256, 0, s, j.keys2.get(), A, shift, j.gmark.get(),
+                  j.rmark.get());
+      } else {
+        ProfScope ps("cub_segmented_sort", s);
+        if (std::getenv("PO_DEBUG_CHECKS")) {
+          std::vector<uint32_t> hs(j.nseg + 1);
+          PO_CUDA(cudaMemcpyAsync(hs.data(), j.seg_begin.get(), (j.nseg + 1) * 4,
+                                  cudaMemcpyDeviceToHost, s));
+          sync(s);
+          bool okk = hs[0] == 0 && hs[j.nseg] == A;
+          for (uint32_t z = 0; z < j.nseg; ++z) okk = okk && hs[z] < hs[z + 1];
+          if (!okk) {
+            fprintf(stderr, "[po debug] bad segments: job %zu round %u A=%u nseg=%u first=%u last=%u\n",
+                    q, j.k, A, j.nseg, hs[0], hs[j.nseg]);
+            for (uint32_t z = 0; z < std::min<uint32_t>(j.nseg, 8); ++z) fprintf(stderr, " %u", hs[z]);
+            fprintf(stderr, "\n");
+          }
+        }
+        size_t need = 0;
+        PO_CUDA(cub::DeviceSegmentedSort::StableSortPairs(
+            nullptr, need, j.keys.get(), j.keys2.get(), j.items.get(), j.items2.get(), int(A),
+            int(j.nseg), j.seg_begin.get(), j.seg_begin.get() + 1, s));
+        if (need > j.seg_tb) {
+          j.seg_tmp.alloc(need, s);
+          j.seg_tb = need;
+        }
+        PO_CUDA(cub::DeviceSegmentedSort::StableSortPairs(
+            j.seg_tmp.get(), need, j.keys.get(), j.keys2.get(), j.items.get(), j.items2.get(),
+            int(A), int(j.nseg), j.seg_begin.get(), j.seg_begin.get() + 1, s));
+        PO_LAUNCH(k_marks_seg, grid_for(A, 256), 256, 0, s, j.keys2.get(), j.segflags.get(), A,
+                  j.gmark.get(), j.rmark.get());
+      }
+      {
+        ProfScope ps("cub_scan", s);
+        b = j.tb;
+        PO_CUDA(cub::DeviceScan::InclusiveScan(j.tmp.get(), b, j.gmark.get(), j.gstart.get(),
+                                               cub::Max(), A, s));
+        b = j.tb;
+        PO_CUDA(cub::DeviceScan::InclusiveScan(j.tmp.get(), b, j.rmark.get(), j.rstart.get(),
+                                               cub::Max(), A, s));
+      }
+      PO_LAUNCH(k_resolve, grid_for(A, 256), 256, 0, s, j.keys2.get(), j.items2.get(),
+                j.gstart.get(), j.rstart.get(), A, j.k, shift, start, seg ? j.grp.get() : nullptr,
+                j.key, j.spec.d_out_pos, j.keep.get(), j.pk2.get());
+      {
+        ProfScope ps("cub_select", s);
+        b = j.tb;
+        PO_CUDA(cub::DeviceSelect::Flagged(j.tmp.get(), b, j.pk2.get(), j.keep.get(), j.pk.get(),
+                                           nsel.get() + 2 * q, A, s));
+      }
+      PO_LAUNCH(k_unpack, grid_for(A, 256), 256, 0, s, j.pk.get(), nsel.get() + 2 * q,
+                j.items.get(), j.grp.get());
+      // segments of the next round: runs of equal group start
+      PO_LAUNCH(k_seg_flags, grid_for(A, 256), 256, 0, s, j.grp.get(), nsel.get() + 2 * q, A,
+                j.segflags.get());
+      {
+        ProfScope ps("cub_select", s);
+        b = j.tb;
+        cub::CountingInputIterator<uint32_t> it(0);
+        PO_CUDA(cub::DeviceSelect::Flagged(j.tmp.get(), b, it, j.segflags.get(), j.seg_begin.get(),
+                                           nsel.get() + 2 * q + 1, A, s));
+      }
+      PO_LAUNCH(k_seg_end, 1, 1, 0, s, j.seg_begin.get(), nsel.get() + 2 * q + 1,
+                nsel.get() + 2 * q);
+      ++j.k;
+    }
+    if (!any) break;
+    PO_CUDA(cudaMemcpyAsync(hn.data(), nsel.get(), 2 * jobs.size() * sizeof(int),
+                            cudaMemcpyDeviceToHost, s));
+    sync(s);
+    if (debug_timing()) {
+      fprintf(stderr, "[po refine] round:");
+      for (size_t q = 0; q < jobs.size(); ++q)
+        fprintf(stderr, " job%zu %u->%d (%d groups)", q, jobs[q]->A, jobs[q]->A ? hn[2 * q] : 0,
+                jobs[q]->A ? hn[2 * q + 1] : 0);
+      fprintf(stderr, "\n");
+    }
+    for (size_t q = 0; q < jobs.size(); ++q)
+      if (jobs[q]->A) {
+        jobs[q]->A = uint32_t(hn[2 * q]);
+        jobs[q]->nseg = uint32_t(hn[2 * q + 1]);
+      }
+  }
+}
+
+void refine_sort(uint32_t n_items, const uint32_t* d_grp_init, uint32_t grp_max,
+                 const RefineKey& key, uint32_t* d_out_pos, cudaStream_t s, uint32_t row_chunk_bits) {
+  RefineJob j;
+  j.n_items = n_items;
+  j.d_grp_init = d_grp_init;
+  j.grp_max = grp_max;
+  j.key = key;
+  j.d_out_pos = d_out_pos;
+  j.row_chunk_bits = row_chunk_bits;
+  refine_sort_multi({j}, s);
 }
 
 }  // namespace po
