@@ -267,17 +267,35 @@ __device__ __forceinline__ uint64_t warp_hash_bytes(const uint8_t* a, uint64_t l
   return hash_finish(warp_sum_u64(sum), len);
 }
 
+// Whole-warp byte compare: all loads issued before any result is used
+// (no early exit), 2 words per lane per step.
 __device__ __forceinline__ bool warp_bytes_equal(const uint8_t* a, const uint8_t* b, uint64_t len,
                                                  const uint8_t* limit, uint32_t lane) {
-  bool ok = true;
+  uint64_t diff = 0;
   const uint64_t words = (len + 7) / 8;
-  for (uint64_t k = lane; k < words && ok; k += 32) {
-    const uint64_t rem = len - 8 * k;
-    const uint32_t take = rem >= 8 ? 8u : uint32_t(rem);
-    ok = mask_low_bytes(load8_unaligned(a + 8 * k, limit), take) ==
-         mask_low_bytes(load8_unaligned(b + 8 * k, limit), take);
+  for (uint64_t k0 = 0; k0 < words; k0 += 64) {
+    const uint64_t k1 = k0 + lane, k2 = k0 + 32 + lane;
+    uint64_t a1 = 0, b1 = 0, a2 = 0, b2 = 0;
+    if (k1 < words) {
+      a1 = load8_unaligned(a + 8 * k1, limit);
+      b1 = load8_unaligned(b + 8 * k1, limit);
+    }
+    if (k2 < words) {
+      a2 = load8_unaligned(a + 8 * k2, limit);
+      b2 = load8_unaligned(b + 8 * k2, limit);
+    }
+    if (k1 < words) {
+      const uint64_t rem = len - 8 * k1;
+      const uint32_t take = rem >= 8 ? 8u : uint32_t(rem);
+      diff |= mask_low_bytes(a1 ^ b1, take);
+    }
+    if (k2 < words) {
+      const uint64_t rem = len - 8 * k2;
+      const uint32_t take = rem >= 8 ? 8u : uint32_t(rem);
+      diff |= mask_low_bytes(a2 ^ b2, take);
+    }
   }
-  return __all_sync(0xffffffffu, ok);
+  return __all_sync(0xffffffffu, diff == 0);
 }
 
 __device__ __forceinline__ bool bytes_equal(const uint8_t* a, const uint8_t* b, uint64_t len,

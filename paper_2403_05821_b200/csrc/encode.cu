@@ -22,6 +22,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "internal.cuh"
 
@@ -246,6 +247,52 @@ __global__ void __launch_bounds__(kDictBlock) k_cell_hash(
   }
 }
 
+// K1 cell_scan (direct): one thread per cell, warps assigned column-major
+// over tiles of 32 rows so the 32 lanes of a warp hash cells of the same
+// column (similar lengths: converged loops). Each step issues 5 independent
+// aligned 8-byte loads (4 words of the cell), so every thread keeps several
+// loads in flight without any shared-memory staging or block barriers.
+__global__ void __launch_bounds__(256) k_cell_hash_cols(
+    const uint8_t* __restrict__ arena, const uint8_t* arena_end,
+    const uint64_t* __restrict__ offsets, uint64_t n, uint32_t m, uint64_t hash_mask,
+    unsigned long long* __restrict__ hashes) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t nwarps_total = ((n + 31) / 32) * m;
+  const uint64_t* lim =
+      reinterpret_cast<const uint64_t*>((reinterpret_cast<uintptr_t>(arena_end) + 7) & ~uintptr_t(7));
+  for (uint64_t wid = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5; wid < nwarps_total;
+       wid += (uint64_t(gridDim.x) * blockDim.x) >> 5) {
+    const uint64_t tile = wid / m;
+    const uint32_t c = uint32_t(wid - tile * m);
+    const uint64_t r = tile * 32 + lane;
+    if (r >= n) continue;
+    const uint64_t i = r * m + c;
+    const uint64_t o0 = offsets[i], len = offsets[i + 1] - o0;
+    const uintptr_t ad = reinterpret_cast<uintptr_t>(arena + o0);
+    const uint64_t* p = reinterpret_cast<const uint64_t*>(ad & ~uintptr_t(7));
+    const uint32_t sh = uint32_t(ad & 7) * 8;
+    const uint64_t words = (len + 7) / 8;
+    uint64_t sum = 0;
+    for (uint64_t k = 0; k < words; k += 4) {
+      uint64_t w[5];
+#pragma unroll
+      for (int u = 0; u < 5; ++u) w[u] = (p + k + u < lim) ? __ldg(p + k + u) : 0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint64_t kk = k + u;
+        if (kk < words) {
+          uint64_t x = sh ? ((w[u] >> sh) | (w[u + 1] << (64 - sh))) : w[u];
+          const uint64_t rem = len - 8 * kk;
+          if (rem < 8) x = mask_low_bytes(x, uint32_t(rem));
+          sum += word_term(x, kk);
+        }
+      }
+    }
+    const uint64_t h = hash_finish(sum, len) & hash_mask;
+    hashes[i] = h ? h : 1;
+  }
+}
+
 __global__ void k_cell_hash_global(const uint8_t* __restrict__ arena, const uint8_t* arena_end,
                                    const uint64_t* __restrict__ offsets, uint64_t total,
                                    uint64_t hash_mask, unsigned long long* __restrict__ hashes) {
@@ -301,53 +348,74 @@ __global__ void __launch_bounds__(256) k_dict_probe(
 // step). A mismatch — two different strings with the same 64-bit hash —
 // flags the cell for K2c.
 // ---------------------------------------------------------------------------
+// Unaligned 4-word step of a byte string: 5 independent aligned loads.
+struct Step4 {
+  uint64_t w[4];
+};
+__device__ __forceinline__ Step4 load_step4(const uint64_t* p, uint32_t sh, const uint64_t* lim) {
+  uint64_t a[5];
+#pragma unroll
+  for (int u = 0; u < 5; ++u) a[u] = (p + u < lim) ? __ldg(p + u) : 0;
+  Step4 r;
+#pragma unroll
+  for (int u = 0; u < 4; ++u) r.w[u] = sh ? ((a[u] >> sh) | (a[u + 1] << (64 - sh))) : a[u];
+  return r;
+}
+
 __global__ void __launch_bounds__(256) k_dict_verify(
     const uint8_t* __restrict__ arena, const uint8_t* arena_end,
-    const uint64_t* __restrict__ offsets, uint64_t total, uint32_t m, uint64_t cap,
+    const uint64_t* __restrict__ offsets, uint64_t n, uint32_t m, uint64_t cap,
     const uint32_t* __restrict__ reps, const unsigned long long* __restrict__ repoffs,
     const uint32_t* __restrict__ slot_of_cell, uint32_t* collided, uint32_t* n_collided) {
-  // A warp takes 32 consecutive cells. Cells up to 64 bytes are compared by
-  // their own lane; longer ones one at a time by the whole warp (lane l takes
-  // words l, l+32, ...: coalesced loads of both strings).
-  constexpr uint64_t kShort = 64;
+  // Warps take 32 rows of one column (similar lengths); every lane compares
+  // its own cell with the representative, 4 words per step with all 10 loads
+  // in flight.
   const uint32_t lane = threadIdx.x & 31;
-  const uint64_t warp0 = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
-  const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
-  for (uint64_t base = warp0 * 32; base < total; base += nwarps * 32) {
-    const uint64_t i = base + lane;
-    bool need = false;
-    uint64_t o0 = 0, len = 0, q0 = 0;
-    if (i < total) {
-      const uint64_t r = i / m;
-      const uint32_t c = uint32_t(i - r * m);
-      const uint64_t sidx = uint64_t(c) * cap + slot_of_cell[i];
-      const uint32_t rep = reps[sidx];
-      if (rep != uint32_t(r)) {
-        o0 = offsets[i];
-        len = offsets[i + 1] - o0;
-        const uint64_t pk = repoffs[sidx];
-        q0 = pk >> 24;
-        uint64_t ql = pk & kLongRep;
-        if (ql == kLongRep) {
-          const uint64_t j = uint64_t(rep) * m + c;
-          ql = offsets[j + 1] - offsets[j];
+  const uint64_t nwarps_total = ((n + 31) / 32) * m;
+  const uint64_t* lim =
+      reinterpret_cast<const uint64_t*>((reinterpret_cast<uintptr_t>(arena_end) + 7) & ~uintptr_t(7));
+  for (uint64_t wid = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5; wid < nwarps_total;
+       wid += (uint64_t(gridDim.x) * blockDim.x) >> 5) {
+    const uint64_t tile = wid / m;
+    const uint32_t c = uint32_t(wid - tile * m);
+    const uint64_t r = tile * 32 + lane;
+    if (r >= n) continue;
+    const uint64_t i = r * m + c;
+    const uint64_t sidx = uint64_t(c) * cap + slot_of_cell[i];
+    const uint32_t rep = reps[sidx];
+    if (rep == uint32_t(r)) continue;  // the representative itself
+    const uint64_t o0 = offsets[i], len = offsets[i + 1] - o0;
+    const uint64_t pk = repoffs[sidx];
+    const uint64_t q0 = pk >> 24;
+    uint64_t ql = pk & kLongRep;
+    if (ql == kLongRep) {
+      const uint64_t j = uint64_t(rep) * m + c;
+      ql = offsets[j + 1] - offsets[j];
+    }
+    bool eq = ql == len;
+    if (eq && len) {
+      const uintptr_t aa = reinterpret_cast<uintptr_t>(arena + o0);
+      const uintptr_t bb = reinterpret_cast<uintptr_t>(arena + q0);
+      const uint64_t* pa = reinterpret_cast<const uint64_t*>(aa & ~uintptr_t(7));
+      const uint64_t* pb = reinterpret_cast<const uint64_t*>(bb & ~uintptr_t(7));
+      const uint32_t sa = uint32_t(aa & 7) * 8, sb = uint32_t(bb & 7) * 8;
+      const uint64_t words = (len + 7) / 8;
+      for (uint64_t k = 0; k < words && eq; k += 4) {
+        const Step4 x = load_step4(pa + k, sa, lim);
+        const Step4 y = load_step4(pb + k, sb, lim);
+        uint64_t d = 0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const uint64_t kk = k + u;
+          if (kk < words) {
+            const uint64_t rem = len - 8 * kk;
+            d |= mask_low_bytes(x.w[u] ^ y.w[u], rem >= 8 ? 8u : uint32_t(rem));
+          }
         }
-        if (ql != len) collided[atomicAdd(n_collided, 1u)] = uint32_t(i);
-        else need = len > 0;
+        eq = d == 0;
       }
     }
-    const bool lng = need && len > kShort;
-    if (need && !lng &&
-        !equal_cell_rep<false>(arena + o0, arena_end, arena + q0, arena_end, len))
-      collided[atomicAdd(n_collided, 1u)] = uint32_t(i);
-    for (unsigned lm = __ballot_sync(0xffffffffu, lng); lm; lm &= lm - 1) {
-      const int src = __ffs(lm) - 1;
-      const uint64_t a = __shfl_sync(0xffffffffu, o0, src);
-      const uint64_t b = __shfl_sync(0xffffffffu, q0, src);
-      const uint64_t l = __shfl_sync(0xffffffffu, len, src);
-      const bool eq = warp_bytes_equal(arena + a, arena + b, l, arena_end, lane);
-      if (int(lane) == src && !eq) collided[atomicAdd(n_collided, 1u)] = uint32_t(i);
-    }
+    if (!eq) collided[atomicAdd(n_collided, 1u)] = uint32_t(i);
   }
 }
 
@@ -669,34 +737,37 @@ void encode(const DeviceTable& t, int tok, int scoring, cudaStream_t s, Encoded&
   {
     // K1: hash every cell. Tiles of whole rows sized so a typical tile uses
     // about 60% of a staging buffer.
-    const uint32_t stage = 32 * 1024;
+    // 32 rows per tile when a row has <= 8 cells: each warp then hashes 32
+    // cells of ONE column (similar lengths, converged loops).
     const double row_bytes = double(t.arena_bytes) / double(n);
-    uint32_t rows_per_tile = std::max<uint32_t>(1, kDictBlock / uint32_t(m));
+    uint32_t rows_per_tile = m <= kDictBlock / 32 ? 32u : std::max<uint32_t>(1, kDictBlock / uint32_t(m));
+    uint32_t stage = 32 * 1024;
+    while (stage < 96 * 1024 && row_bytes * rows_per_tile > stage * 0.6) stage += 16 * 1024;
     while (rows_per_tile > 1 && row_bytes * rows_per_tile > stage * 0.6) rows_per_tile >>= 1;
     const uint32_t smem = 2 * ((stage + 64 + 127) & ~127u);
-    static bool attr_set = false;
-    if (!attr_set) {
+    static int attr_set = 0;
+    if (attr_set < int(smem)) {
       PO_CUDA(cudaFuncSetAttribute(k_cell_hash, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    int(smem)));
-      attr_set = true;
+      attr_set = int(smem);
     }
     DevBuf<unsigned long long> hashes(cells, s);
-    if (m <= kDictBlock) {
+    if (std::getenv("PO_HASH_TMA") && m <= kDictBlock) {
       const uint64_t ntiles = (cells + rows_per_tile * m - 1) / (rows_per_tile * m);
       PO_LAUNCH(k_cell_hash, unsigned(std::min<uint64_t>(ntiles, uint64_t(kSMs) * 3)), kDictBlock,
                 smem, s, t.arena, arena_end, t.offsets, cells, uint32_t(m), rows_per_tile, stage,
                 hmask, hashes.get());
-    } else {  // very wide rows: one thread per cell straight from global memory
-      PO_LAUNCH(k_cell_hash_global, grid_for(cells, 256, 16), 256, 0, s, t.arena, arena_end,
-                t.offsets, cells, hmask, hashes.get());
+    } else {
+      PO_LAUNCH(k_cell_hash_cols, grid_for(((n + 31) / 32) * m * 32, 256, 8), 256, 0, s, t.arena,
+                arena_end, t.offsets, n, uint32_t(m), hmask, hashes.get());
     }
     // K2a/K2b: probe + claim, then byte verification of every duplicate
     PO_LAUNCH(k_dict_probe, grid_for(cells, 256, 32), 256, 0, s, hashes.get(), t.offsets, cells,
               uint32_t(m), cap, keys.get(), reps.get(), repoffs.get(), slot_of_cell.get());
     DevBuf<uint32_t> collided(cells, s), ncol(1, s);
     ncol.zero();
-    PO_LAUNCH(k_dict_verify, grid_for(cells, 256, 32), 256, 0, s, t.arena, arena_end, t.offsets,
-              cells, uint32_t(m), cap, reps.get(), repoffs.get(), slot_of_cell.get(),
+    PO_LAUNCH(k_dict_verify, grid_for(((n + 31) / 32) * m * 32, 256, 8), 256, 0, s, t.arena,
+              arena_end, t.offsets, n, uint32_t(m), cap, reps.get(), repoffs.get(), slot_of_cell.get(),
               collided.get(), ncol.get());
     uint32_t hcol = 0;
     ncol.download(&hcol, 1);

@@ -463,18 +463,31 @@ __global__ void __launch_bounds__(256) k_leaf_stats(
   if (priv)
     for (uint32_t c = threadIdx.x; c < 2 * m; c += blockDim.x) sh[c] = 0;
   __syncthreads();
-  for (uint64_t e = w.lo + threadIdx.x; e < w.hi; e += blockDim.x) {
-    uint32_t c, v;
-    if (!decode_entry(sl.t, colbase, m, e, c, v)) continue;
-    const uint32_t cnt = sl.t.cnt[e];
-    if (cnt == 0 || !mask_has(mask, c)) continue;
-    const unsigned long long l = uint64_t(cnt) * vlen[colbase[c] + v];
-    if (priv) {
-      atomicAdd(&sh[c], 1ull);
-      atomicAdd(&sh[m + c], l);
+  // hashed table: entries of mixed columns; lanes with the same column are
+  // merged per warp before the shared-memory atomics
+  for (uint64_t base = w.lo; base < w.hi; base += blockDim.x) {
+    const uint64_t e = base + threadIdx.x;
+    uint32_t c = 0xFFFFFFFFu, v = 0;
+    unsigned long long l = 0;
+    if (e < w.hi && decode_entry(sl.t, colbase, m, e, c, v)) {
+      const uint32_t cnt = sl.t.cnt[e];
+      if (cnt == 0 || !mask_has(mask, c)) c = 0xFFFFFFFFu;
+      else l = uint64_t(cnt) * vlen[colbase[c] + v];
     } else {
-      atomicAdd(&card[uint64_t(w.slot) * m + c], 1ull);
-      atomicAdd(&tot[uint64_t(w.slot) * m + c], l);
+      c = 0xFFFFFFFFu;
+    }
+    const unsigned grp = __match_any_sync(0xffffffffu, c);
+    auto g = cg::labeled_partition(cg::tiled_partition<32>(cg::this_thread_block()), c);
+    l = cg::reduce(g, l, cg::plus<unsigned long long>());
+    if (c != 0xFFFFFFFFu && int(threadIdx.x & 31) == __ffs(grp) - 1) {
+      const unsigned long long k = __popc(grp);
+      if (priv) {
+        atomicAdd(&sh[c], k);
+        atomicAdd(&sh[m + c], l);
+      } else {
+        atomicAdd(&card[uint64_t(w.slot) * m + c], k);
+        atomicAdd(&tot[uint64_t(w.slot) * m + c], l);
+      }
     }
   }
   if (priv) {
@@ -550,7 +563,7 @@ int classify(const Node& nd, const po_ggr_config& cfg) {
   return SCAN;
 }
 
-constexpr uint64_t kWorkChunk = 8192;
+constexpr uint64_t kWorkChunk = 2048;
 
 bool debug_checks() {
   static const bool on = [] {
@@ -901,7 +914,7 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
       std::vector<uint64_t> seg(ns + 1, 0);
       std::vector<uint32_t> split_nodes(ns);
       std::vector<AggTask> tasks;
-      constexpr uint64_t kRowsPerTask = 8 * kAggBlock;
+      constexpr uint64_t kRowsPerTask = 2 * kAggBlock;
       for (uint32_t j = 0; j < ns; ++j) {
         hsp[j] = splits[j].d;
         split_nodes[j] = uint32_t(splits[j].node);
