@@ -463,28 +463,20 @@ __global__ void k_distinct_info(const uint32_t* col_sel, uint64_t cnt, uint64_t 
   }
 }
 
-__global__ void k_grp_from_col(const uint32_t* col, const uint64_t* colbase, uint64_t D,
-                               uint32_t* grp) {
-  for (uint64_t d = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; d < D;
-       d += uint64_t(gridDim.x) * blockDim.x)
-    grp[d] = uint32_t(colbase[col[d]]);
-}
 
-// raw_pos[d] -> vid; scatter representative row / column / escaped rank
-// into raw (vid) order.
-__global__ void k_scatter_raw(const uint32_t* raw_pos, const uint32_t* esc_pos,
-                              const uint32_t* d_col, const uint32_t* d_row,
+// pos[d] (escaped order) -> vid; scatter representative row / column into
+// vid order.
+__global__ void k_scatter_pos(const uint32_t* pos_of, const uint32_t* d_col, const uint32_t* d_row,
                               const uint32_t* sel_slot, const uint64_t* colbase, uint64_t D,
                               uint64_t cap, uint32_t* slot2vid, uint32_t* row_by_pos,
-                              uint32_t* col_by_pos, uint32_t* esc_rank) {
+                              uint32_t* col_by_pos) {
   for (uint64_t d = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; d < D;
        d += uint64_t(gridDim.x) * blockDim.x) {
-    const uint32_t p = raw_pos[d];
+    const uint32_t p = pos_of[d];
     const uint32_t c = d_col[d];
     slot2vid[uint64_t(c) * cap + sel_slot[d]] = uint32_t(p - colbase[c]);
     row_by_pos[p] = d_row[d];
     col_by_pos[p] = c;
-    esc_rank[p] = uint32_t(esc_pos[d] - colbase[c]);
   }
 }
 
@@ -714,6 +706,9 @@ void encode(const DeviceTable& t, int tok, int scoring, cudaStream_t s, Encoded&
             uint32_t hash_bits_debug) {
   e.n = t.n;
   e.m = t.m;
+  e.arena = t.arena;
+  e.offsets = t.offsets;
+  e.arena_bytes = t.arena_bytes;
   e.card.assign(t.m, 0);
   e.colbase.assign(t.m + 1, 0);
   e.total_len.assign(t.m, 0);
@@ -819,49 +814,41 @@ void encode(const DeviceTable& t, int tok, int scoring, cudaStream_t s, Encoded&
               sel.get(), d_col.get(), d_row.get());
   stage_sel.release();
 
-  // Raw-byte order of the distinct values of each column -> vid.
-  DevBuf<uint32_t> grp(D, s), raw_pos(D, s);
-  PO_LAUNCH(k_grp_from_col, grid_for(D, 256), 256, 0, s, d_col.get(), e.d_colbase.get(), D,
-            grp.get());
-  RefineKey rk;
-  rk.kind = 0;
-  rk.arena = t.arena;
-  rk.arena_bytes = t.arena_bytes;
-  rk.offsets = t.offsets;
-  rk.item_cell_row = d_row.get();
-  rk.item_col = d_col.get();
-  rk.m = uint32_t(m);
-  timing_mark("distinct", s);
-  // Escaped fragment-key order (json_escape(v) + '"') of the same items; both
-  // rank sorts advance in lockstep.
-  RefineKey ek = rk;
-  ek.kind = 1;
+  // Escaped fragment-key order (json_escape(v) + '"') of the distinct values
+  // of each column -> vid. Raw-byte order is only needed for candidate ties
+  // and single-column leaves; the solver ranks those few values on demand.
   DevBuf<uint32_t> esc_pos(D, s);
+  RefineKey ek;
+  ek.kind = 1;
+  ek.arena = t.arena;
+  ek.arena_bytes = t.arena_bytes;
+  ek.offsets = t.offsets;
+  ek.item_cell_row = d_row.get();
+  ek.item_col = d_col.get();
+  ek.m = uint32_t(m);
+  timing_mark("distinct", s);
   {
     // round 0 groups the distinct values by column index
     std::vector<uint32_t> cb32(m);
     for (uint32_t c = 0; c < m; ++c) cb32[c] = uint32_t(e.colbase[c]);
     DevBuf<uint32_t> d_cb32 = to_device(cb32, s);
-    RefineJob jr, je;
-    jr.n_items = je.n_items = uint32_t(D);
-    jr.d_grp_init = je.d_grp_init = d_col.get();
-    jr.d_grp_start = je.d_grp_start = d_cb32.get();
-    jr.n_groups = je.n_groups = uint32_t(m);
-    jr.grp_max = je.grp_max = uint32_t(D);
-    jr.key = rk;
+    RefineJob je;
+    je.n_items = uint32_t(D);
+    je.d_grp_init = d_col.get();
+    je.d_grp_start = d_cb32.get();
+    je.n_groups = uint32_t(m);
+    je.grp_max = uint32_t(D);
     je.key = ek;
-    jr.d_out_pos = raw_pos.get();
     je.d_out_pos = esc_pos.get();
-    refine_sort_multi({jr, je}, s);
+    refine_sort_multi({je}, s);
   }
-  timing_mark("rank_sorts", s);
+  timing_mark("rank_sort", s);
 
   DevBuf<uint32_t> slot2vid(m * cap, s), col_by_pos(D, s);
   e.rep_row.alloc(D, s);
-  e.esc_rank.alloc(D, s);
-  PO_LAUNCH(k_scatter_raw, grid_for(D, 256), 256, 0, s, raw_pos.get(), esc_pos.get(), d_col.get(),
-            d_row.get(), sel.get(), e.d_colbase.get(), D, cap, slot2vid.get(), e.rep_row.get(),
-            col_by_pos.get(), e.esc_rank.get());
+  PO_LAUNCH(k_scatter_pos, grid_for(D, 256), 256, 0, s, esc_pos.get(), d_col.get(), d_row.get(),
+            sel.get(), e.d_colbase.get(), D, cap, slot2vid.get(), e.rep_row.get(),
+            col_by_pos.get());
   keys.release();
   flags.release();
 

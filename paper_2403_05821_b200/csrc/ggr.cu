@@ -124,19 +124,32 @@ struct Cand {
   uint64_t count;  // 0 = no candidate
   uint32_t col;
   uint32_t vid;
+  uint64_t ties;   // entries sharing this (score, count, column) key
+  uint64_t pad;
 };
 
-// Candidate::better_than (ggr.hpp:189-197): exact rational compare of
-// numer/count via u128 cross products (wrapping exactly like the reference),
-// then larger count, lower column, smaller value (vid == raw-byte rank).
-__device__ __forceinline__ bool beats(const Cand& a, const Cand& b) {
-  if (a.count == 0) return false;
-  if (b.count == 0) return true;
-  u128 l = a.numer * u128(b.count), r = b.numer * u128(a.count);
-  if (l != r) return l > r;
-  if (a.count != b.count) return a.count > b.count;
-  if (a.col != b.col) return a.col < b.col;
-  return a.vid < b.vid;
+// Candidate::better_than (ggr.hpp:189-197) up to its last criterion: exact
+// rational compare of numer/count via u128 cross products (wrapping exactly
+// like the reference), then larger count, then lower column. Entries equal on
+// that key are merged and counted; the final tie-break — smaller raw bytes —
+// is resolved afterwards on the tied values only (vids are ranks in the
+// escaped order, not in raw-byte order). The merge is associative and
+// commutative, so any reduction order gives the same result.
+__device__ __forceinline__ Cand merge(const Cand& a, const Cand& b) {
+  if (a.count == 0) return b;
+  if (b.count == 0) return a;
+  const u128 l = a.numer * u128(b.count), r = b.numer * u128(a.count);
+  if (l != r) return l > r ? a : b;
+  if (a.count != b.count) return a.count > b.count ? a : b;
+  if (a.col != b.col) return a.col < b.col ? a : b;
+  Cand c = a;
+  c.ties = a.ties + b.ties;
+  c.vid = a.vid < b.vid ? a.vid : b.vid;
+  return c;
+}
+
+__device__ __forceinline__ bool same_key(const Cand& a, const Cand& b) {
+  return a.count == b.count && a.col == b.col && a.numer == b.numer;
 }
 
 __device__ __forceinline__ Cand shfl_cand(const Cand& a, int delta) {
@@ -148,6 +161,8 @@ __device__ __forceinline__ Cand shfl_cand(const Cand& a, int delta) {
   o.count = __shfl_down_sync(0xffffffffu, a.count, delta);
   o.col = __shfl_down_sync(0xffffffffu, a.col, delta);
   o.vid = __shfl_down_sync(0xffffffffu, a.vid, delta);
+  o.ties = __shfl_down_sync(0xffffffffu, a.ties, delta);
+  o.pad = 0;
   return o;
 }
 
@@ -187,11 +202,7 @@ __global__ void __launch_bounds__(kArgBlock) k_argmax(
   const ScanSlot sl = slots[w.slot];
   const uint32_t* mask = masks + sl.mask_off;
   const uint32_t* wt = weights + sl.w_off;
-  Cand best;
-  best.numer = 0;
-  best.count = 0;
-  best.col = 0;
-  best.vid = 0;
+  Cand best{};
   unsigned long long ncand = 0;
   for (uint64_t e = w.lo + threadIdx.x; e < w.hi; e += blockDim.x) {
     uint32_t c, v;
@@ -209,12 +220,13 @@ __global__ void __launch_bounds__(kArgBlock) k_argmax(
     cd.count = cnt;
     cd.col = c;
     cd.vid = v;
-    if (beats(cd, best)) best = cd;
+    cd.ties = 1;
+    cd.pad = 0;
+    best = merge(best, cd);
   }
-  // block reduction (any order: beats is a total order)
+  // block reduction (any order: merge is associative and commutative)
   for (int d = 16; d > 0; d >>= 1) {
-    Cand o = shfl_cand(best, d);
-    if (beats(o, best)) best = o;
+    best = merge(best, shfl_cand(best, d));
     ncand += __shfl_down_sync(0xffffffffu, ncand, d);
   }
   __shared__ Cand sb[kArgBlock / 32];
@@ -229,7 +241,7 @@ __global__ void __launch_bounds__(kArgBlock) k_argmax(
     Cand b = sb[0];
     unsigned long long n = sc[0];
     for (int i = 1; i < kArgBlock / 32; ++i) {
-      if (beats(sb[i], b)) b = sb[i];
+      b = merge(b, sb[i]);
       n += sc[i];
     }
     partial[blockIdx.x] = b;
@@ -237,24 +249,87 @@ __global__ void __launch_bounds__(kArgBlock) k_argmax(
   }
 }
 
+// Every entry of a tied slot whose (score, count, column) key equals the
+// slot's best: its value is appended to the slot's segment for the raw-byte
+// tie-break (ggr.hpp:196).
+__global__ void k_collect_ties(const WorkItem* __restrict__ work, const ScanSlot* __restrict__ slots,
+                               const uint32_t* __restrict__ masks,
+                               const uint32_t* __restrict__ weights,
+                               const uint64_t* __restrict__ colbase,
+                               const uint64_t* __restrict__ vlen, uint32_t m, uint32_t K,
+                               const Cand* __restrict__ best, const int32_t* __restrict__ tie_group,
+                               const uint32_t* __restrict__ tie_off, uint32_t* cursor,
+                               const uint32_t* __restrict__ rep_row, uint32_t* t_row,
+                               uint32_t* t_col, uint32_t* t_vid, uint32_t* t_grp) {
+  const WorkItem w = work[blockIdx.x];
+  const int32_t g = tie_group[w.slot];
+  if (g < 0) return;
+  const ScanSlot sl = slots[w.slot];
+  const uint32_t* mask = masks + sl.mask_off;
+  const uint32_t* wt = weights + sl.w_off;
+  const Cand b = best[w.slot];
+  for (uint64_t e = w.lo + threadIdx.x; e < w.hi; e += blockDim.x) {
+    uint32_t c, v;
+    if (!decode_work(w, sl.t, colbase, m, e, c, v)) continue;
+    const uint32_t cnt = sl.t.cnt[e];
+    if (cnt != b.count || c != b.col || !mask_has(mask, c)) continue;
+    const uint64_t vl = vlen[colbase[c] + v];
+    uint64_t ptot = 0;
+    for (uint32_t k = 0; k < K; ++k)
+      if (wt[c * K + k]) ptot += uint64_t(wt[c * K + k]) * sl.t.psum[e * K + k];
+    if ((u128(vl) * vl * cnt + ptot) * u128(cnt - 1) != b.numer) continue;
+    const uint32_t at = tie_off[g] + atomicAdd(&cursor[g], 1u);
+    t_row[at] = rep_row[colbase[c] + v];
+    t_col[at] = c;
+    t_vid[at] = v;
+    t_grp[at] = uint32_t(g);
+  }
+}
+
+// After the raw-byte sort of each tie group: the value at the group's first
+// position is the smallest.
+__global__ void k_pick_min(const uint32_t* pos, const uint32_t* t_grp, const uint32_t* t_vid,
+                           const uint32_t* tie_off, uint32_t total, uint32_t* min_vid) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x)
+    if (pos[i] == tie_off[t_grp[i]]) min_vid[t_grp[i]] = t_vid[i];
+}
+
+// Rows of single-column leaves (ggr.hpp:221-231), for their raw-byte sort.
+__global__ void k_raw1_flags(const uint32_t* row_leaf, uint64_t n, const int32_t* leaf_raw1_col,
+                             uint8_t* flags) {
+  for (uint64_t r = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; r < n;
+       r += uint64_t(gridDim.x) * blockDim.x)
+    flags[r] = leaf_raw1_col[row_leaf[r]] >= 0 ? 1 : 0;
+}
+
+__global__ void k_raw1_items(const uint32_t* rows, uint32_t cnt, const uint32_t* row_leaf,
+                             const int32_t* leaf_raw1_col, uint32_t* grp, uint32_t* col) {
+  for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < cnt; k += gridDim.x * blockDim.x) {
+    const uint32_t l = row_leaf[rows[k]];
+    grp[k] = l;
+    col[k] = uint32_t(leaf_raw1_col[l]);
+  }
+}
+
+__global__ void k_raw1_scatter(const uint32_t* rows, const uint32_t* raw_pos, uint32_t cnt,
+                               uint32_t* pos) {
+  for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < cnt; k += gridDim.x * blockDim.x)
+    pos[rows[k]] = raw_pos[k];
+}
+
 // One block per scanning node: reduce its per-chunk partials.
 __global__ void __launch_bounds__(kArgBlock) k_argmax_final(
     const Cand* partial, const unsigned long long* partial_cands, const uint32_t* slot_work_off,
     Cand* out, unsigned long long* out_cands) {
   const uint32_t s = blockIdx.x;
-  Cand b;
-  b.numer = 0;
-  b.count = 0;
-  b.col = 0;
-  b.vid = 0;
+  Cand b{};
   unsigned long long n = 0;
   for (uint32_t i = slot_work_off[s] + threadIdx.x; i < slot_work_off[s + 1]; i += blockDim.x) {
-    if (beats(partial[i], b)) b = partial[i];
+    b = merge(b, partial[i]);
     n += partial_cands[i];
   }
   for (int d = 16; d > 0; d >>= 1) {
-    Cand o = shfl_cand(b, d);
-    if (beats(o, b)) b = o;
+    b = merge(b, shfl_cand(b, d));
     n += __shfl_down_sync(0xffffffffu, n, d);
   }
   __shared__ Cand sb[kArgBlock / 32];
@@ -267,7 +342,7 @@ __global__ void __launch_bounds__(kArgBlock) k_argmax_final(
   __syncthreads();
   if (threadIdx.x == 0) {
     for (int i = 1; i < kArgBlock / 32; ++i) {
-      if (beats(sb[i], sb[0])) sb[0] = sb[i];
+      sb[0] = merge(sb[0], sb[i]);
       sc[0] += sc[i];
     }
     out[s] = sb[0];
@@ -820,6 +895,56 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
     pending.clear();
     if (frontier.empty()) break;
 
+    // ---- raw-byte tie-break among candidates equal on (score, count,
+    // column) (ggr.hpp:196), only for nodes that will split ----
+    {
+      std::vector<int32_t> tie_group(std::max<uint32_t>(nslots, 1), -1);
+      std::vector<uint32_t> tie_off{0}, tie_slot;
+      for (uint32_t i = 0; i < nslots; ++i) {
+        const Cand& b = hbest[i];
+        const bool stops = b.count == 0 || b.numer == 0 ||
+                           b.numer < u128(cfg.hitcount_stop_threshold) * u128(b.count);
+        if (stops || b.ties <= 1) continue;
+        tie_group[i] = int32_t(tie_slot.size());
+        tie_slot.push_back(i);
+        tie_off.push_back(tie_off.back() + uint32_t(b.ties));
+      }
+      if (!tie_slot.empty()) {
+        const uint32_t ng = uint32_t(tie_slot.size()), total = tie_off.back();
+        auto d_tg = to_device(tie_group, s);
+        auto d_toff = to_device(tie_off, s);
+        DevBuf<uint32_t> cursor(ng, s), t_row(total, s), t_col(total, s), t_vid(total, s),
+            t_grp(total, s), t_pos(total, s), min_vid(ng, s);
+        cursor.zero();
+        PO_LAUNCH(k_collect_ties, unsigned(L.work.size()), kArgBlock, 0, s,
+                  reinterpret_cast<WorkItem*>(dp + o_work), reinterpret_cast<ScanSlot*>(dp + o_slots),
+                  reinterpret_cast<uint32_t*>(dp + o_masks), reinterpret_cast<uint32_t*>(dp + o_w),
+                  colbase, vlen, m, K, d_best, d_tg.get(), d_toff.get(), cursor.get(),
+                  e.rep_row.get(), t_row.get(), t_col.get(), t_vid.get(), t_grp.get());
+        RefineJob tj;
+        tj.n_items = total;
+        tj.d_grp_init = t_grp.get();
+        tj.d_grp_start = d_toff.get();
+        tj.n_groups = ng;
+        tj.grp_max = total;
+        tj.key.kind = 0;  // raw bytes
+        tj.key.arena = e.arena;
+        tj.key.arena_bytes = e.arena_bytes;
+        tj.key.offsets = e.offsets;
+        tj.key.item_cell_row = t_row.get();
+        tj.key.item_col = t_col.get();
+        tj.key.m = m;
+        tj.d_out_pos = t_pos.get();
+        refine_sort_multi({tj}, s);
+        PO_LAUNCH(k_pick_min, grid_for(total, 256), 256, 0, s, t_pos.get(), t_grp.get(),
+                  t_vid.get(), d_toff.get(), total, min_vid.get());
+        std::vector<uint32_t> hmin(ng);
+        min_vid.download(hmin.data(), ng);
+        sync(s);
+        for (uint32_t g = 0; g < ng; ++g) hbest[tie_slot[g]].vid = hmin[g];
+      }
+    }
+
     // ---- host decisions (ggr.hpp:276-301) ----
     std::vector<int> next;
     struct SplitH {
@@ -1025,8 +1150,8 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
               h_leaf_orders.begin() + size_t(l) * m);
     // sort keys of the leaf
     std::vector<std::pair<int, uint8_t>> keys;  // (field, kind)
-    if (nd.kind == RAW1) keys.push_back({nd.cols[0], uint8_t(0)});  // raw bytes (ggr.hpp:221-231)
-    else if (nd.kind == FALLBACK)  // fragment keys (ggr.hpp:340-350)
+    // single-column leaves are ordered by raw bytes in a separate string job
+    if (nd.kind == FALLBACK)  // fragment keys (ggr.hpp:340-350)
       for (int f : nd.leaf_order) keys.push_back({f, uint8_t(1)});
     leaf_chunk_off[l] = uint32_t(ks.chunk_nkeys.size());
     leaf_nchunks[l] = ks.add_leaf(keys, e.card, cap0, cap);
@@ -1052,7 +1177,6 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
   RK.kind = 2;
   RK.m = m;
   RK.vid = e.vid.get();
-  RK.esc_rank = e.esc_rank.get();
   RK.colbase = colbase;
   RK.row_leaf = row_leaf.get();
   RK.leaf_chunk_off = d_lco.get();
@@ -1080,7 +1204,62 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
   leaf_job.d_out_pos = pos.get();
   leaf_job.row_chunk_bits0 = ks.widest0;
   leaf_job.row_chunk_bits = ks.widest;
-  refine_sort_multi({leaf_job, fb_sort.job()}, s);
+  // single-column leaves (ggr.hpp:221-231): their rows, ascending row id, are
+  // sorted by the raw bytes of the one column; positions overwrite the main
+  // job's (which leaves them in row order)
+  std::vector<int32_t> leaf_raw1_col(std::max<uint32_t>(nleaves, 1), -1);
+  bool any_raw1 = false;
+  for (uint32_t l = 0; l < nleaves; ++l)
+    if (nodes[leaf_nodes[l]].kind == RAW1) {
+      leaf_raw1_col[l] = nodes[leaf_nodes[l]].cols[0];
+      any_raw1 = true;
+    }
+  DevBuf<uint32_t> raw_rows, raw_grp, raw_col, raw_pos;
+  uint32_t n_raw = 0;
+  std::vector<RefineJob> sort_jobs{leaf_job, fb_sort.job()};
+  if (any_raw1) {
+    auto d_lrc = to_device(leaf_raw1_col, s);
+    DevBuf<uint8_t> flags(n, s);
+    PO_LAUNCH(k_raw1_flags, grid_for(n, 256), 256, 0, s, row_leaf.get(), n, d_lrc.get(),
+              flags.get());
+    raw_rows.alloc(n, s);
+    DevBuf<int> nsel(1, s);
+    cub::CountingInputIterator<uint32_t> it(0);
+    size_t tb = 0;
+    PO_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, it, flags.get(), raw_rows.get(), nsel.get(),
+                                       int(n), s));
+    DevBuf<uint8_t> tmp(tb, s);
+    PO_CUDA(cub::DeviceSelect::Flagged(tmp.get(), tb, it, flags.get(), raw_rows.get(), nsel.get(),
+                                       int(n), s));
+    int hn1 = 0;
+    nsel.download(&hn1, 1);
+    sync(s);
+    n_raw = uint32_t(hn1);
+    raw_grp.alloc(n_raw, s);
+    raw_col.alloc(n_raw, s);
+    raw_pos.alloc(n_raw, s);
+    PO_LAUNCH(k_raw1_items, grid_for(n_raw, 256), 256, 0, s, raw_rows.get(), n_raw, row_leaf.get(),
+              d_lrc.get(), raw_grp.get(), raw_col.get());
+    RefineJob rj;
+    rj.n_items = n_raw;
+    rj.d_grp_init = raw_grp.get();
+    rj.d_grp_start = d_leaf_off.get();
+    rj.n_groups = nleaves;
+    rj.grp_max = uint32_t(n);
+    rj.key.kind = 0;  // raw bytes
+    rj.key.arena = e.arena;
+    rj.key.arena_bytes = e.arena_bytes;
+    rj.key.offsets = e.offsets;
+    rj.key.item_cell_row = raw_rows.get();
+    rj.key.item_col = raw_col.get();
+    rj.key.m = m;
+    rj.d_out_pos = raw_pos.get();
+    sort_jobs.push_back(rj);
+  }
+  refine_sort_multi(sort_jobs, s);
+  if (n_raw)
+    PO_LAUNCH(k_raw1_scatter, grid_for(n_raw, 256), 256, 0, s, raw_rows.get(), raw_pos.get(), n_raw,
+              pos.get());
   timing_mark("leaf+fallback_sort", s);
   if (debug_checks()) {
     DevBuf<unsigned> seen(n, s);

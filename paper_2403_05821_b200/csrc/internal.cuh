@@ -30,23 +30,27 @@ void make_device_table(const po_table* t, int tok, cudaStream_t s, DeviceTable& 
 // Exact dictionary encoding of every column (K1 cell_scan + K2 dict_encode +
 // K3 rank_sort). After encode():
 //   vid[r*m+c]           rank of cell (r,c)'s value among the distinct values
-//                        of column c in raw-byte order (== dense value id)
+//                        of column c in the escaped fragment-key order
+//                        (json_escape(v) followed by '"', scoring.hpp:33-69),
+//                        i.e. the fallback sort order; equal ids <=> equal bytes
 //   card[c], colbase[c]  distinct count and prefix sum (host + device)
 //   the per-distinct arrays below are indexed by colbase[c] + vid:
 //   vlen                 segment length of the value (tokenizer + scoring)
 //   count                occurrences of the value in column c
-//   esc_rank             rank of the value in the escaped fragment-key order
-//                        (json_escape(v) followed by '"', scoring.hpp:33-69)
 struct Encoded {
   uint64_t n = 0;
   uint32_t m = 0;
+  // the table bytes (non-owning; valid for the call) for on-demand raw-byte
+  // comparisons of a few values
+  const uint8_t* arena = nullptr;
+  const uint64_t* offsets = nullptr;
+  uint64_t arena_bytes = 0;
   uint64_t D = 0;  // total distinct values
   std::vector<uint64_t> card, colbase;  // host (colbase has m+1 entries)
   DevBuf<uint64_t> d_colbase;
   DevBuf<uint32_t> vid;       // n*m
   DevBuf<uint64_t> vlen;      // D
   DevBuf<uint32_t> count;     // D
-  DevBuf<uint32_t> esc_rank;  // D
   DevBuf<uint32_t> rep_row;   // D: a row holding the value
   std::vector<uint64_t> total_len;  // host, per column: sum of segment lengths (stats.hpp:38)
 };
@@ -73,7 +77,6 @@ struct RefineKey {
   uint32_t m = 0;
   // row keys
   const uint32_t* vid = nullptr;
-  const uint32_t* esc_rank = nullptr;
   const uint64_t* colbase = nullptr;
   const uint32_t* row_leaf = nullptr;      // row -> leaf index
   const uint32_t* leaf_chunk_off = nullptr;  // leaf -> first chunk descriptor
@@ -81,7 +84,7 @@ struct RefineKey {
   const uint32_t* chunk_key_off = nullptr;   // chunk -> first key
   const uint32_t* chunk_nkeys = nullptr;
   const int32_t* key_field = nullptr;
-  const uint8_t* key_kind = nullptr;  // 0 raw (vid), 1 escaped (esc_rank)
+  const uint8_t* key_kind = nullptr;  // unused (kept for layout); keys are vids (escaped order)
   const uint8_t* key_bits = nullptr;
   uint32_t chunk_bits = 0;       // set by refine_sort: 64 - bits(grp_max)
   uint32_t nsym0 = 0, nsym = 0;  // set by refine_sort: string symbols in round 0 / later

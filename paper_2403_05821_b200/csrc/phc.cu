@@ -133,7 +133,6 @@ FixedOrderSort::FixedOrderSort(const Encoded& e, const std::vector<int>& order, 
   K.kind = 2;
   K.m = e.m;
   K.vid = e.vid.get();
-  K.esc_rank = e.esc_rank.get();
   K.colbase = e.d_colbase.get();
   K.row_leaf = row_leaf_.get();
   K.leaf_chunk_off = lco_.get();

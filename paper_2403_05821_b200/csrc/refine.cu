@@ -73,9 +73,8 @@ __device__ __forceinline__ uint64_t row_chunk(const RefineKey& K, uint32_t row, 
   uint64_t chunk = 0;
   for (uint32_t j = 0; j < nk; ++j) {
     const int32_t f = K.key_field[k0 + j];
-    const uint32_t v = K.vid[uint64_t(row) * K.m + f];
-    const uint32_t rank = K.key_kind[k0 + j] == 0 ? v : K.esc_rank[K.colbase[f] + v];
-    chunk = (chunk << K.key_bits[k0 + j]) | rank;
+    // vids are ranks in the escaped fragment-key order (the fallback order)
+    chunk = (chunk << K.key_bits[k0 + j]) | K.vid[uint64_t(row) * K.m + f];
   }
   return chunk;
 }
