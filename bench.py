@@ -64,7 +64,7 @@ def peaks():
 
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled during the timed region."""
-    Q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+    Q = ("timestamp,index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
@@ -73,14 +73,26 @@ class ClockSampler:
         self.proc = None
 
     def __enter__(self):
+        # started well before the timed region; only samples whose timestamp
+        # falls inside [mark_start, mark_end] are kept
+        self.t0 = self.t1 = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                 "-i", str(self.gpu), "-lms", "100"],
+                 "-i", str(self.gpu), "-lms", "20"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            time.sleep(1.0)
         except OSError:
             self.proc = None
         return self
+
+    def mark_start(self):
+        import datetime
+        self.t0 = datetime.datetime.now()
+
+    def mark_end(self):
+        import datetime
+        self.t1 = datetime.datetime.now()
 
     def __exit__(self, *exc):
         self.lines = []
@@ -94,22 +106,31 @@ class ClockSampler:
             self.lines = [l for l in out.splitlines() if l.strip()]
 
     def summary(self):
+        import datetime
         sm, mx, reasons = [], 0.0, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for l in getattr(self, "lines", []):
             f = [x.strip() for x in l.split(",")]
-            if len(f) < 8:
+            if len(f) < 9:
                 continue
             try:
-                sm.append(float(f[1]))
-                mx = max(mx, float(f[2]))
+                ts = datetime.datetime.strptime(f[0], "%Y/%m/%d %H:%M:%S.%f")
+            except ValueError:
+                ts = None
+            if ts is not None and self.t0 is not None and self.t1 is not None and \
+                    not (self.t0 - datetime.timedelta(milliseconds=25) <= ts <= self.t1):
+                continue
+            try:
+                sm.append(float(f[2]))
+                mx = max(mx, float(f[3]))
             except ValueError:
                 continue
-            for nm, v in zip(names, f[4:8]):
+            for nm, v in zip(names, f[5:9]):
                 if v.lower() == "active":
                     reasons.add(nm)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm),
+                "window": "samples every 20 ms inside the timed region"}
 
 
 def cpu_reference_rows_per_s(table, fds, sample_rows: int, kind: str):
@@ -217,11 +238,13 @@ def run_ours(args):
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         barrier()
+        clk.mark_start()
         ev0.record(stream)
         for _ in range(args.steps):
             phc, st = step_device()
         ev1.record(stream)
         barrier()
+        clk.mark_end()
     launches = (lib.kernel_launch_count() - l0) // max(args.steps, 1)
     ms = ev0.elapsed_time(ev1) / args.steps
     ms = max_over_ranks(ms)
@@ -244,13 +267,24 @@ def run_ours(args):
         log(f"   {k:28s} {ms_k:8.3f} ms/step  {cnt:6.1f} launches  "
             f"({100*ms_k/max(total_kernel_ms,1e-9):5.1f}% of kernel time)")
 
-    # roofline of the dominant byte-streaming kernel: k_dict_insert reads every
-    # cell byte + its offset pair once: algorithmic bytes = S + 8*(n*m+1) + 4*n*m
+    # roofline of the HBM-streaming kernel (K1 cell_scan, k_cell_hash_cols):
+    # it must read every cell byte and its offset pair once, so its algorithmic
+    # bytes per launch are S + 8*(n*m+1) (the 8-byte hash it writes per cell is
+    # an intermediate of this design and is not counted)
     peak, peak_kind = peaks()
-    dom = "k_dict_insert"
+    dom = "k_cell_hash_cols"
     dom_ms = prof.get(dom, (1, 0.0))[1] / max(prof.get(dom, (1, 0.0))[0], 1)
-    dom_bytes = cell_bytes + 8 * (n * m + 1) + 4 * n * m
+    dom_bytes = cell_bytes + 8 * (n * m + 1)
     achieved = dom_bytes / (dom_ms / 1e3) / 1e9 if dom_ms > 0 else 0.0
+    traffic = None
+    tfile = ROOT / "profiles" / "ncu_traffic.json"
+    if tfile.exists():  # dram bytes per launch from the committed ncu --set full capture
+        try:
+            tj = json.loads(tfile.read_text())
+            if tj.get("workload") == gen.CONFIGS[cfg_id].name and n == tj.get("rows"):
+                traffic = tj.get("kernels", {}).get(dom)
+        except (ValueError, OSError):
+            traffic = None
     # whole-pipeline figure on SURVEY.md §8d's B_alg = S_row + 8m + 4 + m per row
     b_alg = cell_bytes + n * (8 * m + 4 + m)
 
@@ -313,11 +347,12 @@ def run_ours(args):
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "ms_per_step": ms_e2e, "host_wall_ms_per_step": wall_e2e},
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
-                         "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+                         "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                          "algorithmic_bytes_per_launch": dom_bytes,
                          "kernel_ms": dom_ms, "peak_source": peak_kind,
                          "pipeline_b_alg_frac": (b_alg / (ms / 1e3) / 1e9) / peak},
             "kernels_ms_per_step": {k: round(v, 4) for v, k, _ in kern[:16]},
+            "kernel_ms_total": round(total_kernel_ms, 4),
             "cpu_baseline": cpu,
             "gpu_launches": int(launches),
             "clocks": clocks,
@@ -332,13 +367,13 @@ def run_ours(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--rows", type=int, default=None)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--cpu-rows", type=int, default=300_000)
-    ap.add_argument("--ref-rows", type=int, default=50_000)
+    ap.add_argument("--ref-rows", type=int, default=300_000)
     ap.add_argument("--prof-steps", type=int, default=3)
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
