@@ -257,13 +257,14 @@ __global__ void __launch_bounds__(256) k_cell_hash_cols(
     const uint64_t* __restrict__ offsets, uint64_t n, uint32_t m, uint64_t hash_mask,
     unsigned long long* __restrict__ hashes) {
   const uint32_t lane = threadIdx.x & 31;
-  const uint64_t nwarps_total = ((n + 31) / 32) * m;
+  const uint64_t ntiles = (n + 31) / 32;
   const uint64_t* lim =
       reinterpret_cast<const uint64_t*>((reinterpret_cast<uintptr_t>(arena_end) + 7) & ~uintptr_t(7));
-  for (uint64_t wid = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5; wid < nwarps_total;
-       wid += (uint64_t(gridDim.x) * blockDim.x) >> 5) {
-    const uint64_t tile = wid / m;
-    const uint32_t c = uint32_t(wid - tile * m);
+  for (uint64_t tile = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5; tile < ntiles;
+       tile += (uint64_t(gridDim.x) * blockDim.x) >> 5)
+  for (uint32_t c = 0; c < m; ++c) {
+    // the warp walks its 32 rows column by column: the bytes of one row are
+    // read by the same lane in consecutive iterations (boundary sectors hit L1)
     const uint64_t r = tile * 32 + lane;
     if (r >= n) continue;
     const uint64_t i = r * m + c;
@@ -371,13 +372,12 @@ __global__ void __launch_bounds__(256) k_dict_verify(
   // its own cell with the representative, 4 words per step with all 10 loads
   // in flight.
   const uint32_t lane = threadIdx.x & 31;
-  const uint64_t nwarps_total = ((n + 31) / 32) * m;
+  const uint64_t ntiles = (n + 31) / 32;
   const uint64_t* lim =
       reinterpret_cast<const uint64_t*>((reinterpret_cast<uintptr_t>(arena_end) + 7) & ~uintptr_t(7));
-  for (uint64_t wid = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5; wid < nwarps_total;
-       wid += (uint64_t(gridDim.x) * blockDim.x) >> 5) {
-    const uint64_t tile = wid / m;
-    const uint32_t c = uint32_t(wid - tile * m);
+  for (uint64_t tile = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5; tile < ntiles;
+       tile += (uint64_t(gridDim.x) * blockDim.x) >> 5)
+  for (uint32_t c = 0; c < m; ++c) {
     const uint64_t r = tile * 32 + lane;
     if (r >= n) continue;
     const uint64_t i = r * m + c;
@@ -753,7 +753,7 @@ void encode(const DeviceTable& t, int tok, int scoring, cudaStream_t s, Encoded&
                 smem, s, t.arena, arena_end, t.offsets, cells, uint32_t(m), rows_per_tile, stage,
                 hmask, hashes.get());
     } else {
-      PO_LAUNCH(k_cell_hash_cols, grid_for(((n + 31) / 32) * m * 32, 256, 8), 256, 0, s, t.arena,
+      PO_LAUNCH(k_cell_hash_cols, grid_for(((n + 31) / 32) * 32, 256, 8), 256, 0, s, t.arena,
                 arena_end, t.offsets, n, uint32_t(m), hmask, hashes.get());
     }
     // K2a/K2b: probe + claim, then byte verification of every duplicate
@@ -761,7 +761,7 @@ void encode(const DeviceTable& t, int tok, int scoring, cudaStream_t s, Encoded&
               uint32_t(m), cap, keys.get(), reps.get(), repoffs.get(), slot_of_cell.get());
     DevBuf<uint32_t> collided(cells, s), ncol(1, s);
     ncol.zero();
-    PO_LAUNCH(k_dict_verify, grid_for(((n + 31) / 32) * m * 32, 256, 8), 256, 0, s, t.arena,
+    PO_LAUNCH(k_dict_verify, grid_for(((n + 31) / 32) * 32, 256, 8), 256, 0, s, t.arena,
               arena_end, t.offsets, n, uint32_t(m), cap, reps.get(), repoffs.get(), slot_of_cell.get(),
               collided.get(), ncol.get());
     uint32_t hcol = 0;
