@@ -570,6 +570,7 @@ __global__ void k_vid(const uint32_t* slot_of_cell, const uint32_t* slot2vid, ui
 // global atomics.
 constexpr uint32_t kSmemBins = 12288;
 constexpr uint32_t kLargeCol = 0xFFFFFFFFu;
+constexpr uint32_t kUniqueCol = 0xFFFFFFFEu;  // card == n: every count is 1
 
 __global__ void __launch_bounds__(512) k_count(const uint32_t* vid, uint64_t n, uint32_t m,
                                                const uint32_t* soff, uint32_t nbins,
@@ -583,7 +584,8 @@ __global__ void __launch_bounds__(512) k_count(const uint32_t* vid, uint64_t n, 
     const uint32_t c = uint32_t(i % m);
     const uint32_t v = vid[i];
     const uint32_t o = soff[c];
-    if (o != kLargeCol) atomicAdd(&h[o + v], 1u);
+    if (o == kUniqueCol) count[colbase[c] + v] = 1u;
+    else if (o != kLargeCol) atomicAdd(&h[o + v], 1u);
     else atomicAdd(&count[colbase[c] + v], 1u);
   }
   __syncthreads();
@@ -593,7 +595,7 @@ __global__ void __launch_bounds__(512) k_count(const uint32_t* vid, uint64_t n, 
     if (h[b]) {
       uint32_t owner = 0, best = 0;
       for (uint32_t cc = 0; cc < m; ++cc)
-        if (soff[cc] != kLargeCol && soff[cc] <= b && soff[cc] >= best) {
+        if (soff[cc] < kUniqueCol && soff[cc] <= b && soff[cc] >= best) {
           best = soff[cc];
           owner = cc;
         }
@@ -601,8 +603,12 @@ __global__ void __launch_bounds__(512) k_count(const uint32_t* vid, uint64_t n, 
     }
 }
 
-// Per-column sum of count*vlen (stats.hpp:38), privatised per block in
-// shared memory (m accumulators) so the global atomics are m per block.
+// Per-column sum of count*vlen (stats.hpp:38). Dictionary positions are
+// grouped by column, so each thread sums a contiguous run of kTotRun entries
+// in a register and flushes only at column changes; the m per-block
+// accumulators in shared memory then take one global atomic each.
+constexpr uint32_t kTotRun = 16;
+
 __global__ void k_total_len(const uint32_t* count, const uint64_t* vlen, const uint32_t* col_by_pos,
                             uint64_t D, uint32_t m, unsigned long long* total) {
   extern __shared__ unsigned long long acc[];
@@ -610,11 +616,27 @@ __global__ void k_total_len(const uint32_t* count, const uint64_t* vlen, const u
   if (priv)
     for (uint32_t c = threadIdx.x; c < m; c += blockDim.x) acc[c] = 0;
   __syncthreads();
-  for (uint64_t p = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; p < D;
-       p += uint64_t(gridDim.x) * blockDim.x) {
-    const unsigned long long v = uint64_t(count[p]) * vlen[p];
-    if (priv) atomicAdd(&acc[col_by_pos[p]], v);
-    else atomicAdd(&total[col_by_pos[p]], v);
+  auto flush = [&](uint32_t c, unsigned long long v) {
+    if (!v) return;
+    if (priv) atomicAdd(&acc[c], v);
+    else atomicAdd(&total[c], v);
+  };
+  const uint64_t runs = (D + kTotRun - 1) / kTotRun;
+  for (uint64_t q = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; q < runs;
+       q += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t lo = q * kTotRun, hi = lo + kTotRun < D ? lo + kTotRun : D;
+    uint32_t cur = col_by_pos[lo];
+    unsigned long long sum = 0;
+    for (uint64_t p = lo; p < hi; ++p) {
+      const uint32_t c = col_by_pos[p];
+      if (c != cur) {
+        flush(cur, sum);
+        cur = c;
+        sum = 0;
+      }
+      sum += uint64_t(count[p]) * vlen[p];
+    }
+    flush(cur, sum);
   }
   if (priv) {
     __syncthreads();
@@ -887,7 +909,8 @@ void encode(const DeviceTable& t, int tok, int scoring, cudaStream_t s, Encoded&
     std::vector<uint32_t> soff(m, kLargeCol);
     uint32_t nbins = 0;
     for (uint32_t c = 0; c < m; ++c)
-      if (nbins + e.card[c] <= kSmemBins) {
+      if (e.card[c] == n) soff[c] = kUniqueCol;
+      else if (nbins + e.card[c] <= kSmemBins) {
         soff[c] = nbins;
         nbins += uint32_t(e.card[c]);
       }
@@ -897,7 +920,7 @@ void encode(const DeviceTable& t, int tok, int scoring, cudaStream_t s, Encoded&
   }
   DevBuf<unsigned long long> tot(m, s);
   tot.zero();
-  PO_LAUNCH(k_total_len, grid_for(D, 256, 2), 256, m <= 4096 ? m * 8 : 0, s, e.count.get(),
+  PO_LAUNCH(k_total_len, grid_for((D + kTotRun - 1) / kTotRun, 256, 2), 256, m <= 4096 ? m * 8 : 0, s, e.count.get(),
             e.vlen.get(), col_by_pos.get(), D, uint32_t(m), tot.get());
   std::vector<unsigned long long> htot(m);
   tot.download(htot.data(), m);

@@ -362,18 +362,36 @@ struct SplitD {
   uint32_t need_rows;
 };
 
-__global__ void k_relabel(uint32_t* node_of_row, uint64_t n, const int32_t* split_of_node,
-                          const SplitD* sp, const uint32_t* vid, uint32_t m, uint32_t* cursor,
-                          const uint64_t* seg_off, uint32_t* blockrows) {
+// Split lookup by binary search over the level's split nodes (ascending
+// node ids), staged in shared memory when they fit.
+constexpr uint32_t kRelabelSmem = 4096;
+
+__global__ void k_relabel(uint32_t* node_of_row, uint64_t n, const uint32_t* split_nodes,
+                          uint32_t ns, const SplitD* sp, const uint32_t* vid, uint32_t m,
+                          uint32_t* cursor, const uint64_t* seg_off, uint32_t* blockrows) {
+  extern __shared__ uint32_t s_nodes[];
   const uint32_t lane = threadIdx.x & 31;
+  const bool staged = ns <= kRelabelSmem;
+  if (staged) {
+    for (uint32_t i = threadIdx.x; i < ns; i += blockDim.x) s_nodes[i] = split_nodes[i];
+    __syncthreads();
+  }
+  const uint32_t* tab = staged ? s_nodes : split_nodes;
   for (uint64_t base = blockIdx.x * uint64_t(blockDim.x); base < n;
        base += uint64_t(gridDim.x) * blockDim.x) {
     const uint64_t r = base + threadIdx.x;
     int32_t j = -1;
     bool inb = false;
     if (r < n) {
-      j = split_of_node[node_of_row[r]];
-      if (j >= 0) {
+      const uint32_t node = node_of_row[r];
+      uint32_t lo = 0, hi = ns;
+      while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (tab[mid] < node) lo = mid + 1;
+        else hi = mid;
+      }
+      if (lo < ns && tab[lo] == node) {
+        j = int32_t(lo);
         const SplitD& d = sp[j];
         inb = vid[r * m + d.col] == d.vid;
         node_of_row[r] = inb ? d.block_id : d.rest_id;
@@ -478,11 +496,6 @@ __global__ void k_dbg_perm(const uint32_t* pos, uint64_t n, unsigned* seen, unsi
   }
 }
 
-__global__ void k_mark_splits(int32_t* split_of_node, const uint32_t* nodes, uint32_t ns,
-                              int clear) {
-  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < ns; j += gridDim.x * blockDim.x)
-    split_of_node[nodes[j]] = clear ? -1 : int32_t(j);
-}
 
 // Root partner sums: psum[colbase[c]+vid(r,c)][k] += len(r, partner k of c).
 __global__ void k_root_psum(const uint32_t* vid, uint64_t n, uint32_t m, uint32_t K,
@@ -734,20 +747,6 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
   }
   DevBuf<uint32_t> node_of_row(n, s);
   node_of_row.zero();
-  std::vector<int32_t> h_split_of_node;
-  DevBuf<int32_t> split_of_node;
-  auto ensure_split_map = [&](size_t need) {
-    if (split_of_node.size() >= need) return;
-    size_t cap = std::max<size_t>(1024, split_of_node.size());
-    while (cap < need) cap *= 2;
-    DevBuf<int32_t> nb(cap, s);
-    nb.fill_bytes(0xFF);
-    if (split_of_node.size())
-      PO_CUDA(cudaMemcpyAsync(nb.get(), split_of_node.get(), split_of_node.size() * sizeof(int32_t),
-                              cudaMemcpyDeviceToDevice, s));
-    split_of_node = std::move(nb);
-  };
-  ensure_split_map(1024);
 
   // Work items over a node's table: dense tables are cut at column
   // boundaries (only the node's active columns), hashed ones in plain chunks.
@@ -1034,7 +1033,8 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
     // ---- K6 split + K4 aggregation ----
     if (!splits.empty()) {
       const uint32_t ns = uint32_t(splits.size());
-      ensure_split_map(nodes.size());
+      std::sort(splits.begin(), splits.end(),
+                [](const SplitH& a, const SplitH& b) { return a.node < b.node; });
       std::vector<SplitD> hsp(ns);
       std::vector<uint64_t> seg(ns + 1, 0);
       std::vector<uint32_t> split_nodes(ns);
@@ -1069,14 +1069,13 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
       auto* d_snodes = reinterpret_cast<uint32_t*>(ds + o_sn);
       auto* d_cursor = reinterpret_cast<uint32_t*>(ds + o_cursor);
       DevBuf<uint32_t> blockrows(std::max<uint64_t>(1, seg[ns]), s);
-      PO_LAUNCH(k_mark_splits, grid_for(ns, 128), 128, 0, s, split_of_node.get(), d_snodes, ns, 0);
-      PO_LAUNCH(k_relabel, grid_for(n, 256), 256, 0, s, node_of_row.get(), n,
-                split_of_node.get(), d_sp, e.vid.get(), m, d_cursor, d_seg, blockrows.get());
+      PO_LAUNCH(k_relabel, grid_for(n, 256), 256, ns <= kRelabelSmem ? ns * 4 : 0, s,
+                node_of_row.get(), n, d_snodes, ns, d_sp, e.vid.get(), m, d_cursor, d_seg,
+                blockrows.get());
       if (!tasks.empty())
         PO_LAUNCH(k_aggregate, unsigned(tasks.size()), kAggBlock, 0, s,
                   reinterpret_cast<AggTask*>(ds + o_tasks), blockrows.get(), d_sp, e.vid.get(),
                   vlen, colbase, m, K, d_dpart.get(), d_npart.get());
-      PO_LAUNCH(k_mark_splits, grid_for(ns, 128), 128, 0, s, split_of_node.get(), d_snodes, ns, 1);
     }
     if (debug_checks()) {
       DevBuf<unsigned long long> hist(nodes.size() + 1, s);

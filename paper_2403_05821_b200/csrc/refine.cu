@@ -108,50 +108,38 @@ __global__ void k_build_keys(const uint32_t* items, const uint32_t* grp, uint32_
   }
 }
 
-// Rounds >= 1 sort within segments (= groups): segment starts of the active
-// array, and the boundary markers from the segment flags + chunk changes.
-// flags over the previous round's item count (the compaction input size):
-// positions at or past the new count are cleared so the selection over the
-// old range only yields real segment starts.
-__global__ void k_seg_flags(const uint32_t* grp, const int* count, uint32_t old_count,
-                            uint8_t* flags) {
-  const uint32_t A = uint32_t(*count);
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < old_count;
-       i += gridDim.x * blockDim.x)
-    flags[i] = (i < A && (i == 0 || grp[i] != grp[i - 1])) ? 1 : 0;
-}
-
 __global__ void k_seg_end(uint32_t* seg_begin, const int* nseg, const int* count) {
   seg_begin[*nseg] = uint32_t(*count);
 }
 
-__global__ void k_marks_seg(const uint64_t* keys, const uint8_t* flags, uint32_t A,
-                            uint32_t* gmark, uint32_t* rmark) {
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < A; i += gridDim.x * blockDim.x) {
-    const bool gb = flags[i] != 0;
-    const bool rb = gb || keys[i] != keys[i - 1];
-    gmark[i] = gb ? i : 0;
-    rmark[i] = rb ? i : 0;
+// Boundary markers for one pair max-scan: (start index of each item's
+// group, start index of its (group, chunk) run). Computed on the fly by the
+// scan's input iterator; rounds >= 1 take group boundaries from the segment
+// flags, round 0 from the group bits of the key.
+struct Marks {
+  const uint64_t* keys;
+  const uint8_t* flags;  // null: round 0
+  uint32_t shift;
+  __device__ __forceinline__ uint2 operator()(uint32_t i) const {
+    if (i == 0) return make_uint2(0, 0);
+    const uint64_t a = keys[i], b = keys[i - 1];
+    const bool gb = flags ? flags[i] != 0 : (shift < 64 && (a >> shift) != (b >> shift));
+    const bool rb = gb || a != b;
+    return make_uint2(gb ? i : 0, rb ? i : 0);
   }
-}
+};
 
-// Boundary markers for the two max-scans: start index of each item's group
-// and of its (group, chunk) run.
-__global__ void k_marks(const uint64_t* keys, uint32_t A, uint32_t shift, uint32_t* gmark,
-                        uint32_t* rmark) {
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < A; i += gridDim.x * blockDim.x) {
-    const bool gb = i == 0 || (keys[i] >> shift) != (keys[i - 1] >> shift);
-    const bool rb = i == 0 || keys[i] != keys[i - 1];
-    gmark[i] = gb ? i : 0;
-    rmark[i] = rb ? i : 0;
+struct Max2 {
+  __device__ __forceinline__ uint2 operator()(const uint2& a, const uint2& b) const {
+    return make_uint2(a.x > b.x ? a.x : b.x, a.y > b.y ? a.y : b.y);
   }
-}
+};
 
 // Resolved items get their final position; the others keep (new group start,
 // item) packed in one word for a single compaction. `start` maps round-0
 // group indices to start positions (null: the group id is the start).
-__global__ void k_resolve(const uint64_t* keys, const uint32_t* items, const uint32_t* gstart,
-                          const uint32_t* rstart, uint32_t A, uint32_t k, uint32_t shift,
+__global__ void k_resolve(const uint64_t* keys, const uint32_t* items, const uint2* starts,
+                          uint32_t A, uint32_t k, uint32_t shift,
                           const uint32_t* start, const uint32_t* seg_grp, RefineKey K,
                           uint32_t* out_pos, uint8_t* keep, uint64_t* packed) {
   const uint64_t cmask = shift >= 64 ? ~0ull : ((1ull << shift) - 1);
@@ -161,12 +149,13 @@ __global__ void k_resolve(const uint64_t* keys, const uint32_t* items, const uin
     if (seg_grp) {
       g = seg_grp[i];  // segmented rounds: group start aligned with the active array
     } else {
-      const uint32_t gid = uint32_t(keys[i] >> shift);
+      const uint32_t gid = shift < 64 ? uint32_t(keys[i] >> shift) : 0u;
       g = start ? start[gid] : gid;
     }
-    const uint32_t pos = g + (i - gstart[i]);
-    const bool run_head = rstart[i] == i;
-    const bool next_head = i + 1 >= A || rstart[i + 1] == i + 1;
+    const uint2 st = starts[i];
+    const uint32_t pos = g + (i - st.x);
+    const bool run_head = st.y == i;
+    const bool next_head = i + 1 >= A || starts[i + 1].y == i + 1;
     bool term;
     if (K.kind == 2) term = row_terminal(K, item, k);
     else term = string_terminal(K, keys[i] & cmask, str_round(K, k).nsym);
@@ -176,16 +165,27 @@ __global__ void k_resolve(const uint64_t* keys, const uint32_t* items, const uin
     } else {
       keep[i] = 1;
     }
-    packed[i] = (uint64_t(g + (rstart[i] - gstart[i])) << 32) | item;
+    packed[i] = (uint64_t(g + (st.y - st.x)) << 32) | item;
   }
 }
 
-__global__ void k_unpack(const uint64_t* packed, const int* count, uint32_t* items, uint32_t* grp) {
+// Unpack the compacted (group start, item) words and flag the segment starts
+// of the next round (runs of equal group start). Flags are written over the
+// previous round's item count: positions at or past the new count are
+// cleared so the selection over the old range only yields real starts.
+__global__ void k_unpack(const uint64_t* packed, const int* count, uint32_t old_count,
+                         uint32_t* items, uint32_t* grp, uint8_t* flags) {
   const uint32_t A = uint32_t(*count);
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < A; i += gridDim.x * blockDim.x) {
-    const uint64_t v = packed[i];
-    items[i] = uint32_t(v);
-    grp[i] = uint32_t(v >> 32);
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < old_count;
+       i += gridDim.x * blockDim.x) {
+    uint8_t f = 0;
+    if (i < A) {
+      const uint64_t v = packed[i];
+      items[i] = uint32_t(v);
+      grp[i] = uint32_t(v >> 32);
+      f = (i == 0 || (v >> 32) != (packed[i - 1] >> 32)) ? 1 : 0;
+    }
+    flags[i] = f;
   }
 }
 
@@ -234,7 +234,8 @@ struct Job {
   uint32_t shift0 = 0, shift = 0;  // chunk bits of round 0 / of later rounds
   int end_bit0 = 0, end_bit = 0;
   size_t tb = 0;
-  DevBuf<uint32_t> items, items2, grp, gstart, rstart, gmark, rmark;
+  DevBuf<uint32_t> items, items2, grp;
+  DevBuf<uint2> starts;
   DevBuf<uint64_t> keys, keys2, pk, pk2;
   DevBuf<uint8_t> keep, tmp, segflags;
   DevBuf<uint32_t> seg_begin;
@@ -282,10 +283,7 @@ void refine_sort_multi(const std::vector<RefineJob>& specs, cudaStream_t s) {
     j->keys2.alloc(n, s);
     j->pk.alloc(n, s);
     j->pk2.alloc(n, s);
-    j->gstart.alloc(n, s);
-    j->rstart.alloc(n, s);
-    j->gmark.alloc(n, s);
-    j->rmark.alloc(n, s);
+    j->starts.alloc(n, s);
     j->keep.alloc(n, s);
     j->segflags.alloc(n, s);
     j->seg_begin.alloc(n + 1, s);
@@ -296,8 +294,11 @@ void refine_sort_multi(const std::vector<RefineJob>& specs, cudaStream_t s) {
     int* nullcount = nullptr;
     PO_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, j->keys.get(), j->keys2.get(),
                                             j->items.get(), j->items2.get(), n, 0, 64, s));
-    PO_CUDA(cub::DeviceScan::InclusiveScan(nullptr, scan_bytes, j->gmark.get(), j->gstart.get(),
-                                           cub::Max(), n, s));
+    {
+      cub::TransformInputIterator<uint2, Marks, cub::CountingInputIterator<uint32_t>> mk(
+          cub::CountingInputIterator<uint32_t>(0), Marks{j->keys2.get(), nullptr, 0});
+      PO_CUDA(cub::DeviceScan::InclusiveScan(nullptr, scan_bytes, mk, j->starts.get(), Max2(), n, s));
+    }
     PO_CUDA(cub::DeviceSelect::Flagged(nullptr, sel_bytes, j->pk2.get(), j->keep.get(),
                                        j->pk.get(), nullcount, n, s));
     j->tb = std::max(sort_bytes, std::max(scan_bytes, sel_bytes));
@@ -324,8 +325,6 @@ void refine_sort_multi(const std::vector<RefineJob>& specs, cudaStream_t s) {
         ProfScope ps("cub_radix_sort", s);
         PO_CUDA(cub::DeviceRadixSort::SortPairs(j.tmp.get(), b, j.keys.get(), j.keys2.get(),
                                                 j.items.get(), j.items2.get(), A, 0, j.end_bit0, s));
-        PO_LAUNCH(k_marks, grid_for(A, 256), 256, 0, s, j.keys2.get(), A, shift, j.gmark.get(),
-                  j.rmark.get());
       } else {
         ProfScope ps("cub_segmented_sort", s);
         if (std::getenv("PO_DEBUG_CHECKS")) {
@@ -353,20 +352,17 @@ void refine_sort_multi(const std::vector<RefineJob>& specs, cudaStream_t s) {
         PO_CUDA(cub::DeviceSegmentedSort::StableSortPairs(
             j.seg_tmp.get(), need, j.keys.get(), j.keys2.get(), j.items.get(), j.items2.get(),
             int(A), int(j.nseg), j.seg_begin.get(), j.seg_begin.get() + 1, s));
-        PO_LAUNCH(k_marks_seg, grid_for(A, 256), 256, 0, s, j.keys2.get(), j.segflags.get(), A,
-                  j.gmark.get(), j.rmark.get());
       }
       {
         ProfScope ps("cub_scan", s);
         b = j.tb;
-        PO_CUDA(cub::DeviceScan::InclusiveScan(j.tmp.get(), b, j.gmark.get(), j.gstart.get(),
-                                               cub::Max(), A, s));
-        b = j.tb;
-        PO_CUDA(cub::DeviceScan::InclusiveScan(j.tmp.get(), b, j.rmark.get(), j.rstart.get(),
-                                               cub::Max(), A, s));
+        cub::TransformInputIterator<uint2, Marks, cub::CountingInputIterator<uint32_t>> mk(
+            cub::CountingInputIterator<uint32_t>(0),
+            Marks{j.keys2.get(), seg ? j.segflags.get() : nullptr, shift});
+        PO_CUDA(cub::DeviceScan::InclusiveScan(j.tmp.get(), b, mk, j.starts.get(), Max2(), A, s));
       }
       PO_LAUNCH(k_resolve, grid_for(A, 256), 256, 0, s, j.keys2.get(), j.items2.get(),
-                j.gstart.get(), j.rstart.get(), A, j.k, shift, start, seg ? j.grp.get() : nullptr,
+                j.starts.get(), A, j.k, shift, start, seg ? j.grp.get() : nullptr,
                 j.key, j.spec.d_out_pos, j.keep.get(), j.pk2.get());
       {
         ProfScope ps("cub_select", s);
@@ -374,11 +370,9 @@ void refine_sort_multi(const std::vector<RefineJob>& specs, cudaStream_t s) {
         PO_CUDA(cub::DeviceSelect::Flagged(j.tmp.get(), b, j.pk2.get(), j.keep.get(), j.pk.get(),
                                            nsel.get() + 2 * q, A, s));
       }
-      PO_LAUNCH(k_unpack, grid_for(A, 256), 256, 0, s, j.pk.get(), nsel.get() + 2 * q,
-                j.items.get(), j.grp.get());
       // segments of the next round: runs of equal group start
-      PO_LAUNCH(k_seg_flags, grid_for(A, 256), 256, 0, s, j.grp.get(), nsel.get() + 2 * q, A,
-                j.segflags.get());
+      PO_LAUNCH(k_unpack, grid_for(A, 256), 256, 0, s, j.pk.get(), nsel.get() + 2 * q, A,
+                j.items.get(), j.grp.get(), j.segflags.get());
       {
         ProfScope ps("cub_select", s);
         b = j.tb;
