@@ -1187,12 +1187,11 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
   RK.key_bits = d_kb.get();
   timing_mark("layout", s);
   // whole-table fallback order (ggr.hpp:379-381) from the dictionary stats;
-  // its row sort runs in lockstep with the leaf sort (every leaf at once)
+  // its PHC comes from prefix groups, its row sort only runs if it wins
   std::vector<double> avg(m);
   for (uint32_t c = 0; c < m; ++c)
     avg[c] = static_cast<double>(e.total_len[c]) / static_cast<double>(n);
   std::vector<int> fb_order = hitcount_order(n, e.card, avg, cfg.stats_variant);
-  FixedOrderSort fb_sort(e, fb_order, s);
   RefineJob leaf_job;
   leaf_job.n_items = uint32_t(n);
   leaf_job.d_grp_init = row_leaf.get();  // round 0: leaf index
@@ -1215,7 +1214,7 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
     }
   DevBuf<uint32_t> raw_rows, raw_grp, raw_col, raw_pos;
   uint32_t n_raw = 0;
-  std::vector<RefineJob> sort_jobs{leaf_job, fb_sort.job()};
+  std::vector<RefineJob> sort_jobs{leaf_job};
   if (any_raw1) {
     auto d_lrc = to_device(leaf_raw1_col, s);
     DevBuf<uint8_t> flags(n, s);
@@ -1259,7 +1258,7 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
   if (n_raw)
     PO_LAUNCH(k_raw1_scatter, grid_for(n_raw, 256), 256, 0, s, raw_rows.get(), raw_pos.get(), n_raw,
               pos.get());
-  timing_mark("leaf+fallback_sort", s);
+  timing_mark("leaf_sort", s);
   if (debug_checks()) {
     DevBuf<unsigned> seen(n, s);
     DevBuf<unsigned long long> bad(1, s);
@@ -1277,14 +1276,20 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
   timing_mark("emit_phc", s);
 
   // ---- whole-table fallback competition (ggr.hpp:379-387) ----
-  DevBuf<uint32_t> fb_perm(n, s);
-  fb_sort.finish(fb_perm.get());
+  const uint64_t fb_phc = fixed_order_phc_device(e, fb_order, s);
+  timing_mark("fallback_phc", s);
   std::vector<int32_t> fo(fb_order.begin(), fb_order.end());
   auto d_fo = to_device(fo, s);
-  const uint64_t fb_phc = phc_device(e, n, nullptr, fb_perm.get(), nullptr, d_fo.get(), s, 1, true);
-  timing_mark("fallback_phc", s);
+  if (debug_checks()) {  // the prefix-group PHC against the materialised sort
+    DevBuf<uint32_t> perm(n, s);
+    sort_all_rows(e, fb_order, perm.get(), s);
+    const uint64_t chk = phc_device(e, n, nullptr, perm.get(), nullptr, d_fo.get(), s, 1, true);
+    if (chk != fb_phc)
+      fprintf(stderr, "[po debug] fallback phc %llu but the sorted order scores %llu\n",
+              (unsigned long long)fb_phc, (unsigned long long)chk);
+  }
   if (fb_phc > out.phc) {  // replace only when strictly better (ggr.hpp:383)
-    PO_CUDA(cudaMemcpyAsync(d_rows, fb_perm.get(), n * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
+    sort_all_rows(e, fb_order, d_rows, s);
     PO_LAUNCH(k_tile_order, grid_for(n * m, 256), 256, 0, s, d_fo.get(), n, m, d_orders);
     out.phc = fb_phc;
   }

@@ -181,6 +181,11 @@ void sort_all_rows(const Encoded& e, const std::vector<int>& order, uint32_t* d_
                    cudaStream_t s);
 
 // The same sort as a refine job (to run in lockstep with other sorts).
+// PHC of the whole table in the lexicographic order of one field order
+// (first request excluded, like the fallback's phc), computed from prefix
+// groups without materialising the sort.
+uint64_t fixed_order_phc_device(const Encoded& e, const std::vector<int>& order, cudaStream_t s);
+
 class FixedOrderSort {
  public:
   FixedOrderSort(const Encoded& e, const std::vector<int>& order, cudaStream_t s);

@@ -94,6 +94,123 @@ uint64_t phc_device(const Encoded& e, uint64_t n_entries, const uint64_t* rows64
   return h;
 }
 
+// PHC of the whole table sorted by one fixed field order, without sorting.
+// In a lexicographic order the rows sharing a prefix (v1..vp) are
+// contiguous, so the adjacent pairs that hit field p are exactly |G|-1 per
+// prefix group G of depth p, each scoring len(v_p)^2:
+//   PHC = sum_p sum_{G at depth p} (|G|-1) len(v_p)^2
+//       = sum_p ( sum_rows len(v_p(row))^2 - sum_{G at depth p} len(v_p(G))^2 ).
+// Prefix groups are refined one field at a time with an exact hash table on
+// (group, value id); a group's id is its table slot. Sums wrap mod 2^64 like
+// the reference's uint64 accumulator, so the identity holds bit-exactly.
+// The row order itself is only materialised when the fallback wins.
+namespace {
+
+constexpr unsigned long long kFbEmpty = ~0ull;
+
+__global__ void k_fb_init(const uint32_t* vid, uint64_t n, uint32_t m, uint32_t f, uint32_t* gid) {
+  for (uint64_t r = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; r < n;
+       r += uint64_t(gridDim.x) * blockDim.x)
+    gid[r] = vid[r * m + f];
+}
+
+// depth 1: value ids are the groups; sum over the column's dictionary of
+// (count - 1) * len^2
+__global__ void k_fb_first(const uint32_t* count, const uint64_t* vlen, uint64_t card,
+                           unsigned long long* acc) {
+  unsigned long long local = 0;
+  for (uint64_t v = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; v < card;
+       v += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t l = vlen[v];
+    local += uint64_t(count[v] - 1) * (l * l);
+  }
+  typedef cub::BlockReduce<unsigned long long, 256> BR;
+  __shared__ typename BR::TempStorage tmp;
+  const unsigned long long blk = BR(tmp).Sum(local);
+  if (threadIdx.x == 0 && blk) atomicAdd(acc, blk);
+}
+
+__global__ void k_fb_depth(const uint32_t* vid, uint64_t n, uint32_t m, uint32_t f,
+                           const uint64_t* vlen_col, uint32_t* gid, unsigned long long* keys,
+                           uint64_t mask, unsigned long long* acc, const unsigned long long* ng_prev,
+                           unsigned long long* ng) {
+  if (*ng_prev == n) {  // every group a singleton: no deeper hits
+    if (blockIdx.x == 0 && threadIdx.x == 0) *ng = n;
+    return;
+  }
+  unsigned long long sum = 0, fresh = 0;
+  for (uint64_t r = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; r < n;
+       r += uint64_t(gridDim.x) * blockDim.x) {
+    const uint32_t v = vid[r * m + f];
+    const unsigned long long key = (uint64_t(gid[r]) << 32) | v;
+    const uint64_t l = vlen_col[v];
+    const unsigned long long sq = l * l;
+    uint64_t slot = fmix64(key) & mask;
+    for (;;) {
+      unsigned long long k = keys[slot];
+      if (k == kFbEmpty) {
+        k = atomicCAS(&keys[slot], kFbEmpty, key);
+        if (k == kFbEmpty) {  // first row of a new group
+          ++fresh;
+          sum -= sq;
+          break;
+        }
+      }
+      if (k == key) break;
+      slot = (slot + 1) & mask;
+    }
+    sum += sq;
+    gid[r] = uint32_t(slot);
+  }
+  typedef cub::BlockReduce<unsigned long long, 256> BR;
+  __shared__ typename BR::TempStorage tmp;
+  const unsigned long long bs = BR(tmp).Sum(sum);
+  __syncthreads();
+  const unsigned long long bf = BR(tmp).Sum(fresh);
+  if (threadIdx.x == 0) {
+    if (bs) atomicAdd(acc, bs);
+    if (bf) atomicAdd(ng, bf);
+  }
+}
+
+}  // namespace
+
+uint64_t fixed_order_phc_device(const Encoded& e, const std::vector<int>& order, cudaStream_t s) {
+  const uint64_t n = e.n;
+  const uint32_t m = e.m;
+  if (n < 2 || order.empty()) return 0;
+  const std::vector<uint64_t>& colbase = e.colbase;
+  DevBuf<unsigned long long> acc(1, s);
+  acc.zero();
+  const int f0 = order[0];
+  PO_LAUNCH(k_fb_first, grid_for(e.card[f0], 256, 4), 256, 0, s, e.count.get() + colbase[f0],
+            e.vlen.get() + colbase[f0], uint64_t(e.card[f0]), acc.get());
+  if (order.size() > 1 && e.card[f0] < n) {
+    uint64_t cap = 1;
+    while (cap < 2 * n) cap <<= 1;
+    if (cap > (1ull << 32)) fail(PO_ERR_SIZE, "table too large for the fallback group table");
+    DevBuf<uint32_t> gid(n, s);
+    DevBuf<unsigned long long> keys(cap, s);
+    DevBuf<unsigned long long> ng(order.size(), s);
+    ng.zero();
+    const unsigned long long c0 = e.card[f0];
+    PO_CUDA(cudaMemcpyAsync(ng.get(), &c0, sizeof(c0), cudaMemcpyHostToDevice, s));
+    PO_LAUNCH(k_fb_init, grid_for(n, 256), 256, 0, s, e.vid.get(), n, m, uint32_t(f0), gid.get());
+    for (size_t p = 1; p < order.size(); ++p) {
+      const int f = order[p];
+      keys.fill_bytes(0xFF);
+      PO_LAUNCH(k_fb_depth, grid_for(n, 256, 8), 256, 0, s, e.vid.get(), n, m, uint32_t(f),
+                e.vlen.get() + colbase[f], gid.get(), keys.get(), cap - 1, acc.get(),
+                ng.get() + (p - 1), ng.get() + p);
+      if (e.card[f] == n) break;  // unique column: every group a singleton below
+    }
+  }
+  unsigned long long h = 0;
+  acc.download(&h, 1);
+  sync(s);
+  return h;
+}
+
 // Keys of a single leaf covering all rows (one field order, escaped ranks),
 // packed into 64-bit chunks next to the group id.
 FixedOrderSort::FixedOrderSort(const Encoded& e, const std::vector<int>& order, cudaStream_t s)

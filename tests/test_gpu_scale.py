@@ -79,3 +79,35 @@ def test_c2_full_fixed_order_sort(c2_full):
         a, b = int(rows[i - 1]), int(rows[i])
         ka, kb = _fragment_key(t, a, order), _fragment_key(t, b, order)
         assert ka < kb or (ka == kb and a < b)
+
+
+_DEBUG_SCRIPT = r"""
+import sys
+sys.path.insert(0, 'tests')
+import paper_2403_05821_b200 as po
+from golden_cases import load_cases
+from paper_2403_05821_b200 import gen
+for name, t, fds, cfg, tok, sc, exp in load_cases():
+    po.ggr(t, fds, cfg, tok, sc)
+for cid, rows in [(1, 20000), (2, 50000), (3, 20000), (4, 20000), (5, 3000)]:
+    po.ggr(gen.generate(cid, n_rows=rows), gen.fds(cid), po.GgrConfig())
+    po.ggr(gen.generate(cid, n_rows=rows), None, po.GgrConfig(hitcount_stop_threshold=0))
+print("done")
+"""
+
+
+def test_internal_debug_checks_clean():
+    """PO_DEBUG_CHECKS cross-checks device invariants inside ggr(): every
+    node's row count, leaf-sort permutation validity, and the prefix-group
+    fallback PHC against the PHC of the materialised fixed-order sort."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    env = dict(os.environ, PO_DEBUG_CHECKS="1")
+    r = subprocess.run([sys.executable, "-c", _DEBUG_SCRIPT], cwd=root, env=env,
+                       capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert "done" in r.stdout
+    assert "[po debug]" not in r.stderr, r.stderr[-2000:]
