@@ -144,6 +144,39 @@ int po_fixed_order_by_stats(uint32_t n_fields, uint64_t total_rows,
                             const uint64_t* cardinality, const double* avg_len,
                             int32_t* out_order);
 
+/* ---- row-sharded solve over several GPUs ---------------
+ * No reference counterpart: the reference ggr() (ggr.hpp:367-394) is one
+ * process on one table. Here every rank (one per GPU) passes a contiguous
+ * range of the table's rows (rank 0 the first rows, rank 1 the next, ...);
+ * the result is bit-identical to po_ggr on the whole table, delivered as one
+ * contiguous slice of the schedule per rank (concatenating the slices in
+ * rank order gives po_ggr's schedule; row ids are global). All ranks call
+ * every po_ggr_sharded together (it is collective). */
+typedef struct po_comm po_comm;   /* a rank's communicator                */
+typedef struct po_slice po_slice; /* a rank's slice of a sharded schedule */
+
+/* NCCL transport, one process per GPU: rank 0 creates the 128-byte id and
+ * ships it to the other ranks (any side channel, e.g. torch.distributed). */
+int po_comm_unique_id(uint8_t* out_id128);
+int po_comm_init_nccl(const uint8_t* id128, int32_t nranks, int32_t rank, po_comm** out);
+/* In-process transport: nranks communicators for nranks host threads of one
+ * process (any devices, several ranks may share one GPU). */
+int po_comm_init_local(int32_t nranks, po_comm** out_array);
+int po_comm_destroy(po_comm* comm);
+
+/* Sharded prefixopt::ggr. `t` holds this rank's rows (same fields on every
+ * rank). The slice handle owns device memory until po_slice_free. */
+int po_ggr_sharded(po_comm* comm, const po_table* t, const po_fd_groups* fds,
+                   const po_ggr_config* cfg, int32_t tokenizer, int32_t scoring,
+                   po_slice** out_slice, uint64_t* out_phc, po_solve_stats* out_stats,
+                   void* stream);
+/* Position of the slice in the schedule and its number of requests. */
+int po_slice_info(const po_slice* slice, uint64_t* out_offset, uint64_t* out_count);
+/* Copies the slice: count global row ids and count*n_fields field indices. */
+int po_slice_copy(const po_slice* slice, uint32_t out_location, uint64_t* out_row_ids,
+                  int32_t* out_field_orders, void* stream);
+void po_slice_free(po_slice* slice);
+
 /* Thread-local message of the last failing call on this thread. */
 const char* po_last_error(void);
 

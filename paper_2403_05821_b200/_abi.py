@@ -161,6 +161,17 @@ class CudaLib:
             [C.c_uint32, C.c_uint64, vp, vp, C.c_int32, vp])
         self.fixed_order_by_stats = _bind(L, "po_fixed_order_by_stats", C.c_int,
                                           [C.c_uint32, C.c_uint64, vp, vp, vp])
+        # row-sharded solve
+        self.comm_unique_id = _bind(L, "po_comm_unique_id", C.c_int, [vp])
+        self.comm_init_nccl = _bind(L, "po_comm_init_nccl", C.c_int,
+                                    [vp, C.c_int32, C.c_int32, C.POINTER(vp)])
+        self.comm_init_local = _bind(L, "po_comm_init_local", C.c_int, [C.c_int32, vp])
+        self.comm_destroy = _bind(L, "po_comm_destroy", C.c_int, [vp])
+        self.ggr_sharded = _bind(L, "po_ggr_sharded", C.c_int,
+                                 [vp, vp, vp, vp, C.c_int32, C.c_int32, C.POINTER(vp), vp, vp, vp])
+        self.slice_info = _bind(L, "po_slice_info", C.c_int, [vp, vp, vp])
+        self.slice_copy = _bind(L, "po_slice_copy", C.c_int, [vp, C.c_uint32, vp, vp, vp])
+        self.slice_free = _bind(L, "po_slice_free", None, [vp])
         self.last_error = _bind(L, "po_last_error", C.c_char_p, [])
         self.build_info = _bind(L, "po_build_info", C.c_char_p, [])
         self.kernel_launch_count = _bind(L, "po_kernel_launch_count", C.c_uint64, [])

@@ -20,7 +20,7 @@ BUILD = REPO / "build" / "cuda"
 OUT = PKG / "libprefixopt_cuda.so"
 GEN_OUT = PKG / "libpogen.so"
 CXX = os.environ.get("CXX", shutil.which("g++") or "g++")
-SOURCES = ["abi.cu", "encode.cu", "refine.cu", "phc.cu", "ggr.cu"]
+SOURCES = ["abi.cu", "encode.cu", "refine.cu", "phc.cu", "ggr.cu", "comm.cu", "shard.cu"]
 
 NVCC = os.environ.get("NVCC", shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -58,7 +58,7 @@ def build(verbose: bool = False, force: bool = False) -> Path:
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
         list(ex.map(run, jobs))
     if force or jobs or _stale(OUT, objs):
-        run([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", str(OUT), *map(str, objs)])
+        run([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", str(OUT), *map(str, objs), "-ldl"])
     gen_src = CSRC / "gen.cpp"
     if force or _stale(GEN_OUT, [gen_src]):
         run([CXX, "-std=c++17", "-O3", "-fPIC", "-shared", "-pthread", "-o", str(GEN_OUT),

@@ -6,9 +6,11 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <memory>
 #include <mutex>
 #include <numeric>
 
+#include "comm.cuh"
 #include "internal.cuh"
 
 namespace po {
@@ -224,6 +226,18 @@ uint64_t phc_call(const po_table* tv, int tok, int scoring, uint64_t n_entries,
 
 using namespace po;
 
+struct po_comm {
+  std::unique_ptr<po::Comm> c;
+};
+
+struct po_slice {
+  uint64_t offset = 0, count = 0;
+  uint32_t m = 0;
+  int device = 0;
+  po::DevBuf<uint64_t> rows;
+  po::DevBuf<int32_t> orders;  // (count + 1) * m, entry i at (i + 1) * m
+};
+
 extern "C" {
 
 int po_ggr(const po_table* t, const po_fd_groups* fds, const po_ggr_config* cfg, int32_t tok,
@@ -360,6 +374,104 @@ int po_fixed_order_by_stats(uint32_t m, uint64_t total_rows, const uint64_t* car
     std::copy(o.begin(), o.end(), out);
   });
 }
+
+int po_comm_unique_id(uint8_t* out_id128) {
+  return guarded([&] {
+    if (!out_id128) fail(PO_ERR_INVALID_ARG, "null id buffer");
+    nccl_unique_id(out_id128);
+  });
+}
+
+int po_comm_init_nccl(const uint8_t* id128, int32_t nranks, int32_t rank, po_comm** out) {
+  return guarded([&] {
+    if (!id128 || !out) fail(PO_ERR_INVALID_ARG, "null argument");
+    auto h = std::make_unique<po_comm>();
+    h->c.reset(make_nccl_comm(id128, nranks, rank));
+    *out = h.release();
+  });
+}
+
+int po_comm_init_local(int32_t nranks, po_comm** out_array) {
+  return guarded([&] {
+    if (!out_array) fail(PO_ERR_INVALID_ARG, "null output array");
+    std::vector<Comm*> cs = make_local_group(nranks);
+    for (int32_t r = 0; r < nranks; ++r) {
+      out_array[r] = new po_comm;
+      out_array[r]->c.reset(cs[r]);
+    }
+  });
+}
+
+int po_comm_destroy(po_comm* comm) {
+  return guarded([&] { delete comm; });
+}
+
+int po_ggr_sharded(po_comm* comm, const po_table* t, const po_fd_groups* fds,
+                   const po_ggr_config* cfg, int32_t tok, int32_t scoring, po_slice** out_slice,
+                   uint64_t* out_phc, po_solve_stats* out_stats, void* stream) {
+  return guarded([&] {
+    auto t0 = std::chrono::steady_clock::now();
+    if (!comm || !cfg || !out_slice || !out_phc) fail(PO_ERR_INVALID_ARG, "null argument");
+    if (cfg->stats_variant < 0 || cfg->stats_variant > 2)
+      fail(PO_ERR_INVALID_ARG, "unknown stats variant");
+    check_modes(tok, scoring);
+    init_pool_once();
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    timing_mark("<start", s);
+    std::vector<std::vector<int>> groups;
+    if (fds && cfg->use_fds)
+      for (uint32_t g = 0; g < fds->n_groups; ++g)
+        groups.emplace_back(fds->members + fds->group_offsets[g],
+                            fds->members + fds->group_offsets[g + 1]);
+    DeviceTable dt;
+    make_device_table(t, tok, s, dt);
+    DistCtx dc;
+    GgrOutput go;
+    ggr_sharded(*comm->c, dt, tok, scoring, groups, *cfg, dc, go, s);
+    auto sl = std::make_unique<po_slice>();
+    sl->offset = dc.slice_offset;
+    sl->count = dc.slice_count;
+    sl->m = dt.m;
+    PO_CUDA(cudaGetDevice(&sl->device));
+    sl->rows = std::move(dc.rows);
+    sl->orders = std::move(dc.orders);
+    sync(s);
+    timing_report("po_ggr_sharded");
+    *out_phc = go.phc;
+    if (out_stats) {
+      *out_stats = go.stats;
+      out_stats->wall_ms =
+          std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    }
+    *out_slice = sl.release();
+  });
+}
+
+int po_slice_info(const po_slice* slice, uint64_t* out_offset, uint64_t* out_count) {
+  return guarded([&] {
+    if (!slice) fail(PO_ERR_INVALID_ARG, "null slice");
+    if (out_offset) *out_offset = slice->offset;
+    if (out_count) *out_count = slice->count;
+  });
+}
+
+int po_slice_copy(const po_slice* slice, uint32_t loc, uint64_t* out_rows, int32_t* out_orders,
+                  void* stream) {
+  return guarded([&] {
+    if (!slice) fail(PO_ERR_INVALID_ARG, "null slice");
+    if (loc != PO_LOC_HOST && loc != PO_LOC_DEVICE) fail(PO_ERR_INVALID_ARG, "bad location");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const cudaMemcpyKind k = loc == PO_LOC_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+    if (slice->count && out_rows)
+      PO_CUDA(cudaMemcpyAsync(out_rows, slice->rows.get(), slice->count * 8, k, s));
+    if (slice->count && slice->m && out_orders)
+      PO_CUDA(cudaMemcpyAsync(out_orders, slice->orders.get() + slice->m,
+                              slice->count * slice->m * sizeof(int32_t), k, s));
+    sync(s);
+  });
+}
+
+void po_slice_free(po_slice* slice) { delete slice; }
 
 const char* po_last_error(void) { return g_err.c_str(); }
 

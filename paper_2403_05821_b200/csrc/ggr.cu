@@ -32,6 +32,7 @@
 #include <memory>
 #include <numeric>
 
+#include "comm.cuh"
 #include "internal.cuh"
 
 namespace cg = cooperative_groups;
@@ -317,6 +318,36 @@ __global__ void k_raw1_scatter(const uint32_t* rows, const uint32_t* raw_pos, ui
     pos[rows[k]] = raw_pos[k];
 }
 
+// Sharded solve: tie-break by the global raw-byte rank (rv, per global dense
+// index): per tie group the entry with the smallest (raw rank, vid).
+__global__ void k_tie_min_raw(const WorkItem* __restrict__ work, const ScanSlot* __restrict__ slots,
+                              const uint32_t* __restrict__ masks,
+                              const uint32_t* __restrict__ weights,
+                              const uint64_t* __restrict__ colbase,
+                              const uint64_t* __restrict__ vlen, uint32_t m, uint32_t K,
+                              const Cand* __restrict__ best, const int32_t* __restrict__ tie_group,
+                              const uint32_t* __restrict__ rv, unsigned long long* minkey) {
+  const WorkItem w = work[blockIdx.x];
+  const int32_t g = tie_group[w.slot];
+  if (g < 0) return;
+  const ScanSlot sl = slots[w.slot];
+  const uint32_t* mask = masks + sl.mask_off;
+  const uint32_t* wt = weights + sl.w_off;
+  const Cand b = best[w.slot];
+  for (uint64_t e = w.lo + threadIdx.x; e < w.hi; e += blockDim.x) {
+    uint32_t c, v;
+    if (!decode_work(w, sl.t, colbase, m, e, c, v)) continue;
+    const uint32_t cnt = sl.t.cnt[e];
+    if (cnt != b.count || c != b.col || !mask_has(mask, c)) continue;
+    const uint64_t vl = vlen[colbase[c] + v];
+    uint64_t ptot = 0;
+    for (uint32_t k = 0; k < K; ++k)
+      if (wt[c * K + k]) ptot += uint64_t(wt[c * K + k]) * sl.t.psum[e * K + k];
+    if ((u128(vl) * vl * cnt + ptot) * u128(cnt - 1) != b.numer) continue;
+    atomicMin(&minkey[g], (uint64_t(rv[colbase[c] + v]) << 32) | v);
+  }
+}
+
 // One block per scanning node: reduce its per-chunk partials.
 __global__ void __launch_bounds__(kArgBlock) k_argmax_final(
     const Cand* partial, const unsigned long long* partial_cands, const uint32_t* slot_work_off,
@@ -474,6 +505,49 @@ __global__ void __launch_bounds__(kAggBlock) k_aggregate(
         if (tk.to_b) atomicAdd(&d.tB.psum[sb * K + k], l);
         if (tk.to_p) atomicAdd(&d.tP.psum[spn * K + k], 0ull - l);
       }
+    }
+  }
+}
+
+// Sharded solve: this rank's block-row aggregate of split j (a private
+// table) as records [key][split<<32 | count][K partner sums].
+__global__ void k_compact_contrib(TDesc t, uint32_t j, uint32_t K, uint64_t* out,
+                                  unsigned long long* cursor) {
+  for (uint64_t e = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; e < t.cap;
+       e += uint64_t(gridDim.x) * blockDim.x) {
+    const unsigned long long key = t.keys[e];
+    if (!key) continue;
+    const uint64_t at = atomicAdd(cursor, 1ull);
+    uint64_t* r = out + at * (2 + K);
+    r[0] = key;
+    r[1] = (uint64_t(j) << 32) | t.cnt[e];
+    for (uint32_t k = 0; k < K; ++k) r[2 + k] = t.psum[e * K + k];
+  }
+}
+
+// Every rank's contributions into the replicated tables: add to the block
+// child's table (columns outside the block columns) and subtract from the
+// parent's table kept by the rest child — the same updates k_aggregate
+// makes from the rows themselves on one GPU.
+__global__ void k_apply_contrib(uint64_t E, const uint64_t* __restrict__ recs, uint32_t K,
+                                const SplitD* __restrict__ sp, const uint32_t* __restrict__ bmask,
+                                uint32_t W, const uint64_t* __restrict__ colbase) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < E;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t* r = recs + i * (2 + K);
+    const unsigned long long key = r[0];
+    const uint32_t j = uint32_t(r[1] >> 32), cnt = uint32_t(r[1]);
+    const uint32_t c = uint32_t(key >> 32) - 1, v = uint32_t(key);
+    const SplitD& d = sp[j];
+    if (d.tB.keys && !((bmask[j * W + (c >> 5)] >> (c & 31)) & 1u)) {
+      const uint64_t sb = tbl_insert(d.tB, key);
+      atomicAdd(&d.tB.cnt[sb], cnt);
+      for (uint32_t k = 0; k < K; ++k) atomicAdd(&d.tB.psum[sb * K + k], (unsigned long long)r[2 + k]);
+    }
+    if (d.tP.cnt) {
+      const uint64_t spn = d.tP.dense ? colbase[c] + v : tbl_find(d.tP, key);
+      atomicSub(&d.tP.cnt[spn], cnt);
+      for (uint32_t k = 0; k < K; ++k) atomicAdd(&d.tP.psum[spn * K + k], 0ull - r[2 + k]);
     }
   }
 }
@@ -685,13 +759,15 @@ struct Pack {
 
 void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups,
                 const po_ggr_config& cfg, uint32_t* d_rows, int32_t* d_orders, GgrOutput& out,
-                cudaStream_t s) {
-  const uint64_t n = e.n;
+                cudaStream_t s, DistCtx* dist) {
+  const uint64_t n = e.n;  // rows held here (all of them on one GPU)
   const uint32_t m = e.m;
+  const uint64_t ng = dist ? dist->n_global : n;  // rows of the whole table
   out = GgrOutput{};
   out.stats.recursive_calls = 1;  // the root call (ggr.hpp:210)
-  if (n == 0) return;
+  if (ng == 0) return;
   if (m == 0) {  // every row, ascending, no fields (ggr.hpp:214-219)
+    if (dist) fail(PO_ERR_ERROR, "internal: sharded solve with no fields");
     PO_LAUNCH(k_iota_u32, grid_for(n, 256), 256, 0, s, d_rows, n);
     return;
   }
@@ -739,7 +815,7 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
   nodes.reserve(1024);
   {
     Node root;
-    root.size = n;
+    root.size = ng;
     root.cols.resize(m);
     std::iota(root.cols.begin(), root.cols.end(), 0);
     root.kind = classify(root, cfg);
@@ -781,6 +857,7 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
       t->psum.zero();
       PO_LAUNCH(k_root_psum, grid_for(n * m, 256), 256, 0, s, e.vid.get(), n, m, K, d_dpart.get(),
                 d_npart.get(), vlen, colbase, t->psum.get());
+      if (dist) dist->comm->allreduce(t->psum.get(), e.D * K, CDtype::U64, COp::Sum, s);
     }
     nodes[0].table = t;
   }
@@ -831,7 +908,7 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
       // their |node| groups are added to candidates_examined directly.
       std::vector<int> scan_cols;
       for (int c : nd.cols)
-        if (e.card[c] == n) unique_groups[i] += nd.size;
+        if (e.card[c] == ng) unique_groups[i] += nd.size;
         else scan_cols.push_back(c);
       sl.mask_off = col_mask(scan_cols, L.masks);
       sl.w_off = uint32_t(L.weights.size());
@@ -908,7 +985,21 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
         tie_slot.push_back(i);
         tie_off.push_back(tie_off.back() + uint32_t(b.ties));
       }
-      if (!tie_slot.empty()) {
+      if (!tie_slot.empty() && dist) {
+        const uint32_t nt = uint32_t(tie_slot.size());
+        const uint32_t* rv = dist->raw_ranks();
+        auto d_tg = to_device(tie_group, s);
+        DevBuf<unsigned long long> mk(nt, s);
+        mk.fill_bytes(0xFF);
+        PO_LAUNCH(k_tie_min_raw, unsigned(L.work.size()), kArgBlock, 0, s,
+                  reinterpret_cast<WorkItem*>(dp + o_work), reinterpret_cast<ScanSlot*>(dp + o_slots),
+                  reinterpret_cast<uint32_t*>(dp + o_masks), reinterpret_cast<uint32_t*>(dp + o_w),
+                  colbase, vlen, m, K, d_best, d_tg.get(), rv, mk.get());
+        std::vector<unsigned long long> hm(nt);
+        mk.download(hm.data(), nt);
+        sync(s);
+        for (uint32_t g = 0; g < nt; ++g) hbest[tie_slot[g]].vid = uint32_t(hm[g]);
+      } else if (!tie_slot.empty()) {
         const uint32_t ng = uint32_t(tie_slot.size()), total = tie_off.back();
         auto d_tg = to_device(tie_group, s);
         auto d_toff = to_device(tie_off, s);
@@ -1072,12 +1163,84 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
       PO_LAUNCH(k_relabel, grid_for(n, 256), 256, ns <= kRelabelSmem ? ns * 4 : 0, s,
                 node_of_row.get(), n, d_snodes, ns, d_sp, e.vid.get(), m, d_cursor, d_seg,
                 blockrows.get());
-      if (!tasks.empty())
+      if (!dist && !tasks.empty())
         PO_LAUNCH(k_aggregate, unsigned(tasks.size()), kAggBlock, 0, s,
                   reinterpret_cast<AggTask*>(ds + o_tasks), blockrows.get(), d_sp, e.vid.get(),
                   vlen, colbase, m, K, d_dpart.get(), d_npart.get());
+      if (dist) {
+        // this rank's block rows -> private tables -> contributions, all-gathered
+        // and applied to the replicated child / parent tables
+        std::vector<uint32_t> lcnt(ns);
+        PO_CUDA(cudaMemcpyAsync(lcnt.data(), d_cursor, ns * 4, cudaMemcpyDeviceToHost, s));
+        sync(s);
+        std::vector<std::unique_ptr<HTable>> priv(ns);
+        std::vector<SplitD> hsp2(hsp);
+        std::vector<AggTask> tasks2;
+        std::vector<uint32_t> bmask(size_t(ns) * W, 0);
+        uint64_t max_entries = 0;
+        for (uint32_t j = 0; j < ns; ++j) {
+          const Node& P = nodes[splits[j].node];
+          for (int c : P.block_cols) bmask[size_t(j) * W + (uint32_t(c) >> 5)] |= 1u << (uint32_t(c) & 31);
+          hsp2[j].tP = TDesc{};
+          if (!hsp[j].need_rows || !lcnt[j]) continue;
+          uint64_t bound = 0;
+          for (int c : P.cols) bound += std::min<uint64_t>(e.card[c], lcnt[j]);
+          uint64_t cap = 64;
+          while (cap < bound + bound / 2) cap <<= 1;
+          auto t = std::make_unique<HTable>();
+          t->cap = cap;
+          t->keys.alloc(cap, s);
+          t->keys.zero();
+          t->cnt.alloc(cap, s);
+          t->cnt.zero();
+          if (K) {
+            t->psum.alloc(cap * K, s);
+            t->psum.zero();
+          }
+          hsp2[j].tB = t->desc();
+          priv[j] = std::move(t);
+          max_entries += bound;
+          for (int c : P.cols)
+            for (uint64_t lo = seg[j]; lo < seg[j] + lcnt[j]; lo += kRowsPerTask)
+              tasks2.push_back(AggTask{j, uint32_t(c), 1u, 0u, lo,
+                                       std::min<uint64_t>(seg[j] + lcnt[j], lo + kRowsPerTask)});
+        }
+        Pack p2;
+        const size_t o_sp2 = p2.add(hsp2), o_t2 = p2.add(tasks2), o_bm = p2.add(bmask);
+        DevBuf<uint8_t> dev2(p2.host.size(), s);
+        dev2.upload(p2.host.data(), p2.host.size());
+        if (!tasks2.empty())
+          PO_LAUNCH(k_aggregate, unsigned(tasks2.size()), kAggBlock, 0, s,
+                    reinterpret_cast<AggTask*>(dev2.get() + o_t2), blockrows.get(),
+                    reinterpret_cast<SplitD*>(dev2.get() + o_sp2), e.vid.get(), vlen, colbase, m,
+                    K, d_dpart.get(), d_npart.get());
+        const uint32_t RW = 2 + K;
+        DevBuf<uint64_t> contrib(std::max<uint64_t>(1, max_entries) * RW, s);
+        DevBuf<unsigned long long> ccur(1, s);
+        ccur.zero();
+        for (uint32_t j = 0; j < ns; ++j)
+          if (priv[j])
+            PO_LAUNCH(k_compact_contrib, grid_for(priv[j]->cap, 256), 256, 0, s, priv[j]->desc(), j,
+                      K, contrib.get(), ccur.get());
+        unsigned long long El = 0;
+        ccur.download(&El, 1);
+        sync(s);
+        priv.clear();
+        const std::vector<uint64_t> Es = dist->comm->allgather_host({uint64_t(El)}, s);
+        std::vector<uint64_t> rbytes(Es.size());
+        uint64_t Et = 0;
+        for (size_t r = 0; r < Es.size(); ++r) {
+          rbytes[r] = Es[r] * RW * 8;
+          Et += Es[r];
+        }
+        DevBuf<uint64_t> allc(std::max<uint64_t>(1, Et) * RW, s);
+        dist->comm->allgatherv(contrib.get(), allc.get(), rbytes, s);
+        PO_LAUNCH(k_apply_contrib, grid_for(Et, 256), 256, 0, s, Et, allc.get(), K, d_sp,
+                  reinterpret_cast<uint32_t*>(dev2.get() + o_bm), W, colbase);
+        sync(s);
+      }
     }
-    if (debug_checks()) {
+    if (debug_checks() && !dist) {
       DevBuf<unsigned long long> hist(nodes.size() + 1, s);
       hist.zero();
       PO_LAUNCH(k_dbg_node_hist, grid_for(n, 256), 256, 0, s, node_of_row.get(), n,
@@ -1155,7 +1318,55 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
     leaf_chunk_off[l] = uint32_t(ks.chunk_nkeys.size());
     leaf_nchunks[l] = ks.add_leaf(keys, e.card, cap0, cap);
   }
-  if (off != n) fail(PO_ERR_ERROR, "internal: leaves do not cover the table");
+  if (off != ng) fail(PO_ERR_ERROR, "internal: leaves do not cover the table");
+  if (dist) {
+    // distributed layout: leaf order, leaf keys, global row id (ggr.hpp:303-350)
+    std::vector<LeafKeys> lk(nleaves);
+    for (uint32_t l = 0; l < nleaves; ++l) {
+      const Node& nd = nodes[leaf_nodes[l]];
+      lk[l].full_order = leaf_full_order[l];
+      if (nd.kind == FALLBACK) {
+        lk[l].kind = 1;
+        lk[l].fields = nd.leaf_order;
+      } else if (nd.kind == RAW1) {
+        lk[l].kind = 2;
+        lk[l].fields = {nd.cols[0]};
+      }
+    }
+    auto d_node_leaf = to_device(node_leaf, s);
+    auto d_leaf_off = to_device(leaf_off, s);
+    DevBuf<uint32_t> row_leaf(n, s), grp(n, s);
+    PO_LAUNCH(k_row_leaf, grid_for(n, 256), 256, 0, s, node_of_row.get(), n, d_node_leaf.get(),
+              d_leaf_off.get(), row_leaf.get(), grp.get());
+    out.phc = dist_layout(*dist, e, row_leaf.get(), lk, s);
+    timing_mark("dist_layout", s);
+    // whole-table fallback competition (ggr.hpp:379-387) from global stats
+    std::vector<double> avg(m);
+    for (uint32_t c = 0; c < m; ++c)
+      avg[c] = static_cast<double>(e.total_len[c]) / static_cast<double>(ng);
+    const std::vector<int> fb_order = hitcount_order(ng, e.card, avg, cfg.stats_variant);
+    DistCtx fb;
+    fb.comm = dist->comm;
+    fb.n_global = ng;
+    fb.row_offset = dist->row_offset;
+    fb.raw_ranks = dist->raw_ranks;
+    row_leaf.zero();
+    LeafKeys one;
+    one.kind = 1;
+    one.fields = fb_order;
+    one.full_order = fb_order;
+    const uint64_t fb_phc = dist_layout(fb, e, row_leaf.get(), {one}, s);
+    if (fb_phc > out.phc) {  // replace only when strictly better (ggr.hpp:383)
+      dist->slice_offset = fb.slice_offset;
+      dist->slice_count = fb.slice_count;
+      dist->rows = std::move(fb.rows);
+      dist->orders = std::move(fb.orders);
+      out.phc = fb_phc;
+    }
+    timing_mark("dist_fallback", s);
+    sync(s);
+    return;
+  }
   ks.pad();
   const auto& chunk_key_off = ks.chunk_key_off;
   const auto& chunk_nkeys = ks.chunk_nkeys;
@@ -1190,8 +1401,8 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
   // its PHC comes from prefix groups, its row sort only runs if it wins
   std::vector<double> avg(m);
   for (uint32_t c = 0; c < m; ++c)
-    avg[c] = static_cast<double>(e.total_len[c]) / static_cast<double>(n);
-  std::vector<int> fb_order = hitcount_order(n, e.card, avg, cfg.stats_variant);
+    avg[c] = static_cast<double>(e.total_len[c]) / static_cast<double>(ng);
+  std::vector<int> fb_order = hitcount_order(ng, e.card, avg, cfg.stats_variant);
   RefineJob leaf_job;
   leaf_job.n_items = uint32_t(n);
   leaf_job.d_grp_init = row_leaf.get();  // round 0: leaf index

@@ -2,12 +2,19 @@
 #pragma once
 
 #include <cstdint>
+#include <functional>
 #include <string>
 #include <vector>
 
 #include "common.cuh"
 
 namespace po {
+
+class Comm;
+
+// Escaped fragment-key order of bytes (refine.cu): code[b] = rank of byte b's
+// json_escape expansion, code[256] = rank of the closing '"'.
+void esc_code_table(uint16_t code[257]);
 
 // Device view of the caller's table (arena/offsets already in HBM).
 struct DeviceTable {
@@ -167,6 +174,13 @@ uint64_t phc_device(const Encoded& e, uint64_t n_entries, const uint64_t* rows64
                     const int32_t* fields, cudaStream_t s, uint64_t first_entry = 1,
                     bool uniform_order = false);
 
+// Same over raw device arrays (vid matrix n_rows x m, per-distinct vlen).
+uint64_t phc_device_raw(const uint32_t* vid, const uint64_t* vlen, const uint64_t* colbase,
+                        uint64_t n_rows, uint32_t m, uint64_t n_entries, const uint64_t* rows64,
+                        const uint32_t* rows32, const uint64_t* order_offsets,
+                        const int32_t* fields, cudaStream_t s, uint64_t first_entry = 1,
+                        bool uniform_order = false);
+
 __global__ void k_invert(const uint32_t* pos, uint64_t n, uint32_t* perm);
 
 // Stats-ranked field order (ggr.hpp:59-84) — host IEEE double, no FMA.
@@ -206,10 +220,48 @@ struct GgrOutput {
   po_solve_stats stats{};
 };
 
+// Row-sharded solving (shard.cu). Every rank holds a
+// contiguous range of the table's rows; value ids are global (escaped-order
+// ranks over the whole table), the value-group tables are replicated (built
+// from exchanged per-rank contributions), rows stay where they are until
+// one distributed sort lays out the final schedule.
+struct DistCtx {
+  Comm* comm = nullptr;
+  uint64_t n_global = 0;
+  uint64_t row_offset = 0;  // global id of local row 0
+  // global raw-byte rank of every global dense index (colbase[c] + vid):
+  // built on first use (collective; every rank asks at the same point)
+  std::function<const uint32_t*()> raw_ranks;
+  // this rank's slice of the emitted schedule
+  uint64_t slice_offset = 0, slice_count = 0;
+  DevBuf<uint64_t> rows;   // slice_count global row ids
+  DevBuf<int32_t> orders;  // (slice_count + 1) * m; entry i at (i + 1) * m
+};
+
+// One leaf of the final layout (DFS order): how its rows are keyed.
+struct LeafKeys {
+  int kind = 0;                 // 0: row id only, 1: escaped ranks of `fields`, 2: raw rank of fields[0]
+  std::vector<int> fields;      // key fields in order
+  std::vector<int> full_order;  // emitted field order (m fields)
+};
+
+// Distributed layout of the local rows (row_leaf[r] = leaf index) in leaf
+// order, then keys, then global row id; fills dc's slice and returns the
+// global PHC of the laid-out schedule (objective.hpp:94-99).
+uint64_t dist_layout(DistCtx& dc, const Encoded& G, const uint32_t* d_row_leaf,
+                     const std::vector<LeafKeys>& leaves, cudaStream_t s);
+
 // GGR (ggr.hpp:144-394) on an encoded table. Writes the emitted schedule to
-// d_rows (u32, n) and d_orders (i32, n*m) on the device.
+// d_rows (u32, n) and d_orders (i32, n*m) on the device. With `dist`, e is
+// this rank's rows under global value ids and the schedule goes to dist's
+// slice instead (d_rows / d_orders unused).
 void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups,
                 const po_ggr_config& cfg, uint32_t* d_rows, int32_t* d_orders, GgrOutput& out,
-                cudaStream_t s);
+                cudaStream_t s, DistCtx* dist = nullptr);
+
+// Row-sharded ggr(): local rows of the table in `t`, collectives over comm.
+void ggr_sharded(Comm& comm, const DeviceTable& t, int tok, int scoring,
+                 const std::vector<std::vector<int>>& fd_groups, const po_ggr_config& cfg,
+                 DistCtx& dc, GgrOutput& out, cudaStream_t s);
 
 }  // namespace po

@@ -74,17 +74,19 @@ __global__ void k_invert(const uint32_t* pos, uint64_t n, uint32_t* perm) {
     perm[pos[r]] = uint32_t(r);
 }
 
-uint64_t phc_device(const Encoded& e, uint64_t n_entries, const uint64_t* rows64,
-                    const uint32_t* rows32, const uint64_t* order_offsets, const int32_t* fields,
-                    cudaStream_t s, uint64_t first_entry, bool uniform_order) {
+uint64_t phc_device_raw(const uint32_t* vid, const uint64_t* vlen, const uint64_t* colbase,
+                        uint64_t n_rows, uint32_t m, uint64_t n_entries, const uint64_t* rows64,
+                        const uint32_t* rows32, const uint64_t* order_offsets,
+                        const int32_t* fields, cudaStream_t s, uint64_t first_entry,
+                        bool uniform_order) {
   if (n_entries <= first_entry) return 0;
   DevBuf<unsigned long long> tot(1, s);
   DevBuf<int> err(1, s);
   tot.zero();
   err.zero();
-  PO_LAUNCH(k_phc, grid_for(n_entries, 256, 8), 256, 0, s, e.vid.get(), e.vlen.get(),
-            e.d_colbase.get(), e.n, e.m, n_entries, first_entry, rows64, rows32, order_offsets,
-            fields, uniform_order ? 1 : 0, tot.get(), err.get());
+  PO_LAUNCH(k_phc, grid_for(n_entries, 256, 8), 256, 0, s, vid, vlen, colbase, n_rows, m,
+            n_entries, first_entry, rows64, rows32, order_offsets, fields, uniform_order ? 1 : 0,
+            tot.get(), err.get());
   unsigned long long h = 0;
   int herr = 0;
   tot.download(&h, 1);
@@ -92,6 +94,13 @@ uint64_t phc_device(const Encoded& e, uint64_t n_entries, const uint64_t* rows64
   sync(s);
   if (herr) fail(PO_ERR_OUT_OF_RANGE, "schedule references a row or field outside the table");
   return h;
+}
+
+uint64_t phc_device(const Encoded& e, uint64_t n_entries, const uint64_t* rows64,
+                    const uint32_t* rows32, const uint64_t* order_offsets, const int32_t* fields,
+                    cudaStream_t s, uint64_t first_entry, bool uniform_order) {
+  return phc_device_raw(e.vid.get(), e.vlen.get(), e.d_colbase.get(), e.n, e.m, n_entries, rows64,
+                        rows32, order_offsets, fields, s, first_entry, uniform_order);
 }
 
 // PHC of the whole table sorted by one fixed field order, without sorting.

@@ -15,6 +15,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <memory>
+#include <mutex>
 
 #include "internal.cuh"
 
@@ -195,33 +196,13 @@ __global__ void k_iota(uint32_t* a, uint32_t n) {
 }
 
 bool g_esc_table_ready = false;
+std::mutex g_esc_mu;
 
 void ensure_esc_table() {
+  std::lock_guard<std::mutex> lk(g_esc_mu);
   if (g_esc_table_ready) return;
-  // Symbol value of each byte in escaped text (scoring.hpp:33-57): plain
-  // bytes keep their value; escapes start with '\' (0x5C) then the escape
-  // letter; \u00XX escapes append the byte itself (hex digits sort like the
-  // byte). The fragment terminator '"' closes every value.
-  std::vector<std::pair<uint32_t, int>> sym;
-  for (int b = 0; b < 256; ++b) {
-    uint32_t v;
-    switch (b) {
-      case '"': v = (0x5Cu << 16) | (0x22u << 8); break;
-      case '\\': v = (0x5Cu << 16) | (0x5Cu << 8); break;
-      case '\b': v = (0x5Cu << 16) | (uint32_t('b') << 8); break;
-      case '\f': v = (0x5Cu << 16) | (uint32_t('f') << 8); break;
-      case '\n': v = (0x5Cu << 16) | (uint32_t('n') << 8); break;
-      case '\r': v = (0x5Cu << 16) | (uint32_t('r') << 8); break;
-      case '\t': v = (0x5Cu << 16) | (uint32_t('t') << 8); break;
-      default:
-        v = b < 0x20 ? ((0x5Cu << 16) | (uint32_t('u') << 8) | uint32_t(b)) : (uint32_t(b) << 16);
-    }
-    sym.push_back({v, b});
-  }
-  sym.push_back({0x22u << 16, 256});
-  std::sort(sym.begin(), sym.end());
   uint16_t code[257];
-  for (size_t r = 0; r < sym.size(); ++r) code[sym[r].second] = uint16_t(r + 1);
+  esc_code_table(code);
   PO_CUDA(cudaMemcpyToSymbol(c_esc_code, code, sizeof(code)));
   g_esc_table_ready = true;
 }
@@ -245,6 +226,33 @@ struct Job {
 };
 
 }  // namespace
+
+// Symbol value of each byte in escaped text (scoring.hpp:33-57): plain
+// bytes keep their value; escapes start with '\' (0x5C) then the escape
+// letter; \u00XX escapes append the byte itself (hex digits sort like the
+// byte). The fragment terminator '"' closes every value. code[b] is the rank
+// of byte b's expansion, code[256] the rank of the terminator.
+void esc_code_table(uint16_t code[257]) {
+  std::vector<std::pair<uint32_t, int>> sym;
+  for (int b = 0; b < 256; ++b) {
+    uint32_t v;
+    switch (b) {
+      case '"': v = (0x5Cu << 16) | (0x22u << 8); break;
+      case '\\': v = (0x5Cu << 16) | (0x5Cu << 8); break;
+      case '\b': v = (0x5Cu << 16) | (uint32_t('b') << 8); break;
+      case '\f': v = (0x5Cu << 16) | (uint32_t('f') << 8); break;
+      case '\n': v = (0x5Cu << 16) | (uint32_t('n') << 8); break;
+      case '\r': v = (0x5Cu << 16) | (uint32_t('r') << 8); break;
+      case '\t': v = (0x5Cu << 16) | (uint32_t('t') << 8); break;
+      default:
+        v = b < 0x20 ? ((0x5Cu << 16) | (uint32_t('u') << 8) | uint32_t(b)) : (uint32_t(b) << 16);
+    }
+    sym.push_back({v, b});
+  }
+  sym.push_back({0x22u << 16, 256});
+  std::sort(sym.begin(), sym.end());
+  for (size_t r = 0; r < sym.size(); ++r) code[sym[r].second] = uint16_t(r + 1);
+}
 
 uint32_t refine_chunk_bits(uint32_t grp_max) { return 64u - uint32_t(bits_for(grp_max)); }
 

@@ -1,14 +1,16 @@
-"""Multi-GPU pieces over torch.distributed (NCCL between B200s; gloo in the
-CPU tests). One process per GPU.
+"""Multi-GPU pieces: one rank per GPU.
 
-Implemented: the row-range-sharded PHC with the one-entry boundary exchange
-(SURVEY.md §8e step 7): a schedule split into contiguous request ranges is
-scored per rank, the first request of every range against the last request
-of the previous range (sent point-to-point), and the per-rank sums are
-all-reduced. The sum is taken modulo 2^64 exactly like the reference's u64
-accumulation (objective.hpp:96-98). The sharded GGR itself (global
-dictionary exchange, per-level histogram merges) is not built yet; see
-DESIGN.md §7.
+* `ggr_sharded` — the row-sharded GGR solve (csrc/shard.cu through
+  po_ggr_sharded): every rank passes a contiguous range of the table's rows
+  and gets back one contiguous slice of the schedule; the slices in rank
+  order are bit-identical to ggr() on the whole table. Collectives run over a
+  `ShardComm`: NCCL between B200s (`nccl_comm`, one process per GPU, the
+  unique id shipped over torch.distributed) or an in-process thread group
+  (`local_comms`, several ranks on one GPU — how the parity tests exercise
+  the sharded path on a 1-GPU box).
+* `sharded_phc` — the row-range-sharded PHC over torch.distributed with the
+  one-entry boundary exchange, whose host logic the
+  gloo tests cover on CPU.
 """
 from __future__ import annotations
 
@@ -18,7 +20,11 @@ import numpy as np
 import torch
 import torch.distributed as dist
 
-from .api import RequestSchedule, SegmentScoring, char_tokenizer, phc as device_phc
+from ._abi import PO_LOC_DEVICE, PO_LOC_HOST, FdView, cuda_lib, po_solve_stats
+from .api import (GgrConfig, RequestSchedule, SegmentScoring, SolveStats, _fd_indices, _view,
+                  char_tokenizer, phc as device_phc)
+import ctypes as C
+from dataclasses import dataclass
 
 _MASK64 = (1 << 64) - 1
 
@@ -84,3 +90,107 @@ def sharded_phc(sched: RequestSchedule, table, tok=None,
     t = torch.tensor([as_i64], dtype=torch.int64, device=device)
     dist.all_reduce(t, group=group)
     return int(t.item()) & _MASK64
+
+
+# ---------------------------------------------------------------------------
+# row-sharded GGR
+# ---------------------------------------------------------------------------
+class ShardComm:
+    """A rank's communicator handle (po_comm)."""
+
+    def __init__(self, handle: int, rank: int, world: int):
+        self.handle, self.rank, self.world = handle, rank, world
+
+    def close(self) -> None:
+        if self.handle:
+            cuda_lib().comm_destroy(self.handle)
+            self.handle = 0
+
+    def __del__(self):  # pragma: no cover - best effort
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def local_comms(world: int) -> list:
+    """`world` communicators of one in-process group (one host thread per rank)."""
+    lib = cuda_lib()
+    arr = (C.c_void_p * world)()
+    lib.check(lib.comm_init_local(world, arr))
+    return [ShardComm(arr[r], r, world) for r in range(world)]
+
+
+def nccl_comm(rank: int | None = None, world: int | None = None, group=None) -> ShardComm:
+    """NCCL communicator over the ranks of an initialised torch.distributed
+    group (the 128-byte NCCL id is broadcast from rank 0 through it)."""
+    lib = cuda_lib()
+    rank = dist.get_rank(group) if rank is None else rank
+    world = dist.get_world_size(group) if world is None else world
+    uid = np.zeros(128, dtype=np.uint8)
+    if rank == 0:
+        lib.check(lib.comm_unique_id(uid.ctypes.data))
+    if world > 1:
+        obj = [uid.tobytes()]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        uid = np.frombuffer(obj[0], dtype=np.uint8).copy()
+    h = C.c_void_p(0)
+    lib.check(lib.comm_init_nccl(uid.ctypes.data, world, rank, C.byref(h)))
+    return ShardComm(h.value, rank, world)
+
+
+@dataclass
+class ShardResult:
+    slice_offset: int          # position of this slice in the whole schedule
+    row_ids: np.ndarray        # u64 global row ids, one per request of the slice
+    field_orders: np.ndarray   # i32 [count, m]
+    phc_score: int             # PHC of the WHOLE schedule (same on every rank)
+    stats: SolveStats
+
+
+def ggr_sharded_into(comm: ShardComm, view, fd_groups: list, cfg: GgrConfig, tok_kind: int,
+                     scoring: int, stream: int = 0, out_location: int | None = PO_LOC_HOST):
+    """po_ggr_sharded on a prepared view of this rank's rows. Returns
+    (slice_offset, count, rows, orders, phc, stats); rows/orders are host
+    arrays (out_location HOST), device tensors (DEVICE) or None (None: the
+    slice stays on the device and is freed)."""
+    lib = cuda_lib()
+    fdv = FdView(fd_groups)
+    sl = C.c_void_p(0)
+    score = C.c_uint64(0)
+    st = po_solve_stats()
+    c = cfg.abi()
+    lib.check(lib.ggr_sharded(comm.handle, view.ref(), fdv.ref(), C.byref(c), tok_kind, scoring,
+                              C.byref(sl), C.byref(score), C.byref(st), stream))
+    try:
+        off, cnt = C.c_uint64(0), C.c_uint64(0)
+        lib.check(lib.slice_info(sl, C.byref(off), C.byref(cnt)))
+        n, m = int(cnt.value), int(view.view.n_fields)
+        rows = orders = None
+        if out_location == PO_LOC_HOST:
+            rows = np.empty(max(n, 1), dtype=np.uint64)
+            orders = np.empty(max(n * m, 1), dtype=np.int32)
+            lib.check(lib.slice_copy(sl, PO_LOC_HOST, rows.ctypes.data, orders.ctypes.data, stream))
+            rows, orders = rows[:n], orders[:n * m].reshape(n, m)
+        elif out_location == PO_LOC_DEVICE:
+            rows = torch.empty(max(n, 1), dtype=torch.int64, device="cuda")
+            orders = torch.empty(max(n * m, 1), dtype=torch.int32, device="cuda")
+            lib.check(lib.slice_copy(sl, PO_LOC_DEVICE, rows.data_ptr(), orders.data_ptr(), stream))
+            rows, orders = rows[:n], orders[:n * m].view(n, m)
+    finally:
+        lib.slice_free(sl)
+    return (int(off.value), n, rows, orders, int(score.value),
+            SolveStats(st.recursive_calls, st.candidates_examined, st.max_depth, st.wall_ms))
+
+
+def ggr_sharded(comm: ShardComm, t, fds=None, cfg: GgrConfig | None = None, tok=None,
+                scoring: SegmentScoring = SegmentScoring.value_only,
+                stream: int = 0) -> ShardResult:
+    """Row-sharded prefixopt::ggr (ggr.hpp:367-394): `t` is this rank's
+    contiguous range of rows (rank order = row order). Collective."""
+    cfg = cfg or GgrConfig()
+    tok = tok or char_tokenizer()
+    view = _view(t, tok, scoring)
+    off, n, rows, orders, phc_score, st = ggr_sharded_into(
+        comm, view, _fd_indices(t, fds, cfg), cfg, tok.kind, int(scoring), stream)
+    return ShardResult(off, rows, orders, phc_score, st)

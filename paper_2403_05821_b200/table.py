@@ -75,6 +75,18 @@ class Table:
         t._arena, t._offsets, t._n = arena, offsets, int(n_rows)
         return t
 
+    def row_slice(self, lo: int, hi: int) -> "Table":
+        """Rows [lo, hi) as a table of their own (one rank's shard)."""
+        m = len(self._names)
+        lo, hi = max(0, lo), min(self._n, hi)
+        hi = max(lo, hi)
+        if m == 0:
+            return Table.from_arena(self._names, np.zeros(0, np.uint8), np.zeros(1, np.uint64),
+                                    hi - lo)
+        a, b = int(self._offsets[lo * m]), int(self._offsets[hi * m])
+        return Table.from_arena(self._names, self._arena[a:b], self._offsets[lo * m:hi * m + 1] - a,
+                                hi - lo)
+
     # --- accessors (table.hpp:44-66) -------------------------------------
     def row_count(self) -> int:
         return self._n

@@ -123,7 +123,7 @@ inline SolveResult ggr(const Table& t, const FunctionalDependencySet& fds, const
   detail::TableAbi tv(t, tok, scoring);
   const std::size_t n = t.row_count(), m = t.field_count();
   std::vector<std::uint64_t> rows(n ? n : 1);
-  std::vector<std::int32_t> orders(n * m ? n * m : 1);
+  std::vector<std::int32_t> orders(n * m != 0 ? n * m : 1);
   std::uint64_t score = 0;
   po_solve_stats st{};
   detail::check(po_ggr(&tv.view, &fv, &c, tv.tok_kind, tv.scoring, PO_LOC_HOST, rows.data(),
