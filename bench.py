@@ -14,9 +14,13 @@ larger than L2 (126 MB), so no explicit flush is needed between steps.
   e2e     the same call through the C ABI with pinned HOST buffers: the
           arena+offsets H2D copy and the schedule D2H copy are inside every
           step
-Under torchrun (N>1) every rank runs an independent replica on its own copy
-of the table (row-sharded multi-GPU GGR is not built yet): scaling "weak",
-value = N * rows / max-over-ranks time.
+Under torchrun (N>1) the table is N times larger (1M rows per GPU: weak
+scaling) and row-range sharded: rank r generates and holds rows
+[r*1M, (r+1)*1M) and the ranks solve ONE table together through
+po_ggr_sharded over NCCL (global dictionary sample sort, replicated
+value-group tables from exchanged contributions, distributed leaf sort;
+csrc/shard.cu). value = N * rows / max-over-ranks time; each rank's slice of
+the schedule stays in HBM. --sharded forces that path at N=1 as well.
 
 --impl reference times the reference C++ implementation (oracle/_ref, the
 unmodified prefixopt headers compiled from /root/reference; the CPU port in
@@ -196,8 +200,10 @@ def run_ours(args):
 
     lib = cuda_lib()
     cfg_id = args.config
+    sharded = world > 1 or args.sharded
     t0 = time.time()
-    table = gen.generate(cfg_id, n_rows=args.rows)
+    n_per = args.rows if args.rows is not None else gen.CONFIGS[cfg_id].rows
+    table = gen.generate(cfg_id, n_rows=n_per, row_begin=rank * n_per if sharded else 0)
     n, m = table.row_count(), table.field_count()
     cell_bytes = table.cell_bytes
     log(f"[rank {rank}] generated {gen.CONFIGS[cfg_id].name}: {n} rows, {cell_bytes/1e9:.3f} GB "
@@ -214,7 +220,15 @@ def run_ours(args):
     d_rows = torch.empty(n, dtype=torch.int64, device="cuda")
     d_orders = torch.empty(n * m, dtype=torch.int32, device="cuda")
 
+    comm = None
+    if sharded:
+        from paper_2403_05821_b200.dist import ggr_sharded_into, nccl_comm
+        comm = nccl_comm(rank, world)
+
     def step_device():
+        if sharded:
+            r = ggr_sharded_into(comm, dview, fd_idx, cfg, 0, 0, sp, out_location=None)
+            return r[4], r[5]
         return po.ggr_into(dview, fd_idx, cfg, 0, 0, PO_LOC_DEVICE, d_rows, d_orders, sp)
 
     def barrier():
@@ -296,6 +310,9 @@ def run_ours(args):
     h_orders = torch.empty(n * m, dtype=torch.int32).pin_memory()
 
     def step_e2e():
+        if sharded:
+            r = ggr_sharded_into(comm, hview, fd_idx, cfg, 0, 0, sp, out_location=PO_LOC_HOST)
+            return r[4], r[5]
         return po.ggr_into(hview, fd_idx, cfg, 0, 0, PO_LOC_HOST, h_rows, h_orders, sp)
 
     for _ in range(max(1, args.warmup // 2)):
@@ -316,7 +333,7 @@ def run_ours(args):
         raise RuntimeError(f"e2e PHC {phc_e2e} != device-resident PHC {phc}")
 
     cpu = None
-    if rank == 0 and not args.no_cpu:
+    if rank == 0 and world == 1 and not args.no_cpu:
         try:
             rate, secs, kind, ns, res = cpu_reference_rows_per_s(table, fds, args.cpu_rows,
                                                                  "reference")
@@ -334,11 +351,14 @@ def run_ours(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
             "data": "synthetic",
-            "config": {"workload": gen.CONFIGS[cfg_id].name, "rows": n, "fields": m,
+            "config": {"workload": gen.CONFIGS[cfg_id].name if not sharded else
+                       f"{gen.CONFIGS[cfg_id].name} x{world} (rows {world * n}, {n} per GPU)",
+                       "rows": world * n, "rows_per_gpu": n, "fields": m,
                        "cell_bytes": cell_bytes, "ggr_config": "defaults (4/2/100000, fds on)",
                        "tokenizer": "char", "scoring": "value_only",
                        "l2": "inputs (arena+offsets) larger than the 126 MB L2; no flush",
-                       "parallelism": "single GPU" if world == 1 else f"{world} independent replicas"},
+                       "parallelism": (f"dp{world}: one table row-range sharded, NCCL "
+                                       "(po_ggr_sharded)") if sharded else "single GPU"},
             "phc": int(phc),
             "solve_stats": {"recursive_calls": st.recursive_calls,
                             "candidates_examined": st.candidates_examined,
@@ -358,6 +378,8 @@ def run_ours(args):
             "clocks": clocks,
         }
         print(json.dumps(line), flush=True)
+    if comm is not None:
+        comm.close()
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
@@ -376,6 +398,8 @@ def main():
     ap.add_argument("--ref-rows", type=int, default=300_000)
     ap.add_argument("--prof-steps", type=int, default=3)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--sharded", action="store_true",
+                    help="use the row-sharded solver even at N=1 (NCCL, world size 1)")
     args = ap.parse_args()
     if args.warmup < 3:
         log("warning: --warmup < 3 violates the timing rules")

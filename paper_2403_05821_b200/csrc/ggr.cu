@@ -513,12 +513,18 @@ __global__ void __launch_bounds__(kAggBlock) k_aggregate(
 // table) as records [key][split<<32 | count][K partner sums].
 __global__ void k_compact_contrib(TDesc t, uint32_t j, uint32_t K, uint64_t* out,
                                   unsigned long long* cursor) {
+  const uint32_t lane = threadIdx.x & 31;
+  // t.cap is a power of two >= 64 and the grid a multiple of 32 threads, so a
+  // warp stays converged through the loop (warp-aggregated cursor)
   for (uint64_t e = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; e < t.cap;
        e += uint64_t(gridDim.x) * blockDim.x) {
     const unsigned long long key = t.keys[e];
+    const unsigned has = __ballot_sync(0xffffffffu, key != 0);
+    unsigned long long base = 0;
+    if (lane == 0 && has) base = atomicAdd(cursor, (unsigned long long)__popc(has));
+    base = __shfl_sync(0xffffffffu, base, 0);
     if (!key) continue;
-    const uint64_t at = atomicAdd(cursor, 1ull);
-    uint64_t* r = out + at * (2 + K);
+    uint64_t* r = out + (base + __popc(has & ((1u << lane) - 1))) * (2 + K);
     r[0] = key;
     r[1] = (uint64_t(j) << 32) | t.cnt[e];
     for (uint32_t k = 0; k < K; ++k) r[2 + k] = t.psum[e * K + k];

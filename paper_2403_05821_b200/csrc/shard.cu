@@ -194,18 +194,63 @@ __global__ void k_gather_u64(const uint64_t* src, const uint64_t* idx, uint32_t 
 }
 
 // owner side ----------------------------------------------------------------
-__global__ void k_meta_cols(uint64_t R, const uint2* meta, uint32_t* col, uint64_t* lens,
-                            uint32_t* iota, uint32_t* zeros, uint32_t* hist) {
+// The owner receives one run per source rank (run r = items [ro[r], ro[r+1])),
+// each sorted by (column, byte order). Merged position of an item = its index
+// in its run + the number of items of every other run that precede it (equal
+// values: runs of lower rank first), so no re-sort is needed.
+__global__ void k_meta_lens(uint64_t R, const uint2* meta, uint64_t* lens) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < R;
+       i += uint64_t(gridDim.x) * blockDim.x)
+    lens[i] = meta[i].y;
+  if (blockIdx.x == 0 && threadIdx.x == 0) lens[R] = 0;
+}
+
+// cstart[c] = merged position of the first item of column c
+__global__ void k_col_starts(uint32_t m, int N, const uint64_t* ro, const uint2* meta,
+                             uint32_t* cstart) {
+  const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c > m) return;
+  uint64_t tot = 0;
+  for (int r = 0; r < N; ++r) {
+    uint64_t lo = ro[r], hi = ro[r + 1];
+    while (lo < hi) {
+      const uint64_t mid = (lo + hi) >> 1;
+      if (meta[mid].x < c) lo = mid + 1;
+      else hi = mid;
+    }
+    tot += lo - ro[r];
+  }
+  cstart[c] = uint32_t(tot);
+}
+
+__device__ __forceinline__ int cmp_item(int kind, const uint2* meta, const uint64_t* offs,
+                                        const uint8_t* bytes, uint64_t a, uint64_t b) {
+  const uint2 ma = meta[a], mb = meta[b];
+  if (ma.x != mb.x) return ma.x < mb.x ? -1 : 1;
+  return cmp_bytes(c_code[kind], bytes + offs[a], ma.y, bytes + offs[b], mb.y);
+}
+
+__global__ void k_merge_pos_str(uint64_t R, int N, const uint64_t* ro, const uint2* meta,
+                                const uint64_t* offs, const uint8_t* bytes, int kind,
+                                uint32_t* pos) {
   for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < R;
        i += uint64_t(gridDim.x) * blockDim.x) {
-    const uint2 mt = meta[i];
-    col[i] = mt.x;
-    lens[i] = mt.y;
-    iota[i] = uint32_t(i);
-    zeros[i] = 0;
-    atomicAdd(&hist[mt.x], 1u);
+    int r = 0;
+    while (i >= ro[r + 1]) ++r;
+    uint64_t p = i - ro[r];
+    for (int q = 0; q < N; ++q) {
+      if (q == r) continue;
+      uint64_t lo = ro[q], hi = ro[q + 1];
+      while (lo < hi) {  // items of run q before item i
+        const uint64_t mid = (lo + hi) >> 1;
+        const int c = cmp_item(kind, meta, offs, bytes, mid, i);
+        if (c < 0 || (c == 0 && q < r)) lo = mid + 1;
+        else hi = mid;
+      }
+      p += lo - ro[q];
+    }
+    pos[i] = uint32_t(p);
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) lens[R] = 0;
 }
 
 // new[k] = sorted value k differs from value k-1 (column or bytes)
@@ -246,6 +291,15 @@ __global__ void k_rank_out(uint64_t R, const uint32_t* pos, const uint2* meta, c
        i += uint64_t(gridDim.x) * blockDim.x) {
     const uint32_t c = meta[i].x;
     out[i] = uint32_t(gstart[c] + (u[pos[i]] - u[cstart[c]]));
+  }
+}
+
+__global__ void k_local_ranks(uint64_t D, const uint32_t* ord, const uint32_t* icol,
+                              const uint64_t* colbase, uint32_t* out) {
+  for (uint64_t k = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; k < D;
+       k += uint64_t(gridDim.x) * blockDim.x) {
+    const uint32_t i = ord ? ord[k] : uint32_t(k);
+    out[i] = uint32_t(k - colbase[icol[i]]);
   }
 }
 
@@ -338,6 +392,14 @@ DevBuf<uint32_t> global_ranks(Comm& comm, const Encoded& L, const uint32_t* d_ic
   }
   const uint32_t* d_ord = ord.get();
 
+  if (N == 1) {  // one rank: the local order is the global order
+    card_g = L.card;
+    DevBuf<uint32_t> grank(D, s);
+    PO_LAUNCH(k_local_ranks, grid_for(D, 256), 256, 0, s, D, d_ord, d_icol, L.d_colbase.get(),
+              grank.get());
+    return grank;
+  }
+
   // splitters from regular samples of every rank
   constexpr uint32_t S = 128;
   DevBuf<SampleRec> smp(S, s), all(size_t(S) * N, s);
@@ -417,41 +479,26 @@ DevBuf<uint32_t> global_ranks(Comm& comm, const Encoded& L, const uint32_t* d_ic
   std::vector<uint64_t> dcount(m, 0);
   DevBuf<uint32_t> rrank(R, s);
   DevBuf<uint32_t> u;
-  std::vector<uint32_t> cstart(m + 1, 0);
   DevBuf<uint32_t> d_cstart;
   DevBuf<uint32_t> pos;
   if (R) {
-    DevBuf<uint32_t> rcol(R, s), iota(R, s), zeros(R, s), hist(m, s);
     DevBuf<uint64_t> rlens(R + 1, s), roffs(R + 1, s);
-    hist.zero();
-    PO_LAUNCH(k_meta_cols, grid_for(R, 256), 256, 0, s, R, rmeta.get(), rcol.get(), rlens.get(),
-              iota.get(), zeros.get(), hist.get());
+    PO_LAUNCH(k_meta_lens, grid_for(R + 1, 256), 256, 0, s, R, rmeta.get(), rlens.get());
     exclusive_scan_u64(rlens.get(), roffs.get(), R + 1, s);
-    std::vector<uint32_t> hh(m);
-    hist.download(hh.data(), m);
-    sync(s);
-    for (uint32_t c = 0; c < m; ++c) cstart[c + 1] = cstart[c] + hh[c];
-    d_cstart = to_device(cstart, s);
+    std::vector<uint64_t> ro(N + 1, 0);
+    for (int r = 0; r < N; ++r) ro[r + 1] = ro[r] + r_items[r];
+    auto d_ro = to_device(ro, s);
+    d_cstart.alloc(m + 1, s);
+    PO_LAUNCH(k_col_starts, (m + 1 + 127) / 128, 128, 0, s, m, N, d_ro.get(), rmeta.get(),
+              d_cstart.get());
     pos.alloc(R, s);
-    RefineJob j;
-    j.n_items = uint32_t(R);
-    j.d_grp_init = rcol.get();
-    j.d_grp_start = d_cstart.get();
-    j.n_groups = m;
-    j.grp_max = uint32_t(R);
-    j.key.kind = kind;
-    j.key.arena = rbytes.get();
-    j.key.arena_bytes = RB;
-    j.key.offsets = roffs.get();
-    j.key.item_cell_row = iota.get();
-    j.key.item_col = zeros.get();
-    j.key.m = 1;
-    j.d_out_pos = pos.get();
-    refine_sort_multi({j}, s);
+    PO_LAUNCH(k_merge_pos_str, grid_for(R, 256), 256, 0, s, R, N, d_ro.get(), rmeta.get(),
+              roffs.get(), rbytes.get(), kind, pos.get());
     DevBuf<uint32_t> perm(R, s), flags(R, s);
     PO_LAUNCH(k_invert, grid_for(R, 256), 256, 0, s, pos.get(), R, perm.get());
     PO_LAUNCH(k_new_flags, grid_for(R, 256), 256, 0, s, R, perm.get(), rmeta.get(), roffs.get(),
               rbytes.get(), flags.get());
+    rbytes.release();
     u.alloc(R, s);
     inclusive_scan_u32(flags.get(), u.get(), R, s);
     DevBuf<uint64_t> d_dc(m, s);
@@ -555,6 +602,42 @@ __global__ void k_key_word(uint64_t n, const uint64_t* recs, uint32_t stride, ui
     keys[i] = recs[uint64_t(perm ? perm[i] : uint32_t(i)) * stride + w];
 }
 
+// merged position of record i among the owner's N sorted runs (keys unique)
+__global__ void k_merge_pos_rec(uint64_t R, int N, const uint64_t* ro, const uint64_t* recs,
+                                RecFmt f, uint32_t* pos) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < R;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    int r = 0;
+    while (i >= ro[r + 1]) ++r;
+    const uint64_t* key = recs + i * f.stride;
+    uint64_t p = i - ro[r];
+    for (int q = 0; q < N; ++q) {
+      if (q == r) continue;
+      uint64_t lo = ro[q], hi = ro[q + 1];
+      while (lo < hi) {
+        const uint64_t mid = (lo + hi) >> 1;
+        const uint64_t* a = recs + mid * f.stride;
+        int c = 0;
+        for (uint32_t w = 0; w < f.W && !c; ++w)
+          if (a[w] != key[w]) c = a[w] < key[w] ? -1 : 1;
+        if (c < 0) lo = mid + 1;
+        else hi = mid;
+      }
+      p += lo - ro[q];
+    }
+    pos[i] = uint32_t(p);
+  }
+}
+
+__global__ void k_scatter_recs(uint64_t n, const uint64_t* recs, uint32_t stride, const uint32_t* pos,
+                               uint64_t* out) {
+  for (uint64_t t = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; t < n * stride;
+       t += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t i = t / stride, k = t - i * stride;
+    out[uint64_t(pos[i]) * stride + k] = recs[t];
+  }
+}
+
 __global__ void k_gather_recs(uint64_t n, const uint64_t* recs, uint32_t stride, const uint32_t* perm,
                               uint64_t* out) {
   for (uint64_t t = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; t < n * stride;
@@ -577,8 +660,8 @@ __global__ void k_iota64(uint64_t* a, uint64_t n, uint64_t base) {
 }
 
 // Stable LSD sort of records by their W key words; result in `out`.
-void sort_recs(const uint64_t* recs, uint64_t n, const RecFmt& f, DevBuf<uint64_t>& out,
-               cudaStream_t s) {
+void sort_recs(const uint64_t* recs, uint64_t n, const RecFmt& f, uint32_t key_bits,
+               DevBuf<uint64_t>& out, cudaStream_t s) {
   out.alloc(n * f.stride, s);
   if (!n) return;
   DevBuf<uint64_t> k0(n, s), k1(n, s);
@@ -591,9 +674,11 @@ void sort_recs(const uint64_t* recs, uint64_t n, const RecFmt& f, DevBuf<uint64_
   for (int w = int(f.W) - 1; w >= 0; --w) {
     PO_LAUNCH(k_key_word, grid_for(n, 256), 256, 0, s, n, recs, f.stride, uint32_t(w), p0.get(),
               k0.get());
+    // keys are packed from the top: the last word's low bits are padding
+    const int begin = w == int(f.W) - 1 ? int(64 * f.W - key_bits) : 0;
     ProfScope ps("cub_radix_sort", s);
     PO_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(), tb, k0.get(), k1.get(), p0.get(), p1.get(),
-                                            int(n), 0, 64, s));
+                                            int(n), begin, 64, s));
     std::swap(p0, p1);
   }
   PO_LAUNCH(k_gather_recs, grid_for(n * f.stride, 256), 256, 0, s, n, recs, f.stride, p0.get(),
@@ -705,7 +790,7 @@ uint64_t dist_layout(DistCtx& dc, const Encoded& G, const uint32_t* d_row_leaf,
   DevBuf<uint64_t> recs(n * f.stride, s), sorted;
   PO_LAUNCH(k_row_recs, grid_for(n, 256), 256, 0, s, n, f, G.vid.get(), d_row_leaf, P, rvid,
             G.d_colbase.get(), dc.row_offset, recs.get());
-  sort_recs(recs.get(), n, f, sorted, s);
+  sort_recs(recs.get(), n, f, T, sorted, s);
   recs.release();
 
   // sample sort: splitters from regular samples of every rank's sorted keys
@@ -741,11 +826,22 @@ uint64_t dist_layout(DistCtx& dc, const Encoded& G, const uint32_t* d_row_leaf,
   const std::vector<uint64_t> rb = comm.exchange_counts(sb, s);
   uint64_t R = 0;
   for (int r = 0; r < N; ++r) R += rb[r] / (f.stride * 8);
-  DevBuf<uint64_t> mine(R * f.stride, s), fin;
-  comm.alltoallv(sorted.get(), sb, mine.get(), rb, s);
-  sorted.release();
-  sort_recs(mine.get(), R, f, fin, s);
-  mine.release();
+  DevBuf<uint64_t> fin(R * f.stride, s);
+  if (N == 1) {
+    fin = std::move(sorted);
+  } else {
+    DevBuf<uint64_t> mine(R * f.stride, s);
+    comm.alltoallv(sorted.get(), sb, mine.get(), rb, s);
+    sorted.release();
+    std::vector<uint64_t> ro(N + 1, 0);
+    for (int r = 0; r < N; ++r) ro[r + 1] = ro[r] + rb[r] / (f.stride * 8);
+    auto d_ro = to_device(ro, s);
+    DevBuf<uint32_t> pos(R, s);
+    PO_LAUNCH(k_merge_pos_rec, grid_for(R, 256), 256, 0, s, R, N, d_ro.get(), mine.get(), f,
+              pos.get());
+    PO_LAUNCH(k_scatter_recs, grid_for(R * f.stride, 256), 256, 0, s, R, mine.get(), f.stride,
+              pos.get(), fin.get());
+  }
 
   // slice position
   const std::vector<uint64_t> counts = comm.allgather_host({R}, s);
