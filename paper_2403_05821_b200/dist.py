@@ -121,6 +121,15 @@ def local_comms(world: int) -> list:
     return [ShardComm(arr[r], r, world) for r in range(world)]
 
 
+def share_id(uid: np.ndarray, world: int, group=None) -> np.ndarray:
+    """Rank 0's 128-byte communicator id on every rank (torch.distributed)."""
+    if world <= 1:
+        return uid
+    obj = [uid.tobytes()]
+    dist.broadcast_object_list(obj, src=0, group=group)
+    return np.frombuffer(obj[0], dtype=np.uint8).copy()
+
+
 def nccl_comm(rank: int | None = None, world: int | None = None, group=None) -> ShardComm:
     """NCCL communicator over the ranks of an initialised torch.distributed
     group (the 128-byte NCCL id is broadcast from rank 0 through it)."""
@@ -130,10 +139,7 @@ def nccl_comm(rank: int | None = None, world: int | None = None, group=None) -> 
     uid = np.zeros(128, dtype=np.uint8)
     if rank == 0:
         lib.check(lib.comm_unique_id(uid.ctypes.data))
-    if world > 1:
-        obj = [uid.tobytes()]
-        dist.broadcast_object_list(obj, src=0, group=group)
-        uid = np.frombuffer(obj[0], dtype=np.uint8).copy()
+    uid = share_id(uid, world, group)
     h = C.c_void_p(0)
     lib.check(lib.comm_init_nccl(uid.ctypes.data, world, rank, C.byref(h)))
     return ShardComm(h.value, rank, world)
