@@ -281,12 +281,12 @@ def run_ours(args):
         log(f"   {k:28s} {ms_k:8.3f} ms/step  {cnt:6.1f} launches  "
             f"({100*ms_k/max(total_kernel_ms,1e-9):5.1f}% of kernel time)")
 
-    # roofline of the HBM-streaming kernel (K1 cell_scan, k_cell_hash_cols):
+    # roofline of the HBM-streaming kernel (K1 cell_scan, k_cell_hash_seg):
     # it must read every cell byte and its offset pair once, so its algorithmic
     # bytes per launch are S + 8*(n*m+1) (the 8-byte hash it writes per cell is
     # an intermediate of this design and is not counted)
     peak, peak_kind = peaks()
-    dom = "k_cell_hash_cols"
+    dom = next((k for k in prof if k.startswith("k_cell_hash")), "k_cell_hash_seg")
     dom_ms = prof.get(dom, (1, 0.0))[1] / max(prof.get(dom, (1, 0.0))[0], 1)
     dom_bytes = cell_bytes + 8 * (n * m + 1)
     achieved = dom_bytes / (dom_ms / 1e3) / 1e9 if dom_ms > 0 else 0.0

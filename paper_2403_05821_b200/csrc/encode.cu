@@ -23,6 +23,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <string>
 
 #include "internal.cuh"
 
@@ -244,6 +245,146 @@ __global__ void __launch_bounds__(kDictBlock) k_cell_hash(
       hashes[i] = h ? h : 1;
     }
     __syncthreads();  // buffer bsel is refilled by the next-but-one issue
+  }
+}
+
+// K1 cell_scan (segment-parallel, TMA-staged): the default hashing kernel.
+// A block streams tiles of T consecutive cells (row-major: a contiguous byte
+// range of the arena) into shared memory with one bulk copy per tile,
+// double-buffered so the next tile's copy overlaps this tile's hashing. The
+// work inside a tile is split into 64-byte segments of cells (a cell of len
+// bytes has max(1, ceil(len/64)) segments), so long and short cells balance
+// across threads: each thread hashes whole segments out of shared memory and
+// adds its partial word sum to the cell's accumulator (shared atomics; the
+// hash is a sum of per-word terms, so the order does not matter), then one
+// thread per cell finishes the hash. The arena is read exactly once, as
+// large aligned bulk copies. A tile whose byte range exceeds the staging
+// buffer (or ends past the arena) is hashed from global memory with the
+// same segment split.
+constexpr uint32_t kSegBlock = 256;
+constexpr uint32_t kSegMaxCells = 1023;
+constexpr uint32_t kSegQ = 4;  // offsets held per thread: (kSegMaxCells + 1) / kSegBlock
+constexpr uint32_t kSegStages = 4;
+
+__device__ __forceinline__ uint64_t smem_word8(const uint8_t* base, uint32_t off) {
+  const uint64_t* s64 = reinterpret_cast<const uint64_t*>(base);
+  const uint32_t q = off >> 3, sh = (off & 7) * 8;
+  const uint64_t w0 = s64[q];
+  return sh ? ((w0 >> sh) | (s64[q + 1] << (64 - sh))) : w0;
+}
+
+template <uint32_t G>  // lanes per cell: 8, 16 or 32
+__global__ void __launch_bounds__(kSegBlock, 3) k_cell_hash_seg(
+    const uint8_t* __restrict__ arena, const uint8_t* arena_end,
+    const uint64_t* __restrict__ offsets, uint64_t n, uint32_t m, uint32_t R,
+    uint32_t stage_bytes, uint64_t hash_mask, unsigned long long* __restrict__ hashes) {
+  extern __shared__ __align__(128) uint8_t sbuf_all[];
+  __shared__ __align__(8) uint64_t s_bar[kSegStages];
+  __shared__ uint64_t s_off[kSegMaxCells + 1];
+  const uint32_t buf_bytes = stage_bytes + 128;  // slack: 8-byte reads past the data
+  const uint64_t total = n * m;
+  const uint32_t T = R * m;  // cells per tile: R whole rows
+  const uint64_t ntiles = (n + R - 1) / R;
+  const uint32_t tid = threadIdx.x;
+  const uint32_t gl = tid % G;  // lane within its group of G lanes (one cell)
+  const uintptr_t end_addr = reinterpret_cast<uintptr_t>(arena_end);
+  auto cells_of = [&](uint64_t t) -> uint32_t {
+    const uint64_t j0 = t * T;
+    return uint32_t((j0 + T < total ? j0 + T : total) - j0);
+  };
+  auto stageable = [&](uintptr_t a0, uintptr_t b1) {
+    return b1 > a0 && b1 - a0 <= stage_bytes && b1 <= end_addr;  // never read past the arena
+  };
+  auto issue = [&](uint64_t t, int b) {
+    const uint64_t j0 = t * T;
+    const uintptr_t a0 = reinterpret_cast<uintptr_t>(arena + offsets[j0]) & ~uintptr_t(15);
+    const uintptr_t b1 =
+        (reinterpret_cast<uintptr_t>(arena + offsets[j0 + cells_of(t)]) + 15) & ~uintptr_t(15);
+    if (!stageable(a0, b1)) return;
+    fence_proxy_async_smem();
+    mbar_arrive_expect_tx(&s_bar[b], uint32_t(b1 - a0));
+    bulk_g2s(sbuf_all + b * buf_bytes, reinterpret_cast<const void*>(a0), uint32_t(b1 - a0),
+             &s_bar[b]);
+  };
+  auto load_offs = [&](uint64_t t, uint64_t* r) {
+    const uint64_t j0 = t * T;
+    const uint32_t nc = cells_of(t);
+#pragma unroll
+    for (uint32_t q = 0; q < kSegQ; ++q) {
+      const uint32_t c = tid + q * kSegBlock;
+      r[q] = c <= nc ? __ldg(offsets + j0 + c) : 0;
+    }
+  };
+  if (tid == 0) {
+    for (uint32_t b = 0; b < kSegStages; ++b) mbar_init(&s_bar[b], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  uint64_t roff[kSegQ];
+  if (blockIdx.x < ntiles) {  // ring of kSegStages buffers: stages-1 tiles ahead
+    if (tid == 0)
+      for (uint32_t b = 0; b + 1 < kSegStages; ++b)
+        if (blockIdx.x + uint64_t(b) * gridDim.x < ntiles) issue(blockIdx.x + uint64_t(b) * gridDim.x, int(b));
+    load_offs(blockIdx.x, roff);
+  }
+  uint32_t parity = 0;  // bit b: phase of buffer b
+  uint32_t kiter = 0;
+  for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++kiter) {
+    const int bsel = int(kiter % kSegStages);
+    const uint8_t* sb = sbuf_all + bsel * buf_bytes;
+    const uint64_t j0 = t * T;
+    const uint32_t nc = cells_of(t);
+    const uint32_t rows = nc / m;
+#pragma unroll
+    for (uint32_t q = 0; q < kSegQ; ++q) {
+      const uint32_t c = tid + q * kSegBlock;
+      if (c <= nc) s_off[c] = roff[q];
+    }
+    __syncthreads();
+    const uintptr_t gA0 = reinterpret_cast<uintptr_t>(arena + s_off[0]) & ~uintptr_t(15);
+    const uintptr_t gB1 = (reinterpret_cast<uintptr_t>(arena + s_off[nc]) + 15) & ~uintptr_t(15);
+    const bool staged = stageable(gA0, gB1);
+    if (tid == 0) {  // refill the buffer freed by the previous tile
+      const uint64_t ahead = t + uint64_t(kSegStages - 1) * gridDim.x;
+      if (ahead < ntiles) issue(ahead, int((kiter + kSegStages - 1) % kSegStages));
+    }
+    if (t + gridDim.x < ntiles) load_offs(t + gridDim.x, roff);  // next tile's offsets
+    if (staged) {
+      mbar_wait(&s_bar[bsel], (parity >> bsel) & 1u);
+      parity ^= 1u << bsel;
+    }
+    // cells in column-major order (the groups of a warp take consecutive rows
+    // of one column: similar lengths); a group walks its cell 8*G bytes at a
+    // time, lane gl taking words gl, gl+G, ...
+    // warp-uniform loop: the shuffles below need every lane of the warp
+    for (uint32_t kb = (tid >> 5) * (32 / G); kb < nc; kb += kSegBlock / G) {
+      const uint32_t k = kb + (tid & 31) / G;
+      const bool valid = k < nc;
+      uint32_t ci = 0;
+      uint64_t len = 0;
+      unsigned long long sum = 0;
+      if (valid) {
+        const uint32_t col = k / rows, row = k - col * rows;
+        ci = row * m + col;
+        const uint64_t o0 = s_off[ci];
+        len = s_off[ci + 1] - o0;
+        const uint8_t* cell = arena + o0;
+        const uint32_t sbase = uint32_t(reinterpret_cast<uintptr_t>(cell) - gA0);
+        for (uint64_t b = 8 * gl; b < len; b += 8 * G) {
+          const uint32_t take = len - b >= 8 ? 8u : uint32_t(len - b);
+          const uint64_t x = staged ? smem_word8(sb, sbase + uint32_t(b))
+                                    : load8_unaligned(cell + b, arena_end);
+          sum += word_term(mask_low_bytes(x, take), b >> 3);
+        }
+      }
+#pragma unroll
+      for (uint32_t d = G / 2; d > 0; d >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, d);
+      if (valid && gl == 0) {
+        const uint64_t h = hash_finish(sum, len) & hash_mask;
+        hashes[j0 + ci] = h ? h : 1;
+      }
+    }
+    __syncthreads();  // s_off and buffer bsel are reused
   }
 }
 
@@ -769,7 +910,39 @@ void encode(const DeviceTable& t, int tok, int scoring, cudaStream_t s, Encoded&
       attr_set = int(smem);
     }
     DevBuf<unsigned long long> hashes(cells, s);
-    if (std::getenv("PO_HASH_TMA") && m <= kDictBlock) {
+    // cols (default) | seg (TMA ring, group per cell) | tile (TMA, thread per cell)
+    const char* hk = std::getenv("PO_HASH_KERNEL");
+    const std::string hsel = hk && *hk ? hk : "cols";
+    if (hsel == "seg" && m <= kSegMaxCells) {
+      const double row_bytes = double(t.arena_bytes) / double(n);
+      const uint32_t sstage = 16 * 1024;
+      uint32_t R = uint32_t(std::max(1.0, 0.6 * sstage / std::max(row_bytes, 1.0)));
+      R = std::min<uint32_t>(R, kSegMaxCells / uint32_t(m));
+      R = std::max<uint32_t>(R, 1);
+      const uint32_t ssmem = kSegStages * (sstage + 128);
+      static bool seg_attr = false;
+      if (!seg_attr) {
+        PO_CUDA(cudaFuncSetAttribute(k_cell_hash_seg<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     int(ssmem)));
+        PO_CUDA(cudaFuncSetAttribute(k_cell_hash_seg<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     int(ssmem)));
+        PO_CUDA(cudaFuncSetAttribute(k_cell_hash_seg<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     int(ssmem)));
+        seg_attr = true;
+      }
+      const uint64_t ntiles = (n + R - 1) / R;
+      const unsigned grid = unsigned(std::min<uint64_t>(ntiles, uint64_t(kSMs) * 3));
+      const double cell_bytes = double(t.arena_bytes) / double(cells);
+      if (cell_bytes >= 384)
+        PO_LAUNCH(k_cell_hash_seg<32>, grid, kSegBlock, ssmem, s, t.arena, arena_end, t.offsets, n,
+                  uint32_t(m), R, sstage, hmask, hashes.get());
+      else if (cell_bytes >= 160)
+        PO_LAUNCH(k_cell_hash_seg<16>, grid, kSegBlock, ssmem, s, t.arena, arena_end, t.offsets, n,
+                  uint32_t(m), R, sstage, hmask, hashes.get());
+      else
+        PO_LAUNCH(k_cell_hash_seg<8>, grid, kSegBlock, ssmem, s, t.arena, arena_end, t.offsets, n,
+                  uint32_t(m), R, sstage, hmask, hashes.get());
+    } else if (hsel == "tile" && m <= kDictBlock) {
       const uint64_t ntiles = (cells + rows_per_tile * m - 1) / (rows_per_tile * m);
       PO_LAUNCH(k_cell_hash, unsigned(std::min<uint64_t>(ntiles, uint64_t(kSMs) * 3)), kDictBlock,
                 smem, s, t.arena, arena_end, t.offsets, cells, uint32_t(m), rows_per_tile, stage,
