@@ -144,6 +144,17 @@ int po_fixed_order_by_stats(uint32_t n_fields, uint64_t total_rows,
                             const uint64_t* cardinality, const double* avg_len,
                             int32_t* out_order);
 
+/* Partition-signature comparison of field pairs: the core of
+ * prefixopt::validate_fds (fd.hpp:66-109) and discover_fds (fd.hpp:114-141).
+ * sig_f[r] = first row holding row r's value in field f (partition_signature,
+ * fd.hpp:56-64). For pair k: out_first_diff[k] = first row r with
+ * sig_{pair_a[k]}[r] != sig_{pair_b[k]}[r] (n_rows when the partitions are
+ * identical); out_sig_a[k] / out_sig_b[k] = the two signatures at that row
+ * (the witness rows). Host outputs; values compared as raw bytes. */
+int po_fd_compare(const po_table* t, uint32_t n_pairs, const int32_t* pair_a,
+                  const int32_t* pair_b, uint64_t* out_first_diff, uint64_t* out_sig_a,
+                  uint64_t* out_sig_b, void* stream);
+
 /* ---- row-sharded solve over several GPUs ---------------
  * No reference counterpart: the reference ggr() (ggr.hpp:367-394) is one
  * process on one table. Here every rank (one per GPU) passes a contiguous

@@ -401,6 +401,18 @@ void check_perm(uint32_t m, const int32_t* order) {
   }
 }
 
+// partition_signature (fd.hpp:56-64) restated by sorting: rows ordered by
+// (value bytes, row id); every row's signature is the first row of its run.
+std::vector<uint64_t> signature(const Tab& t, int f) {
+  std::vector<uint64_t> idx(t.n), sig(t.n);
+  std::iota(idx.begin(), idx.end(), 0);
+  std::stable_sort(idx.begin(), idx.end(),
+                   [&](uint64_t a, uint64_t b) { return t.cell(a, f) < t.cell(b, f); });
+  for (uint64_t i = 0; i < t.n; ++i)
+    sig[idx[i]] = (i > 0 && t.cell(idx[i], f) == t.cell(idx[i - 1], f)) ? sig[idx[i - 1]] : idx[i];
+  return sig;
+}
+
 template <class F>
 int guarded(F&& fn) {
   try {
@@ -513,6 +525,74 @@ int oracle_fixed_order_by_hitcount_stats(uint32_t m, uint64_t total_rows, const 
     std::vector<double> a(avg, avg + m);
     std::vector<int> o = hitcount_order(total_rows, c, a, variant);
     std::copy(o.begin(), o.end(), out);
+  });
+}
+
+// validate_fds (fd.hpp:66-109): overlap check, then per group the first
+// member whose signature differs from the first member's; the witness row
+// pair is the earlier row of the matching side and the first differing row.
+int oracle_validate_fds(const po_table* tv, const po_fd_groups* fds, uint8_t* out_satisfied,
+                        uint8_t* out_has_witness, uint64_t* out_row_a, uint64_t* out_row_b,
+                        int32_t* out_agree, int32_t* out_differ) {
+  return guarded([&] {
+    Tab t(tv);
+    std::vector<char> claimed(t.m, 0);
+    for (uint32_t k = 0; k < fds->group_offsets[fds->n_groups]; ++k) {
+      const int32_t f = fds->members[k];
+      if (f < 0 || f >= int32_t(t.m)) fail(PO_ERR_SCHEMA, "unknown field");
+      if (claimed[f]) fail(PO_ERR_SCHEMA, "field appears in more than one FD group");
+      claimed[f] = 1;
+    }
+    for (uint32_t g = 0; g < fds->n_groups; ++g) {
+      const uint32_t b0 = fds->group_offsets[g], b1 = fds->group_offsets[g + 1];
+      out_satisfied[g] = 1;
+      out_has_witness[g] = 0;
+      if (b1 - b0 < 2 || t.n < 2) continue;
+      const int32_t base = fds->members[b0];
+      const std::vector<uint64_t> bs = signature(t, base);
+      for (uint32_t k = b0 + 1; k < b1 && out_satisfied[g]; ++k) {
+        const std::vector<uint64_t> os = signature(t, fds->members[k]);
+        for (uint64_t r = 0; r < t.n; ++r) {
+          if (bs[r] == os[r]) continue;
+          out_satisfied[g] = 0;
+          out_has_witness[g] = 1;
+          const bool base_earlier = bs[r] != r;
+          out_row_a[g] = base_earlier ? bs[r] : os[r];
+          out_row_b[g] = r;
+          out_agree[g] = base_earlier ? base : fds->members[k];
+          out_differ[g] = base_earlier ? fds->members[k] : base;
+          break;
+        }
+      }
+    }
+  });
+}
+
+// discover_fds (fd.hpp:114-141): size cap, then fields joined to the first
+// earlier class with an identical signature; singleton classes dropped.
+int oracle_discover_fds(const po_table* tv, uint64_t max_rows, int32_t* out_group_of_field) {
+  return guarded([&] {
+    Tab t(tv);
+    if (t.n > max_rows) fail(PO_ERR_SIZE, "discover_fds: table exceeds the row cap");
+    std::vector<std::vector<uint64_t>> class_sig;
+    std::vector<std::vector<int>> members;
+    for (uint32_t f = 0; f < t.m; ++f) {
+      std::vector<uint64_t> sg = signature(t, int(f));
+      size_t c = 0;
+      while (c < class_sig.size() && class_sig[c] != sg) ++c;
+      if (c == class_sig.size()) {
+        class_sig.push_back(std::move(sg));
+        members.push_back({});
+      }
+      members[c].push_back(int(f));
+    }
+    int32_t g = 0;
+    for (uint32_t f = 0; f < t.m; ++f) out_group_of_field[f] = -1;
+    for (const auto& mem : members) {
+      if (mem.size() < 2) continue;
+      for (int f : mem) out_group_of_field[f] = g;
+      ++g;
+    }
   });
 }
 

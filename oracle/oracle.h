@@ -38,6 +38,11 @@ extern "C" {
                                             const uint64_t* cardinality,                 \
                                             const double* avg_len, int32_t variant,      \
                                             int32_t* out_order);                         \
+  int prefix##validate_fds(const po_table* t, const po_fd_groups* fds, uint8_t* out_satisfied, \
+                           uint8_t* out_has_witness, uint64_t* out_row_a,                \
+                           uint64_t* out_row_b, int32_t* out_agree, int32_t* out_differ); \
+  int prefix##discover_fds(const po_table* t, uint64_t max_rows,                         \
+                           int32_t* out_group_of_field);                                 \
   const char* prefix##last_error(void);
 
 PO_ORACLE_DECLARE(oracle_)

@@ -44,6 +44,8 @@ class OracleLib:
         self._stats = _bind(L, p + "compute_stats", C.c_int, [vp, C.c_int32, C.c_int32, vp, vp])
         self._fohs = _bind(L, p + "fixed_order_by_hitcount_stats", C.c_int,
                            [C.c_uint32, C.c_uint64, vp, vp, C.c_int32, vp])
+        self._vfd = _bind(L, p + "validate_fds", C.c_int, [vp, vp, vp, vp, vp, vp, vp, vp])
+        self._dfd = _bind(L, p + "discover_fds", C.c_int, [vp, C.c_uint64, vp])
         self._err = _bind(L, p + "last_error", C.c_char_p, [])
 
     def _check(self, code):
@@ -122,3 +124,47 @@ def oracle(kind: str = "port") -> OracleLib:
 
 def available(kind: str) -> bool:
     return PATHS[kind].exists()
+
+
+def _fd_oracle_methods():
+    """validate_fds / discover_fds on the oracle libraries, with the same
+    result types as paper_2403_05821_b200.api."""
+    from paper_2403_05821_b200.api import (FdGroupReport, FdValidationReport, FdWitness,
+                                           FunctionalDependencySet)
+
+    def validate_fds(self, t, fds):
+        groups = fds.groups if isinstance(fds, FunctionalDependencySet) else (fds or [])
+        idx = [[t.require_field(nm) for nm in g] for g in groups]
+        k = max(len(groups), 1)
+        sat = np.zeros(k, np.uint8)
+        hw = np.zeros(k, np.uint8)
+        ra = np.zeros(k, np.uint64)
+        rb = np.zeros(k, np.uint64)
+        ag = np.zeros(k, np.int32)
+        df = np.zeros(k, np.int32)
+        view = t.view()
+        self._check(self._vfd(view.ref(), FdView(idx).ref(), sat.ctypes.data, hw.ctypes.data,
+                              ra.ctypes.data, rb.ctypes.data, ag.ctypes.data, df.ctypes.data))
+        rep = FdValidationReport()
+        for g, grp in enumerate(groups):
+            w = None
+            if hw[g]:
+                pos = {f: i for i, f in enumerate(idx[g])}
+                w = FdWitness(int(ra[g]), int(rb[g]), grp[pos[int(ag[g])]], grp[pos[int(df[g])]])
+            rep.groups.append(FdGroupReport(list(grp), bool(sat[g]), w))
+        return rep
+
+    def discover_fds(self, t, max_rows=10000):
+        m = t.field_count()
+        out = np.zeros(max(m, 1), np.int32)
+        view = t.view()
+        self._check(self._dfd(view.ref(), max_rows, out.ctypes.data))
+        ng = int(out[:m].max()) + 1 if m else 0
+        groups = [[t.field_name(f) for f in range(m) if out[f] == g] for g in range(ng)]
+        return FunctionalDependencySet(groups, True)
+
+    OracleLib.validate_fds = validate_fds
+    OracleLib.discover_fds = discover_fds
+
+
+_fd_oracle_methods()

@@ -13,6 +13,7 @@
 #include <unordered_map>
 #include <vector>
 
+#include "prefixopt/fd.hpp"
 #include "prefixopt/ggr.hpp"
 #include "prefixopt/objective.hpp"
 #include "prefixopt/stats.hpp"
@@ -219,6 +220,47 @@ int ref_fixed_order_by_hitcount_stats(uint32_t m, uint64_t total_rows, const uin
     for (uint32_t f = 0; f < m; ++f) st.fields.push_back({"f" + std::to_string(f), card[f], avg[f]});
     std::vector<int> o = prefixopt::fixed_order_by_hitcount_stats(st, variant_of(variant));
     std::copy(o.begin(), o.end(), out);
+  });
+}
+
+// prefixopt::validate_fds (fd.hpp:66-109). Groups arrive as field indices;
+// agree/differ fields are returned as indices.
+int ref_validate_fds(const po_table* tv, const po_fd_groups* fds, uint8_t* out_satisfied,
+                     uint8_t* out_has_witness, uint64_t* out_row_a, uint64_t* out_row_b,
+                     int32_t* out_agree, int32_t* out_differ) {
+  return guarded([&] {
+    prefixopt::Table t = to_table(tv);
+    prefixopt::FunctionalDependencySet set;
+    for (uint32_t g = 0; g < fds->n_groups; ++g) {
+      std::vector<std::string> names;
+      for (uint32_t k = fds->group_offsets[g]; k < fds->group_offsets[g + 1]; ++k)
+        names.push_back(t.field_name(fds->members[k]));
+      set.groups.push_back(names);
+    }
+    const prefixopt::FdValidationReport rep = prefixopt::validate_fds(t, set);
+    for (size_t g = 0; g < rep.groups.size(); ++g) {
+      const auto& gr = rep.groups[g];
+      out_satisfied[g] = gr.satisfied ? 1 : 0;
+      out_has_witness[g] = gr.witness ? 1 : 0;
+      if (gr.witness) {
+        out_row_a[g] = gr.witness->row_a;
+        out_row_b[g] = gr.witness->row_b;
+        out_agree[g] = t.require_field(gr.witness->agree_field);
+        out_differ[g] = t.require_field(gr.witness->differ_field);
+      }
+    }
+  });
+}
+
+// prefixopt::discover_fds (fd.hpp:114-141): out_group_of_field[f] = index of
+// the reported group holding field f, -1 when f is in no group.
+int ref_discover_fds(const po_table* tv, uint64_t max_rows, int32_t* out_group_of_field) {
+  return guarded([&] {
+    prefixopt::Table t = to_table(tv);
+    const prefixopt::FunctionalDependencySet set = prefixopt::discover_fds(t, max_rows);
+    for (size_t f = 0; f < t.field_count(); ++f) out_group_of_field[f] = -1;
+    for (size_t g = 0; g < set.groups.size(); ++g)
+      for (const auto& nm : set.groups[g]) out_group_of_field[t.require_field(nm)] = int32_t(g);
   });
 }
 

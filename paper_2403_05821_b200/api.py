@@ -23,7 +23,7 @@ import numpy as np
 
 from ._abi import (PO_LOC_DEVICE, PO_LOC_HOST, FdView, TableView, _ptr, cuda_lib,
                    po_ggr_config, po_solve_stats)
-from .errors import DomainError, SchemaError
+from .errors import DomainError, SchemaError, SizeError
 from .table import Table, _to_bytes
 
 
@@ -440,6 +440,108 @@ def hitcount(t: Table, field_name, value, fds=None, tok: Tokenizer = _CHAR,
     return HitCountResult(tot * float(count - 1), [fname] + [t.field_name(o) for o in inferred])
 
 
+# --------------------------------------------------------------------------
+# functional dependencies (fd.hpp:28-141): signatures compared on the GPU
+# --------------------------------------------------------------------------
+@dataclass
+class FdWitness:
+    row_a: int
+    row_b: int
+    agree_field: object
+    differ_field: object
+
+
+@dataclass
+class FdGroupReport:
+    group: list
+    satisfied: bool = False
+    witness: FdWitness | None = None
+
+
+@dataclass
+class FdValidationReport:
+    groups: list = field(default_factory=list)
+
+    def all_satisfied(self) -> bool:
+        return all(g.satisfied for g in self.groups)
+
+
+def _fd_compare(t: Table, pa: list, pb: list):
+    """po_fd_compare: first differing row of each pair's partition signatures
+    (fd.hpp:56-64) and both signatures there."""
+    n = t.row_count()
+    k = len(pa)
+    first = np.full(max(k, 1), n, dtype=np.uint64)
+    sa = np.zeros(max(k, 1), dtype=np.uint64)
+    sb = np.zeros(max(k, 1), dtype=np.uint64)
+    if k:
+        lib = cuda_lib()
+        a = np.asarray(pa, dtype=np.int32)
+        b = np.asarray(pb, dtype=np.int32)
+        view = t.view()
+        lib.check(lib.fd_compare(view.ref(), k, a.ctypes.data, b.ctypes.data, first.ctypes.data,
+                                 sa.ctypes.data, sb.ctypes.data, 0))
+    return first[:k], sa[:k], sb[:k]
+
+
+def validate_fds(t: Table, fds) -> FdValidationReport:
+    """prefixopt::validate_fds (fd.hpp:66-109)."""
+    groups = fds.groups if isinstance(fds, FunctionalDependencySet) else (fds or [])
+    claimed = set()
+    for g in groups:
+        for nm in g:
+            t.require_field(nm)
+            key = nm if isinstance(nm, bytes) else str(nm).encode()
+            if key in claimed:
+                raise SchemaError(f"field appears in more than one FD group: {key.decode('utf-8', 'replace')}")
+            claimed.add(key)
+    n = t.row_count()
+    pa, pb, first_pair = [], [], []
+    for g in groups:
+        first_pair.append(len(pa))
+        if len(g) >= 2 and n >= 2:
+            for k in range(1, len(g)):
+                pa.append(t.require_field(g[0]))
+                pb.append(t.require_field(g[k]))
+    diff, sa, sb = _fd_compare(t, pa, pb)
+    rep = FdValidationReport()
+    for gi, g in enumerate(groups):
+        gr = FdGroupReport(list(g), True, None)
+        if len(g) >= 2 and n >= 2:
+            for k in range(1, len(g)):
+                q = first_pair[gi] + k - 1
+                r = int(diff[q])
+                if r >= n:
+                    continue
+                gr.satisfied = False
+                base_earlier = int(sa[q]) != r
+                gr.witness = FdWitness(int(sa[q]) if base_earlier else int(sb[q]), r,
+                                       g[0] if base_earlier else g[k],
+                                       g[k] if base_earlier else g[0])
+                break
+        rep.groups.append(gr)
+    return rep
+
+
+def discover_fds(t: Table, max_rows: int = 10000) -> FunctionalDependencySet:
+    """prefixopt::discover_fds (fd.hpp:114-141)."""
+    n, m = t.row_count(), t.field_count()
+    if n > max_rows:
+        raise SizeError(f"discover_fds: table has {n} rows, cap is {max_rows}")
+    pairs = [(i, j) for i in range(m) for j in range(i + 1, m)]
+    diff, _, _ = _fd_compare(t, [p[0] for p in pairs], [p[1] for p in pairs])
+    same = {p: int(d) >= n for p, d in zip(pairs, diff)}
+    classes: list = []  # (first field, members)
+    for f in range(m):
+        for c in classes:
+            if same[(c[0], f)]:
+                c[1].append(t.field_name(f))
+                break
+        else:
+            classes.append((f, [t.field_name(f)]))
+    return FunctionalDependencySet([c[1] for c in classes if len(c[1]) >= 2], True)
+
+
 # low-level entry for callers holding device buffers (bench.py, multi-GPU)
 def ggr_into(view: TableView, fd_groups: list, cfg: GgrConfig, tok_kind: int, scoring: int,
              out_location: int, out_rows, out_orders, stream: int = 0):
@@ -463,5 +565,6 @@ __all__ = [
     "SolveStats", "SolveResult", "FieldStats", "ColumnStats", "ggr", "phc", "hit",
     "sort_rows_fixed_order", "compute_stats", "fixed_order_by_hitcount_stats",
     "fixed_order_by_stats", "original_order_schedule", "hitcount", "HitCountResult", "ggr_into",
-    "PO_LOC_HOST", "PO_LOC_DEVICE",
+    "PO_LOC_HOST", "PO_LOC_DEVICE", "FdWitness", "FdGroupReport", "FdValidationReport",
+    "validate_fds", "discover_fds",
 ]

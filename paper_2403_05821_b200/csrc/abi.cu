@@ -375,6 +375,26 @@ int po_fixed_order_by_stats(uint32_t m, uint64_t total_rows, const uint64_t* car
   });
 }
 
+int po_fd_compare(const po_table* t, uint32_t n_pairs, const int32_t* pair_a,
+                  const int32_t* pair_b, uint64_t* out_first_diff, uint64_t* out_sig_a,
+                  uint64_t* out_sig_b, void* stream) {
+  return guarded([&] {
+    if (n_pairs && (!pair_a || !pair_b || !out_first_diff))
+      fail(PO_ERR_INVALID_ARG, "null argument");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    Prepared p;
+    prepare(t, PO_TOK_CHAR, PO_SCORE_VALUE, s, p);
+    std::vector<int32_t> pa(pair_a, pair_a + n_pairs), pb(pair_b, pair_b + n_pairs);
+    std::vector<uint64_t> fd, sa, sb;
+    fd_compare_device(p.e, pa, pb, fd, sa, sb, s);
+    for (uint32_t k = 0; k < n_pairs; ++k) {
+      out_first_diff[k] = fd[k];
+      if (out_sig_a) out_sig_a[k] = sa[k];
+      if (out_sig_b) out_sig_b[k] = sb[k];
+    }
+  });
+}
+
 int po_comm_unique_id(uint8_t* out_id128) {
   return guarded([&] {
     if (!out_id128) fail(PO_ERR_INVALID_ARG, "null id buffer");

@@ -1046,6 +1046,7 @@ void encode(const DeviceTable& t, int tok, int scoring, cudaStream_t s, Encoded&
             col_by_pos.get());
   keys.release();
   flags.release();
+  timing_mark("scatter_pos", s);
 
   // Segment length per distinct value.
   std::vector<uint64_t> nchar(m), nword(m);
@@ -1070,12 +1071,14 @@ void encode(const DeviceTable& t, int tok, int scoring, cudaStream_t s, Encoded&
             e.rep_row.get(), col_by_pos.get(), D, uint32_t(m), tok, scoring, d_nchar.get(),
             d_nword.get(), e.vlen.get());
 
+  timing_mark("vlen", s);
   // vid matrix (row-major) and occurrence counts.
   e.vid.alloc(cells, s);
   PO_LAUNCH(k_vid, grid_for(cells, 256), 256, 0, s, slot_of_cell.get(), slot2vid.get(), n,
             uint32_t(m), cap, e.vid.get());
   slot_of_cell.release();
   slot2vid.release();
+  timing_mark("vid", s);
   e.count.alloc(D, s);
   e.count.zero();
   {
@@ -1091,6 +1094,7 @@ void encode(const DeviceTable& t, int tok, int scoring, cudaStream_t s, Encoded&
     PO_LAUNCH(k_count, grid_for(cells, 512, 2), 512, nbins * sizeof(uint32_t), s, e.vid.get(), n,
               uint32_t(m), d_soff.get(), nbins, e.d_colbase.get(), e.count.get());
   }
+  timing_mark("count", s);
   DevBuf<unsigned long long> tot(m, s);
   tot.zero();
   PO_LAUNCH(k_total_len, grid_for((D + kTotRun - 1) / kTotRun, 256, 2), 256, m <= 4096 ? m * 8 : 0, s, e.count.get(),

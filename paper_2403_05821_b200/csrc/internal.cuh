@@ -220,6 +220,13 @@ struct GgrOutput {
   po_solve_stats stats{};
 };
 
+// FD checks (fd.cu): for every field pair (pa[k], pb[k]) the first row where
+// their partition signatures (fd.hpp:56-64) differ (n if identical) and the
+// two signatures at that row.
+void fd_compare_device(const Encoded& e, const std::vector<int32_t>& pa,
+                       const std::vector<int32_t>& pb, std::vector<uint64_t>& first_diff,
+                       std::vector<uint64_t>& sig_a, std::vector<uint64_t>& sig_b, cudaStream_t s);
+
 // Row-sharded solving (shard.cu). Every rank holds a
 // contiguous range of the table's rows; value ids are global (escaped-order
 // ranks over the whole table), the value-group tables are replicated (built

@@ -60,3 +60,33 @@ def test_oracle_phc_sort_stats_match_reference():
                 assert pc.tolist() == rc.tolist() and pt.tolist() == rt.tolist()
                 entries = [(r, rng.sample(range(m), rng.randint(0, m))) for r in rng.sample(range(n), n)]
                 assert P.phc(entries, t, tok, sc) == R.phc(entries, t, tok, sc)
+
+
+# ---- functional dependencies (fd.hpp:56-141) ------------------------------
+import random as _random
+
+from fd_cases import known_fd_cases
+from tables import ALPHABETS as _ALPHA, random_table as _rt
+
+
+@pytest.mark.parametrize("kind", ["port", "reference"])
+def test_fd_oracle_known_answers(kind):
+    if kind == "reference" and not available("reference"):
+        pytest.skip("oracle/_ref not built")
+    for name, check in known_fd_cases():
+        check(oracle(kind))
+
+
+def test_fd_port_matches_reference():
+    if not available("reference"):
+        pytest.skip("oracle/_ref not built")
+    rng = _random.Random(20240101)
+    P, R = oracle("port"), oracle("reference")
+    for _ in range(400):
+        t = _rt(rng, 14, 5, _ALPHA["ab"], max_len=2)
+        assert P.discover_fds(t, 100) == R.discover_fds(t, 100)
+        names = [t.field_name(f) for f in range(t.field_count())]
+        rng.shuffle(names)
+        cut = rng.randint(0, len(names))
+        groups = [g for g in (names[:cut], names[cut:]) if g]
+        assert P.validate_fds(t, groups) == R.validate_fds(t, groups)
