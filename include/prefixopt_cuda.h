@@ -155,6 +155,29 @@ int po_fd_compare(const po_table* t, uint32_t n_pairs, const int32_t* pair_a,
                   const int32_t* pair_b, uint64_t* out_first_diff, uint64_t* out_sig_a,
                   uint64_t* out_sig_b, void* stream);
 
+/* prefixopt::render_prompt (objective.hpp:102-131) of every entry of a
+ * schedule (CSR field orders as in po_phc; arrays at sched_location):
+ * prompt i = out_bytes[out_offsets[i] .. out_offsets[i+1]). Call with
+ * out_bytes == NULL to get the total size in *out_total (out_offsets is
+ * filled either way, n_entries + 1 values); then again with a buffer of at
+ * least that many bytes (else PO_ERR_SIZE). Outputs at out_location. A row or
+ * field outside the table -> PO_ERR_OUT_OF_RANGE (Table::cell). */
+int po_render_prompts(const po_table* t, uint64_t n_entries, const uint64_t* row_ids,
+                      const uint64_t* order_offsets, const int32_t* order_fields,
+                      uint32_t sched_location, const uint8_t* system_prompt,
+                      uint64_t system_prompt_len, const uint8_t* question, uint64_t question_len,
+                      uint32_t out_location, uint64_t* out_offsets, uint8_t* out_bytes,
+                      uint64_t out_capacity, uint64_t* out_total, void* stream);
+
+/* prefixopt::dedup (cost.hpp:171-186), byte-exact: strings
+ * arena[offsets[i] .. offsets[i+1]) (i < n, at `location`). Host outputs:
+ * out_expansion[i] = index of string i's unique; out_unique_first[u] =
+ * original index of unique u (uniques in first-occurrence order, n slots);
+ * *out_n_unique. */
+int po_dedup(uint64_t n, const uint8_t* arena, const uint64_t* offsets, uint32_t location,
+             uint64_t* out_expansion, uint64_t* out_unique_first, uint64_t* out_n_unique,
+             void* stream);
+
 /* ---- row-sharded solve over several GPUs ---------------
  * No reference counterpart: the reference ggr() (ggr.hpp:367-394) is one
  * process on one table. Here every rank (one per GPU) passes a contiguous

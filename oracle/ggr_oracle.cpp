@@ -596,6 +596,63 @@ int oracle_discover_fds(const po_table* tv, uint64_t max_rows, int32_t* out_grou
   });
 }
 
+// render_prompt (objective.hpp:118-131) = [sp '\n'][q '\n'] + render_body
+// (objective.hpp:102-115) = '{' + join(", ", '"' esc(name) '": "' esc(v) '"') + '}'.
+int oracle_render_prompts(const po_table* tv, uint64_t n_entries, const uint64_t* rows,
+                          const uint64_t* offs, const int32_t* fields, const uint8_t* sp,
+                          uint64_t sp_len, const uint8_t* q, uint64_t q_len,
+                          uint64_t* out_offsets, uint8_t* out_bytes, uint64_t capacity,
+                          uint64_t* out_total) {
+  return guarded([&] {
+    Tab t(tv);
+    std::string prefix;
+    if (sp && sp_len) prefix += std::string(reinterpret_cast<const char*>(sp), sp_len) + "\n";
+    if (q && q_len) prefix += std::string(reinterpret_cast<const char*>(q), q_len) + "\n";
+    uint64_t pos = 0;
+    out_offsets[0] = 0;
+    for (uint64_t i = 0; i < n_entries; ++i) {
+      std::string p = prefix + "{";
+      for (uint64_t k = offs[i]; k < offs[i + 1]; ++k) {
+        if (k > offs[i]) p += ", ";
+        const std::string_view v = t.cell(rows[i], fields[k]);  // range-checked
+        p += "\"" + escape(t.names[fields[k]]) + "\": \"" + escape(v) + "\"";
+      }
+      p += "}";
+      if (out_bytes && pos + p.size() <= capacity) std::memcpy(out_bytes + pos, p.data(), p.size());
+      pos += p.size();
+      out_offsets[i + 1] = pos;
+    }
+    *out_total = pos;
+  });
+}
+
+// dedup (cost.hpp:171-186) restated by sorting: stable order by bytes, the
+// first index of each run of equal strings names the unique; uniques are
+// numbered by first occurrence.
+int oracle_dedup(uint64_t n, const uint8_t* arena, const uint64_t* offsets,
+                 uint64_t* out_expansion, uint64_t* out_unique_first, uint64_t* out_n_unique) {
+  return guarded([&] {
+    auto str = [&](uint64_t i) {
+      return std::string_view(reinterpret_cast<const char*>(arena) + offsets[i],
+                              offsets[i + 1] - offsets[i]);
+    };
+    std::vector<uint64_t> idx(n), first(n);
+    std::iota(idx.begin(), idx.end(), 0);
+    std::stable_sort(idx.begin(), idx.end(), [&](uint64_t a, uint64_t b) { return str(a) < str(b); });
+    for (uint64_t k = 0; k < n; ++k)
+      first[idx[k]] = (k > 0 && str(idx[k]) == str(idx[k - 1])) ? first[idx[k - 1]] : idx[k];
+    std::vector<uint64_t> uid(n, 0);
+    uint64_t nu = 0;
+    for (uint64_t i = 0; i < n; ++i)
+      if (first[i] == i) {
+        uid[i] = nu;
+        out_unique_first[nu++] = i;
+      }
+    for (uint64_t i = 0; i < n; ++i) out_expansion[i] = uid[first[i]];
+    *out_n_unique = nu;
+  });
+}
+
 const char* oracle_last_error(void) { return g_err.c_str(); }
 
 }  // extern "C"

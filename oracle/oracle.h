@@ -43,6 +43,15 @@ extern "C" {
                            uint64_t* out_row_b, int32_t* out_agree, int32_t* out_differ); \
   int prefix##discover_fds(const po_table* t, uint64_t max_rows,                         \
                            int32_t* out_group_of_field);                                 \
+  int prefix##render_prompts(const po_table* t, uint64_t n_entries, const uint64_t* row_ids, \
+                             const uint64_t* order_offsets, const int32_t* order_fields,  \
+                             const uint8_t* system_prompt, uint64_t system_prompt_len,    \
+                             const uint8_t* question, uint64_t question_len,              \
+                             uint64_t* out_offsets, uint8_t* out_bytes, uint64_t capacity, \
+                             uint64_t* out_total);                                          \
+  int prefix##dedup(uint64_t n, const uint8_t* arena, const uint64_t* offsets,             \
+                    uint64_t* out_expansion, uint64_t* out_unique_first,                   \
+                    uint64_t* out_n_unique);                                               \
   const char* prefix##last_error(void);
 
 PO_ORACLE_DECLARE(oracle_)

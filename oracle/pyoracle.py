@@ -46,6 +46,10 @@ class OracleLib:
                            [C.c_uint32, C.c_uint64, vp, vp, C.c_int32, vp])
         self._vfd = _bind(L, p + "validate_fds", C.c_int, [vp, vp, vp, vp, vp, vp, vp, vp])
         self._dfd = _bind(L, p + "discover_fds", C.c_int, [vp, C.c_uint64, vp])
+        self._render = _bind(L, p + "render_prompts", C.c_int,
+                             [vp, C.c_uint64, vp, vp, vp, vp, C.c_uint64, vp, C.c_uint64, vp, vp,
+                              C.c_uint64, vp])
+        self._dedup = _bind(L, p + "dedup", C.c_int, [C.c_uint64, vp, vp, vp, vp, vp])
         self._err = _bind(L, p + "last_error", C.c_char_p, [])
 
     def _check(self, code):
@@ -168,3 +172,45 @@ def _fd_oracle_methods():
 
 
 _fd_oracle_methods()
+
+
+def _render_dedup_oracle_methods():
+    from paper_2403_05821_b200.api import DedupResult, _sched_args
+    from paper_2403_05821_b200.table import _to_bytes
+
+    def render_prompts(self, s, t, system_prompt=b"", question=b""):
+        view = t.view()
+        n = s.size()
+        _, rows_p, offs_p, flds_p = _sched_args(s)
+        sp, q = _to_bytes(system_prompt), _to_bytes(question)
+        sp_a = np.frombuffer(sp or b"\0", dtype=np.uint8)
+        q_a = np.frombuffer(q or b"\0", dtype=np.uint8)
+        out_off = np.zeros(n + 1, dtype=np.uint64)
+        total = C.c_uint64(0)
+        args = (view.ref(), n, rows_p, offs_p, flds_p,
+                sp_a.ctypes.data, len(sp), q_a.ctypes.data, len(q), out_off.ctypes.data)
+        self._check(self._render(*args, None, 0, C.byref(total)))
+        arena = np.empty(max(int(total.value), 1), dtype=np.uint8)
+        self._check(self._render(*args, arena.ctypes.data, arena.size, C.byref(total)))
+        buf = arena.tobytes()
+        return [buf[int(out_off[i]):int(out_off[i + 1])] for i in range(n)]
+
+    def dedup(self, prompts):
+        items = [_to_bytes(p) for p in prompts]
+        n = len(items)
+        offs = np.zeros(n + 1, dtype=np.uint64)
+        if n:
+            np.cumsum([len(x) for x in items], out=offs[1:])
+        arena = np.frombuffer(b"".join(items) or b"\0", dtype=np.uint8)
+        ex = np.zeros(max(n, 1), dtype=np.uint64)
+        uf = np.zeros(max(n, 1), dtype=np.uint64)
+        nu = C.c_uint64(0)
+        self._check(self._dedup(n, arena.ctypes.data, offs.ctypes.data, ex.ctypes.data,
+                                uf.ctypes.data, C.byref(nu)))
+        return DedupResult([items[int(i)] for i in uf[:int(nu.value)]], [int(x) for x in ex[:n]])
+
+    OracleLib.render_prompts = render_prompts
+    OracleLib.dedup = dedup
+
+
+_render_dedup_oracle_methods()

@@ -8,11 +8,13 @@
 // The output goes to oracle/_ref/ (git-ignored, shipped to the GPU box).
 
 #include <chrono>
+#include <cstring>
 #include <stdexcept>
 #include <string>
 #include <unordered_map>
 #include <vector>
 
+#include "prefixopt/cost.hpp"
 #include "prefixopt/fd.hpp"
 #include "prefixopt/ggr.hpp"
 #include "prefixopt/objective.hpp"
@@ -261,6 +263,52 @@ int ref_discover_fds(const po_table* tv, uint64_t max_rows, int32_t* out_group_o
     for (size_t f = 0; f < t.field_count(); ++f) out_group_of_field[f] = -1;
     for (size_t g = 0; g < set.groups.size(); ++g)
       for (const auto& nm : set.groups[g]) out_group_of_field[t.require_field(nm)] = int32_t(g);
+  });
+}
+
+// prefixopt::render_prompt (objective.hpp:118-131) of every entry; sizes
+// first (out_bytes == NULL), then the bytes.
+int ref_render_prompts(const po_table* tv, uint64_t n_entries, const uint64_t* rows,
+                       const uint64_t* offs, const int32_t* fields, const uint8_t* sp,
+                       uint64_t sp_len, const uint8_t* q, uint64_t q_len, uint64_t* out_offsets,
+                       uint8_t* out_bytes, uint64_t capacity, uint64_t* out_total) {
+  return guarded([&] {
+    prefixopt::Table t = to_table(tv);
+    const std::string_view spv(reinterpret_cast<const char*>(sp), sp ? sp_len : 0);
+    const std::string_view qv(reinterpret_cast<const char*>(q), q ? q_len : 0);
+    uint64_t pos = 0;
+    out_offsets[0] = 0;
+    for (uint64_t i = 0; i < n_entries; ++i) {
+      prefixopt::ScheduleEntry e;
+      e.row_id = rows[i];
+      e.field_order.assign(fields + offs[i], fields + offs[i + 1]);
+      const std::string p = prefixopt::render_prompt(e, t, spv, qv);
+      if (out_bytes && pos + p.size() <= capacity) std::memcpy(out_bytes + pos, p.data(), p.size());
+      pos += p.size();
+      out_offsets[i + 1] = pos;
+    }
+    *out_total = pos;
+  });
+}
+
+// prefixopt::dedup (cost.hpp:171-186)
+int ref_dedup(uint64_t n, const uint8_t* arena, const uint64_t* offsets, uint64_t* out_expansion,
+              uint64_t* out_unique_first, uint64_t* out_n_unique) {
+  return guarded([&] {
+    std::vector<std::string> prompts;
+    for (uint64_t i = 0; i < n; ++i)
+      prompts.emplace_back(reinterpret_cast<const char*>(arena) + offsets[i],
+                           offsets[i + 1] - offsets[i]);
+    const prefixopt::DedupResult d = prefixopt::dedup(prompts);
+    std::vector<char> seen(d.uniques.size(), 0);
+    for (uint64_t i = 0; i < n; ++i) {
+      out_expansion[i] = d.expansion_map[i];
+      if (!seen[d.expansion_map[i]]) {
+        seen[d.expansion_map[i]] = 1;
+        out_unique_first[d.expansion_map[i]] = i;
+      }
+    }
+    *out_n_unique = d.uniques.size();
   });
 }
 

@@ -542,6 +542,61 @@ def discover_fds(t: Table, max_rows: int = 10000) -> FunctionalDependencySet:
     return FunctionalDependencySet([c[1] for c in classes if len(c[1]) >= 2], True)
 
 
+# --------------------------------------------------------------------------
+# prompt rendering and byte-exact dedup (objective.hpp:102-131, cost.hpp:171-186)
+# --------------------------------------------------------------------------
+def render_prompts_arena(s: RequestSchedule, t: Table, system_prompt: bytes = b"",
+                         question: bytes = b"", stream: int = 0):
+    """render_prompt of every entry on the GPU: (bytes arena, u64 offsets)."""
+    lib = cuda_lib()
+    view = t.view()
+    n = s.size()
+    _, rows_p, offs_p, flds_p = _sched_args(s)
+    sp = _to_bytes(system_prompt)
+    q = _to_bytes(question)
+    sp_a = np.frombuffer(sp or b"\0", dtype=np.uint8)
+    q_a = np.frombuffer(q or b"\0", dtype=np.uint8)
+    out_off = np.zeros(n + 1, dtype=np.uint64)
+    total = C.c_uint64(0)
+    args = (view.ref(), n, rows_p, offs_p, flds_p, PO_LOC_HOST, sp_a.ctypes.data,
+            len(sp), q_a.ctypes.data, len(q), PO_LOC_HOST, out_off.ctypes.data)
+    lib.check(lib.render_prompts(*args, None, 0, C.byref(total), stream))
+    arena = np.empty(max(int(total.value), 1), dtype=np.uint8)
+    lib.check(lib.render_prompts(*args, arena.ctypes.data, arena.size, C.byref(total), stream))
+    return arena[:int(total.value)], out_off
+
+
+def render_prompts(s: RequestSchedule, t: Table, system_prompt: bytes = b"",
+                   question: bytes = b"") -> list:
+    """[render_prompt(e, t, system_prompt, question) for e in s] (objective.hpp:118-131)."""
+    arena, off = render_prompts_arena(s, t, system_prompt, question)
+    buf = arena.tobytes()
+    return [buf[int(off[i]):int(off[i + 1])] for i in range(s.size())]
+
+
+@dataclass
+class DedupResult:
+    uniques: list            # first-occurrence order
+    expansion_map: list      # original index -> unique index
+
+
+def dedup(prompts) -> DedupResult:
+    """prefixopt::dedup (cost.hpp:171-186), byte-exact, on the GPU dictionary."""
+    lib = cuda_lib()
+    items = [_to_bytes(p) for p in prompts]
+    n = len(items)
+    offs = np.zeros(n + 1, dtype=np.uint64)
+    if n:
+        np.cumsum([len(x) for x in items], out=offs[1:])
+    arena = np.frombuffer(b"".join(items) or b"\0", dtype=np.uint8)
+    ex = np.zeros(max(n, 1), dtype=np.uint64)
+    uf = np.zeros(max(n, 1), dtype=np.uint64)
+    nu = C.c_uint64(0)
+    lib.check(lib.dedup(n, arena.ctypes.data, offs.ctypes.data, PO_LOC_HOST, ex.ctypes.data,
+                        uf.ctypes.data, C.byref(nu), 0))
+    return DedupResult([items[int(i)] for i in uf[:int(nu.value)]], [int(x) for x in ex[:n]])
+
+
 # low-level entry for callers holding device buffers (bench.py, multi-GPU)
 def ggr_into(view: TableView, fd_groups: list, cfg: GgrConfig, tok_kind: int, scoring: int,
              out_location: int, out_rows, out_orders, stream: int = 0):
@@ -566,5 +621,6 @@ __all__ = [
     "sort_rows_fixed_order", "compute_stats", "fixed_order_by_hitcount_stats",
     "fixed_order_by_stats", "original_order_schedule", "hitcount", "HitCountResult", "ggr_into",
     "PO_LOC_HOST", "PO_LOC_DEVICE", "FdWitness", "FdGroupReport", "FdValidationReport",
-    "validate_fds", "discover_fds",
+    "validate_fds", "discover_fds", "render_prompts", "render_prompts_arena", "DedupResult",
+    "dedup",
 ]

@@ -395,6 +395,76 @@ int po_fd_compare(const po_table* t, uint32_t n_pairs, const int32_t* pair_a,
   });
 }
 
+int po_render_prompts(const po_table* t, uint64_t n_entries, const uint64_t* rows,
+                      const uint64_t* offs, const int32_t* fields, uint32_t sched_loc,
+                      const uint8_t* sp, uint64_t sp_len, const uint8_t* q, uint64_t q_len,
+                      uint32_t out_loc, uint64_t* out_offsets, uint8_t* out_bytes,
+                      uint64_t out_capacity, uint64_t* out_total, void* stream) {
+  return guarded([&] {
+    if (sched_loc != PO_LOC_HOST && sched_loc != PO_LOC_DEVICE)
+      fail(PO_ERR_INVALID_ARG, "bad schedule location");
+    if (out_loc != PO_LOC_HOST && out_loc != PO_LOC_DEVICE)
+      fail(PO_ERR_INVALID_ARG, "bad output location");
+    if (!out_offsets || !out_total || (n_entries && (!rows || !offs)))
+      fail(PO_ERR_INVALID_ARG, "null argument");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    init_pool_once();
+    DeviceTable dt;
+    make_device_table(t, PO_TOK_CHAR, s, dt);
+    uint64_t nfields = 0;
+    if (n_entries) {
+      if (sched_loc == PO_LOC_HOST) nfields = offs[n_entries];
+      else {
+        PO_CUDA(cudaMemcpyAsync(&nfields, offs + n_entries, 8, cudaMemcpyDeviceToHost, s));
+        sync(s);
+      }
+    }
+    DevBuf<uint64_t> own_rows, own_offs;
+    DevBuf<int32_t> own_fields;
+    const uint64_t* d_rows = stage(rows, n_entries, sched_loc, own_rows, s);
+    const uint64_t* d_offs = stage(offs, n_entries + 1, sched_loc, own_offs, s);
+    const int32_t* d_fields = stage(fields, nfields, sched_loc, own_fields, s);
+    DevBuf<uint64_t> o;
+    DevBuf<uint8_t> b;
+    uint64_t total = 0;
+    render_prompts_device(dt, n_entries, d_rows, d_offs, d_fields,
+                          std::string(reinterpret_cast<const char*>(sp), sp ? sp_len : 0),
+                          std::string(reinterpret_cast<const char*>(q), q ? q_len : 0), o, b,
+                          total, s);
+    const cudaMemcpyKind k = out_loc == PO_LOC_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+    PO_CUDA(cudaMemcpyAsync(out_offsets, o.get(), (n_entries + 1) * 8, k, s));
+    *out_total = total;
+    if (out_bytes) {
+      if (out_capacity < total) fail(PO_ERR_SIZE, "render: output buffer too small");
+      if (total) PO_CUDA(cudaMemcpyAsync(out_bytes, b.get(), total, k, s));
+    }
+    sync(s);
+  });
+}
+
+int po_dedup(uint64_t n, const uint8_t* arena, const uint64_t* offsets, uint32_t loc,
+             uint64_t* out_expansion, uint64_t* out_unique_first, uint64_t* out_n_unique,
+             void* stream) {
+  return guarded([&] {
+    if (!out_expansion || !out_unique_first || !out_n_unique || (n && (!arena || !offsets)))
+      fail(PO_ERR_INVALID_ARG, "null argument");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    init_pool_once();
+    const char* name = "prompt";
+    const uint64_t name_len = 6;
+    po_table tv{n, 1u, loc, &name, &name_len, arena, offsets, nullptr};
+    DeviceTable dt;
+    make_device_table(&tv, PO_TOK_CHAR, s, dt);
+    DevBuf<uint64_t> ex(std::max<uint64_t>(n, 1), s), uf(std::max<uint64_t>(n, 1), s);
+    uint64_t nu = 0;
+    dedup_device(dt, ex.get(), uf.get(), nu, s);
+    ex.download(out_expansion, n);
+    uf.download(out_unique_first, nu);
+    sync(s);
+    *out_n_unique = nu;
+  });
+}
+
 int po_comm_unique_id(uint8_t* out_id128) {
   return guarded([&] {
     if (!out_id128) fail(PO_ERR_INVALID_ARG, "null id buffer");

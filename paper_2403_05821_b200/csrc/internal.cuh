@@ -227,6 +227,18 @@ void fd_compare_device(const Encoded& e, const std::vector<int32_t>& pa,
                        const std::vector<int32_t>& pb, std::vector<uint64_t>& first_diff,
                        std::vector<uint64_t>& sig_a, std::vector<uint64_t>& sig_b, cudaStream_t s);
 
+// render_prompt over a schedule (render.cu, objective.hpp:102-131): prompt i
+// at out_bytes[out_off[i] .. out_off[i+1]); schedule arrays on the device.
+void render_prompts_device(const DeviceTable& t, uint64_t n_entries, const uint64_t* rows,
+                           const uint64_t* order_offsets, const int32_t* fields,
+                           const std::string& system_prompt, const std::string& question,
+                           DevBuf<uint64_t>& out_off, DevBuf<uint8_t>& out_bytes,
+                           uint64_t& total, cudaStream_t s);
+// dedup (cost.hpp:171-186) of the one-column table t's strings: expansion
+// map and, per unique in first-occurrence order, its first index.
+void dedup_device(const DeviceTable& t, uint64_t* d_expansion, uint64_t* d_unique_first,
+                  uint64_t& n_unique, cudaStream_t s);
+
 // Row-sharded solving (shard.cu). Every rank holds a
 // contiguous range of the table's rows; value ids are global (escaped-order
 // ranks over the whole table), the value-group tables are replicated (built

@@ -90,3 +90,39 @@ def test_fd_port_matches_reference():
         cut = rng.randint(0, len(names))
         groups = [g for g in (names[:cut], names[cut:]) if g]
         assert P.validate_fds(t, groups) == R.validate_fds(t, groups)
+
+
+# ---- prompt rendering + dedup (objective.hpp:102-131, cost.hpp:171-186) ----
+def _random_schedule(rng, t):
+    from paper_2403_05821_b200 import RequestSchedule
+    n, m = t.row_count(), t.field_count()
+    ent = [(rng.randrange(n), rng.sample(range(m), rng.randint(0, m)))
+           for _ in range(rng.randint(0, 25))]
+    return RequestSchedule.from_entries(ent)
+
+
+def test_render_dedup_port_matches_reference():
+    if not available("reference"):
+        pytest.skip("oracle/_ref not built")
+    rng = _random.Random(99)
+    P, R = oracle("port"), oracle("reference")
+    for _ in range(150):
+        t = _rt(rng, 15, 4, _ALPHA["all"], max_len=4)
+        s = _random_schedule(rng, t)
+        sp = bytes(rng.randrange(256) for _ in range(rng.randint(0, 4)))
+        q = b"Which?" if rng.random() < 0.5 else b""
+        a = P.render_prompts(s, t, sp, q)
+        assert a == R.render_prompts(s, t, sp, q)
+        dup = a + a[: rng.randint(0, len(a))]
+        rng.shuffle(dup)
+        assert P.dedup(dup) == R.dedup(dup)
+
+
+def test_render_known_answer():
+    # render_body / render_prompt format (objective.hpp:102-131)
+    from paper_2403_05821_b200 import RequestSchedule, Table
+    t = Table([b"title", b"q\"t"], [[b"Dune", b"a\nb"]])
+    s = RequestSchedule.from_entries([(0, [1, 0]), (0, [])])
+    want = [b'SYS\nQ\n{"q\\"t": "a\\nb", "title": "Dune"}', b"SYS\nQ\n{}"]
+    for kind in ("port",) + (("reference",) if available("reference") else ()):
+        assert oracle(kind).render_prompts(s, t, b"SYS", b"Q") == want
