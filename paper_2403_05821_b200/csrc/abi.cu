@@ -110,6 +110,48 @@ void timing_report(const char* call) {
 }
 
 namespace {
+struct PinnedArena {
+  uint8_t* base = nullptr;
+  size_t cap = 0, used = 0;
+  cudaStream_t last = nullptr;
+  ~PinnedArena() {
+    if (base) cudaFreeHost(base);
+  }
+};
+thread_local PinnedArena g_pin;
+}  // namespace
+
+void h2d_async(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+  if (!bytes) return;
+  PinnedArena& a = g_pin;
+  if (bytes > kPinnedSmallCopy) {
+    PO_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
+    return;
+  }
+  if (!a.base) {
+    a.cap = 32u << 20;
+    if (cudaMallocHost(reinterpret_cast<void**>(&a.base), a.cap) != cudaSuccess) {
+      (void)cudaGetLastError();
+      a.base = nullptr;
+      a.cap = 0;
+      PO_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
+      return;
+    }
+  }
+  const size_t need = (bytes + 15) & ~size_t(15);
+  if (a.used + need > a.cap || (a.last && a.last != s)) {
+    // recycle: every earlier copy out of the arena must have completed
+    if (a.last) PO_CUDA(cudaStreamSynchronize(a.last));
+    a.used = 0;
+  }
+  uint8_t* p = a.base + a.used;
+  a.used += need;
+  a.last = s;
+  std::memcpy(p, src, bytes);
+  PO_CUDA(cudaMemcpyAsync(dst, p, bytes, cudaMemcpyHostToDevice, s));
+}
+
+namespace {
 
 // Keep freed stream-ordered allocations cached in the device pool between
 // calls instead of returning them to the driver at every synchronisation.

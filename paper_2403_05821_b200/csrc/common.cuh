@@ -76,6 +76,13 @@ inline unsigned grid_for(uint64_t work, unsigned block, unsigned max_waves = 16)
   return unsigned(g);
 }
 
+// Small host->device copies (per-level descriptors, key schedules, column
+// tables) are staged through a per-thread pinned arena so cudaMemcpyAsync
+// stays asynchronous (a copy from pageable memory may synchronise the
+// stream and stall the launch queue). Larger copies (caller data) go direct.
+constexpr size_t kPinnedSmallCopy = 1 << 20;
+void h2d_async(void* dst, const void* src, size_t bytes, cudaStream_t s);
+
 // ---------------------------------------------------------------------------
 // stream-ordered device buffer (cudaMallocAsync on the call's stream)
 // ---------------------------------------------------------------------------
@@ -119,7 +126,7 @@ class DevBuf {
   T* get() const { return p_; }
   size_t size() const { return n_; }
   void upload(const T* h, size_t n) {
-    if (n) PO_CUDA(cudaMemcpyAsync(p_, h, n * sizeof(T), cudaMemcpyHostToDevice, s_));
+    if (n) h2d_async(p_, h, n * sizeof(T), s_);
   }
   void download(T* h, size_t n) const {
     if (n) PO_CUDA(cudaMemcpyAsync(h, p_, n * sizeof(T), cudaMemcpyDeviceToHost, s_));

@@ -586,6 +586,52 @@ __global__ void k_dict_fixup(const uint8_t* __restrict__ arena, const uint8_t* a
   }
 }
 
+// Occupied dictionary slots of every column, compacted per column into
+// sel[c*cap ..] (any order: the rank sort orders them). A block takes a chunk
+// of kCompactChunk slots of one column (cap is a power of two >= 64; chunks
+// never straddle columns), counts its occupied slots, reserves them with ONE
+// atomic, then writes them in order (the second read of the chunk hits L1/L2).
+constexpr uint32_t kCompactChunk = 4096;
+__global__ void __launch_bounds__(256) k_compact_slots(const unsigned long long* __restrict__ keys,
+                                                       uint64_t cap, uint64_t total, uint32_t* sel,
+                                                       int* count) {
+  __shared__ int s_warp[8];
+  __shared__ int s_base;
+  const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const uint64_t chunk = cap < kCompactChunk ? cap : kCompactChunk;
+  for (uint64_t c0 = blockIdx.x * chunk; c0 < total; c0 += uint64_t(gridDim.x) * chunk) {
+    const uint64_t col = c0 / cap;
+    int mine = 0;
+    for (uint64_t i = c0 + threadIdx.x; i < c0 + chunk; i += 256) mine += keys[i] != 0;
+    for (int d = 16; d > 0; d >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, d);
+    if (lane == 0) s_warp[wid] = mine;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int t = 0;
+      for (int w = 0; w < 8; ++w) t += s_warp[w];
+      s_base = t ? atomicAdd(&count[col], t) : 0;
+    }
+    __syncthreads();
+    int base = s_base;
+    // ordered write: 256 slots per step, block-wide exclusive prefix of the step
+    for (uint64_t b = c0; b < c0 + chunk; b += 256) {
+      const bool occ = b + threadIdx.x < c0 + chunk && keys[b + threadIdx.x] != 0;
+      const unsigned bal = __ballot_sync(0xffffffffu, occ);
+      if (lane == 0) s_warp[wid] = __popc(bal);
+      __syncthreads();
+      int before = 0, step = 0;
+      for (int w = 0; w < 8; ++w) {
+        before += w < int(wid) ? s_warp[w] : 0;
+        step += s_warp[w];
+      }
+      if (occ)
+        sel[col * cap + base + before + __popc(bal & ((1u << lane) - 1))] = uint32_t(b + threadIdx.x - col * cap);
+      base += step;
+      __syncthreads();
+    }
+  }
+}
+
 __global__ void k_occupied(const unsigned long long* keys, uint64_t cap, uint8_t* flags) {
   for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < cap;
        i += uint64_t(gridDim.x) * blockDim.x)
@@ -972,21 +1018,13 @@ void encode(const DeviceTable& t, int tok, int scoring, cudaStream_t s, Encoded&
   // Distinct values per column (occupied slots): every column is compacted
   // into its own region of `stage` without host round trips, then one D2H of
   // the m counts gives the cardinalities and the packed layout.
-  DevBuf<uint8_t> flags(cap, s);
   DevBuf<uint32_t> stage_sel(m * cap, s);
   DevBuf<int> nsel(m, s);
-  size_t tmp_bytes = 0;
-  cub::CountingInputIterator<uint32_t> it(0);
-  PO_CUDA(cub::DeviceSelect::Flagged(nullptr, tmp_bytes, it, flags.get(), stage_sel.get(),
-                                     nsel.get(), int(cap), s));
-  DevBuf<uint8_t> tmp(tmp_bytes, s);
-  for (uint32_t c = 0; c < m; ++c) {
-    PO_LAUNCH(k_occupied, grid_for(cap, 256), 256, 0, s, keys.get() + uint64_t(c) * cap, cap,
-              flags.get());
-    ProfScope ps("cub_select", s);
-    PO_CUDA(cub::DeviceSelect::Flagged(tmp.get(), tmp_bytes, it, flags.get(),
-                                       stage_sel.get() + uint64_t(c) * cap, nsel.get() + c,
-                                       int(cap), s));
+  nsel.zero();
+  {
+    const uint64_t chunks = (m * cap + kCompactChunk - 1) / kCompactChunk;
+    PO_LAUNCH(k_compact_slots, unsigned(std::min<uint64_t>(chunks, uint64_t(kSMs) * 8)), 256, 0, s,
+              keys.get(), cap, m * cap, stage_sel.get(), nsel.get());
   }
   {
     std::vector<int> hk(m);
@@ -1045,7 +1083,6 @@ void encode(const DeviceTable& t, int tok, int scoring, cudaStream_t s, Encoded&
             sel.get(), e.d_colbase.get(), D, cap, slot2vid.get(), e.rep_row.get(),
             col_by_pos.get());
   keys.release();
-  flags.release();
   timing_mark("scatter_pos", s);
 
   // Segment length per distinct value.

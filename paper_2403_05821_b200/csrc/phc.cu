@@ -203,7 +203,7 @@ uint64_t fixed_order_phc_device(const Encoded& e, const std::vector<int>& order,
     DevBuf<unsigned long long> ng(order.size(), s);
     ng.zero();
     const unsigned long long c0 = e.card[f0];
-    PO_CUDA(cudaMemcpyAsync(ng.get(), &c0, sizeof(c0), cudaMemcpyHostToDevice, s));
+    h2d_async(ng.get(), &c0, sizeof(c0), s);
     PO_LAUNCH(k_fb_init, grid_for(n, 256), 256, 0, s, e.vid.get(), n, m, uint32_t(f0), gid.get());
     for (size_t p = 1; p < order.size(); ++p) {
       const int f = order[p];
