@@ -103,19 +103,48 @@ void timing_report(const char* call) {
     agg[k] += v;
     tot += v;
   }
-  fprintf(stderr, "[po timing] %s total %.3f ms:", call, tot);
-  for (auto& k : order) fprintf(stderr, " %s=%.3f", k.c_str(), agg[k]);
-  fprintf(stderr, "\n");
+  std::string line = "[po timing] " + std::string(call) + " total " + std::to_string(tot) + " ms:";
+  for (auto& k : order)
+    if (k != "<start") line += " " + k + "=" + std::to_string(agg[k]);
+  line += "\n";
+  fputs(line.c_str(), stderr);  // one write: lines of concurrent ranks stay whole
   g_marks.clear();
 }
 
 namespace {
+// Pinned staging memory is recycled across threads (a thread's arena goes
+// back to a free list when the thread exits): callers that run each call on
+// a fresh host thread must not pay cudaMallocHost / cudaFreeHost (which
+// synchronises the device) per call.
+std::mutex g_pin_mu;
+std::vector<std::pair<uint8_t*, size_t>> g_pin_free;
+
 struct PinnedArena {
   uint8_t* base = nullptr;
   size_t cap = 0, used = 0;
   cudaStream_t last = nullptr;
   ~PinnedArena() {
-    if (base) cudaFreeHost(base);
+    if (!base) return;
+    if (last) cudaStreamSynchronize(last);  // copies out of the arena are done
+    std::lock_guard<std::mutex> lk(g_pin_mu);
+    g_pin_free.push_back({base, cap});
+  }
+  void acquire() {
+    {
+      std::lock_guard<std::mutex> lk(g_pin_mu);
+      if (!g_pin_free.empty()) {
+        base = g_pin_free.back().first;
+        cap = g_pin_free.back().second;
+        g_pin_free.pop_back();
+        return;
+      }
+    }
+    cap = 32u << 20;
+    if (cudaMallocHost(reinterpret_cast<void**>(&base), cap) != cudaSuccess) {
+      (void)cudaGetLastError();
+      base = nullptr;
+      cap = 0;
+    }
   }
 };
 thread_local PinnedArena g_pin;
@@ -129,11 +158,8 @@ void h2d_async(void* dst, const void* src, size_t bytes, cudaStream_t s) {
     return;
   }
   if (!a.base) {
-    a.cap = 32u << 20;
-    if (cudaMallocHost(reinterpret_cast<void**>(&a.base), a.cap) != cudaSuccess) {
-      (void)cudaGetLastError();
-      a.base = nullptr;
-      a.cap = 0;
+    a.acquire();
+    if (!a.base) {
       PO_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
       return;
     }

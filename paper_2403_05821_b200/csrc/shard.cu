@@ -174,7 +174,7 @@ __global__ void k_sorted_lens(uint64_t D, const uint32_t* ord, LocalDict d, uint
 
 // One warp per value (in sorted order): (column, length) record + bytes.
 __global__ void k_pack_values(uint64_t D, const uint32_t* ord, LocalDict d, const uint64_t* boff,
-                              uint2* meta, uint8_t* bytes) {
+                              const uint8_t* lim, uint2* meta, uint8_t* bytes) {
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t warps = uint64_t(gridDim.x) * (blockDim.x >> 5);
   for (uint64_t k = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5; k < D; k += warps) {
@@ -184,7 +184,11 @@ __global__ void k_pack_values(uint64_t D, const uint32_t* ord, LocalDict d, cons
     d.str(i, p, len);
     if (lane == 0) meta[k] = make_uint2(d.icol[i], uint32_t(len));
     uint8_t* dst = bytes + boff[k];
-    for (uint64_t t = lane; t < len; t += 32) dst[t] = p[t];
+    for (uint64_t t = 8 * lane; t < len; t += 256) {  // 8 bytes per lane per step
+      const uint64_t w = load8_unaligned(p + t, lim);
+      const uint32_t nb = len - t >= 8 ? 8u : uint32_t(len - t);
+      for (uint32_t b = 0; b < nb; ++b) dst[t + b] = uint8_t(w >> (8 * b));
+    }
   }
 }
 
@@ -205,34 +209,39 @@ __global__ void k_meta_lens(uint64_t R, const uint2* meta, uint64_t* lens) {
   if (blockIdx.x == 0 && threadIdx.x == 0) lens[R] = 0;
 }
 
-// cstart[c] = merged position of the first item of column c
-__global__ void k_col_starts(uint32_t m, int N, const uint64_t* ro, const uint2* meta,
-                             uint32_t* cstart) {
-  const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c > m) return;
-  uint64_t tot = 0;
-  for (int r = 0; r < N; ++r) {
-    uint64_t lo = ro[r], hi = ro[r + 1];
-    while (lo < hi) {
-      const uint64_t mid = (lo + hi) >> 1;
-      if (meta[mid].x < c) lo = mid + 1;
-      else hi = mid;
+// Byte-order compare 8 bytes per step: the first differing byte comes from
+// the lowest set byte of x ^ y (little-endian words), then its order code
+// decides; a proper prefix compares the end code against the next byte.
+__device__ __forceinline__ int cmp_bytes_w(int kind, const uint8_t* a, uint64_t la,
+                                           const uint8_t* b, uint64_t lb, const uint8_t* lim) {
+  const uint16_t* code = c_code[kind];
+  const uint64_t n = la < lb ? la : lb;
+  for (uint64_t i = 0; i < n; i += 8) {
+    const uint64_t x = load8_unaligned(a + i, lim), y = load8_unaligned(b + i, lim);
+    const uint64_t d = mask_low_bytes(x ^ y, n - i >= 8 ? 8u : uint32_t(n - i));
+    if (d) {
+      const uint32_t sh = uint32_t(__ffsll((long long)d) - 1) & ~7u;
+      const uint32_t ca = code[(x >> sh) & 0xFF], cb = code[(y >> sh) & 0xFF];
+      return ca < cb ? -1 : 1;
     }
-    tot += lo - ro[r];
   }
-  cstart[c] = uint32_t(tot);
+  if (la == lb) return 0;
+  const uint32_t x = la == n ? code[256] : code[a[n]];
+  const uint32_t y = lb == n ? code[256] : code[b[n]];
+  return x < y ? -1 : 1;
 }
 
 __device__ __forceinline__ int cmp_item(int kind, const uint2* meta, const uint64_t* offs,
-                                        const uint8_t* bytes, uint64_t a, uint64_t b) {
+                                        const uint8_t* bytes, const uint8_t* lim, uint64_t a,
+                                        uint64_t b) {
   const uint2 ma = meta[a], mb = meta[b];
   if (ma.x != mb.x) return ma.x < mb.x ? -1 : 1;
-  return cmp_bytes(c_code[kind], bytes + offs[a], ma.y, bytes + offs[b], mb.y);
+  return cmp_bytes_w(kind, bytes + offs[a], ma.y, bytes + offs[b], mb.y, lim);
 }
 
 __global__ void k_merge_pos_str(uint64_t R, int N, const uint64_t* ro, const uint2* meta,
-                                const uint64_t* offs, const uint8_t* bytes, int kind,
-                                uint32_t* pos) {
+                                const uint64_t* offs, const uint8_t* bytes, const uint8_t* lim,
+                                int kind, uint32_t* pos) {
   for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < R;
        i += uint64_t(gridDim.x) * blockDim.x) {
     int r = 0;
@@ -243,7 +252,7 @@ __global__ void k_merge_pos_str(uint64_t R, int N, const uint64_t* ro, const uin
       uint64_t lo = ro[q], hi = ro[q + 1];
       while (lo < hi) {  // items of run q before item i
         const uint64_t mid = (lo + hi) >> 1;
-        const int c = cmp_item(kind, meta, offs, bytes, mid, i);
+        const int c = cmp_item(kind, meta, offs, bytes, lim, mid, i);
         if (c < 0 || (c == 0 && q < r)) lo = mid + 1;
         else hi = mid;
       }
@@ -255,7 +264,8 @@ __global__ void k_merge_pos_str(uint64_t R, int N, const uint64_t* ro, const uin
 
 // new[k] = sorted value k differs from value k-1 (column or bytes)
 __global__ void k_new_flags(uint64_t R, const uint32_t* perm, const uint2* meta,
-                            const uint64_t* offs, const uint8_t* bytes, uint32_t* flags) {
+                            const uint64_t* offs, const uint8_t* bytes, const uint8_t* lim,
+                            uint32_t* flags) {
   for (uint64_t k = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; k < R;
        k += uint64_t(gridDim.x) * blockDim.x) {
     uint32_t f = 1;
@@ -263,14 +273,7 @@ __global__ void k_new_flags(uint64_t R, const uint32_t* perm, const uint2* meta,
       const uint32_t a = perm[k], b = perm[k - 1];
       const uint2 ma = meta[a], mb = meta[b];
       if (ma.x == mb.x && ma.y == mb.y) {
-        const uint8_t* pa = bytes + offs[a];
-        const uint8_t* pb = bytes + offs[b];
-        f = 0;
-        for (uint32_t t = 0; t < ma.y; ++t)
-          if (pa[t] != pb[t]) {
-            f = 1;
-            break;
-          }
+        f = cmp_bytes_w(0, bytes + offs[a], ma.y, bytes + offs[b], mb.y, lim) != 0;
       }
     }
     flags[k] = f;
@@ -444,7 +447,8 @@ DevBuf<uint32_t> global_ranks(Comm& comm, const Encoded& L, const uint32_t* d_ic
   }
   DevBuf<uint2> meta(D, s);
   DevBuf<uint8_t> sbytes(bb[N], s);
-  PO_LAUNCH(k_pack_values, grid_for(D * 32, 256), 256, 0, s, D, d_ord, ld, boff.get(), meta.get(),
+  PO_LAUNCH(k_pack_values, grid_for(D * 32, 256), 256, 0, s, D, d_ord, ld, boff.get(),
+            L.arena + L.arena_bytes, meta.get(),
             sbytes.get());
   std::vector<uint64_t> s_items(N), s_bytes(N), s_meta(N);
   for (int r = 0; r < N; ++r) {
@@ -452,22 +456,33 @@ DevBuf<uint32_t> global_ranks(Comm& comm, const Encoded& L, const uint32_t* d_ic
     s_meta[r] = s_items[r] * sizeof(uint2);
     s_bytes[r] = bb[r + 1] - bb[r];
   }
-  std::vector<uint64_t> both(2 * N);
+  // per destination: items, bytes and items per column (the sorted order
+  // groups columns: column c holds positions [colbase[c], colbase[c+1]))
+  const size_t W = 2 + size_t(m);
+  std::vector<uint64_t> both(W * N, 0);
   for (int r = 0; r < N; ++r) {
-    both[r] = s_items[r];
-    both[N + r] = s_bytes[r];
+    both[size_t(r) * W] = s_items[r];
+    both[size_t(r) * W + 1] = s_bytes[r];
+    for (uint32_t c = 0; c < m; ++c) {
+      const uint64_t lo = std::max(bounds[r], L.colbase[c]);
+      const uint64_t hi = std::min(bounds[r + 1], L.colbase[c + 1]);
+      both[size_t(r) * W + 2 + c] = hi > lo ? hi - lo : 0;
+    }
   }
-  // recv sizes: [src][dst] items then bytes
-  const std::vector<uint64_t> allc = comm.allgather_host(both, s);
+  const std::vector<uint64_t> allc = comm.allgather_host(both, s);  // [src][dst][W]
   std::vector<uint64_t> r_items(N), r_meta(N), r_bytes(N);
+  std::vector<uint32_t> cstart(m + 1, 0);
   uint64_t R = 0, RB = 0;
   for (int r = 0; r < N; ++r) {
-    r_items[r] = allc[size_t(r) * 2 * N + comm.rank()];
-    r_bytes[r] = allc[size_t(r) * 2 * N + N + comm.rank()];
+    const uint64_t* e = &allc[(size_t(r) * N + comm.rank()) * W];
+    r_items[r] = e[0];
+    r_bytes[r] = e[1];
     r_meta[r] = r_items[r] * sizeof(uint2);
     R += r_items[r];
     RB += r_bytes[r];
+    for (uint32_t c = 0; c < m; ++c) cstart[c + 1] += uint32_t(e[2 + c]);
   }
+  for (uint32_t c = 0; c < m; ++c) cstart[c + 1] += cstart[c];  // merged column starts
   DevBuf<uint2> rmeta(R, s);
   DevBuf<uint8_t> rbytes(RB, s);
   comm.alltoallv(meta.get(), s_meta, rmeta.get(), r_meta, s);
@@ -488,16 +503,14 @@ DevBuf<uint32_t> global_ranks(Comm& comm, const Encoded& L, const uint32_t* d_ic
     std::vector<uint64_t> ro(N + 1, 0);
     for (int r = 0; r < N; ++r) ro[r + 1] = ro[r] + r_items[r];
     auto d_ro = to_device(ro, s);
-    d_cstart.alloc(m + 1, s);
-    PO_LAUNCH(k_col_starts, (m + 1 + 127) / 128, 128, 0, s, m, N, d_ro.get(), rmeta.get(),
-              d_cstart.get());
+    d_cstart = to_device(cstart, s);
     pos.alloc(R, s);
     PO_LAUNCH(k_merge_pos_str, grid_for(R, 256), 256, 0, s, R, N, d_ro.get(), rmeta.get(),
-              roffs.get(), rbytes.get(), kind, pos.get());
+              roffs.get(), rbytes.get(), rbytes.get() + RB, kind, pos.get());
     DevBuf<uint32_t> perm(R, s), flags(R, s);
     PO_LAUNCH(k_invert, grid_for(R, 256), 256, 0, s, pos.get(), R, perm.get());
     PO_LAUNCH(k_new_flags, grid_for(R, 256), 256, 0, s, R, perm.get(), rmeta.get(), roffs.get(),
-              rbytes.get(), flags.get());
+              rbytes.get(), rbytes.get() + RB, flags.get());
     rbytes.release();
     u.alloc(R, s);
     inclusive_scan_u32(flags.get(), u.get(), R, s);
