@@ -451,7 +451,9 @@ int po_fd_compare(const po_table* t, uint32_t n_pairs, const int32_t* pair_a,
       fail(PO_ERR_INVALID_ARG, "null argument");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     Prepared p;
-    prepare(t, PO_TOK_CHAR, PO_SCORE_VALUE, s, p);
+    init_pool_once();
+    make_device_table(t, PO_TOK_CHAR, s, p.t);
+    encode(p.t, PO_TOK_CHAR, PO_SCORE_VALUE, s, p.e, debug_hash_bits(), /*ordered=*/false);
     std::vector<int32_t> pa(pair_a, pair_a + n_pairs), pb(pair_b, pair_b + n_pairs);
     std::vector<uint64_t> fd, sa, sb;
     fd_compare_device(p.e, pa, pb, fd, sa, sb, s);

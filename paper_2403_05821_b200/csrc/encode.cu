@@ -570,8 +570,9 @@ __global__ void k_dict_fixup(const uint8_t* __restrict__ arena, const uint8_t* a
                              const uint64_t* __restrict__ offsets, uint32_t m, uint64_t cap,
                              const unsigned long long* __restrict__ hashes,
                              unsigned long long* keys, uint32_t* reps, unsigned long long* repoffs,
-                             const uint32_t* collided, uint32_t n_collided,
+                             const uint32_t* collided, const uint32_t* n_collided_dev,
                              uint32_t* slot_of_cell) {
+  const uint32_t n_collided = *n_collided_dev;  // read on the device: no host round trip
   for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < n_collided;
        q += gridDim.x * blockDim.x) {
     const uint64_t i = collided[q];
@@ -630,6 +631,12 @@ __global__ void __launch_bounds__(256) k_compact_slots(const unsigned long long*
       __syncthreads();
     }
   }
+}
+
+__global__ void k_iota_pos(uint32_t* a, uint64_t n) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
+       i += uint64_t(gridDim.x) * blockDim.x)
+    a[i] = uint32_t(i);
 }
 
 __global__ void k_occupied(const unsigned long long* keys, uint64_t cap, uint8_t* flags) {
@@ -912,7 +919,7 @@ void make_device_table(const po_table* t, int tok, cudaStream_t s, DeviceTable& 
 }
 
 void encode(const DeviceTable& t, int tok, int scoring, cudaStream_t s, Encoded& e,
-            uint32_t hash_bits_debug) {
+            uint32_t hash_bits_debug, bool ordered) {
   e.n = t.n;
   e.m = t.m;
   e.arena = t.arena;
@@ -1005,13 +1012,10 @@ void encode(const DeviceTable& t, int tok, int scoring, cudaStream_t s, Encoded&
     PO_LAUNCH(k_dict_verify, grid_for(((n + 31) / 32) * 32, 256, 8), 256, 0, s, t.arena,
               arena_end, t.offsets, n, uint32_t(m), cap, reps.get(), repoffs.get(), slot_of_cell.get(),
               collided.get(), ncol.get());
-    uint32_t hcol = 0;
-    ncol.download(&hcol, 1);
-    sync(s);
-    if (hcol)  // K2c: exact resolution of 64-bit hash collisions
-      PO_LAUNCH(k_dict_fixup, grid_for(hcol, 128), 128, 0, s, t.arena, arena_end, t.offsets,
-                uint32_t(m), cap, hashes.get(), keys.get(), reps.get(), repoffs.get(),
-                collided.get(), hcol, slot_of_cell.get());
+    // K2c: exact resolution of 64-bit hash collisions (almost always no work)
+    PO_LAUNCH(k_dict_fixup, kSMs, 128, 0, s, t.arena, arena_end, t.offsets, uint32_t(m), cap,
+              hashes.get(), keys.get(), reps.get(), repoffs.get(), collided.get(), ncol.get(),
+              slot_of_cell.get());
   }
 
   timing_mark("dict", s);
@@ -1060,7 +1064,9 @@ void encode(const DeviceTable& t, int tok, int scoring, cudaStream_t s, Encoded&
   ek.item_col = d_col.get();
   ek.m = uint32_t(m);
   timing_mark("distinct", s);
-  {
+  if (!ordered) {  // identity only (dedup, FD checks): ids in compaction order
+    PO_LAUNCH(k_iota_pos, grid_for(D, 256), 256, 0, s, esc_pos.get(), D);
+  } else {
     // round 0 groups the distinct values by column index
     std::vector<uint32_t> cb32(m);
     for (uint32_t c = 0; c < m; ++c) cb32[c] = uint32_t(e.colbase[c]);

@@ -868,6 +868,19 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
     nodes[0].table = t;
   }
 
+  // whole-table fallback (ggr.hpp:379-381): its order comes from the
+  // dictionary stats alone, so its PHC runs on a side stream while the level
+  // loop below waits on its per-level synchronisations
+  std::unique_ptr<FallbackPhc> fb_async;
+  std::vector<int> fb_order;
+  if (!dist) {
+    std::vector<double> avg(m);
+    for (uint32_t c = 0; c < m; ++c)
+      avg[c] = static_cast<double>(e.total_len[c]) / static_cast<double>(ng);
+    fb_order = hitcount_order(ng, e.card, avg, cfg.stats_variant);
+    fb_async = std::make_unique<FallbackPhc>(e, fb_order, s);
+  }
+
   DevBuf<uint8_t> pack_dev;
   auto upload = [&](Pack& pk) -> uint8_t* {
     pack_dev.alloc(pk.host.size(), s);
@@ -1403,12 +1416,6 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
   RK.key_kind = d_kk.get();
   RK.key_bits = d_kb.get();
   timing_mark("layout", s);
-  // whole-table fallback order (ggr.hpp:379-381) from the dictionary stats;
-  // its PHC comes from prefix groups, its row sort only runs if it wins
-  std::vector<double> avg(m);
-  for (uint32_t c = 0; c < m; ++c)
-    avg[c] = static_cast<double>(e.total_len[c]) / static_cast<double>(ng);
-  std::vector<int> fb_order = hitcount_order(ng, e.card, avg, cfg.stats_variant);
   RefineJob leaf_job;
   leaf_job.n_items = uint32_t(n);
   leaf_job.d_grp_init = row_leaf.get();  // round 0: leaf index
@@ -1493,7 +1500,7 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
   timing_mark("emit_phc", s);
 
   // ---- whole-table fallback competition (ggr.hpp:379-387) ----
-  const uint64_t fb_phc = fixed_order_phc_device(e, fb_order, s);
+  const uint64_t fb_phc = fb_async->get();  // prefix-group PHC from the side stream
   timing_mark("fallback_phc", s);
   std::vector<int32_t> fo(fb_order.begin(), fb_order.end());
   auto d_fo = to_device(fo, s);

@@ -62,8 +62,10 @@ struct Encoded {
   std::vector<uint64_t> total_len;  // host, per column: sum of segment lengths (stats.hpp:38)
 };
 
+// ordered = false: ids are exact but in no particular order (equality-only
+// callers: dedup, FD checks) — the escaped-order rank sort is skipped.
 void encode(const DeviceTable& t, int tok, int scoring, cudaStream_t s, Encoded& e,
-            uint32_t hash_bits_debug = 64);
+            uint32_t hash_bits_debug = 64, bool ordered = true);
 
 // Segmented refinement sort (rank_sort / multikey_sort engine).
 // Items [0, n_items) start in groups whose ids are their final start
@@ -199,6 +201,21 @@ void sort_all_rows(const Encoded& e, const std::vector<int>& order, uint32_t* d_
 // (first request excluded, like the fallback's phc), computed from prefix
 // groups without materialising the sort.
 uint64_t fixed_order_phc_device(const Encoded& e, const std::vector<int>& order, cudaStream_t s);
+
+// The same PHC computed on a side stream, overlapping the caller's stream
+// (the GGR level loop): constructed once the dictionary is on the caller's
+// stream, get() waits for the result.
+class FallbackPhc {
+ public:
+  FallbackPhc(const Encoded& e, const std::vector<int>& order, cudaStream_t main);
+  ~FallbackPhc();
+  uint64_t get();
+
+ private:
+  void launch(const Encoded& e, const std::vector<int>& order, cudaStream_t s);
+  DevBuf<unsigned long long> acc_, keys_, ng_;
+  DevBuf<uint32_t> gid_;
+};
 
 class FixedOrderSort {
  public:

@@ -5,6 +5,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstdlib>
 #include <numeric>
 
 #include "internal.cuh"
@@ -183,6 +184,86 @@ __global__ void k_fb_depth(const uint32_t* vid, uint64_t n, uint32_t m, uint32_t
 }
 
 }  // namespace
+
+namespace {
+struct SideStream {
+  cudaStream_t s = nullptr;
+  cudaEvent_t ready = nullptr, done = nullptr;
+  unsigned long long* host = nullptr;  // pinned result slot
+  ~SideStream() {
+    if (s) cudaStreamDestroy(s);
+    if (ready) cudaEventDestroy(ready);
+    if (done) cudaEventDestroy(done);
+    if (host) cudaFreeHost(host);
+  }
+};
+thread_local SideStream g_side;
+}  // namespace
+
+FallbackPhc::FallbackPhc(const Encoded& e, const std::vector<int>& order, cudaStream_t main) {
+  SideStream& ss = g_side;
+  if (!ss.s) {
+    PO_CUDA(cudaStreamCreateWithFlags(&ss.s, cudaStreamNonBlocking));
+    PO_CUDA(cudaEventCreateWithFlags(&ss.ready, cudaEventDisableTiming));
+    PO_CUDA(cudaEventCreateWithFlags(&ss.done, cudaEventDisableTiming));
+    PO_CUDA(cudaMallocHost(reinterpret_cast<void**>(&ss.host), sizeof(unsigned long long)));
+  }
+  static const bool side = [] {
+    const char* v = std::getenv("PO_FB_SIDE");
+    return !(v && *v == '0');
+  }();
+  // the side stream starts once the dictionary (vid, count, vlen) is written
+  cudaStream_t st = side ? ss.s : main;
+  if (side) {
+    PO_CUDA(cudaEventRecord(ss.ready, main));
+    PO_CUDA(cudaStreamWaitEvent(ss.s, ss.ready, 0));
+  }
+  launch(e, order, st);
+  PO_CUDA(cudaMemcpyAsync(ss.host, acc_.get(), sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                          st));
+  PO_CUDA(cudaEventRecord(ss.done, st));
+}
+
+uint64_t FallbackPhc::get() {
+  PO_CUDA(cudaEventSynchronize(g_side.done));
+  return *g_side.host;
+}
+
+FallbackPhc::~FallbackPhc() {
+  if (g_side.done) cudaEventSynchronize(g_side.done);  // buffers are freed on the side stream
+}
+
+void FallbackPhc::launch(const Encoded& e, const std::vector<int>& order, cudaStream_t s) {
+  const uint64_t n = e.n;
+  const uint32_t m = e.m;
+  acc_.alloc(1, s);
+  acc_.zero();
+  if (n < 2 || order.empty()) return;
+  const std::vector<uint64_t>& colbase = e.colbase;
+  const int f0 = order[0];
+  PO_LAUNCH(k_fb_first, grid_for(e.card[f0], 256, 4), 256, 0, s, e.count.get() + colbase[f0],
+            e.vlen.get() + colbase[f0], uint64_t(e.card[f0]), acc_.get());
+  if (order.size() > 1 && e.card[f0] < n) {
+    uint64_t cap = 1;
+    while (cap < 2 * n) cap <<= 1;
+    if (cap > (1ull << 32)) fail(PO_ERR_SIZE, "table too large for the fallback group table");
+    gid_.alloc(n, s);
+    keys_.alloc(cap, s);
+    ng_.alloc(order.size(), s);
+    ng_.zero();
+    const unsigned long long c0 = e.card[f0];
+    h2d_async(ng_.get(), &c0, sizeof(c0), s);
+    PO_LAUNCH(k_fb_init, grid_for(n, 256), 256, 0, s, e.vid.get(), n, m, uint32_t(f0), gid_.get());
+    for (size_t p = 1; p < order.size(); ++p) {
+      const int f = order[p];
+      keys_.fill_bytes(0xFF);
+      PO_LAUNCH(k_fb_depth, grid_for(n, 256, 8), 256, 0, s, e.vid.get(), n, m, uint32_t(f),
+                e.vlen.get() + colbase[f], gid_.get(), keys_.get(), cap - 1, acc_.get(),
+                ng_.get() + (p - 1), ng_.get() + p);
+      if (e.card[f] == n) break;  // unique column: every group a singleton below
+    }
+  }
+}
 
 uint64_t fixed_order_phc_device(const Encoded& e, const std::vector<int>& order, cudaStream_t s) {
   const uint64_t n = e.n;
