@@ -178,6 +178,20 @@ int po_dedup(uint64_t n, const uint8_t* arena, const uint64_t* offsets, uint32_t
              uint64_t* out_expansion, uint64_t* out_unique_first, uint64_t* out_n_unique,
              void* stream);
 
+/* prefixopt::simulate (cache_sim.hpp:223-285) with EvictionPolicy::none
+ * (unbounded cache) over prompts arena[offsets[i] .. offsets[i+1]) (at
+ * `location`) and the char or word tokenizer. Host outputs per request (n
+ * slots each, any may be NULL): input tokens, credited hit (raw hit if >=
+ * min_cacheable_prefix_tokens, else 0), miss = input - hit, written =
+ * input - raw hit; out_totals[3] = total input, hit, miss. n == 0 ->
+ * PO_ERR_DOMAIN (the reference's "prompt list is empty"). LRU eviction is
+ * sequential by definition and has no GPU entry point. */
+int po_replay_unbounded(uint64_t n, const uint8_t* arena, const uint64_t* offsets,
+                        uint32_t location, int32_t tokenizer,
+                        uint64_t min_cacheable_prefix_tokens, uint64_t* out_input_tokens,
+                        uint64_t* out_hit_tokens, uint64_t* out_miss_tokens,
+                        uint64_t* out_written_tokens, uint64_t* out_totals, void* stream);
+
 /* ---- row-sharded solve over several GPUs ---------------
  * No reference counterpart: the reference ggr() (ggr.hpp:367-394) is one
  * process on one table. Here every rank (one per GPU) passes a contiguous

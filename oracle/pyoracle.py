@@ -214,3 +214,76 @@ def _render_dedup_oracle_methods():
 
 
 _render_dedup_oracle_methods()
+
+
+def _simulate_oracle_methods():
+    """simulate (cache_sim.hpp:223-285): the reference itself through the
+    shim (ref_simulate), and for kind="port" a brute-force restatement for
+    eviction none: raw hit = max over earlier prompts of the common token
+    prefix (what an unbounded trie returns)."""
+    from paper_2403_05821_b200.api import CacheConfig, RequestSim, SimReport
+    from paper_2403_05821_b200.errors import DomainError
+    from paper_2403_05821_b200.table import _to_bytes
+
+    WS = set(b" \t\n\r\f\v")
+
+    def tokens(p, kind):  # tokenizer.hpp:33-73
+        if kind == 0:
+            return list(p)
+        out, cur = [], bytearray()
+        for c in p:
+            if c in WS:
+                if cur:
+                    out.append(bytes(cur))
+                    cur = bytearray()
+            else:
+                cur.append(c)
+        if cur:
+            out.append(bytes(cur))
+        return out
+
+    def simulate(self, prompts, cfg=None, tok=None):
+        from paper_2403_05821_b200.api import char_tokenizer
+        cfg = cfg or CacheConfig()
+        tok = tok or char_tokenizer()
+        items = [_to_bytes(p) for p in prompts]
+        if not items:
+            raise DomainError("simulate: prompt list is empty")
+        if self.kind == "reference":
+            n = len(items)
+            offs = np.zeros(n + 1, np.uint64)
+            np.cumsum([len(x) for x in items], out=offs[1:])
+            arena = np.frombuffer(b"".join(items) or b"\0", np.uint8)
+            outs = [np.zeros(n, np.uint64) for _ in range(4)]
+            unc = np.zeros(n, np.uint8)
+            tot = np.zeros(4, np.uint64)
+            fn = _bind(C.CDLL(str(self.path)), "ref_simulate", C.c_int,
+                       [C.c_uint64, C.c_void_p, C.c_void_p, C.c_int32, C.c_uint64, C.c_int32,
+                        C.c_uint64] + [C.c_void_p] * 6)
+            self._check(fn(n, arena.ctypes.data, offs.ctypes.data, tok.kind, cfg.capacity_tokens,
+                           1 if cfg.eviction == "lru" else 0, cfg.min_cacheable_prefix_tokens,
+                           *(o.ctypes.data for o in outs), unc.ctypes.data, tot.ctypes.data))
+            reqs = [RequestSim(int(a), int(b), int(c), int(d), bool(u))
+                    for a, b, c, d, u in zip(*outs, unc)]
+            ti, th, tm, ev = (int(x) for x in tot)
+            return SimReport(reqs, ti, th, tm, ev, th / ti if ti else 0.0)
+        seqs = [tokens(p, tok.kind) for p in items]
+        reqs = []
+        for i, sq in enumerate(seqs):
+            raw = 0
+            for j in range(i):
+                o = seqs[j]
+                k = 0
+                while k < len(sq) and k < len(o) and sq[k] == o[k]:
+                    k += 1
+                raw = max(raw, k)
+            hit = raw if raw >= cfg.min_cacheable_prefix_tokens else 0
+            reqs.append(RequestSim(len(sq), hit, len(sq) - hit, len(sq) - raw))
+        ti = sum(r.input_tokens for r in reqs)
+        th = sum(r.hit_tokens for r in reqs)
+        return SimReport(reqs, ti, th, ti - th, 0, th / ti if ti else 0.0)
+
+    OracleLib.simulate = simulate
+
+
+_simulate_oracle_methods()

@@ -14,6 +14,7 @@
 #include <unordered_map>
 #include <vector>
 
+#include "prefixopt/cache_sim.hpp"
 #include "prefixopt/cost.hpp"
 #include "prefixopt/fd.hpp"
 #include "prefixopt/ggr.hpp"
@@ -309,6 +310,37 @@ int ref_dedup(uint64_t n, const uint8_t* arena, const uint64_t* offsets, uint64_
       }
     }
     *out_n_unique = d.uniques.size();
+  });
+}
+
+// prefixopt::simulate (cache_sim.hpp:223-285): eviction 0 = none, 1 = lru.
+int ref_simulate(uint64_t n, const uint8_t* arena, const uint64_t* offsets, int32_t tok,
+                 uint64_t capacity, int32_t eviction, uint64_t min_cacheable, uint64_t* out_input,
+                 uint64_t* out_hit, uint64_t* out_miss, uint64_t* out_written,
+                 uint8_t* out_uncacheable, uint64_t* out_totals) {
+  return guarded([&] {
+    std::vector<std::string> prompts;
+    for (uint64_t i = 0; i < n; ++i)
+      prompts.emplace_back(reinterpret_cast<const char*>(arena) + offsets[i],
+                           offsets[i + 1] - offsets[i]);
+    prefixopt::CacheConfig cfg;
+    cfg.capacity_tokens = capacity;
+    cfg.eviction = eviction ? prefixopt::EvictionPolicy::lru : prefixopt::EvictionPolicy::none;
+    cfg.min_cacheable_prefix_tokens = min_cacheable;
+    const prefixopt::Tokenizer& tk =
+        tok == PO_TOK_WORD ? prefixopt::word_tokenizer() : prefixopt::char_tokenizer();
+    const prefixopt::SimReport r = prefixopt::simulate(prompts, cfg, tk);
+    for (uint64_t i = 0; i < n; ++i) {
+      out_input[i] = r.requests[i].input_tokens;
+      out_hit[i] = r.requests[i].hit_tokens;
+      out_miss[i] = r.requests[i].miss_tokens;
+      out_written[i] = r.requests[i].written_tokens;
+      out_uncacheable[i] = r.requests[i].uncacheable ? 1 : 0;
+    }
+    out_totals[0] = r.total_input;
+    out_totals[1] = r.total_hit;
+    out_totals[2] = r.total_miss;
+    out_totals[3] = r.evicted_tokens;
   });
 }
 

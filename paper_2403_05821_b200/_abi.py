@@ -167,6 +167,9 @@ class CudaLib:
                                     [vp, C.c_uint64, vp, vp, vp, C.c_uint32, vp, C.c_uint64, vp,
                                      C.c_uint64, C.c_uint32, vp, vp, C.c_uint64, vp, vp])
         self.dedup = _bind(L, "po_dedup", C.c_int, [C.c_uint64, vp, vp, C.c_uint32, vp, vp, vp, vp])
+        self.replay_unbounded = _bind(L, "po_replay_unbounded", C.c_int,
+                                      [C.c_uint64, vp, vp, C.c_uint32, C.c_int32, C.c_uint64,
+                                       vp, vp, vp, vp, vp, vp])
         # row-sharded solve
         self.comm_unique_id = _bind(L, "po_comm_unique_id", C.c_int, [vp])
         self.comm_init_nccl = _bind(L, "po_comm_init_nccl", C.c_int,

@@ -597,6 +597,99 @@ def dedup(prompts) -> DedupResult:
     return DedupResult([items[int(i)] for i in uf[:int(nu.value)]], [int(x) for x in ex[:n]])
 
 
+# --------------------------------------------------------------------------
+# prefix-cache replay, unbounded cache (cache_sim.hpp:29-299)
+# --------------------------------------------------------------------------
+@dataclass
+class CacheConfig:
+    capacity_tokens: int = 0            # 0 = unbounded; ignored under eviction none
+    eviction: str = "none"              # "none" | "lru"
+    min_cacheable_prefix_tokens: int = 0
+
+
+@dataclass
+class RequestSim:
+    input_tokens: int = 0
+    hit_tokens: int = 0
+    miss_tokens: int = 0
+    written_tokens: int = 0
+    uncacheable: bool = False
+
+
+@dataclass
+class SimReport:
+    requests: list = field(default_factory=list)
+    total_input: int = 0
+    total_hit: int = 0
+    total_miss: int = 0
+    evicted_tokens: int = 0
+    phr: float = 0.0
+
+
+def _strings_arena(items):
+    n = len(items)
+    offs = np.zeros(n + 1, dtype=np.uint64)
+    if n:
+        np.cumsum([len(x) for x in items], out=offs[1:])
+    return np.frombuffer(b"".join(items) or b"\0", dtype=np.uint8), offs
+
+
+def simulate(prompts, cfg: CacheConfig | None = None, tok: Tokenizer = _CHAR) -> SimReport:
+    """prefixopt::simulate (cache_sim.hpp:223-285) for eviction none on the
+    GPU: raw hit = longest token prefix shared with any earlier prompt."""
+    cfg = cfg or CacheConfig()
+    items = [_to_bytes(p) for p in prompts]
+    if not items:
+        raise DomainError("simulate: prompt list is empty")
+    if cfg.eviction not in ("none", "lru"):
+        raise SchemaError(f"unknown eviction policy: {cfg.eviction} (expected 'none' or 'lru')")
+    if cfg.eviction == "lru":
+        if cfg.capacity_tokens == 0:
+            raise SchemaError("simulate: lru eviction needs a finite capacity "
+                              "(capacity 0 means unbounded, use eviction none)")
+        raise SchemaError("simulate: lru eviction replays strictly sequentially; only eviction "
+                          "none runs on the GPU")
+    if tok.kind not in (0, 1):
+        raise SchemaError("simulate: char or word tokenizer")
+    lib = cuda_lib()
+    n = len(items)
+    arena, offs = _strings_arena(items)
+    out = [np.zeros(n, dtype=np.uint64) for _ in range(4)]
+    tot = np.zeros(3, dtype=np.uint64)
+    lib.check(lib.replay_unbounded(n, arena.ctypes.data, offs.ctypes.data, PO_LOC_HOST, tok.kind,
+                                   int(cfg.min_cacheable_prefix_tokens), *(o.ctypes.data for o in out),
+                                   tot.ctypes.data, 0))
+    reqs = [RequestSim(int(a), int(b), int(c), int(d)) for a, b, c, d in zip(*out)]
+    ti, th, tm = (int(x) for x in tot)
+    return SimReport(reqs, ti, th, tm, 0, th / ti if ti else 0.0)
+
+
+def validate_schedule(s: RequestSchedule, t: Table) -> None:
+    """prefixopt::validate_schedule (objective.hpp:34-52)."""
+    n, m = t.row_count(), t.field_count()
+    seen = set()
+    for e in s.entries():
+        r, order = e.row_id, e.field_order
+        if r >= n:
+            raise SchemaError(f"schedule references row {r} outside table of {n} rows")
+        if r in seen:
+            raise SchemaError(f"schedule lists row {r} twice")
+        seen.add(r)
+        if any(f < 0 or f >= m for f in order):
+            raise SchemaError(f"schedule entry for row {r} names a field outside the schema")
+        if len(set(order)) != len(order):
+            raise SchemaError(f"schedule entry for row {r} repeats a field")
+
+
+def phr_for_schedule(s: RequestSchedule, t: Table, system_prompt: bytes = b"",
+                     question: bytes = b"", cfg: CacheConfig | None = None,
+                     tok: Tokenizer = _CHAR) -> SimReport:
+    """prefixopt::phr_for_schedule (cache_sim.hpp:290-299): render every entry
+    (GPU) and replay (GPU, eviction none)."""
+    validate_schedule(s, t)
+    return simulate(render_prompts(s, t, system_prompt, question), cfg, tok)
+
+
 # low-level entry for callers holding device buffers (bench.py, multi-GPU)
 def ggr_into(view: TableView, fd_groups: list, cfg: GgrConfig, tok_kind: int, scoring: int,
              out_location: int, out_rows, out_orders, stream: int = 0):
@@ -622,5 +715,6 @@ __all__ = [
     "fixed_order_by_stats", "original_order_schedule", "hitcount", "HitCountResult", "ggr_into",
     "PO_LOC_HOST", "PO_LOC_DEVICE", "FdWitness", "FdGroupReport", "FdValidationReport",
     "validate_fds", "discover_fds", "render_prompts", "render_prompts_arena", "DedupResult",
-    "dedup",
+    "dedup", "CacheConfig", "RequestSim", "SimReport", "simulate", "validate_schedule",
+    "phr_for_schedule",
 ]

@@ -535,6 +535,47 @@ int po_dedup(uint64_t n, const uint8_t* arena, const uint64_t* offsets, uint32_t
   });
 }
 
+int po_replay_unbounded(uint64_t n, const uint8_t* arena, const uint64_t* offsets, uint32_t loc,
+                        int32_t tok, uint64_t min_cacheable, uint64_t* out_input,
+                        uint64_t* out_hit, uint64_t* out_miss, uint64_t* out_written,
+                        uint64_t* out_totals, void* stream) {
+  return guarded([&] {
+    if (n == 0) fail(PO_ERR_DOMAIN, "simulate: prompt list is empty");
+    if (tok != PO_TOK_CHAR && tok != PO_TOK_WORD)
+      fail(PO_ERR_INVALID_ARG, "replay: char or word tokenizer");
+    if (!arena || !offsets) fail(PO_ERR_INVALID_ARG, "null argument");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    init_pool_once();
+    const char* name = "prompt";
+    const uint64_t name_len = 6;
+    po_table tv{n, 1u, loc, &name, &name_len, arena, offsets, nullptr};
+    DeviceTable dt;
+    make_device_table(&tv, PO_TOK_CHAR, s, dt);
+    DevBuf<uint64_t> in(n, s), raw(n, s);
+    replay_unbounded_device(dt, tok, in.get(), raw.get(), s);
+    std::vector<uint64_t> hin(n), hraw(n);
+    in.download(hin.data(), n);
+    raw.download(hraw.data(), n);
+    sync(s);
+    uint64_t ti = 0, th = 0, tm = 0;
+    for (uint64_t i = 0; i < n; ++i) {  // cache_sim.hpp:266-279
+      const uint64_t hit = hraw[i] >= min_cacheable ? hraw[i] : 0;
+      if (out_input) out_input[i] = hin[i];
+      if (out_hit) out_hit[i] = hit;
+      if (out_miss) out_miss[i] = hin[i] - hit;
+      if (out_written) out_written[i] = hin[i] - hraw[i];
+      ti += hin[i];
+      th += hit;
+      tm += hin[i] - hit;
+    }
+    if (out_totals) {
+      out_totals[0] = ti;
+      out_totals[1] = th;
+      out_totals[2] = tm;
+    }
+  });
+}
+
 int po_comm_unique_id(uint8_t* out_id128) {
   return guarded([&] {
     if (!out_id128) fail(PO_ERR_INVALID_ARG, "null id buffer");

@@ -76,7 +76,11 @@ void encode(const DeviceTable& t, int tok, int scoring, cudaStream_t s, Encoded&
 // out_pos[item] receives the item's final position. grp_max must bound every
 // group id of every round, i.e. the largest start position (n_items - 1).
 struct RefineKey {
-  int kind = 0;  // 0 = string (raw order), 1 = string (escaped order), 2 = row keys
+  // 0 = string (raw order), 1 = string (escaped order), 2 = row keys,
+  // 3 = u16 symbol streams (arena holds uint16 codes >= 2, offsets count
+  // symbols; end of stream = 1): token sequences of the word tokenizer
+  int kind = 0;
+  uint64_t skip = 0;  // string kinds: symbols [0, skip) are shared by every item
   // string keys
   const uint8_t* arena = nullptr;
   uint64_t arena_bytes = 0;
@@ -255,6 +259,12 @@ void render_prompts_device(const DeviceTable& t, uint64_t n_entries, const uint6
 // map and, per unique in first-occurrence order, its first index.
 void dedup_device(const DeviceTable& t, uint64_t* d_expansion, uint64_t* d_unique_first,
                   uint64_t& n_unique, cudaStream_t s);
+
+// simulate() under an unbounded cache (replay.cu, cache_sim.hpp:223-285):
+// per prompt of the one-column table pt, its input tokens and raw hit (the
+// longest token prefix shared with any earlier prompt); device outputs.
+void replay_unbounded_device(const DeviceTable& pt, int tok, uint64_t* d_input, uint64_t* d_raw,
+                             cudaStream_t s);
 
 // Row-sharded solving (shard.cu). Every rank holds a
 // contiguous range of the table's rows; value ids are global (escaped-order

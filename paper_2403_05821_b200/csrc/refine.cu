@@ -28,7 +28,7 @@ __constant__ uint16_t c_esc_code[257];  // byte -> code in escaped order; [256] 
 constexpr uint16_t kRawEnd = 1;  // raw codes: end = 1, byte b = b + 2
 
 __device__ __forceinline__ uint32_t end_code(const RefineKey& K) {
-  return K.kind == 0 ? kRawEnd : c_esc_code[256];
+  return K.kind == 1 ? c_esc_code[256] : kRawEnd;  // raw bytes / symbol streams: 1
 }
 
 // Symbols [base, base + nsym) of a string as 9-bit codes (the end marker at
@@ -43,13 +43,18 @@ __device__ __forceinline__ uint64_t string_chunk(const RefineKey& K, uint32_t it
   const uint64_t o0 = K.offsets[i];
   const uint64_t len = K.offsets[i + 1] - o0;
   const uint8_t* p = K.arena + o0;
+  const uint16_t* p16 = reinterpret_cast<const uint16_t*>(K.arena) + o0;
   uint64_t chunk = 0;
   for (uint32_t j = 0; j < nsym; ++j) {
-    const uint64_t pos = base + j;
+    const uint64_t pos = base + j + K.skip;
     uint32_t code;
     if (pos < len) {
-      const uint8_t b = p[pos];
-      code = K.kind == 0 ? uint32_t(b) + 2 : c_esc_code[b];
+      if (K.kind == 3) {
+        code = p16[pos];  // symbol streams hold their codes (>= 2)
+      } else {
+        const uint8_t b = p[pos];
+        code = K.kind == 0 ? uint32_t(b) + 2 : c_esc_code[b];
+      }
     } else {
       code = pos == len ? end_code(K) : 0;
     }

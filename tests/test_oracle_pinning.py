@@ -126,3 +126,30 @@ def test_render_known_answer():
     want = [b'SYS\nQ\n{"q\\"t": "a\\nb", "title": "Dune"}', b"SYS\nQ\n{}"]
     for kind in ("port",) + (("reference",) if available("reference") else ()):
         assert oracle(kind).render_prompts(s, t, b"SYS", b"Q") == want
+
+
+# ---- prefix-cache replay, eviction none (cache_sim.hpp:223-285) -----------
+def test_simulate_port_matches_reference():
+    if not available("reference"):
+        pytest.skip("oracle/_ref not built")
+    from paper_2403_05821_b200 import CacheConfig, char_tokenizer, word_tokenizer
+    rng = _random.Random(8)
+    P, R = oracle("port"), oracle("reference")
+    for _ in range(200):
+        alpha = rng.choice([b"ab", b"ab  \n", b"a b\tc\x0b", bytes(range(256))])
+        ps = [bytes(rng.choice(alpha) for _ in range(rng.randint(0, 14)))
+              for _ in range(rng.randint(1, 25))]
+        for tok in (char_tokenizer(), word_tokenizer()):
+            cfg = CacheConfig(min_cacheable_prefix_tokens=rng.choice([0, 1, 3, 6]))
+            assert P.simulate(ps, cfg, tok) == R.simulate(ps, cfg, tok)
+
+
+def test_simulate_known_answers():
+    # test_cache_sim.cpp:51-60: k identical prompts hit (k-1)/k of their tokens
+    from paper_2403_05821_b200 import word_tokenizer
+    for kind in ("port",) + (("reference",) if available("reference") else ()):
+        for k in (2, 3, 5, 8):
+            rep = oracle(kind).simulate([b"the same prompt body"] * k, None, word_tokenizer())
+            assert rep.phr == (k - 1) / k
+            assert rep.requests[0].hit_tokens == 0
+            assert all(r.hit_tokens == r.input_tokens for r in rep.requests[1:])
