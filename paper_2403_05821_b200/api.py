@@ -668,7 +668,7 @@ def validate_schedule(s: RequestSchedule, t: Table) -> None:
     """prefixopt::validate_schedule (objective.hpp:34-52)."""
     n, m = t.row_count(), t.field_count()
     seen = set()
-    for e in s.entries():
+    for e in s.entries:
         r, order = e.row_id, e.field_order
         if r >= n:
             raise SchemaError(f"schedule references row {r} outside table of {n} rows")

@@ -66,9 +66,10 @@ def test_ggr_schedule_c1_phr():
         prompts = po.render_prompts(sched, t, b"You are a critic.", b"Rate it:")
         for tok in TOKS:
             assert po.simulate(prompts, None, tok) == R.simulate(prompts, None, tok)
-    ggr_phr = po.phr_for_schedule(res.schedule, t, b"You are a critic.", b"Rate it:").phr
-    orig_phr = po.phr_for_schedule(orig, t, b"You are a critic.", b"Rate it:").phr
-    assert ggr_phr > orig_phr
+    # unbounded cache: total hits depend on the prompt set, not its order
+    # (every prompt's tokens end up in the trie exactly once)
+    got = po.phr_for_schedule(res.schedule, t, b"You are a critic.", b"Rate it:")
+    assert got == R.simulate(po.render_prompts(res.schedule, t, b"You are a critic.", b"Rate it:"))
 
 
 def test_errors():
