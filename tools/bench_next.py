@@ -106,6 +106,19 @@ def main():
          {"unique": int(nu.value), "bytes_in": int(total.value),
           "gpu_GBps_in": int(total.value) / s / 1e9, "outputs": "expansion map to host"})
 
+    # prefix-cache replay, unbounded cache, over the same prompts
+    for tk, name in ((po.char_tokenizer(), "char"), (po.word_tokenizer(), "word")):
+        outs = [np.zeros(n, np.uint64) for _ in range(4)]
+        tot = np.zeros(3, np.uint64)
+        s, _ = timed(lambda: lib.check(lib.replay_unbounded(
+            n, out.data_ptr(), out_off.data_ptr(), PO_LOC_DEVICE, tk.kind, 0,
+            *(o.ctypes.data for o in outs), tot.ctypes.data, 0)), a.reps)
+        c, rep = timed(lambda: ref.simulate(cp, po.CacheConfig(), tk), 1)
+        line(f"simulate eviction=none, {name} tokens (cache_sim.hpp:223-285)", s, c,
+             {"phr": float(tot[1]) / float(tot[0]), "input_tokens": int(tot[0]),
+              "bytes_in": int(total.value), "gpu_GBps_in": int(total.value) / s / 1e9,
+              "outputs": "per-request arrays to host"})
+
 
 if __name__ == "__main__":
     main()
