@@ -192,6 +192,22 @@ int po_replay_unbounded(uint64_t n, const uint8_t* arena, const uint64_t* offset
                         uint64_t* out_hit_tokens, uint64_t* out_miss_tokens,
                         uint64_t* out_written_tokens, uint64_t* out_totals, void* stream);
 
+/* prefixopt::load_csv (table.hpp:114-215): RFC-4180 text (at `location`)
+ * parsed on the GPU into a table; same errors as the reference
+ * (PO_ERR_STRUCTURAL: missing header row, unterminated quoted field, a line
+ * with the wrong number of cells; PO_ERR_SCHEMA: duplicate header field,
+ * empty field name). The handle owns the parsed table until po_csv_free. */
+typedef struct po_csv po_csv;
+int po_load_csv(const uint8_t* data, uint64_t len, uint32_t location, po_csv** out, void* stream);
+int po_csv_info(const po_csv* csv, uint64_t* out_rows, uint32_t* out_fields,
+                uint64_t* out_arena_bytes, uint64_t* out_names_bytes);
+/* arena (arena_bytes), offsets (rows*fields + 1, row-major) at out_location;
+ * names (names_bytes) and name_offsets (fields + 1) on the host. */
+int po_csv_copy(const po_csv* csv, uint32_t out_location, uint8_t* out_arena,
+                uint64_t* out_offsets, uint8_t* out_names, uint64_t* out_name_offsets,
+                void* stream);
+void po_csv_free(po_csv* csv);
+
 /* ---- row-sharded solve over several GPUs ---------------
  * No reference counterpart: the reference ggr() (ggr.hpp:367-394) is one
  * process on one table. Here every rank (one per GPU) passes a contiguous

@@ -287,3 +287,105 @@ def _simulate_oracle_methods():
 
 
 _simulate_oracle_methods()
+
+
+def _csv_oracle_methods():
+    """load_csv (table.hpp:114-215): the reference itself through the shim;
+    for kind="port" a restatement of detail::read_csv_record + load_csv."""
+    from paper_2403_05821_b200.errors import SchemaError, StructuralError
+    from paper_2403_05821_b200.table import Table
+
+    def read_record(d, i, line):
+        # table.hpp:117-178: returns (cells, i, line, blank, start_line) or None at EOF
+        if i >= len(d):
+            return None
+        cells, cell = [], bytearray()
+        quoted = any_quote = any_content = False
+        start = line
+        while True:
+            if i >= len(d):
+                if quoted:
+                    raise StructuralError(
+                        f"csv: unterminated quoted field starting near line {start}")
+                cells.append(bytes(cell))
+                return cells, i, line, (not any_quote and len(cells) == 1 and not cells[0]), start
+            ch = d[i]
+            i += 1
+            if quoted:
+                if ch == 0x22:
+                    if i < len(d) and d[i] == 0x22:
+                        cell.append(0x22)
+                        i += 1
+                    else:
+                        quoted = False
+                else:
+                    if ch == 0x0A:
+                        line += 1
+                    cell.append(ch)
+            elif ch == 0x22 and not cell and not any_content:
+                quoted = any_quote = any_content = True
+            elif ch == 0x2C:
+                cells.append(bytes(cell))
+                cell = bytearray()
+                any_content = False
+            elif ch == 0x0D or ch == 0x0A:
+                if ch == 0x0D and i < len(d) and d[i] == 0x0A:
+                    i += 1
+                line += 1
+                cells.append(bytes(cell))
+                return cells, i, line, (not any_quote and len(cells) == 1 and not cells[0]), start
+            else:
+                cell.append(ch)
+                any_content = True
+
+    def load_csv(self, data):
+        data = bytes(data)
+        if self.kind == "reference":
+            fn = _bind(C.CDLL(str(self.path)), "ref_load_csv", C.c_int,
+                       [C.c_void_p, C.c_uint64] + [C.c_void_p] * 8)
+            buf = np.frombuffer(data or b"\0", np.uint8)
+            rows, fields = C.c_uint64(0), C.c_uint32(0)
+            ab, nb = C.c_uint64(0), C.c_uint64(0)
+            args = (buf.ctypes.data, len(data), C.byref(rows), C.byref(fields), C.byref(ab),
+                    C.byref(nb))
+            self._check(fn(*args, None, None, None, None))
+            n, m = int(rows.value), int(fields.value)
+            arena = np.zeros(max(int(ab.value), 1), np.uint8)
+            offs = np.zeros(n * m + 1, np.uint64)
+            names = np.zeros(max(int(nb.value), 1), np.uint8)
+            noff = np.zeros(m + 1, np.uint64)
+            self._check(fn(*args, arena.ctypes.data, offs.ctypes.data, names.ctypes.data,
+                           noff.ctypes.data))
+            nb_ = names.tobytes()
+            return Table.from_arena([nb_[int(noff[f]):int(noff[f + 1])] for f in range(m)],
+                                    arena, offs, n)
+        first = read_record(data, 0, 1)
+        if first is None:
+            raise StructuralError("csv: missing header row")
+        header, i, line, _, _ = first
+        seen = set()
+        for nm in header:
+            if nm in seen:
+                raise SchemaError(f"csv: duplicate header field: {nm.decode('latin-1')}")
+            seen.add(nm)
+        rows = []
+        while True:
+            rec = read_record(data, i, line)
+            if rec is None:
+                break
+            cells, i, line, blank, start = rec
+            if blank and i >= len(data):
+                break
+            if len(cells) != len(header):
+                raise StructuralError(f"csv: line {start} has {len(cells)} cells, "
+                                      f"expected {len(header)}")
+            rows.append(cells)
+        for k, nm in enumerate(header):
+            if not nm:
+                raise SchemaError(f"field {k} has an empty name")
+        return Table(header, rows)
+
+    OracleLib.load_csv = load_csv
+
+
+_csv_oracle_methods()

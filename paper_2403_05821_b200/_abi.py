@@ -170,6 +170,11 @@ class CudaLib:
         self.replay_unbounded = _bind(L, "po_replay_unbounded", C.c_int,
                                       [C.c_uint64, vp, vp, C.c_uint32, C.c_int32, C.c_uint64,
                                        vp, vp, vp, vp, vp, vp])
+        self.load_csv = _bind(L, "po_load_csv", C.c_int, [vp, C.c_uint64, C.c_uint32,
+                                                          C.POINTER(vp), vp])
+        self.csv_info = _bind(L, "po_csv_info", C.c_int, [vp, vp, vp, vp, vp])
+        self.csv_copy = _bind(L, "po_csv_copy", C.c_int, [vp, C.c_uint32, vp, vp, vp, vp, vp])
+        self.csv_free = _bind(L, "po_csv_free", None, [vp])
         # row-sharded solve
         self.comm_unique_id = _bind(L, "po_comm_unique_id", C.c_int, [vp])
         self.comm_init_nccl = _bind(L, "po_comm_init_nccl", C.c_int,

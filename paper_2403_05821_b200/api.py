@@ -690,6 +690,39 @@ def phr_for_schedule(s: RequestSchedule, t: Table, system_prompt: bytes = b"",
     return simulate(render_prompts(s, t, system_prompt, question), cfg, tok)
 
 
+# --------------------------------------------------------------------------
+# CSV ingest (table.hpp:114-215)
+# --------------------------------------------------------------------------
+def load_csv(source) -> Table:
+    """prefixopt::load_csv on the GPU: `source` is the CSV text (bytes) or a
+    path. Same table and same errors as the reference."""
+    if isinstance(source, (bytes, bytearray, memoryview)):
+        data = bytes(source)
+    else:
+        with open(source, "rb") as fh:
+            data = fh.read()
+    lib = cuda_lib()
+    buf = np.frombuffer(data or b"\0", dtype=np.uint8)
+    h = C.c_void_p(0)
+    lib.check(lib.load_csv(buf.ctypes.data, len(data), PO_LOC_HOST, C.byref(h), 0))
+    try:
+        rows, fields = C.c_uint64(0), C.c_uint32(0)
+        ab, nb = C.c_uint64(0), C.c_uint64(0)
+        lib.check(lib.csv_info(h, C.byref(rows), C.byref(fields), C.byref(ab), C.byref(nb)))
+        n, m = int(rows.value), int(fields.value)
+        arena = np.empty(max(int(ab.value), 1), dtype=np.uint8)
+        offs = np.empty(n * m + 1, dtype=np.uint64)
+        names = np.empty(max(int(nb.value), 1), dtype=np.uint8)
+        noff = np.empty(m + 1, dtype=np.uint64)
+        lib.check(lib.csv_copy(h, PO_LOC_HOST, arena.ctypes.data, offs.ctypes.data,
+                               names.ctypes.data, noff.ctypes.data, 0))
+    finally:
+        lib.csv_free(h)
+    nb_ = names.tobytes()
+    field_names = [nb_[int(noff[f]):int(noff[f + 1])] for f in range(m)]
+    return Table.from_arena(field_names, arena, offs, n)
+
+
 # low-level entry for callers holding device buffers (bench.py, multi-GPU)
 def ggr_into(view: TableView, fd_groups: list, cfg: GgrConfig, tok_kind: int, scoring: int,
              out_location: int, out_rows, out_orders, stream: int = 0):
@@ -716,5 +749,5 @@ __all__ = [
     "PO_LOC_HOST", "PO_LOC_DEVICE", "FdWitness", "FdGroupReport", "FdValidationReport",
     "validate_fds", "discover_fds", "render_prompts", "render_prompts_arena", "DedupResult",
     "dedup", "CacheConfig", "RequestSim", "SimReport", "simulate", "validate_schedule",
-    "phr_for_schedule",
+    "phr_for_schedule", "load_csv",
 ]

@@ -9,6 +9,7 @@
 #include <memory>
 #include <mutex>
 #include <numeric>
+#include <unordered_set>
 
 #include "comm.cuh"
 #include "internal.cuh"
@@ -238,6 +239,14 @@ void prepare(const po_table* tv, int tok, int scoring, cudaStream_t s, Prepared&
   encode(p.t, tok, scoring, s, p.e, debug_hash_bits());
 }
 
+// offsets of the data cells of a parsed CSV (po_csv_copy)
+__global__ void k_csv_offsets(const uint64_t* cell_end, uint64_t first, uint64_t count,
+                              uint64_t base, uint64_t* out) {
+  for (uint64_t k = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; k <= count;
+       k += uint64_t(gridDim.x) * blockDim.x)
+    out[k] = (first + k == 0 ? 0 : cell_end[first + k - 1]) - base;
+}
+
 __global__ void k_u32_to_u64(const uint32_t* a, uint64_t n, uint64_t* b) {
   for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
        i += uint64_t(gridDim.x) * blockDim.x)
@@ -296,6 +305,17 @@ using namespace po;
 
 struct po_comm {
   std::unique_ptr<po::Comm> c;
+};
+
+struct po_csv {
+  uint64_t rows = 0;
+  uint32_t fields = 0;
+  uint64_t first_cell = 0;   // first data cell
+  uint64_t base = 0;         // arena offset of the first data byte
+  uint64_t data_bytes = 0;
+  std::string names;
+  std::vector<uint64_t> name_off;
+  po::CsvParsed parsed;
 };
 
 struct po_slice {
@@ -575,6 +595,122 @@ int po_replay_unbounded(uint64_t n, const uint8_t* arena, const uint64_t* offset
     }
   });
 }
+
+int po_load_csv(const uint8_t* data, uint64_t len, uint32_t loc, po_csv** out, void* stream) {
+  return guarded([&] {
+    if (!out || (len && !data)) fail(PO_ERR_INVALID_ARG, "null argument");
+    if (loc != PO_LOC_HOST && loc != PO_LOC_DEVICE) fail(PO_ERR_INVALID_ARG, "bad location");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    init_pool_once();
+    DevBuf<uint8_t> own;
+    const uint8_t* d = data;
+    if (loc == PO_LOC_HOST && len) {
+      own.alloc(len, s);
+      own.upload(data, len);
+      d = own.get();
+    }
+    auto c = std::make_unique<po_csv>();
+    CsvParsed& P = c->parsed;
+    load_csv_device(d, len, P, s);
+    const uint64_t R = P.n_records;
+    auto unterminated = [&](uint64_t r) {
+      fail(PO_ERR_STRUCTURAL, "csv: unterminated quoted field starting near line " +
+                                  std::to_string(P.rec_start_line[r]));
+    };
+    // load_csv's order of checks (table.hpp:190-214)
+    if (R == 0) fail(PO_ERR_STRUCTURAL, "csv: missing header row");
+    if (R == 1 && P.unterminated) unterminated(0);
+    const uint64_t H = P.rec_end_cell[0];
+    std::vector<uint64_t> hend(H);
+    P.cell_end.download(hend.data(), H);
+    uint64_t hbytes = H ? hend[H - 1] : 0;
+    std::string hb(hbytes, '\0');
+    if (hbytes) PO_CUDA(cudaMemcpyAsync(hb.data(), P.arena.get(), hbytes, cudaMemcpyDeviceToHost, s));
+    sync(s);
+    std::vector<std::string> names;
+    for (uint64_t i = 0; i < H; ++i) names.push_back(hb.substr(i ? hend[i - 1] : 0, hend[i] - (i ? hend[i - 1] : 0)));
+    {
+      std::unordered_set<std::string> seen;
+      for (const auto& nm : names)
+        if (!seen.insert(nm).second) fail(PO_ERR_SCHEMA, "csv: duplicate header field: " + nm);
+    }
+    uint64_t rows_end = R;  // records [1, rows_end) are data rows
+    for (uint64_t r = 1; r < R; ++r) {
+      const bool last = r + 1 == R;
+      if (last && P.unterminated) unterminated(r);
+      if (last && P.rec_blank[r]) {  // trailing blank line
+        rows_end = r;
+        break;
+      }
+      const uint64_t cells = P.rec_end_cell[r] - P.rec_end_cell[r - 1];
+      if (cells != H)
+        fail(PO_ERR_STRUCTURAL, "csv: line " + std::to_string(P.rec_start_line[r]) + " has " +
+                                    std::to_string(cells) + " cells, expected " + std::to_string(H));
+    }
+    for (uint64_t i = 0; i < H; ++i)  // Table's constructor (table.hpp:28-33)
+      if (names[i].empty())
+        fail(PO_ERR_SCHEMA, "field " + std::to_string(i) + " has an empty name");
+    if (H >= (uint64_t(1) << 31)) fail(PO_ERR_SIZE, "csv: too many fields");
+    c->fields = uint32_t(H);
+    c->rows = rows_end - 1;
+    c->first_cell = H;
+    c->base = hbytes;
+    uint64_t data_end = hbytes;
+    if (c->rows && H) {
+      const uint64_t last_cell = H + c->rows * H - 1;
+      PO_CUDA(cudaMemcpyAsync(&data_end, P.cell_end.get() + last_cell, 8, cudaMemcpyDeviceToHost, s));
+      sync(s);
+    }
+    c->data_bytes = data_end - hbytes;
+    c->name_off.assign(1, 0);
+    for (const auto& nm : names) {
+      c->names += nm;
+      c->name_off.push_back(c->names.size());
+    }
+    *out = c.release();
+  });
+}
+
+int po_csv_info(const po_csv* c, uint64_t* rows, uint32_t* fields, uint64_t* arena_bytes,
+                uint64_t* names_bytes) {
+  return guarded([&] {
+    if (!c) fail(PO_ERR_INVALID_ARG, "null csv");
+    if (rows) *rows = c->rows;
+    if (fields) *fields = c->fields;
+    if (arena_bytes) *arena_bytes = c->data_bytes;
+    if (names_bytes) *names_bytes = c->names.size();
+  });
+}
+
+int po_csv_copy(const po_csv* c, uint32_t loc, uint8_t* arena, uint64_t* offsets, uint8_t* names,
+                uint64_t* name_offsets, void* stream) {
+  return guarded([&] {
+    if (!c) fail(PO_ERR_INVALID_ARG, "null csv");
+    if (loc != PO_LOC_HOST && loc != PO_LOC_DEVICE) fail(PO_ERR_INVALID_ARG, "bad location");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const cudaMemcpyKind k = loc == PO_LOC_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+    const uint64_t cells = c->rows * c->fields;
+    if (arena && c->data_bytes)
+      PO_CUDA(cudaMemcpyAsync(arena, c->parsed.arena.get() + c->base, c->data_bytes, k, s));
+    if (offsets) {
+      DevBuf<uint64_t> tmp;
+      uint64_t* dst = offsets;
+      if (loc == PO_LOC_HOST) {
+        tmp.alloc(cells + 1, s);
+        dst = tmp.get();
+      }
+      PO_LAUNCH(k_csv_offsets, grid_for(cells + 1, 256), 256, 0, s, c->parsed.cell_end.get(),
+                c->first_cell, cells, c->base, dst);
+      if (loc == PO_LOC_HOST) tmp.download(offsets, cells + 1);
+    }
+    if (names && !c->names.empty()) std::memcpy(names, c->names.data(), c->names.size());
+    if (name_offsets)
+      std::memcpy(name_offsets, c->name_off.data(), c->name_off.size() * sizeof(uint64_t));
+    sync(s);
+  });
+}
+
+void po_csv_free(po_csv* c) { delete c; }
 
 int po_comm_unique_id(uint8_t* out_id128) {
   return guarded([&] {

@@ -266,6 +266,20 @@ void dedup_device(const DeviceTable& t, uint64_t* d_expansion, uint64_t* d_uniqu
 void replay_unbounded_device(const DeviceTable& pt, int tok, uint64_t* d_input, uint64_t* d_raw,
                              cudaStream_t s);
 
+// CSV ingest (csv.cu, table.hpp:114-215): every record's cells in file order.
+// Cell i = arena[cell_end[i-1] .. cell_end[i]) (cell_end[-1] = 0); record r =
+// cells [rec_end_cell[r-1], rec_end_cell[r]); rec_blank: an empty unquoted
+// line; unterminated: EOF inside quotes (the last record).
+struct CsvParsed {
+  uint64_t content_bytes = 0, n_cells = 0, n_records = 0;
+  bool unterminated = false;
+  DevBuf<uint8_t> arena;
+  DevBuf<uint64_t> cell_end;
+  std::vector<uint64_t> rec_end_cell, rec_start_line;
+  std::vector<uint8_t> rec_blank;
+};
+void load_csv_device(const uint8_t* d, uint64_t len, CsvParsed& out, cudaStream_t s);
+
 // Row-sharded solving (shard.cu). Every rank holds a
 // contiguous range of the table's rows; value ids are global (escaped-order
 // ranks over the whole table), the value-group tables are replicated (built

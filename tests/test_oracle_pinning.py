@@ -153,3 +153,20 @@ def test_simulate_known_answers():
             assert rep.phr == (k - 1) / k
             assert rep.requests[0].hit_tokens == 0
             assert all(r.hit_tokens == r.input_tokens for r in rep.requests[1:])
+
+
+# ---- CSV ingest (table.hpp:114-215) ----------------------------------------
+def test_csv_port_matches_reference():
+    if not available("reference"):
+        pytest.skip("oracle/_ref not built")
+    from csv_util import SOUPS, outcome, to_csv
+    rng = _random.Random(31)
+    P, R = oracle("port"), oracle("reference")
+    for _ in range(1500):
+        alpha = rng.choice(SOUPS)
+        d = bytes(rng.choice(alpha) for _ in range(rng.randint(0, 50)))
+        assert outcome(P.load_csv, d) == outcome(R.load_csv, d)
+    for _ in range(100):
+        t = _rt(rng, 12, 4, _ALPHA["esc"], max_len=5, min_len=0)
+        d = to_csv(t, rng.choice([b"\n", b"\r\n", b"\r"]))
+        assert outcome(P.load_csv, d) == outcome(R.load_csv, d)
