@@ -119,6 +119,24 @@ def main():
               "bytes_in": int(total.value), "gpu_GBps_in": int(total.value) / s / 1e9,
               "outputs": "per-request arrays to host"})
 
+    # CSV ingest: the table written as CSV, text resident in HBM
+    sys.path.insert(0, str(ROOT / "tests"))
+    from csv_util import to_csv
+    text = to_csv(t)
+    d_text = torch.from_numpy(np.frombuffer(text, np.uint8).copy()).cuda()
+    small_text = to_csv(small)
+
+    def csv_call():
+        h = C.c_void_p(0)
+        lib.check(lib.load_csv(d_text.data_ptr(), len(text), PO_LOC_DEVICE, C.byref(h), 0))
+        lib.csv_free(h)
+
+    s, _ = timed(csv_call, a.reps)
+    c, _ = timed(lambda: ref.load_csv(small_text), 1)
+    line("load_csv (table.hpp:114-215)", s, c,
+         {"bytes_in": len(text), "gpu_GBps_in": len(text) / s / 1e9,
+          "outputs": "parsed table in HBM (handle)"})
+
 
 if __name__ == "__main__":
     main()
