@@ -17,6 +17,7 @@
 namespace po {
 
 std::atomic<uint64_t> g_launches{0};
+thread_local uint64_t g_syncs = 0;
 std::atomic<int> g_profile{0};
 
 namespace {
@@ -104,7 +105,9 @@ void timing_report(const char* call) {
     agg[k] += v;
     tot += v;
   }
-  std::string line = "[po timing] " + std::string(call) + " total " + std::to_string(tot) + " ms:";
+  std::string line = "[po timing] " + std::string(call) + " total " + std::to_string(tot) +
+                     " ms, " + std::to_string(g_syncs) + " stream syncs:";
+  g_syncs = 0;
   for (auto& k : order)
     if (k != "<start") line += " " + k + "=" + std::to_string(agg[k]);
   line += "\n";

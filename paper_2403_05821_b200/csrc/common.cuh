@@ -145,7 +145,11 @@ DevBuf<T> to_device(const std::vector<T>& v, cudaStream_t s) {
   return d;
 }
 
-inline void sync(cudaStream_t s) { PO_CUDA(cudaStreamSynchronize(s)); }
+extern thread_local uint64_t g_syncs;  // host synchronisations of this thread (debug timing)
+inline void sync(cudaStream_t s) {
+  ++g_syncs;
+  PO_CUDA(cudaStreamSynchronize(s));
+}
 
 // Host wall-time breakdown of one call (PO_DEBUG_TIMING=1): synchronises the
 // stream at every mark, so it perturbs the timing it reports; debug only.

@@ -1001,7 +1001,13 @@ void encode(const DeviceTable& t, int tok, int scoring, cudaStream_t s, Encoded&
                 smem, s, t.arena, arena_end, t.offsets, cells, uint32_t(m), rows_per_tile, stage,
                 hmask, hashes.get());
     } else {
-      PO_LAUNCH(k_cell_hash_cols, grid_for(((n + 31) / 32) * 32, 256, 8), 256, 0, s, t.arena,
+      static const unsigned hb = [] {  // resident blocks per SM (experiment knob)
+        const char* v = std::getenv("PO_HASH_BLOCKS_PER_SM");
+        return v && *v ? unsigned(std::atoi(v)) : 0u;
+      }();
+      const unsigned g = hb ? std::min<unsigned>(grid_for(((n + 31) / 32) * 32, 256, 8), kSMs * hb)
+                            : grid_for(((n + 31) / 32) * 32, 256, 8);
+      PO_LAUNCH(k_cell_hash_cols, g, 256, 0, s, t.arena,
                 arena_end, t.offsets, n, uint32_t(m), hmask, hashes.get());
     }
     // K2a/K2b: probe + claim, then byte verification of every duplicate

@@ -89,28 +89,43 @@ __device__ __forceinline__ bool row_terminal(const RefineKey& K, uint32_t row, u
   return k + 1 >= K.leaf_nchunks[K.row_leaf[row]];
 }
 
-// Per-round layout of a string key: round 0 takes nsym0 symbols, later
-// rounds nsym each.
+// Per-round layout of a string key: two 64-bit words per round. Round 0:
+// word A = nsym0 symbols next to the group id, word B = the next nsym (7);
+// later rounds: A and B each nsym symbols (segments carry the group).
 struct StrRound {
   uint64_t base;
   uint32_t nsym;
 };
 __device__ __forceinline__ StrRound str_round(const RefineKey& K, uint32_t k) {
   if (k == 0) return {0, K.nsym0};
-  return {uint64_t(K.nsym0) + uint64_t(k - 1) * K.nsym, K.nsym};
+  return {uint64_t(K.nsym0) + uint64_t(K.nsym) + uint64_t(k - 1) * 2 * K.nsym, K.nsym};
+}
+__device__ __forceinline__ StrRound str_round_b(const RefineKey& K, uint32_t k) {
+  const StrRound a = str_round(K, k);
+  return {a.base + a.nsym, K.nsym};
 }
 
 __global__ void k_build_keys(const uint32_t* items, const uint32_t* grp, uint32_t A, uint32_t k,
-                             uint32_t shift, RefineKey K, uint64_t* keys) {
+                             uint32_t shift, RefineKey K, uint64_t* keys, uint64_t* keys_b) {
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < A; i += gridDim.x * blockDim.x) {
     uint64_t chunk;
     if (K.kind == 2) {
       chunk = row_chunk(K, items[i], k);
     } else {
-      const StrRound sr = str_round(K, k);
+      const StrRound sr = str_round(K, k), sb = str_round_b(K, k);
       chunk = string_chunk(K, items[i], sr.base, sr.nsym);
+      keys_b[i] = string_chunk(K, items[i], sb.base, sb.nsym);
     }
     keys[i] = shift < 64 ? ((uint64_t(grp[i]) << shift) | chunk) : chunk;
+  }
+}
+
+__global__ void k_gather_kv(const uint32_t* perm, uint32_t A, const uint64_t* k_in,
+                            const uint32_t* v_in, uint64_t* k_out, uint32_t* v_out) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < A; i += gridDim.x * blockDim.x) {
+    const uint32_t p = perm[i];
+    k_out[i] = k_in[p];
+    v_out[i] = v_in[p];
   }
 }
 
@@ -126,11 +141,12 @@ struct Marks {
   const uint64_t* keys;
   const uint8_t* flags;  // null: round 0
   uint32_t shift;
+  const uint64_t* keys_b;  // string rounds: the second key word (null: row keys)
   __device__ __forceinline__ uint2 operator()(uint32_t i) const {
     if (i == 0) return make_uint2(0, 0);
     const uint64_t a = keys[i], b = keys[i - 1];
     const bool gb = flags ? flags[i] != 0 : (shift < 64 && (a >> shift) != (b >> shift));
-    const bool rb = gb || a != b;
+    const bool rb = gb || a != b || (keys_b && keys_b[i] != keys_b[i - 1]);
     return make_uint2(gb ? i : 0, rb ? i : 0);
   }
 };
@@ -144,7 +160,8 @@ struct Max2 {
 // Resolved items get their final position; the others keep (new group start,
 // item) packed in one word for a single compaction. `start` maps round-0
 // group indices to start positions (null: the group id is the start).
-__global__ void k_resolve(const uint64_t* keys, const uint32_t* items, const uint2* starts,
+__global__ void k_resolve(const uint64_t* keys, const uint64_t* keys_b, const uint32_t* items,
+                          const uint2* starts,
                           uint32_t A, uint32_t k, uint32_t shift,
                           const uint32_t* start, const uint32_t* seg_grp, RefineKey K,
                           uint32_t* out_pos, uint8_t* keep, uint64_t* packed) {
@@ -164,7 +181,9 @@ __global__ void k_resolve(const uint64_t* keys, const uint32_t* items, const uin
     const bool next_head = i + 1 >= A || starts[i + 1].y == i + 1;
     bool term;
     if (K.kind == 2) term = row_terminal(K, item, k);
-    else term = string_terminal(K, keys[i] & cmask, str_round(K, k).nsym);
+    else
+      term = string_terminal(K, keys[i] & cmask, str_round(K, k).nsym) ||
+             string_terminal(K, keys_b[i], str_round_b(K, k).nsym);
     if ((run_head && next_head) || term) {
       out_pos[item] = pos;
       keep[i] = 0;
@@ -223,6 +242,9 @@ struct Job {
   DevBuf<uint32_t> items, items2, grp;
   DevBuf<uint2> starts;
   DevBuf<uint64_t> keys, keys2, pk, pk2;
+  // string kinds: second key word (by position, then sorted), gather scratch
+  DevBuf<uint64_t> kb, kb2, k1g;
+  DevBuf<uint32_t> perm1, perm2, pos_iota, itg;
   DevBuf<uint8_t> keep, tmp, segflags;
   DevBuf<uint32_t> seg_begin;
   uint32_t nseg = 0;
@@ -301,6 +323,16 @@ void refine_sort_multi(const std::vector<RefineJob>& specs, cudaStream_t s) {
     j->segflags.alloc(n, s);
     j->seg_begin.alloc(n + 1, s);
     PO_LAUNCH(k_iota, grid_for(n, 256), 256, 0, s, j->items.get(), n);
+    if (j->key.kind != 2) {
+      j->kb.alloc(n, s);
+      j->kb2.alloc(n, s);
+      j->k1g.alloc(n, s);
+      j->perm1.alloc(n, s);
+      j->perm2.alloc(n, s);
+      j->pos_iota.alloc(n, s);
+      j->itg.alloc(n, s);
+      PO_LAUNCH(k_iota, grid_for(n, 256), 256, 0, s, j->pos_iota.get(), n);
+    }
     PO_CUDA(cudaMemcpyAsync(j->grp.get(), sp.d_grp_init, n * sizeof(uint32_t),
                             cudaMemcpyDeviceToDevice, s));
     size_t sort_bytes = 0, scan_bytes = 0, sel_bytes = 0;
@@ -309,7 +341,7 @@ void refine_sort_multi(const std::vector<RefineJob>& specs, cudaStream_t s) {
                                             j->items.get(), j->items2.get(), n, 0, 64, s));
     {
       cub::TransformInputIterator<uint2, Marks, cub::CountingInputIterator<uint32_t>> mk(
-          cub::CountingInputIterator<uint32_t>(0), Marks{j->keys2.get(), nullptr, 0});
+          cub::CountingInputIterator<uint32_t>(0), Marks{j->keys2.get(), nullptr, 0, nullptr});
       PO_CUDA(cub::DeviceScan::InclusiveScan(nullptr, scan_bytes, mk, j->starts.get(), Max2(), n, s));
     }
     PO_CUDA(cub::DeviceSelect::Flagged(nullptr, sel_bytes, j->pk2.get(), j->keep.get(),
@@ -331,50 +363,59 @@ void refine_sort_multi(const std::vector<RefineJob>& specs, cudaStream_t s) {
       const bool seg = j.k > 0;  // rounds >= 1: segmented sort inside groups
       const uint32_t shift = seg ? 64u : j.shift0;
       const uint32_t* start = seg ? nullptr : j.spec.d_grp_start;
+      const bool two = j.key.kind != 2;  // string keys: two words per round
       PO_LAUNCH(k_build_keys, grid_for(A, 256), 256, 0, s, j.items.get(), j.grp.get(), A, j.k,
-                shift, j.key, j.keys.get());
+                shift, j.key, j.keys.get(), two ? j.kb.get() : nullptr);
       size_t b = j.tb;
-      if (!seg) {
-        ProfScope ps("cub_radix_sort", s);
-        PO_CUDA(cub::DeviceRadixSort::SortPairs(j.tmp.get(), b, j.keys.get(), j.keys2.get(),
-                                                j.items.get(), j.items2.get(), A, 0, j.end_bit0, s));
-      } else {
-        ProfScope ps("cub_segmented_sort", s);
-        if (std::getenv("PO_DEBUG_CHECKS")) {
-          std::vector<uint32_t> hs(j.nseg + 1);
-          PO_CUDA(cudaMemcpyAsync(hs.data(), j.seg_begin.get(), (j.nseg + 1) * 4,
-                                  cudaMemcpyDeviceToHost, s));
-          sync(s);
-          bool okk = hs[0] == 0 && hs[j.nseg] == A;
-          for (uint32_t z = 0; z < j.nseg; ++z) okk = okk && hs[z] < hs[z + 1];
-          if (!okk) {
-            fprintf(stderr, "[po debug] bad segments: job %zu round %u A=%u nseg=%u first=%u last=%u\n",
-                    q, j.k, A, j.nseg, hs[0], hs[j.nseg]);
-            for (uint32_t z = 0; z < std::min<uint32_t>(j.nseg, 8); ++z) fprintf(stderr, " %u", hs[z]);
-            fprintf(stderr, "\n");
-          }
+      // one stable sort pass over the active items: a radix sort in round 0,
+      // a segmented sort inside the unresolved groups later
+      auto sort_pass = [&](const uint64_t* kin, uint64_t* kout, const uint32_t* vin, uint32_t* vout,
+                           int end_bit) {
+        if (!seg) {
+          ProfScope ps("cub_radix_sort", s);
+          b = j.tb;
+          PO_CUDA(cub::DeviceRadixSort::SortPairs(j.tmp.get(), b, kin, kout, vin, vout, A, 0,
+                                                  end_bit, s));
+          return;
         }
+        ProfScope ps("cub_segmented_sort", s);
         size_t need = 0;
-        PO_CUDA(cub::DeviceSegmentedSort::StableSortPairs(
-            nullptr, need, j.keys.get(), j.keys2.get(), j.items.get(), j.items2.get(), int(A),
-            int(j.nseg), j.seg_begin.get(), j.seg_begin.get() + 1, s));
+        PO_CUDA(cub::DeviceSegmentedSort::StableSortPairs(nullptr, need, kin, kout, vin, vout,
+                                                          int(A), int(j.nseg), j.seg_begin.get(),
+                                                          j.seg_begin.get() + 1, s));
         if (need > j.seg_tb) {
           j.seg_tmp.alloc(need, s);
           j.seg_tb = need;
         }
-        PO_CUDA(cub::DeviceSegmentedSort::StableSortPairs(
-            j.seg_tmp.get(), need, j.keys.get(), j.keys2.get(), j.items.get(), j.items2.get(),
-            int(A), int(j.nseg), j.seg_begin.get(), j.seg_begin.get() + 1, s));
+        PO_CUDA(cub::DeviceSegmentedSort::StableSortPairs(j.seg_tmp.get(), need, kin, kout, vin,
+                                                          vout, int(A), int(j.nseg),
+                                                          j.seg_begin.get(), j.seg_begin.get() + 1,
+                                                          s));
+      };
+      if (two) {
+        // LSD over the two words: by word B, then stably by word A
+        sort_pass(j.kb.get(), j.kb2.get(), j.pos_iota.get(), j.perm1.get(), 64);
+        PO_LAUNCH(k_gather_kv, grid_for(A, 256), 256, 0, s, j.perm1.get(), A, j.keys.get(),
+                  j.items.get(), j.k1g.get(), j.itg.get());
+        sort_pass(j.k1g.get(), j.keys2.get(), j.pos_iota.get(), j.perm2.get(),
+                  seg ? 64 : j.end_bit0);
+        PO_LAUNCH(k_gather_kv, grid_for(A, 256), 256, 0, s, j.perm2.get(), A, j.kb2.get(),
+                  j.itg.get(), j.kb.get(), j.items2.get());
+      } else {
+        sort_pass(j.keys.get(), j.keys2.get(), j.items.get(), j.items2.get(),
+                  seg ? 64 : j.end_bit0);
       }
       {
         ProfScope ps("cub_scan", s);
         b = j.tb;
         cub::TransformInputIterator<uint2, Marks, cub::CountingInputIterator<uint32_t>> mk(
             cub::CountingInputIterator<uint32_t>(0),
-            Marks{j.keys2.get(), seg ? j.segflags.get() : nullptr, shift});
+            Marks{j.keys2.get(), seg ? j.segflags.get() : nullptr, shift,
+                  two ? j.kb.get() : nullptr});
         PO_CUDA(cub::DeviceScan::InclusiveScan(j.tmp.get(), b, mk, j.starts.get(), Max2(), A, s));
       }
-      PO_LAUNCH(k_resolve, grid_for(A, 256), 256, 0, s, j.keys2.get(), j.items2.get(),
+      PO_LAUNCH(k_resolve, grid_for(A, 256), 256, 0, s, j.keys2.get(), two ? j.kb.get() : nullptr,
+                j.items2.get(),
                 j.starts.get(), A, j.k, shift, start, seg ? j.grp.get() : nullptr,
                 j.key, j.spec.d_out_pos, j.keep.get(), j.pk2.get());
       {
