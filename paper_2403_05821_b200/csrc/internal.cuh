@@ -81,6 +81,7 @@ struct RefineKey {
   // symbols; end of stream = 1): token sequences of the word tokenizer
   int kind = 0;
   uint64_t skip = 0;  // string kinds: symbols [0, skip) are shared by every item
+  uint32_t* item_off = nullptr;  // string kinds (set by refine_sort): symbols consumed per item
   // string keys
   const uint8_t* arena = nullptr;
   uint64_t arena_bytes = 0;

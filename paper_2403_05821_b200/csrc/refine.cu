@@ -106,19 +106,105 @@ __device__ __forceinline__ StrRound str_round_b(const RefineKey& K, uint32_t k) 
 }
 
 __global__ void k_build_keys(const uint32_t* items, const uint32_t* grp, uint32_t A, uint32_t k,
-                             uint32_t shift, RefineKey K, uint64_t* keys, uint64_t* keys_b) {
+                             uint32_t shift, uint32_t nsym_a, RefineKey K, uint64_t* keys,
+                             uint64_t* keys_b) {
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < A; i += gridDim.x * blockDim.x) {
     uint64_t chunk;
     if (K.kind == 2) {
       chunk = row_chunk(K, items[i], k);
     } else {
-      const StrRound sr = str_round(K, k), sb = str_round_b(K, k);
-      chunk = string_chunk(K, items[i], sr.base, sr.nsym);
-      keys_b[i] = string_chunk(K, items[i], sb.base, sb.nsym);
+      // per-item offset: rounds consume 2 words, segments skip shared prefixes
+      const uint32_t na = nsym_a;
+      const uint64_t base = K.item_off[items[i]];
+      chunk = string_chunk(K, items[i], base, na);
+      keys_b[i] = string_chunk(K, items[i], base + na, K.nsym);
     }
     keys[i] = shift < 64 ? ((uint64_t(grp[i]) << shift) | chunk) : chunk;
   }
 }
+
+// String rounds: symbols consumed by the round for every item still active.
+__global__ void k_advance(const uint32_t* items, const int* count, uint32_t consumed,
+                          uint32_t* item_off) {
+  const uint32_t A = uint32_t(*count);
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < A; i += gridDim.x * blockDim.x)
+    item_off[items[i]] += consumed;
+}
+
+// Shared-prefix skip of the next round's segments: the symbols every member
+// shares with its segment's head (members share their offset), minimum per
+// segment. Long common prefixes then cost one round instead of one round per
+// 14 symbols.
+__device__ __forceinline__ uint64_t sym_lcp(const RefineKey& K, uint32_t a, uint32_t b,
+                                            uint64_t off) {
+  const uint64_t ia = uint64_t(K.item_cell_row[a]) * K.m + K.item_col[a];
+  const uint64_t ib = uint64_t(K.item_cell_row[b]) * K.m + K.item_col[b];
+  const uint64_t la = K.offsets[ia + 1] - K.offsets[ia], lb = K.offsets[ib + 1] - K.offsets[ib];
+  const uint64_t st = off + K.skip;
+  if (st >= la || st >= lb) return 0;
+  const uint64_t n = (la < lb ? la : lb) - st;  // symbols to compare
+  const uint32_t us = K.kind == 3 ? 2u : 1u;    // bytes per symbol
+  const uint8_t* pa = K.arena + (K.offsets[ia] + st) * us;
+  const uint8_t* pb = K.arena + (K.offsets[ib] + st) * us;
+  const uint8_t* lim = K.arena + K.arena_bytes;
+  const uint64_t nb = n * us;
+  for (uint64_t t = 0; t < nb; t += 8) {
+    const uint64_t d = mask_low_bytes(load8_unaligned(pa + t, lim) ^ load8_unaligned(pb + t, lim),
+                                      nb - t >= 8 ? 8u : uint32_t(nb - t));
+    if (d) return (t + uint64_t(__ffsll((long long)d) - 1) / 8) / us;
+  }
+  return n;
+}
+
+__global__ void k_skip_init(const uint8_t* flags, const int* count, uint32_t* seg_skip) {
+  const uint32_t A = uint32_t(*count);
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < A; i += gridDim.x * blockDim.x)
+    if (flags[i]) seg_skip[i] = 0xFFFFFFFFu;
+}
+
+__global__ void k_skip_lcp(const uint32_t* items, const uint32_t* head, const int* count,
+                           RefineKey K, uint32_t* seg_skip) {
+  const uint32_t A = uint32_t(*count);
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < A; i += gridDim.x * blockDim.x) {
+    const uint32_t h = head[i];
+    if (h == i) continue;
+    const uint64_t l = sym_lcp(K, items[i], items[h], K.item_off[items[i]]);
+    atomicMin(&seg_skip[h], uint32_t(l < 0xFFFFFFFEull ? l : 0xFFFFFFFEull));
+  }
+}
+
+__global__ void k_skip_apply(const uint32_t* items, const uint32_t* head, const int* count,
+                             const uint32_t* seg_skip, uint32_t* item_off) {
+  const uint32_t A = uint32_t(*count);
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < A; i += gridDim.x * blockDim.x) {
+    const uint32_t sk = seg_skip[head[i]];
+    if (sk != 0xFFFFFFFFu) item_off[items[i]] += sk;
+  }
+}
+
+bool seg_radix_rows() {  // experiment knob: row-key rounds by radix with segment prefix
+  static const bool on = [] {
+    const char* v = std::getenv("PO_SEGRADIX_ROWS");
+    return v && *v == '1';
+  }();
+  return on;
+}
+
+struct FlagU32 {
+  const uint8_t* flags;
+  __device__ __forceinline__ uint32_t operator()(uint32_t i) const { return flags[i]; }
+};
+__global__ void k_minus_one(uint32_t* a, uint32_t A) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < A; i += gridDim.x * blockDim.x) a[i] -= 1;
+}
+
+struct HeadOf {  // segment head position of active index i (max-scan input)
+  const uint8_t* flags;
+  __device__ __forceinline__ uint32_t operator()(uint32_t i) const { return flags[i] ? i : 0u; }
+};
+struct MaxU32 {
+  __device__ __forceinline__ uint32_t operator()(uint32_t a, uint32_t b) const { return a > b ? a : b; }
+};
 
 __global__ void k_gather_kv(const uint32_t* perm, uint32_t A, const uint64_t* k_in,
                             const uint32_t* v_in, uint64_t* k_out, uint32_t* v_out) {
@@ -162,7 +248,7 @@ struct Max2 {
 // group indices to start positions (null: the group id is the start).
 __global__ void k_resolve(const uint64_t* keys, const uint64_t* keys_b, const uint32_t* items,
                           const uint2* starts,
-                          uint32_t A, uint32_t k, uint32_t shift,
+                          uint32_t A, uint32_t k, uint32_t shift, uint32_t nsym_a,
                           const uint32_t* start, const uint32_t* seg_grp, RefineKey K,
                           uint32_t* out_pos, uint8_t* keep, uint64_t* packed) {
   const uint64_t cmask = shift >= 64 ? ~0ull : ((1ull << shift) - 1);
@@ -182,8 +268,8 @@ __global__ void k_resolve(const uint64_t* keys, const uint64_t* keys_b, const ui
     bool term;
     if (K.kind == 2) term = row_terminal(K, item, k);
     else
-      term = string_terminal(K, keys[i] & cmask, str_round(K, k).nsym) ||
-             string_terminal(K, keys_b[i], str_round_b(K, k).nsym);
+      term = string_terminal(K, keys[i] & cmask, nsym_a) ||
+             string_terminal(K, keys_b[i], K.nsym);
     if ((run_head && next_head) || term) {
       out_pos[item] = pos;
       keep[i] = 0;
@@ -244,7 +330,7 @@ struct Job {
   DevBuf<uint64_t> keys, keys2, pk, pk2;
   // string kinds: second key word (by position, then sorted), gather scratch
   DevBuf<uint64_t> kb, kb2, k1g;
-  DevBuf<uint32_t> perm1, perm2, pos_iota, itg;
+  DevBuf<uint32_t> perm1, perm2, pos_iota, itg, item_off, head, seg_skip, segidx;
   DevBuf<uint8_t> keep, tmp, segflags;
   DevBuf<uint32_t> seg_begin;
   uint32_t nseg = 0;
@@ -322,6 +408,7 @@ void refine_sort_multi(const std::vector<RefineJob>& specs, cudaStream_t s) {
     j->keep.alloc(n, s);
     j->segflags.alloc(n, s);
     j->seg_begin.alloc(n + 1, s);
+    j->segidx.alloc(n, s);
     PO_LAUNCH(k_iota, grid_for(n, 256), 256, 0, s, j->items.get(), n);
     if (j->key.kind != 2) {
       j->kb.alloc(n, s);
@@ -331,6 +418,11 @@ void refine_sort_multi(const std::vector<RefineJob>& specs, cudaStream_t s) {
       j->perm2.alloc(n, s);
       j->pos_iota.alloc(n, s);
       j->itg.alloc(n, s);
+      j->item_off.alloc(n, s);
+      j->item_off.zero();
+      j->head.alloc(n, s);
+      j->seg_skip.alloc(n, s);
+      j->key.item_off = j->item_off.get();
       PO_LAUNCH(k_iota, grid_for(n, 256), 256, 0, s, j->pos_iota.get(), n);
     }
     PO_CUDA(cudaMemcpyAsync(j->grp.get(), sp.d_grp_init, n * sizeof(uint32_t),
@@ -360,18 +452,49 @@ void refine_sort_multi(const std::vector<RefineJob>& specs, cudaStream_t s) {
       if (!j.A) continue;
       any = true;
       const uint32_t A = j.A;
-      const bool seg = j.k > 0;  // rounds >= 1: segmented sort inside groups
-      const uint32_t shift = seg ? 64u : j.shift0;
+      const bool seg = j.k > 0;  // rounds >= 1: sorts inside the unresolved groups
       const uint32_t* start = seg ? nullptr : j.spec.d_grp_start;
       const bool two = j.key.kind != 2;  // string keys: two words per round
-      PO_LAUNCH(k_build_keys, grid_for(A, 256), 256, 0, s, j.items.get(), j.grp.get(), A, j.k,
-                shift, j.key, j.keys.get(), two ? j.kb.get() : nullptr);
+      // Rounds >= 1: one global radix sort with the segment index in the high
+      // key bits (segments keep their positions) when the chunk still fits,
+      // else CUB's segmented sort.
+      uint32_t shift = seg ? 64u : j.shift0;
+      uint32_t nsym_a = seg ? j.key.nsym : j.key.nsym0;
+      bool segradix = false;
+      if (seg) {
+        const uint32_t sbits = uint32_t(bits_for(j.nseg ? j.nseg - 1 : 0));
+        if (two && (64 - sbits) / 9 >= 1) {
+          segradix = true;
+          shift = 64 - sbits;
+          nsym_a = std::min<uint32_t>(j.key.nsym, shift / 9);
+        } else if (!two && seg_radix_rows() &&
+                   sbits + (j.spec.row_chunk_bits ? j.spec.row_chunk_bits : 64) <= 64) {
+          segradix = true;
+          shift = 64 - sbits;
+        }
+        if (segradix) {  // segment index of every active position
+          ProfScope ps("cub_scan", s);
+          cub::TransformInputIterator<uint32_t, FlagU32, cub::CountingInputIterator<uint32_t>> fi(
+              cub::CountingInputIterator<uint32_t>(0), FlagU32{j.segflags.get()});
+          size_t hb = 0;
+          PO_CUDA(cub::DeviceScan::InclusiveSum(nullptr, hb, fi, j.segidx.get(), A, s));
+          if (hb > j.tb) {
+            j.tmp.alloc(hb, s);
+            j.tb = hb;
+          }
+          PO_CUDA(cub::DeviceScan::InclusiveSum(j.tmp.get(), hb, fi, j.segidx.get(), A, s));
+          PO_LAUNCH(k_minus_one, grid_for(A, 256), 256, 0, s, j.segidx.get(), A);
+        }
+      }
+      PO_LAUNCH(k_build_keys, grid_for(A, 256), 256, 0, s, j.items.get(),
+                segradix ? j.segidx.get() : j.grp.get(), A, j.k, shift, nsym_a, j.key,
+                j.keys.get(), two ? j.kb.get() : nullptr);
       size_t b = j.tb;
       // one stable sort pass over the active items: a radix sort in round 0,
       // a segmented sort inside the unresolved groups later
       auto sort_pass = [&](const uint64_t* kin, uint64_t* kout, const uint32_t* vin, uint32_t* vout,
                            int end_bit) {
-        if (!seg) {
+        if (!seg || segradix) {
           ProfScope ps("cub_radix_sort", s);
           b = j.tb;
           PO_CUDA(cub::DeviceRadixSort::SortPairs(j.tmp.get(), b, kin, kout, vin, vout, A, 0,
@@ -398,7 +521,7 @@ void refine_sort_multi(const std::vector<RefineJob>& specs, cudaStream_t s) {
         PO_LAUNCH(k_gather_kv, grid_for(A, 256), 256, 0, s, j.perm1.get(), A, j.keys.get(),
                   j.items.get(), j.k1g.get(), j.itg.get());
         sort_pass(j.k1g.get(), j.keys2.get(), j.pos_iota.get(), j.perm2.get(),
-                  seg ? 64 : j.end_bit0);
+                  seg ? 64 : j.end_bit0);  // segradix: the segment index is in the top bits
         PO_LAUNCH(k_gather_kv, grid_for(A, 256), 256, 0, s, j.perm2.get(), A, j.kb2.get(),
                   j.itg.get(), j.kb.get(), j.items2.get());
       } else {
@@ -416,7 +539,7 @@ void refine_sort_multi(const std::vector<RefineJob>& specs, cudaStream_t s) {
       }
       PO_LAUNCH(k_resolve, grid_for(A, 256), 256, 0, s, j.keys2.get(), two ? j.kb.get() : nullptr,
                 j.items2.get(),
-                j.starts.get(), A, j.k, shift, start, seg ? j.grp.get() : nullptr,
+                j.starts.get(), A, j.k, shift, nsym_a, start, seg ? j.grp.get() : nullptr,
                 j.key, j.spec.d_out_pos, j.keep.get(), j.pk2.get());
       {
         ProfScope ps("cub_select", s);
@@ -436,6 +559,30 @@ void refine_sort_multi(const std::vector<RefineJob>& specs, cudaStream_t s) {
       }
       PO_LAUNCH(k_seg_end, 1, 1, 0, s, j.seg_begin.get(), nsel.get() + 2 * q + 1,
                 nsel.get() + 2 * q);
+      if (two) {
+        // next round: advance past this round's symbols, then skip the
+        // prefix every member of a segment shares
+        const int* cnt = nsel.get() + 2 * q;
+        PO_LAUNCH(k_advance, grid_for(A, 256), 256, 0, s, j.items.get(), cnt,
+                  nsym_a + j.key.nsym, j.item_off.get());
+        {
+          ProfScope ps("cub_scan", s);
+          size_t hb = 0;
+          cub::TransformInputIterator<uint32_t, HeadOf, cub::CountingInputIterator<uint32_t>> hi(
+              cub::CountingInputIterator<uint32_t>(0), HeadOf{j.segflags.get()});
+          PO_CUDA(cub::DeviceScan::InclusiveScan(nullptr, hb, hi, j.head.get(), MaxU32(), A, s));
+          if (hb > j.tb) {
+            j.tmp.alloc(hb, s);
+            j.tb = hb;
+          }
+          PO_CUDA(cub::DeviceScan::InclusiveScan(j.tmp.get(), hb, hi, j.head.get(), MaxU32(), A, s));
+        }
+        PO_LAUNCH(k_skip_init, grid_for(A, 256), 256, 0, s, j.segflags.get(), cnt, j.seg_skip.get());
+        PO_LAUNCH(k_skip_lcp, grid_for(A, 256), 256, 0, s, j.items.get(), j.head.get(), cnt, j.key,
+                  j.seg_skip.get());
+        PO_LAUNCH(k_skip_apply, grid_for(A, 256), 256, 0, s, j.items.get(), j.head.get(), cnt,
+                  j.seg_skip.get(), j.item_off.get());
+      }
       ++j.k;
     }
     if (!any) break;
