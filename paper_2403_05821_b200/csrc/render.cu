@@ -54,7 +54,8 @@ struct Sched {
   const int32_t* fields;
 };
 
-__global__ void k_prompt_len(const uint8_t* __restrict__ arena, const uint64_t* __restrict__ offsets,
+__global__ void k_prompt_len(const uint8_t* __restrict__ arena, const uint8_t* arena_end,
+                             const uint64_t* __restrict__ offsets,
                              uint64_t n_rows, uint32_t m, Sched sc, uint64_t n_entries,
                              const uint64_t* __restrict__ name_esc_len, uint64_t prefix_len,
                              uint64_t* out_len, int* err) {
@@ -74,7 +75,11 @@ __global__ void k_prompt_len(const uint8_t* __restrict__ arena, const uint64_t* 
       const uint64_t c = r * m + f;
       const uint8_t* v = arena + offsets[c];
       const uint64_t len = offsets[c + 1] - offsets[c];
-      for (uint64_t j = lane; j < len; j += 32) tot += esc_len_b(v[j]);
+      for (uint64_t j = 8 * lane; j < len; j += 256) {  // 8 bytes per lane per step
+        const uint64_t w = load8_unaligned(v + j, arena_end);
+        const uint32_t nb = len - j >= 8 ? 8u : uint32_t(len - j);
+        for (uint32_t k = 0; k < nb; ++k) tot += esc_len_b(uint8_t(w >> (8 * k)));
+      }
       if (lane == 0) tot += (p > a ? 2 : 0) + 1 + name_esc_len[f] + 4 + 1;
     }
     for (int d = 16; d > 0; d >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, d);
@@ -82,20 +87,33 @@ __global__ void k_prompt_len(const uint8_t* __restrict__ arena, const uint64_t* 
   }
 }
 
-// warp-cooperative escaped copy of `len` bytes to dst; returns bytes written
+// warp-cooperative escaped copy of `len` bytes to dst; returns bytes
+// written. Each lane takes 8 bytes per step (256 per warp step): their
+// escaped sizes are summed, one warp prefix sum places every lane's output.
 __device__ __forceinline__ uint64_t warp_esc_copy(const uint8_t* src, uint64_t len, uint8_t* dst,
-                                                  uint32_t lane) {
+                                                  const uint8_t* src_end, uint32_t lane) {
   uint64_t pos = 0;
-  for (uint64_t base = 0; base < len; base += 32) {
-    const uint64_t j = base + lane;
-    const uint8_t c = j < len ? src[j] : 0;
-    const uint32_t el = j < len ? esc_len_b(c) : 0;
+  for (uint64_t base = 0; base < len; base += 256) {
+    const uint64_t j = base + 8 * lane;
+    const uint32_t nb = j < len ? (len - j >= 8 ? 8u : uint32_t(len - j)) : 0u;
+    const uint64_t w = nb ? load8_unaligned(src + j, src_end) : 0;
+    uint32_t el = 0;
+    for (uint32_t k = 0; k < nb; ++k) el += esc_len_b(uint8_t(w >> (8 * k)));
     uint32_t incl = el;
     for (int d = 1; d < 32; d <<= 1) {
       const uint32_t y = __shfl_up_sync(0xffffffffu, incl, d);
       if (int(lane) >= d) incl += y;
     }
-    if (j < len) esc_write(c, dst + pos + (incl - el));
+    uint8_t* o = dst + pos + (incl - el);
+    if (el == nb) {  // nothing to escape: plain bytes
+      for (uint32_t k = 0; k < nb; ++k) o[k] = uint8_t(w >> (8 * k));
+    } else {
+      for (uint32_t k = 0; k < nb; ++k) {
+        const uint8_t c = uint8_t(w >> (8 * k));
+        esc_write(c, o);
+        o += esc_len_b(c);
+      }
+    }
     pos += __shfl_sync(0xffffffffu, incl, 31);
   }
   return pos;
@@ -106,7 +124,8 @@ __device__ __forceinline__ void warp_copy(const uint8_t* src, uint64_t len, uint
   for (uint64_t j = lane; j < len; j += 32) dst[j] = src[j];
 }
 
-__global__ void k_prompt_write(const uint8_t* __restrict__ arena, const uint64_t* __restrict__ offsets,
+__global__ void k_prompt_write(const uint8_t* __restrict__ arena, const uint8_t* arena_end,
+                               const uint64_t* __restrict__ offsets,
                                uint32_t m, Sched sc, uint64_t n_entries,
                                const uint8_t* __restrict__ names_esc,
                                const uint64_t* __restrict__ name_off, const uint8_t* prefix,
@@ -140,7 +159,7 @@ __global__ void k_prompt_write(const uint8_t* __restrict__ arena, const uint64_t
       }
       w += 4;
       const uint64_t c = r * m + f;
-      w += warp_esc_copy(arena + offsets[c], offsets[c + 1] - offsets[c], o + w, lane);
+      w += warp_esc_copy(arena + offsets[c], offsets[c + 1] - offsets[c], o + w, arena_end, lane);
       if (lane == 0) o[w] = '"';
       ++w;
     }
@@ -231,7 +250,8 @@ void render_prompts_device(const DeviceTable& t, uint64_t n_entries, const uint6
   lens.zero();
   DevBuf<int> err(1, s);
   err.zero();
-  PO_LAUNCH(k_prompt_len, grid_for(n_entries * 32, 256), 256, 0, s, t.arena, t.offsets, t.n, m, sc,
+  PO_LAUNCH(k_prompt_len, grid_for(n_entries * 32, 256), 256, 0, s, t.arena,
+            t.arena + t.arena_bytes, t.offsets, t.n, m, sc,
             n_entries, d_name_len.get(), uint64_t(prefix.size()), lens.get(), err.get());
   size_t tb = 0;
   PO_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, lens.get(), out_off.get(), int64_t(n_entries + 1), s));
@@ -243,7 +263,8 @@ void render_prompts_device(const DeviceTable& t, uint64_t n_entries, const uint6
   sync(s);
   if (herr) fail(PO_ERR_OUT_OF_RANGE, "schedule references a row or field outside the table");
   out_bytes.alloc(std::max<uint64_t>(total, 1), s);
-  PO_LAUNCH(k_prompt_write, grid_for(n_entries * 32, 256), 256, 0, s, t.arena, t.offsets, m, sc,
+  PO_LAUNCH(k_prompt_write, grid_for(n_entries * 32, 256), 256, 0, s, t.arena,
+            t.arena + t.arena_bytes, t.offsets, m, sc,
             n_entries, d_names.get(), d_name_off.get(), d_prefix.get(), uint64_t(prefix.size()),
             out_off.get(), out_bytes.get());
 }
