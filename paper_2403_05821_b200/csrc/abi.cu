@@ -234,12 +234,15 @@ struct Prepared {
   Encoded e;
 };
 
-void prepare(const po_table* tv, int tok, int scoring, cudaStream_t s, Prepared& p) {
+// ordered = false for callers that only need value identity (phc, hit,
+// compute_stats): the escaped-order rank job is not started.
+void prepare(const po_table* tv, int tok, int scoring, cudaStream_t s, Prepared& p,
+             bool ordered = true) {
   check_modes(tok, scoring);
   init_pool_once();
   make_device_table(tv, tok, s, p.t);
   timing_mark("table_h2d", s);
-  encode(p.t, tok, scoring, s, p.e, debug_hash_bits());
+  encode(p.t, tok, scoring, s, p.e, debug_hash_bits(), ordered);
 }
 
 // offsets of the data cells of a parsed CSV (po_csv_copy)
@@ -283,7 +286,7 @@ uint64_t phc_call(const po_table* tv, int tok, int scoring, uint64_t n_entries,
   if (loc != PO_LOC_HOST && loc != PO_LOC_DEVICE) fail(PO_ERR_INVALID_ARG, "bad schedule location");
   if (n_entries && (!rows || !offs)) fail(PO_ERR_INVALID_ARG, "null schedule arrays");
   Prepared p;
-  prepare(tv, tok, scoring, s, p);
+  prepare(tv, tok, scoring, s, p, /*ordered=*/false);  // PHC needs identity only
   uint64_t nfields = 0;
   if (n_entries) {
     if (loc == PO_LOC_HOST) nfields = offs[n_entries];
@@ -437,7 +440,7 @@ int po_compute_stats(const po_table* t, int32_t tok, int32_t scoring, uint64_t* 
   return guarded([&] {
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     Prepared p;
-    prepare(t, tok, scoring, s, p);
+    prepare(t, tok, scoring, s, p, /*ordered=*/false);  // cardinality + lengths only
     for (uint32_t f = 0; f < p.e.m; ++f) {
       out_card[f] = p.e.card[f];
       out_total[f] = p.e.total_len[f];
