@@ -222,12 +222,18 @@ void check_modes(int tok, int scoring) {
     fail(PO_ERR_INVALID_ARG, "unknown scoring mode");
 }
 
+}  // namespace
+
+// PO_DEBUG_HASH_BITS=k keeps k bits of every cell hash (forces collisions:
+// tests of the exact dictionary), 64 otherwise.
 uint32_t debug_hash_bits() {
   const char* v = std::getenv("PO_DEBUG_HASH_BITS");
   if (!v || !*v) return 64;
   int b = std::atoi(v);
   return (b <= 0 || b > 64) ? 64u : uint32_t(b);
 }
+
+namespace {
 
 struct Prepared {
   DeviceTable t;

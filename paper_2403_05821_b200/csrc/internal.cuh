@@ -64,6 +64,8 @@ struct Encoded {
 
 // ordered = false: ids are exact but in no particular order (equality-only
 // callers: dedup, FD checks) — the escaped-order rank sort is skipped.
+uint32_t debug_hash_bits();  // PO_DEBUG_HASH_BITS (abi.cu)
+
 void encode(const DeviceTable& t, int tok, int scoring, cudaStream_t s, Encoded& e,
             uint32_t hash_bits_debug = 64, bool ordered = true);
 

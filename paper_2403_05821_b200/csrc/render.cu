@@ -275,7 +275,7 @@ void dedup_device(const DeviceTable& t, uint64_t* d_expansion, uint64_t* d_uniqu
   n_unique = 0;
   if (n == 0) return;
   Encoded e;
-  encode(t, PO_TOK_CHAR, PO_SCORE_VALUE, s, e, 64, /*ordered=*/false);
+  encode(t, PO_TOK_CHAR, PO_SCORE_VALUE, s, e, debug_hash_bits(), /*ordered=*/false);
   DevBuf<uint32_t> first(e.D, s), flag(n + 1, s), uex(n + 1, s);
   first.fill_bytes(0xFF);
   PO_LAUNCH(k_first_index, grid_for(n, 256), 256, 0, s, e.vid.get(), n, first.get());

@@ -937,7 +937,7 @@ void ggr_sharded(Comm& comm, const DeviceTable& t, int tok, int scoring,
     return;
   }
   Encoded L;
-  encode(t, tok, scoring, s, L);
+  encode(t, tok, scoring, s, L, debug_hash_bits());
   timing_mark("local_encode", s);
   DevBuf<uint32_t> icol(L.D, s);
   PO_LAUNCH(k_item_col, grid_for(L.D, 256), 256, 0, s, L.D, L.d_colbase.get(), m, icol.get());

@@ -57,3 +57,15 @@ def test_render_dedup_ggr_schedule_c1():
 def test_dedup_edge_cases():
     for prompts in ([], [b""], [b"", b""], [b"a", b"b", b"a", b"", b"b"], [bytes([0]) * 70] * 3):
         assert po.dedup(prompts) == oracle("port").dedup(prompts)
+
+
+def test_dedup_and_fd_with_hash_collisions(monkeypatch):
+    monkeypatch.setenv("PO_DEBUG_HASH_BITS", "3")
+    rng = random.Random(23)
+    P = oracle("port")
+    for _ in range(20):
+        ps = [bytes(rng.randrange(256) for _ in range(rng.randint(0, 6))) for _ in range(60)]
+        ps += [rng.choice(ps) for _ in range(30)]
+        assert po.dedup(ps) == P.dedup(ps)
+        t = random_table(rng, 40, 4, ALPHABETS["all"], max_len=4, min_len=0)
+        assert po.discover_fds(t, 1000) == P.discover_fds(t, 1000)

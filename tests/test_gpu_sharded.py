@@ -165,3 +165,13 @@ def test_nccl_transport_world1():
     res = run_sharded(t, 1, comms=[comm])
     assert_same(t, res, ref)
     comm.close()
+
+
+def test_sharded_hash_collisions(monkeypatch):
+    # 3-bit hashes: the local dictionaries must separate colliding values on
+    # their bytes; the global dictionary compares bytes at the owners anyway
+    monkeypatch.setenv("PO_DEBUG_HASH_BITS", "3")
+    rng = random.Random(17)
+    for _ in range(15):
+        t = random_table(rng, 50, 4, ALPHABETS["all"], max_len=5, min_len=0)
+        check(t, rng.choice([2, 3]), None, rng.choice([po.GgrConfig(), po.exact_config()]))
