@@ -56,13 +56,36 @@ struct TDesc {
 struct HTable {
   bool dense = false;
   uint64_t cap = 0;
-  DevBuf<unsigned long long> keys;
-  DevBuf<uint32_t> cnt;
-  DevBuf<unsigned long long> psum;
-  TDesc desc() const {
-    return TDesc{keys.get(), cnt.get(), psum.get(), cap, dense ? 1u : 0u, 0u};
-  }
+  unsigned long long* keys = nullptr;
+  uint32_t* cnt = nullptr;
+  unsigned long long* psum = nullptr;
+  std::shared_ptr<DevBuf<uint8_t>> mem;  // backing allocation (shared by a level's tables)
+  TDesc desc() const { return TDesc{keys, cnt, psum, cap, dense ? 1u : 0u, 0u}; }
 };
+
+// The hashed tables ts (cap set) carved out of ONE zeroed allocation: a
+// level's new tables cost one cudaMallocAsync and one memset instead of three
+// of each per table (host launch overhead between the level's syncs).
+void alloc_tables(const std::vector<HTable*>& ts, uint32_t K, cudaStream_t s) {
+  if (ts.empty()) return;
+  auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
+  size_t total = 0;
+  for (const HTable* t : ts) total += al(t->cap * 8) + al(t->cap * 4) + (K ? al(t->cap * K * 8) : 0);
+  auto mem = std::make_shared<DevBuf<uint8_t>>(total, s);
+  mem->zero();
+  uint8_t* p = mem->get();
+  for (HTable* t : ts) {
+    t->keys = reinterpret_cast<unsigned long long*>(p);
+    p += al(t->cap * 8);
+    t->cnt = reinterpret_cast<uint32_t*>(p);
+    p += al(t->cap * 4);
+    if (K) {
+      t->psum = reinterpret_cast<unsigned long long*>(p);
+      p += al(t->cap * K * 8);
+    }
+    t->mem = mem;
+  }
+}
 
 __device__ __forceinline__ uint64_t tkey_hash(unsigned long long k) { return fmix64(k); }
 
@@ -855,15 +878,16 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
     auto t = std::make_shared<HTable>();
     t->dense = true;
     t->cap = e.D;
-    t->cnt.alloc(e.D, s);
-    PO_CUDA(cudaMemcpyAsync(t->cnt.get(), e.count.get(), e.D * sizeof(uint32_t),
+    t->mem = std::make_shared<DevBuf<uint8_t>>(e.D * 4 + 256 + (K ? e.D * K * 8 : 0), s);
+    t->cnt = reinterpret_cast<uint32_t*>(t->mem->get());
+    if (K) t->psum = reinterpret_cast<unsigned long long*>(t->mem->get() + ((e.D * 4 + 255) & ~uint64_t(255)));
+    PO_CUDA(cudaMemcpyAsync(t->cnt, e.count.get(), e.D * sizeof(uint32_t),
                             cudaMemcpyDeviceToDevice, s));
     if (K) {
-      t->psum.alloc(e.D * K, s);
-      t->psum.zero();
+      PO_CUDA(cudaMemsetAsync(t->psum, 0, e.D * K * 8, s));
       PO_LAUNCH(k_root_psum, grid_for(n * m, 256), 256, 0, s, e.vid.get(), n, m, K, d_dpart.get(),
-                d_npart.get(), vlen, colbase, t->psum.get());
-      if (dist) dist->comm->allreduce(t->psum.get(), e.D * K, CDtype::U64, COp::Sum, s);
+                d_npart.get(), vlen, colbase, t->psum);
+      if (dist) dist->comm->allreduce(t->psum, e.D * K, CDtype::U64, COp::Sum, s);
     }
     nodes[0].table = t;
   }
@@ -1061,6 +1085,7 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
       SplitD d;
     };
     std::vector<SplitH> splits;
+    std::vector<HTable*> new_tables;  // block children's tables of this level
     for (uint32_t i = 0; i < nslots; ++i) {
       const int id = frontier[i];
       out.stats.candidates_examined += hn[i] + unique_groups[i];
@@ -1108,17 +1133,9 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
         uint64_t cap = 64;
         while (cap < bound + bound / 2) cap <<= 1;
         auto t = std::make_shared<HTable>();
-        t->cap = cap;
-        t->keys.alloc(cap, s);
-        t->keys.zero();
-        t->cnt.alloc(cap, s);
-        t->cnt.zero();
-        if (K) {
-          t->psum.alloc(cap * K, s);
-          t->psum.zero();
-        }
+        t->cap = cap;  // memory: alloc_tables after the level's decisions
         B.table = t;
-        d.tB = t->desc();
+        new_tables.push_back(t.get());
       }
       if (needR) {
         R.table = P.table;
@@ -1139,6 +1156,10 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
         else if (nodes[ch].kind == FALLBACK) pending.push_back(ch);
       }
     }
+
+    alloc_tables(new_tables, K, s);
+    for (SplitH& sh : splits)
+      if (nodes[sh.d.block_id].table) sh.d.tB = nodes[sh.d.block_id].table->desc();
 
     // ---- K6 split + K4 aggregation ----
     if (!splits.empty()) {
@@ -1208,14 +1229,7 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
           while (cap < bound + bound / 2) cap <<= 1;
           auto t = std::make_unique<HTable>();
           t->cap = cap;
-          t->keys.alloc(cap, s);
-          t->keys.zero();
-          t->cnt.alloc(cap, s);
-          t->cnt.zero();
-          if (K) {
-            t->psum.alloc(cap * K, s);
-            t->psum.zero();
-          }
+          alloc_tables({t.get()}, K, s);
           hsp2[j].tB = t->desc();
           priv[j] = std::move(t);
           max_entries += bound;
