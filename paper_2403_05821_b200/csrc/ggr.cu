@@ -905,12 +905,20 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
     fb_async = std::make_unique<FallbackPhc>(e, fb_order, s);
   }
 
+  // per-level scratch, grown only (stream order makes the reuse safe: a
+  // level's copies and kernels queue behind the previous level's kernels)
   DevBuf<uint8_t> pack_dev;
+  auto grow = [&](auto& buf, size_t n) {
+    if (buf.size() < n) buf.alloc(std::max(n, 2 * buf.size()), s);
+  };
   auto upload = [&](Pack& pk) -> uint8_t* {
-    pack_dev.alloc(pk.host.size(), s);
+    grow(pack_dev, pk.host.size());
     pack_dev.upload(pk.host.data(), pk.host.size());
     return pack_dev.get();
   };
+  DevBuf<Cand> partial;
+  DevBuf<unsigned long long> pcands;
+  DevBuf<uint8_t> res;
 
   // Leaf statistics -> stats-ranked field order of a fallback leaf
   // (ggr.hpp:319-338). hc/ht: per (leaf slot, column) distinct count and
@@ -981,11 +989,11 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
     const size_t o_work = pk.add(L.work), o_swo = pk.add(L.slot_work_off);
     const size_t o_sslots = pk.add(S.slots), o_smasks = pk.add(S.masks), o_swork = pk.add(S.work);
     uint8_t* dp = upload(pk);
-    DevBuf<Cand> partial(std::max<size_t>(1, L.work.size()), s);
-    DevBuf<unsigned long long> pcands(std::max<size_t>(1, L.work.size()), s);
+    grow(partial, std::max<size_t>(1, L.work.size()));
+    grow(pcands, std::max<size_t>(1, L.work.size()));
     // results: [best Cand x nslots][ncand u64 x nslots][card u64 x nleaf*m][tot u64 x nleaf*m]
     const size_t res_bytes = nslots * (sizeof(Cand) + 8) + 2 * nleaf * m * 8;
-    DevBuf<uint8_t> res(std::max<size_t>(16, res_bytes), s);
+    grow(res, std::max<size_t>(16, res_bytes));
     Cand* d_best = reinterpret_cast<Cand*>(res.get());
     auto* d_ncand = reinterpret_cast<unsigned long long*>(res.get() + nslots * sizeof(Cand));
     auto* d_card = d_ncand + nslots;
