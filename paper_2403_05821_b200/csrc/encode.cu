@@ -435,16 +435,6 @@ __global__ void __launch_bounds__(256) k_cell_hash_cols(
   }
 }
 
-__global__ void k_cell_hash_global(const uint8_t* __restrict__ arena, const uint8_t* arena_end,
-                                   const uint64_t* __restrict__ offsets, uint64_t total,
-                                   uint64_t hash_mask, unsigned long long* __restrict__ hashes) {
-  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < total;
-       i += uint64_t(gridDim.x) * blockDim.x) {
-    const uint64_t o0 = offsets[i];
-    const uint64_t h = hash_cell<false>(arena + o0, offsets[i + 1] - o0, arena_end) & hash_mask;
-    hashes[i] = h ? h : 1;
-  }
-}
 
 // ---------------------------------------------------------------------------
 // K2a probe: one thread per cell, full occupancy, no barriers. The first
@@ -639,11 +629,6 @@ __global__ void k_iota_pos(uint32_t* a, uint64_t n) {
     a[i] = uint32_t(i);
 }
 
-__global__ void k_occupied(const unsigned long long* keys, uint64_t cap, uint8_t* flags) {
-  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < cap;
-       i += uint64_t(gridDim.x) * blockDim.x)
-    flags[i] = keys[i] != 0;
-}
 
 __global__ void k_distinct_info(const uint32_t* col_sel, uint64_t cnt, uint64_t base, uint32_t c,
                                 uint64_t cap, const uint32_t* reps, uint32_t* sel_slot,
