@@ -892,18 +892,6 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
     nodes[0].table = t;
   }
 
-  // whole-table fallback (ggr.hpp:379-381): its order comes from the
-  // dictionary stats alone, so its PHC runs on a side stream while the level
-  // loop below waits on its per-level synchronisations
-  std::unique_ptr<FallbackPhc> fb_async;
-  std::vector<int> fb_order;
-  if (!dist) {
-    std::vector<double> avg(m);
-    for (uint32_t c = 0; c < m; ++c)
-      avg[c] = static_cast<double>(e.total_len[c]) / static_cast<double>(ng);
-    fb_order = hitcount_order(ng, e.card, avg, cfg.stats_variant);
-    fb_async = std::make_unique<FallbackPhc>(e, fb_order, s);
-  }
 
   // per-level scratch, grown only (stream order makes the reuse safe: a
   // level's copies and kernels queue behind the previous level's kernels)
@@ -1381,7 +1369,13 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
               d_leaf_off.get(), row_leaf.get(), grp.get());
     out.phc = dist_layout(*dist, e, row_leaf.get(), lk, s);
     timing_mark("dist_layout", s);
-    // whole-table fallback competition (ggr.hpp:379-387) from global stats
+    // whole-table fallback competition (ggr.hpp:379-387) from global stats;
+    // the bound uses the replicated counts, so every rank decides alike
+    if (fallback_cannot_win(e, out.phc, s)) {
+      timing_mark("dist_fallback_bound", s);
+      sync(s);
+      return;
+    }
     std::vector<double> avg(m);
     for (uint32_t c = 0; c < m; ++c)
       avg[c] = static_cast<double>(e.total_len[c]) / static_cast<double>(ng);
@@ -1522,7 +1516,15 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
   timing_mark("emit_phc", s);
 
   // ---- whole-table fallback competition (ggr.hpp:379-387) ----
-  const uint64_t fb_phc = fb_async->get();  // prefix-group PHC from the side stream
+  if (!debug_checks() && fallback_cannot_win(e, out.phc, s)) {
+    timing_mark("fallback_bound", s);
+    return;
+  }
+  std::vector<double> avg(m);
+  for (uint32_t c = 0; c < m; ++c)
+    avg[c] = static_cast<double>(e.total_len[c]) / static_cast<double>(ng);
+  const std::vector<int> fb_order = hitcount_order(ng, e.card, avg, cfg.stats_variant);
+  const uint64_t fb_phc = fixed_order_phc_device(e, fb_order, s);  // prefix groups, no sort
   timing_mark("fallback_phc", s);
   std::vector<int32_t> fo(fb_order.begin(), fb_order.end());
   auto d_fo = to_device(fo, s);

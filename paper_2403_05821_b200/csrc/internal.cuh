@@ -209,20 +209,9 @@ void sort_all_rows(const Encoded& e, const std::vector<int>& order, uint32_t* d_
 // groups without materialising the sort.
 uint64_t fixed_order_phc_device(const Encoded& e, const std::vector<int>& order, cudaStream_t s);
 
-// The same PHC computed on a side stream, overlapping the caller's stream
-// (the GGR level loop): constructed once the dictionary is on the caller's
-// stream, get() waits for the result.
-class FallbackPhc {
- public:
-  FallbackPhc(const Encoded& e, const std::vector<int>& order, cudaStream_t main);
-  ~FallbackPhc();
-  uint64_t get();
-
- private:
-  void launch(const Encoded& e, const std::vector<int>& order, cudaStream_t s);
-  DevBuf<unsigned long long> acc_, keys_, ng_;
-  DevBuf<uint32_t> gid_;
-};
+// True when the whole-table fallback's PHC provably cannot exceed `phc`
+// (an upper bound from the dictionary counts and lengths, phc.cu).
+bool fallback_cannot_win(const Encoded& e, uint64_t phc, cudaStream_t s);
 
 class FixedOrderSort {
  public:

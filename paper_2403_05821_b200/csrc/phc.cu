@@ -186,83 +186,39 @@ __global__ void k_fb_depth(const uint32_t* vid, uint64_t n, uint32_t m, uint32_t
 }  // namespace
 
 namespace {
-struct SideStream {
-  cudaStream_t s = nullptr;
-  cudaEvent_t ready = nullptr, done = nullptr;
-  unsigned long long* host = nullptr;  // pinned result slot
-  ~SideStream() {
-    if (s) cudaStreamDestroy(s);
-    if (ready) cudaEventDestroy(ready);
-    if (done) cudaEventDestroy(done);
-    if (host) cudaFreeHost(host);
+// sum over the distinct values of (count - 1) * len^2, in double
+__global__ void k_fb_bound(const uint32_t* __restrict__ count, const uint64_t* __restrict__ vlen,
+                           uint64_t D, double* out) {
+  double local = 0;
+  for (uint64_t d = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; d < D;
+       d += uint64_t(gridDim.x) * blockDim.x) {
+    const double l = double(vlen[d]);
+    local += double(count[d] - 1) * l * l;
   }
-};
-thread_local SideStream g_side;
+  typedef cub::BlockReduce<double, 256> BR;
+  __shared__ typename BR::TempStorage tmp;
+  const double b = BR(tmp).Sum(local);
+  if (threadIdx.x == 0 && b > 0) atomicAdd(out, b);
+}
 }  // namespace
 
-FallbackPhc::FallbackPhc(const Encoded& e, const std::vector<int>& order, cudaStream_t main) {
-  SideStream& ss = g_side;
-  if (!ss.s) {
-    PO_CUDA(cudaStreamCreateWithFlags(&ss.s, cudaStreamNonBlocking));
-    PO_CUDA(cudaEventCreateWithFlags(&ss.ready, cudaEventDisableTiming));
-    PO_CUDA(cudaEventCreateWithFlags(&ss.done, cudaEventDisableTiming));
-    PO_CUDA(cudaMallocHost(reinterpret_cast<void**>(&ss.host), sizeof(unsigned long long)));
-  }
-  static const bool side = [] {
-    const char* v = std::getenv("PO_FB_SIDE");
-    return !(v && *v == '0');
-  }();
-  // the side stream starts once the dictionary (vid, count, vlen) is written
-  cudaStream_t st = side ? ss.s : main;
-  if (side) {
-    PO_CUDA(cudaEventRecord(ss.ready, main));
-    PO_CUDA(cudaStreamWaitEvent(ss.s, ss.ready, 0));
-  }
-  launch(e, order, st);
-  PO_CUDA(cudaMemcpyAsync(ss.host, acc_.get(), sizeof(unsigned long long), cudaMemcpyDeviceToHost,
-                          st));
-  PO_CUDA(cudaEventRecord(ss.done, st));
-}
-
-uint64_t FallbackPhc::get() {
-  PO_CUDA(cudaEventSynchronize(g_side.done));
-  return *g_side.host;
-}
-
-FallbackPhc::~FallbackPhc() {
-  if (g_side.done) cudaEventSynchronize(g_side.done);  // buffers are freed on the side stream
-}
-
-void FallbackPhc::launch(const Encoded& e, const std::vector<int>& order, cudaStream_t s) {
-  const uint64_t n = e.n;
-  const uint32_t m = e.m;
-  acc_.alloc(1, s);
-  acc_.zero();
-  if (n < 2 || order.empty()) return;
-  const std::vector<uint64_t>& colbase = e.colbase;
-  const int f0 = order[0];
-  PO_LAUNCH(k_fb_first, grid_for(e.card[f0], 256, 4), 256, 0, s, e.count.get() + colbase[f0],
-            e.vlen.get() + colbase[f0], uint64_t(e.card[f0]), acc_.get());
-  if (order.size() > 1 && e.card[f0] < n) {
-    uint64_t cap = 1;
-    while (cap < 2 * n) cap <<= 1;
-    if (cap > (1ull << 32)) fail(PO_ERR_SIZE, "table too large for the fallback group table");
-    gid_.alloc(n, s);
-    keys_.alloc(cap, s);
-    ng_.alloc(order.size(), s);
-    ng_.zero();
-    const unsigned long long c0 = e.card[f0];
-    h2d_async(ng_.get(), &c0, sizeof(c0), s);
-    PO_LAUNCH(k_fb_init, grid_for(n, 256), 256, 0, s, e.vid.get(), n, m, uint32_t(f0), gid_.get());
-    for (size_t p = 1; p < order.size(); ++p) {
-      const int f = order[p];
-      keys_.fill_bytes(0xFF);
-      PO_LAUNCH(k_fb_depth, grid_for(n, 256, 8), 256, 0, s, e.vid.get(), n, m, uint32_t(f),
-                e.vlen.get() + colbase[f], gid_.get(), keys_.get(), cap - 1, acc_.get(),
-                ng_.get() + (p - 1), ng_.get() + p);
-      if (e.card[f] == n) break;  // unique column: every group a singleton below
-    }
-  }
+// The whole-table fallback's PHC is at most sum_f sum_v (count(v) - 1) *
+// len(v)^2: at every prefix depth the pairs hitting field f inside groups
+// whose last value is v number at most count(v) - 1. When that bound is below
+// 2^64 (no wraparound) and not above the recursion's PHC, the fallback cannot
+// be strictly better (ggr.hpp:383) and its PHC / sort are skipped. Every term
+// is computed in double; the relative error of the sum is below 1e-9.
+bool fallback_cannot_win(const Encoded& e, uint64_t phc, cudaStream_t s) {
+  if (e.D == 0) return true;
+  DevBuf<double> acc(1, s);
+  acc.zero();
+  PO_LAUNCH(k_fb_bound, grid_for(e.D, 256, 4), 256, 0, s, e.count.get(), e.vlen.get(), e.D,
+            acc.get());
+  double ub = 0;
+  acc.download(&ub, 1);
+  sync(s);
+  const double ub_hi = ub * (1.0 + 1e-9) + 1.0;
+  return ub_hi < 1.8e19 && ub_hi < double(phc) * (1.0 - 1e-15);
 }
 
 uint64_t fixed_order_phc_device(const Encoded& e, const std::vector<int>& order, cudaStream_t s) {
