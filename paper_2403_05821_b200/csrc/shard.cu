@@ -184,11 +184,15 @@ __global__ void k_pack_values(uint64_t D, const uint32_t* ord, LocalDict d, cons
     d.str(i, p, len);
     if (lane == 0) meta[k] = make_uint2(d.icol[i], uint32_t(len));
     uint8_t* dst = bytes + boff[k];
-    for (uint64_t t = 8 * lane; t < len; t += 256) {  // 8 bytes per lane per step
-      const uint64_t w = load8_unaligned(p + t, lim);
-      const uint32_t nb = len - t >= 8 ? 8u : uint32_t(len - t);
-      for (uint32_t b = 0; b < nb; ++b) dst[t + b] = uint8_t(w >> (8 * b));
-    }
+    // aligned 8-byte stores for the destination words fully inside the value
+    // (other values share the edge words: bytes there)
+    const uintptr_t da = reinterpret_cast<uintptr_t>(dst);
+    const uint64_t head = std::min<uint64_t>(len, (8 - (da & 7)) & 7);
+    const uint64_t body = (len - head) & ~uint64_t(7);
+    if (lane < head) dst[lane] = p[lane];
+    uint64_t* dw = reinterpret_cast<uint64_t*>(dst + head);
+    for (uint64_t t = 8 * lane; t < body; t += 256) dw[t >> 3] = load8_unaligned(p + head + t, lim);
+    for (uint64_t t = head + body + lane; t < len; t += 32) dst[t] = p[t];
   }
 }
 
