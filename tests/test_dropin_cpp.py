@@ -7,7 +7,8 @@ from pathlib import Path
 import pytest
 
 BIN = Path(__file__).resolve().parent.parent / "proj" / "tests" / "bin"
-TESTS = ["test_objective", "test_solver_greedy", "test_solver_exact", "acceptance"]
+TESTS = ["test_objective", "test_solver_greedy", "test_solver_exact", "acceptance",
+         "test_b200_ext"]
 
 
 @pytest.mark.gpu
