@@ -78,17 +78,22 @@ thread_local std::vector<std::pair<std::string, double>> g_marks;
 thread_local std::chrono::steady_clock::time_point g_mark_t0;
 }  // namespace
 
-bool debug_timing() {
-  static const bool on = [] {
+// PO_DEBUG_TIMING=1: phase times with a stream sync at every mark (GPU time
+// per phase); PO_DEBUG_TIMING=host: host timestamps only, no syncs (where the
+// host thread itself waits).
+int timing_mode() {
+  static const int mode = [] {
     const char* v = std::getenv("PO_DEBUG_TIMING");
-    return v && *v && *v != '0';
+    if (!v || !*v || *v == '0') return 0;
+    return std::string(v) == "host" ? 2 : 1;
   }();
-  return on;
+  return mode;
 }
+bool debug_timing() { return timing_mode() != 0; }
 
 void timing_mark(const char* phase, cudaStream_t s) {
   if (!debug_timing()) return;
-  sync(s);
+  if (timing_mode() == 1) sync(s);
   auto now = std::chrono::steady_clock::now();
   if (!g_marks.empty() || phase[0] == '<')
     g_marks.push_back({phase, std::chrono::duration<double, std::milli>(now - g_mark_t0).count()});

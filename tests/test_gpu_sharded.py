@@ -175,3 +175,9 @@ def test_sharded_hash_collisions(monkeypatch):
     for _ in range(15):
         t = random_table(rng, 50, 4, ALPHABETS["all"], max_len=5, min_len=0)
         check(t, rng.choice([2, 3]), None, rng.choice([po.GgrConfig(), po.exact_config()]))
+
+
+def test_c2_full_sharded_8():
+    # the bench's largest world size, one full C2 table split 8 ways
+    t = gen.generate(2)
+    check(t, 8)
