@@ -117,7 +117,7 @@ __global__ void k_build_keys(const uint32_t* items, const uint32_t* grp, uint32_
       const uint32_t na = nsym_a;
       const uint64_t base = K.item_off[items[i]];
       chunk = string_chunk(K, items[i], base, na);
-      keys_b[i] = string_chunk(K, items[i], base + na, K.nsym);
+      if (keys_b) keys_b[i] = string_chunk(K, items[i], base + na, K.nsym);
     }
     keys[i] = shift < 64 ? ((uint64_t(grp[i]) << shift) | chunk) : chunk;
   }
@@ -180,6 +180,14 @@ __global__ void k_skip_apply(const uint32_t* items, const uint32_t* head, const 
     const uint32_t sk = seg_skip[head[i]];
     if (sk != 0xFFFFFFFFu) item_off[items[i]] += sk;
   }
+}
+
+bool two_words_round0() {  // experiment knob: two key words in round 0 too
+  static const bool on = [] {
+    const char* v = std::getenv("PO_TWO_WORDS_ROUND0");
+    return !(v && *v == '0');
+  }();
+  return on;
 }
 
 bool seg_radix_rows() {  // experiment knob: row-key rounds by radix with segment prefix
@@ -269,7 +277,7 @@ __global__ void k_resolve(const uint64_t* keys, const uint64_t* keys_b, const ui
     if (K.kind == 2) term = row_terminal(K, item, k);
     else
       term = string_terminal(K, keys[i] & cmask, nsym_a) ||
-             string_terminal(K, keys_b[i], K.nsym);
+             (keys_b && string_terminal(K, keys_b[i], K.nsym));
     if ((run_head && next_head) || term) {
       out_pos[item] = pos;
       keep[i] = 0;
@@ -454,7 +462,10 @@ void refine_sort_multi(const std::vector<RefineJob>& specs, cudaStream_t s) {
       const uint32_t A = j.A;
       const bool seg = j.k > 0;  // rounds >= 1: sorts inside the unresolved groups
       const uint32_t* start = seg ? nullptr : j.spec.d_grp_start;
-      const bool two = j.key.kind != 2;  // string keys: two words per round
+      const bool strk = j.key.kind != 2;  // string keys
+      // two key words per round (LSD) — in round 0 only when asked: there the
+      // extra pass covers every item, later rounds only the unresolved ones
+      const bool two = strk && (seg || two_words_round0());
       // Rounds >= 1: one global radix sort with the segment index in the high
       // key bits (segments keep their positions) when the chunk still fits,
       // else CUB's segmented sort.
@@ -559,12 +570,12 @@ void refine_sort_multi(const std::vector<RefineJob>& specs, cudaStream_t s) {
       }
       PO_LAUNCH(k_seg_end, 1, 1, 0, s, j.seg_begin.get(), nsel.get() + 2 * q + 1,
                 nsel.get() + 2 * q);
-      if (two) {
+      if (strk) {
         // next round: advance past this round's symbols, then skip the
         // prefix every member of a segment shares
         const int* cnt = nsel.get() + 2 * q;
         PO_LAUNCH(k_advance, grid_for(A, 256), 256, 0, s, j.items.get(), cnt,
-                  nsym_a + j.key.nsym, j.item_off.get());
+                  nsym_a + (two ? j.key.nsym : 0), j.item_off.get());
         {
           ProfScope ps("cub_scan", s);
           size_t hb = 0;
