@@ -247,13 +247,22 @@ struct Prepared {
 
 // ordered = false for callers that only need value identity (phc, hit,
 // compute_stats): the escaped-order rank job is not started.
+// Unique columns stay unranked (Encoded::unranked) unless PO_RANK_UNIQUE=1.
+bool rank_unique_columns() {
+  static const bool on = [] {
+    const char* v = std::getenv("PO_RANK_UNIQUE");
+    return v && *v == '1';
+  }();
+  return on;
+}
+
 void prepare(const po_table* tv, int tok, int scoring, cudaStream_t s, Prepared& p,
              bool ordered = true) {
   check_modes(tok, scoring);
   init_pool_once();
   make_device_table(tv, tok, s, p.t);
   timing_mark("table_h2d", s);
-  encode(p.t, tok, scoring, s, p.e, debug_hash_bits(), ordered);
+  encode(p.t, tok, scoring, s, p.e, debug_hash_bits(), ordered, rank_unique_columns());
 }
 
 // offsets of the data cells of a parsed CSV (po_csv_copy)

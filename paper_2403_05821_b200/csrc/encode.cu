@@ -629,6 +629,29 @@ __global__ void k_iota_pos(uint32_t* a, uint64_t n) {
     a[i] = uint32_t(i);
 }
 
+// Items of the ranked columns only: item k -> distinct index d (the ranked
+// columns' d-ranges, rbase[j] .. + (rpre[j+1] - rpre[j]), concatenated).
+__global__ void k_ranked_items(const uint64_t* rbase, const uint64_t* rpre, uint32_t nr,
+                               uint64_t total, const uint32_t* d_row, const uint32_t* d_col,
+                               uint32_t* sub_d, uint32_t* sub_row, uint32_t* sub_col) {
+  for (uint64_t k = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; k < total;
+       k += uint64_t(gridDim.x) * blockDim.x) {
+    uint32_t j = 0;
+    while (j + 1 < nr && rpre[j + 1] <= k) ++j;
+    const uint64_t d = rbase[j] + (k - rpre[j]);
+    sub_d[k] = uint32_t(d);
+    sub_row[k] = d_row[d];
+    sub_col[k] = d_col[d];
+  }
+}
+
+__global__ void k_scatter_sub(const uint32_t* sub_d, const uint32_t* sub_pos, uint64_t total,
+                              uint32_t* pos) {
+  for (uint64_t k = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; k < total;
+       k += uint64_t(gridDim.x) * blockDim.x)
+    pos[sub_d[k]] = sub_pos[k];
+}
+
 
 __global__ void k_distinct_info(const uint32_t* col_sel, uint64_t cnt, uint64_t base, uint32_t c,
                                 uint64_t cap, const uint32_t* reps, uint32_t* sel_slot,
@@ -904,7 +927,7 @@ void make_device_table(const po_table* t, int tok, cudaStream_t s, DeviceTable& 
 }
 
 void encode(const DeviceTable& t, int tok, int scoring, cudaStream_t s, Encoded& e,
-            uint32_t hash_bits_debug, bool ordered) {
+            uint32_t hash_bits_debug, bool ordered, bool rank_unique) {
   e.n = t.n;
   e.m = t.m;
   e.arena = t.arena;
@@ -1055,22 +1078,52 @@ void encode(const DeviceTable& t, int tok, int scoring, cudaStream_t s, Encoded&
   ek.item_col = d_col.get();
   ek.m = uint32_t(m);
   timing_mark("distinct", s);
-  if (!ordered) {  // identity only (dedup, FD checks): ids in compaction order
+  // rank_unique = false: a column with a distinct value per row (n > 1)
+  // keeps ids in compaction order (Encoded::unranked); its order is only
+  // needed to break ties inside a sort, which sorts by its bytes instead.
+  e.unranked.assign(m, 0);
+  if (ordered && !rank_unique && n > 1)
+    for (uint32_t c = 0; c < m; ++c) e.unranked[c] = e.card[c] == n;
+  std::vector<uint64_t> rbase, rpre{0};
+  for (uint32_t c = 0; c < m; ++c)
+    if (!e.unranked[c] && e.card[c]) {
+      rbase.push_back(e.colbase[c]);
+      rpre.push_back(rpre.back() + e.card[c]);
+    }
+  const uint64_t n_ranked = rpre.back();
+  if (!ordered || n_ranked < D)  // identity (dedup, FD checks, unranked columns)
     PO_LAUNCH(k_iota_pos, grid_for(D, 256), 256, 0, s, esc_pos.get(), D);
-  } else {
+  if (ordered && n_ranked) {
     // round 0 groups the distinct values by column index
     std::vector<uint32_t> cb32(m);
     for (uint32_t c = 0; c < m; ++c) cb32[c] = uint32_t(e.colbase[c]);
     DevBuf<uint32_t> d_cb32 = to_device(cb32, s);
     RefineJob je;
-    je.n_items = uint32_t(D);
-    je.d_grp_init = d_col.get();
-    je.d_grp_start = d_cb32.get();
     je.n_groups = uint32_t(m);
     je.grp_max = uint32_t(D);
     je.key = ek;
-    je.d_out_pos = esc_pos.get();
-    refine_sort_multi({je}, s);
+    je.d_grp_start = d_cb32.get();
+    if (n_ranked == D) {
+      je.n_items = uint32_t(D);
+      je.d_grp_init = d_col.get();
+      je.d_out_pos = esc_pos.get();
+      refine_sort_multi({je}, s);
+    } else {
+      DevBuf<uint64_t> d_rbase = to_device(rbase, s), d_rpre = to_device(rpre, s);
+      DevBuf<uint32_t> sub_d(n_ranked, s), sub_row(n_ranked, s), sub_col(n_ranked, s),
+          sub_pos(n_ranked, s);
+      PO_LAUNCH(k_ranked_items, grid_for(n_ranked, 256), 256, 0, s, d_rbase.get(), d_rpre.get(),
+                uint32_t(rbase.size()), n_ranked, d_row.get(), d_col.get(), sub_d.get(),
+                sub_row.get(), sub_col.get());
+      je.n_items = uint32_t(n_ranked);
+      je.d_grp_init = sub_col.get();
+      je.key.item_cell_row = sub_row.get();
+      je.key.item_col = sub_col.get();
+      je.d_out_pos = sub_pos.get();
+      refine_sort_multi({je}, s);
+      PO_LAUNCH(k_scatter_sub, grid_for(n_ranked, 256), 256, 0, s, sub_d.get(), sub_pos.get(),
+                n_ranked, esc_pos.get());
+    }
   }
   timing_mark("rank_sort", s);
 

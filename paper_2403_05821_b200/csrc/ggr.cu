@@ -1329,6 +1329,7 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
   std::vector<uint32_t> leaf_off(nleaves, 0), leaf_chunk_off(nleaves), leaf_nchunks(nleaves);
   std::vector<int32_t> h_leaf_orders(size_t(nleaves) * m);
   KeySchedule ks;
+  TieSpec ties;
   // round 0 groups the rows by leaf index; later rounds by start position
   const int cap0 = int(refine_chunk_bits(nleaves ? nleaves - 1 : 0));
   const int cap = 64;  // rounds >= 1 sort inside groups: the chunk alone
@@ -1342,8 +1343,18 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
     // sort keys of the leaf
     std::vector<std::pair<int, uint8_t>> keys;  // (field, kind)
     // single-column leaves are ordered by raw bytes in a separate string job
+    ties.tie_col.push_back(-1);
     if (nd.kind == FALLBACK)  // fragment keys (ggr.hpp:340-350)
-      for (int f : nd.leaf_order) keys.push_back({f, uint8_t(1)});
+      for (int f : nd.leaf_order) {
+        if (e.is_unranked(f)) {  // distinct per row: break_unranked_ties
+          ties.tie_col.back() = f;
+          break;
+        }
+        keys.push_back({f, uint8_t(1)});
+      }
+    if (ties.tie_col.back() >= 0)
+      for (const auto& k : keys) ties.key_fields.push_back(k.first);
+    ties.key_off.push_back(uint32_t(ties.key_fields.size()));
     leaf_chunk_off[l] = uint32_t(ks.chunk_nkeys.size());
     leaf_nchunks[l] = ks.add_leaf(keys, e.card, cap0, cap);
   }
@@ -1499,6 +1510,10 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
     PO_LAUNCH(k_raw1_scatter, grid_for(n_raw, 256), 256, 0, s, raw_rows.get(), raw_pos.get(), n_raw,
               pos.get());
   timing_mark("leaf_sort", s);
+  if (ties.any()) {
+    break_unranked_ties(e, ties, row_leaf.get(), d_leaf_off.get(), pos.get(), s);
+    timing_mark("leaf_ties", s);
+  }
   if (debug_checks()) {
     DevBuf<unsigned> seen(n, s);
     DevBuf<unsigned long long> bad(1, s);

@@ -60,6 +60,11 @@ struct Encoded {
   DevBuf<uint32_t> count;     // D
   DevBuf<uint32_t> rep_row;   // D: a row holding the value
   std::vector<uint64_t> total_len;  // host, per column: sum of segment lengths (stats.hpp:38)
+  // host, per column (empty = none): ids of a unique column left in
+  // compaction order (encode(rank_unique = false)); sorts break ties on it
+  // by its escaped bytes (break_unranked_ties)
+  std::vector<uint8_t> unranked;
+  bool is_unranked(int c) const { return !unranked.empty() && unranked[c]; }
 };
 
 // ordered = false: ids are exact but in no particular order (equality-only
@@ -67,7 +72,7 @@ struct Encoded {
 uint32_t debug_hash_bits();  // PO_DEBUG_HASH_BITS (abi.cu)
 
 void encode(const DeviceTable& t, int tok, int scoring, cudaStream_t s, Encoded& e,
-            uint32_t hash_bits_debug = 64, bool ordered = true);
+            uint32_t hash_bits_debug = 64, bool ordered = true, bool rank_unique = true);
 
 // Segmented refinement sort (rank_sort / multikey_sort engine).
 // Items [0, n_items) start in groups whose ids are their final start
@@ -213,6 +218,38 @@ uint64_t fixed_order_phc_device(const Encoded& e, const std::vector<int>& order,
 // (an upper bound from the dictionary counts and lengths, phc.cu).
 bool fallback_cannot_win(const Encoded& e, uint64_t phc, cudaStream_t s);
 
+// Leaves whose key list stops before an unranked column (Encoded::unranked):
+// per leaf that column (-1: none) and the ranked key fields sorted before it
+// (CSR). break_unranked_ties re-sorts every run of rows that tie on those
+// keys by the column's escaped bytes (kind-1 string refine), updating pos.
+struct TieSpec {
+  std::vector<int32_t> tie_col;
+  std::vector<uint32_t> key_off{0};
+  std::vector<int32_t> key_fields;
+  bool any() const {
+    for (int32_t c : tie_col)
+      if (c >= 0) return true;
+    return false;
+  }
+};
+// Positions of the rows of short tied runs (2..max_len rows; run[q] = start
+// position of q's run, run_len[start] = its length) by the escaped bytes of
+// col_of_leaf[row_leaf[row]] (distinct within a run): pos[perm[q]] = start +
+// rank. One thread per position; longer runs are left alone (refine.cu).
+void rank_short_runs(const uint8_t* arena, const uint64_t* offsets, uint32_t m,
+                     const uint32_t* perm, const uint32_t* run, const uint32_t* run_len,
+                     const uint32_t* row_leaf, const int32_t* col_of_leaf, uint64_t n,
+                     uint32_t max_len, uint32_t* pos, cudaStream_t s);
+// The same for the positions items[0, nt) of longer runs: 126-bit prefix
+// keys, then a quadratic count per run (work = sum of squared run lengths;
+// max_len = the longest run).
+void rank_long_runs(const uint8_t* arena, const uint64_t* offsets, uint32_t m, const uint32_t* perm,
+                    const uint32_t* run, const uint32_t* run_len, const uint32_t* row_leaf,
+                    const int32_t* col_of_leaf, const uint32_t* items, uint32_t nt, uint64_t n,
+                    uint32_t max_len, uint32_t* pos, cudaStream_t s);
+void break_unranked_ties(const Encoded& e, const TieSpec& ts, const uint32_t* row_leaf,
+                         const uint32_t* d_leaf_off, uint32_t* pos, cudaStream_t s);
+
 class FixedOrderSort {
  public:
   FixedOrderSort(const Encoded& e, const std::vector<int>& order, cudaStream_t s);
@@ -220,6 +257,8 @@ class FixedOrderSort {
   void finish(uint32_t* d_perm);  // after the job ran: d_perm[pos] = row
 
  private:
+  const Encoded& e_;
+  TieSpec ties_;
   uint64_t n_ = 0;
   cudaStream_t s_;
   RefineJob job_;

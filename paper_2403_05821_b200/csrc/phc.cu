@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <map>
 #include <numeric>
 
 #include "internal.cuh"
@@ -257,14 +258,219 @@ uint64_t fixed_order_phc_device(const Encoded& e, const std::vector<int>& order,
   return h;
 }
 
+namespace {
+
+// Run heads of the tie-break: position q starts a run unless the row before
+// it (same leaf) agrees on every ranked key of the leaf. Non-tie leaves:
+// every position its own run.
+__global__ void k_tie_heads(const uint32_t* perm, uint64_t n, uint32_t m,
+                            const uint32_t* __restrict__ vid, const uint32_t* row_leaf,
+                            const uint32_t* leaf_off, const int32_t* tie_col,
+                            const uint32_t* key_off, const int32_t* key_fields, uint32_t* head) {
+  for (uint64_t q = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; q < n;
+       q += uint64_t(gridDim.x) * blockDim.x) {
+    const uint32_t r = perm[q], l = row_leaf[r];
+    bool start = tie_col[l] < 0 || q == leaf_off[l];
+    if (!start) {
+      const uint32_t rp = perm[q - 1];
+      for (uint32_t k = key_off[l]; k < key_off[l + 1]; ++k) {
+        const int32_t f = key_fields[k];
+        if (vid[uint64_t(rp) * m + f] != vid[uint64_t(r) * m + f]) {
+          start = true;
+          break;
+        }
+      }
+    }
+    head[q] = start ? uint32_t(q) : 0u;
+  }
+}
+
+struct MaxOp {
+  __device__ __forceinline__ uint32_t operator()(uint32_t a, uint32_t b) const {
+    return a > b ? a : b;
+  }
+};
+
+// run_len[start] of every run (written at its last position)
+__global__ void k_run_len(const uint32_t* run, uint64_t n, uint32_t* run_len) {
+  for (uint64_t q = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; q < n;
+       q += uint64_t(gridDim.x) * blockDim.x)
+    if (q + 1 == n || run[q + 1] != run[q]) run_len[run[q]] = uint32_t(q - run[q] + 1);
+}
+
+// work of the quadratic long-run ranking: sum of squared long-run lengths
+// (and work[1] = the longest run)
+__global__ void k_long_work(const uint32_t* run, const uint32_t* run_len, uint64_t n,
+                            uint32_t max_short, unsigned long long* work) {
+  unsigned long long local = 0, mx = 0;
+  for (uint64_t q = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; q < n;
+       q += uint64_t(gridDim.x) * blockDim.x)
+    if (run[q] == q && run_len[q] > max_short) {
+      local += uint64_t(run_len[q]) * run_len[q];
+      mx = max(mx, (unsigned long long)run_len[q]);
+    }
+  for (int o = 16; o; o >>= 1) {
+    local += __shfl_down_sync(0xffffffffu, local, o);
+    mx = max(mx, __shfl_down_sync(0xffffffffu, mx, o));
+  }
+  if ((threadIdx.x & 31) == 0 && local) {
+    atomicAdd(work, local);
+    atomicMax(work + 1, mx);
+  }
+}
+
+// positions in runs longer than max_short (left to the refine job)
+__global__ void k_tie_flags(const uint32_t* run, const uint32_t* run_len, uint64_t n,
+                            uint32_t max_short, uint8_t* flag) {
+  for (uint64_t q = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; q < n;
+       q += uint64_t(gridDim.x) * blockDim.x)
+    flag[q] = run_len[run[q]] > (max_short > 1 ? max_short : 1);
+}
+
+__global__ void k_tie_items(const uint32_t* items, uint32_t nt, const uint32_t* perm,
+                            const uint32_t* run, const uint32_t* row_leaf, const int32_t* tie_col,
+                            uint32_t* t_row, uint32_t* t_grp, uint32_t* t_col) {
+  for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < nt; k += gridDim.x * blockDim.x) {
+    const uint32_t q = items[k], r = perm[q];
+    t_row[k] = r;
+    t_grp[k] = run[q];
+    t_col[k] = uint32_t(tie_col[row_leaf[r]]);
+  }
+}
+
+__global__ void k_tie_scatter(const uint32_t* t_row, const uint32_t* t_pos, uint32_t nt,
+                              uint32_t* pos) {
+  for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < nt; k += gridDim.x * blockDim.x)
+    pos[t_row[k]] = t_pos[k];
+}
+
+}  // namespace
+
+// PO_SHORT_RUN_MAX: longest tied run ranked by direct comparisons (default 32)
+uint32_t short_run_max() {
+  const char* e = std::getenv("PO_SHORT_RUN_MAX");
+  return e && *e ? uint32_t(std::atoi(e)) : 32u;
+}
+
+// PO_LONG_RUN_BUDGET: largest sum of squared long-run lengths ranked by
+// direct counting (default 2^29, a few tenths of a ms at most); above it a sort.
+uint64_t long_run_budget() {
+  const char* e = std::getenv("PO_LONG_RUN_BUDGET");
+  return e && *e ? uint64_t(std::strtoull(e, nullptr, 10)) : (1ull << 29);
+}
+
+// Values of an unranked column are distinct (one per row), so after this
+// every tied run is totally ordered, as a sort by the column's escaped rank
+// would order it.
+void break_unranked_ties(const Encoded& e, const TieSpec& ts, const uint32_t* row_leaf,
+                         const uint32_t* d_leaf_off, uint32_t* pos, cudaStream_t s) {
+  const uint64_t n = e.n;
+  if (n < 2 || !ts.any()) return;
+  auto d_tc = to_device(ts.tie_col, s);
+  auto d_ko = to_device(ts.key_off, s);
+  std::vector<int32_t> kf = ts.key_fields;
+  if (kf.empty()) kf.push_back(0);
+  auto d_kf = to_device(kf, s);
+  DevBuf<uint32_t> perm(n, s), run(n, s), items(n, s);
+  PO_LAUNCH(k_invert, grid_for(n, 256), 256, 0, s, pos, n, perm.get());
+  timing_mark("ties_setup", s);
+  PO_LAUNCH(k_tie_heads, grid_for(n, 256), 256, 0, s, perm.get(), n, e.m, e.vid.get(), row_leaf,
+            d_leaf_off, d_tc.get(), d_ko.get(), d_kf.get(), run.get());
+  size_t tb = 0;
+  PO_CUDA(cub::DeviceScan::InclusiveScan(nullptr, tb, run.get(), run.get(), MaxOp(), int(n), s));
+  {
+    DevBuf<uint8_t> tmp(tb, s);
+    PO_CUDA(cub::DeviceScan::InclusiveScan(tmp.get(), tb, run.get(), run.get(), MaxOp(), int(n), s));
+  }
+  // short runs: each position ranks itself against its run (quadratic, no
+  // sort); long runs: a kind-1 string refine job
+  const uint32_t max_short = short_run_max();
+  DevBuf<uint32_t> run_len(n, s);
+  PO_LAUNCH(k_run_len, grid_for(n, 256), 256, 0, s, run.get(), n, run_len.get());
+  timing_mark("ties_runs", s);
+  rank_short_runs(e.arena, e.offsets, e.m, perm.get(), run.get(), run_len.get(), row_leaf,
+                  d_tc.get(), n, max_short, pos, s);
+  timing_mark("ties_short", s);
+  DevBuf<uint8_t> flag(n, s);
+  PO_LAUNCH(k_tie_flags, grid_for(n, 256), 256, 0, s, run.get(), run_len.get(), n, max_short,
+            flag.get());
+  DevBuf<int> nsel(1, s);
+  cub::CountingInputIterator<uint32_t> it(0);
+  tb = 0;
+  PO_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, it, flag.get(), items.get(), nsel.get(), int(n), s));
+  {
+    DevBuf<uint8_t> tmp(tb, s);
+    PO_CUDA(cub::DeviceSelect::Flagged(tmp.get(), tb, it, flag.get(), items.get(), nsel.get(),
+                                       int(n), s));
+  }
+  const uint32_t ms = max_short > 1 ? max_short : 1;
+  DevBuf<unsigned long long> work(2, s);
+  work.zero();
+  PO_LAUNCH(k_long_work, grid_for(n, 256), 256, 0, s, run.get(), run_len.get(), n, ms, work.get());
+  int hn = 0;
+  unsigned long long hw[2] = {0, 0};
+  PO_CUDA(cudaMemcpyAsync(&hn, nsel.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
+  PO_CUDA(cudaMemcpyAsync(hw, work.get(), sizeof(hw), cudaMemcpyDeviceToHost, s));
+  sync(s);
+  const uint32_t nt = uint32_t(hn);
+  if (debug_timing()) {
+    std::vector<uint32_t> hr(n), hl(n);
+    PO_CUDA(cudaMemcpyAsync(hr.data(), run.get(), n * 4, cudaMemcpyDeviceToHost, s));
+    PO_CUDA(cudaMemcpyAsync(hl.data(), run_len.get(), n * 4, cudaMemcpyDeviceToHost, s));
+    sync(s);
+    std::map<uint32_t, uint64_t> hist;  // log2 bucket -> runs
+    uint32_t mx = 0;
+    for (uint64_t q = 0; q < n; ++q)
+      if (hr[q] == q && hl[q] > 1) {
+        hist[31 - __builtin_clz(hl[q])]++;
+        mx = std::max(mx, hl[q]);
+      }
+    fprintf(stderr, "[po ties] %u positions in long runs; max run %u; runs by log2 len:", nt, mx);
+    for (auto& kv : hist) fprintf(stderr, " %u:%llu", kv.first, (unsigned long long)kv.second);
+    fprintf(stderr, "\n");
+  }
+  if (nt == 0) return;
+  if (hw[0] <= long_run_budget()) {  // quadratic per run, no sort
+    rank_long_runs(e.arena, e.offsets, e.m, perm.get(), run.get(), run_len.get(), row_leaf,
+                   d_tc.get(), items.get(), nt, n, uint32_t(hw[1]), pos, s);
+    return;
+  }
+  DevBuf<uint32_t> t_row(nt, s), t_grp(nt, s), t_col(nt, s), t_pos(nt, s);
+  PO_LAUNCH(k_tie_items, grid_for(nt, 256), 256, 0, s, items.get(), nt, perm.get(), run.get(),
+            row_leaf, d_tc.get(), t_row.get(), t_grp.get(), t_col.get());
+  RefineJob tj;
+  tj.n_items = nt;
+  tj.d_grp_init = t_grp.get();  // run start positions
+  tj.grp_max = uint32_t(n);
+  tj.key.kind = 1;  // escaped bytes: the order of the column's ranks
+  tj.key.arena = e.arena;
+  tj.key.arena_bytes = e.arena_bytes;
+  tj.key.offsets = e.offsets;
+  tj.key.item_cell_row = t_row.get();
+  tj.key.item_col = t_col.get();
+  tj.key.m = e.m;
+  tj.d_out_pos = t_pos.get();
+  refine_sort_multi({tj}, s);
+  PO_LAUNCH(k_tie_scatter, grid_for(nt, 256), 256, 0, s, t_row.get(), t_pos.get(), nt, pos);
+}
+
 // Keys of a single leaf covering all rows (one field order, escaped ranks),
 // packed into 64-bit chunks next to the group id.
 FixedOrderSort::FixedOrderSort(const Encoded& e, const std::vector<int>& order, cudaStream_t s)
-    : n_(e.n), s_(s) {
+    : e_(e), n_(e.n), s_(s) {
   if (n_ == 0) return;
   KeySchedule ks;
   std::vector<std::pair<int, uint8_t>> keys;
-  for (int f : order) keys.push_back({f, uint8_t(1)});  // escaped ranks
+  ties_.tie_col.assign(1, -1);
+  for (int f : order) {
+    if (e.is_unranked(f)) {  // distinct per row: its bytes break the remaining ties
+      ties_.tie_col[0] = f;
+      break;
+    }
+    keys.push_back({f, uint8_t(1)});  // escaped ranks
+    ties_.key_fields.push_back(f);
+  }
+  ties_.key_off.push_back(uint32_t(ties_.key_fields.size()));
   // one round-0 group (index 0, start 0); later rounds: start positions < n
   // rounds >= 1 sort inside groups: their chunks may use all 64 bits
   const uint32_t nch = ks.add_leaf(keys, e.card, int(refine_chunk_bits(0)), 64);
@@ -308,6 +514,7 @@ FixedOrderSort::FixedOrderSort(const Encoded& e, const std::vector<int>& order, 
 }
 
 void FixedOrderSort::finish(uint32_t* d_perm) {
+  if (n_) break_unranked_ties(e_, ties_, row_leaf_.get(), start_.get(), pos_.get(), s_);
   if (n_) PO_LAUNCH(k_invert, grid_for(n_, 256), 256, 0, s_, pos_.get(), n_, d_perm);
 }
 

@@ -615,6 +615,155 @@ void refine_sort_multi(const std::vector<RefineJob>& specs, cudaStream_t s) {
   }
 }
 
+namespace {
+
+// -1 / 1: a before / after b in escaped fragment order (distinct strings).
+// The expansions are prefix-free, so the first differing raw byte (or the
+// end of the shorter string, the closing '"') decides.
+__device__ __forceinline__ bool esc_less(const uint8_t* a, uint64_t la, const uint8_t* b,
+                                         uint64_t lb) {
+  const uint64_t mn = la < lb ? la : lb;
+  uint64_t i = 0;
+  while (i < mn && a[i] == b[i]) ++i;
+  const uint32_t ca = i < la ? c_esc_code[a[i]] : c_esc_code[256];
+  const uint32_t cb = i < lb ? c_esc_code[b[i]] : c_esc_code[256];
+  return ca < cb;
+}
+
+// Thread per position of a short run (2..max_len rows of one leaf, distinct
+// values of column col_of_leaf[leaf]): its rank among the run's values.
+__global__ void k_rank_short_runs(const uint8_t* __restrict__ arena,
+                                  const uint64_t* __restrict__ offsets, uint32_t m,
+                                  const uint32_t* perm, const uint32_t* run,
+                                  const uint32_t* run_len, const uint32_t* row_leaf,
+                                  const int32_t* col_of_leaf, uint64_t n, uint32_t max_len,
+                                  uint32_t* pos) {
+  for (uint64_t q = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; q < n;
+       q += uint64_t(gridDim.x) * blockDim.x) {
+    const uint32_t st = run[q], L = run_len[st];
+    if (L < 2 || L > max_len) continue;
+    const uint32_t r = perm[q];
+    const uint32_t c = uint32_t(col_of_leaf[row_leaf[r]]);
+    const uint64_t ia = uint64_t(r) * m + c;
+    const uint8_t* a = arena + offsets[ia];
+    const uint64_t la = offsets[ia + 1] - offsets[ia];
+    uint32_t rank = 0;
+    for (uint32_t j = st; j < st + L; ++j) {
+      if (j == q) continue;
+      const uint64_t ib = uint64_t(perm[j]) * m + c;
+      rank += esc_less(arena + offsets[ib], offsets[ib + 1] - offsets[ib], a, la);
+    }
+    pos[r] = st + rank;
+  }
+}
+
+// Escaped codes of symbols [7w, 7w + 7) of a string, 9 bits each (end marker
+// at len, zero padding after): comparing (word 0, word 1) orders the first 14
+// symbols of the fragment keys.
+__device__ __forceinline__ uint64_t esc_word(const uint8_t* p, uint64_t len, uint32_t w) {
+  uint64_t chunk = 0;
+  for (uint32_t j = 0; j < 7; ++j) {
+    const uint64_t i = 7ull * w + j;
+    const uint32_t code = i < len ? c_esc_code[p[i]] : (i == len ? c_esc_code[256] : 0u);
+    chunk = (chunk << 9) | code;
+  }
+  return chunk;
+}
+
+__global__ void k_long_keys(const uint8_t* __restrict__ arena, const uint64_t* __restrict__ offsets,
+                            uint32_t m, const uint32_t* perm, const uint32_t* row_leaf,
+                            const int32_t* col_of_leaf, const uint32_t* items, uint32_t nt,
+                            uint64_t* k0, uint64_t* k1) {
+  for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < nt; k += gridDim.x * blockDim.x) {
+    const uint32_t q = items[k], r = perm[q];
+    const uint64_t i = uint64_t(r) * m + uint32_t(col_of_leaf[row_leaf[r]]);
+    const uint8_t* p = arena + offsets[i];
+    const uint64_t len = offsets[i + 1] - offsets[i];
+    k0[q] = esc_word(p, len, 0);
+    k1[q] = esc_word(p, len, 1);
+  }
+}
+
+// Positions of long runs: part p of the run (kLongPart positions
+// from st + y * kLongPart) is counted against the position's 14-symbol keys;
+// keys equal on all 14 symbols fall back to a full escaped comparison. Runs
+// are split so the longest one does not serialise on a few warps; positions
+// of one run are consecutive in items[], so a warp's loads of k0[j] / k1[j]
+// coincide.
+constexpr uint32_t kLongPart = 512;
+
+__global__ void k_rank_long_runs(const uint8_t* __restrict__ arena,
+                                 const uint64_t* __restrict__ offsets, uint32_t m,
+                                 const uint32_t* perm, const uint32_t* run, const uint32_t* run_len,
+                                 const uint32_t* row_leaf, const int32_t* col_of_leaf,
+                                 const uint32_t* items, uint32_t nt, const uint64_t* __restrict__ k0,
+                                 const uint64_t* __restrict__ k1, uint32_t gx, uint32_t* rank_out) {
+  const uint32_t part = blockIdx.x / gx;  // blocks [part * gx, (part + 1) * gx): one part
+  const uint32_t k = (blockIdx.x - part * gx) * blockDim.x + threadIdx.x;
+  if (k >= nt) return;
+  const uint32_t q = items[k], st = run[q], L = run_len[st];
+  const uint32_t lo = st + part * kLongPart;
+  if (lo >= st + L) return;
+  const uint32_t hi = min(st + L, lo + kLongPart);
+  const uint64_t a0 = k0[q], a1 = k1[q];
+  uint32_t rank = 0, eq = 0;
+#pragma unroll 8
+  for (uint32_t j = lo; j < hi; ++j) {
+    const uint64_t b0 = k0[j], b1 = k1[j];
+    rank += (b0 < a0) | ((b0 == a0) & (b1 < a1));
+    eq += (b0 == a0) & (b1 == a1);
+  }
+  if (eq > uint32_t(q >= lo && q < hi)) {  // shared 14-symbol prefixes: compare bytes
+    const uint32_t r = perm[q];
+    const uint32_t c = uint32_t(col_of_leaf[row_leaf[r]]);
+    const uint64_t ia = uint64_t(r) * m + c;
+    for (uint32_t j = lo; j < hi; ++j) {
+      if (j == q || k0[j] != a0 || k1[j] != a1) continue;
+      const uint64_t ib = uint64_t(perm[j]) * m + c;
+      rank += esc_less(arena + offsets[ib], offsets[ib + 1] - offsets[ib], arena + offsets[ia],
+                       offsets[ia + 1] - offsets[ia]);
+    }
+  }
+  if (rank) atomicAdd(rank_out + k, rank);
+}
+
+__global__ void k_long_place(const uint32_t* items, uint32_t nt, const uint32_t* perm,
+                             const uint32_t* run, const uint32_t* rank, uint32_t* pos) {
+  for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < nt; k += gridDim.x * blockDim.x) {
+    const uint32_t q = items[k];
+    pos[perm[q]] = run[q] + rank[k];
+  }
+}
+
+}  // namespace
+
+void rank_short_runs(const uint8_t* arena, const uint64_t* offsets, uint32_t m,
+                     const uint32_t* perm, const uint32_t* run, const uint32_t* run_len,
+                     const uint32_t* row_leaf, const int32_t* col_of_leaf, uint64_t n,
+                     uint32_t max_len, uint32_t* pos, cudaStream_t s) {
+  if (n == 0) return;
+  ensure_esc_table();
+  PO_LAUNCH(k_rank_short_runs, grid_for(n, 256), 256, 0, s, arena, offsets, m, perm, run, run_len,
+            row_leaf, col_of_leaf, n, max_len, pos);
+}
+
+void rank_long_runs(const uint8_t* arena, const uint64_t* offsets, uint32_t m, const uint32_t* perm,
+                    const uint32_t* run, const uint32_t* run_len, const uint32_t* row_leaf,
+                    const int32_t* col_of_leaf, const uint32_t* items, uint32_t nt, uint64_t n,
+                    uint32_t max_len, uint32_t* pos, cudaStream_t s) {
+  if (nt == 0) return;
+  ensure_esc_table();
+  DevBuf<uint64_t> k0(n, s), k1(n, s);
+  PO_LAUNCH(k_long_keys, grid_for(nt, 256), 256, 0, s, arena, offsets, m, perm, row_leaf,
+            col_of_leaf, items, nt, k0.get(), k1.get());
+  DevBuf<uint32_t> rank(nt, s);
+  rank.zero();
+  const uint32_t gx = (nt + 255) / 256, parts = (max_len + kLongPart - 1) / kLongPart;
+  PO_LAUNCH(k_rank_long_runs, gx * parts, 256, 0, s, arena, offsets, m, perm, run, run_len,
+            row_leaf, col_of_leaf, items, nt, k0.get(), k1.get(), gx, rank.get());
+  PO_LAUNCH(k_long_place, grid_for(nt, 256), 256, 0, s, items, nt, perm, run, rank.get(), pos);
+}
+
 void refine_sort(uint32_t n_items, const uint32_t* d_grp_init, uint32_t grp_max,
                  const RefineKey& key, uint32_t* d_out_pos, cudaStream_t s, uint32_t row_chunk_bits) {
   RefineJob j;

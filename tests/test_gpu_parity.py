@@ -130,6 +130,47 @@ def test_sort_rows_fixed_order_and_stats_vs_oracle():
                 assert [f.avg_len for f in st.fields] == [float(x) / n for x in tot.tolist()]
 
 
+def _unique_column_table(rng, n, m_low, prefix_len):
+    """A column with one distinct value per row (shared prefixes, bytes that
+    JSON escaping reorders) next to low-cardinality columns."""
+    alpha = ALPHABETS["esc"] + b"\x7f\xc3"
+    uniq = set()
+    while len(uniq) < n:
+        uniq.add(b"p" * rng.randint(0, prefix_len)
+                 + bytes(rng.choice(alpha) for _ in range(rng.randint(0, 4))))
+    uniq = list(uniq)
+    rng.shuffle(uniq)
+    rows = [[bytes([97 + rng.randrange(3)]) * rng.randint(1, 2) for _ in range(m_low)] + [u]
+            for u in uniq]
+    k = rng.randrange(m_low + 1)
+    rows = [r[:k] + [r[-1]] + r[k:-1] for r in rows]
+    return po.Table([f"f{i}" for i in range(m_low + 1)], rows), k
+
+
+@pytest.mark.parametrize("short_max,long_budget", [(None, None), ("0", None), ("0", "0"),
+                                                   ("4", "0")])
+def test_unique_columns_tie_break_on_bytes(monkeypatch, short_max, long_budget):
+    # unique columns are left unranked by the solver; every sort that reaches
+    # one orders its tied runs by the column's escaped bytes instead: short
+    # runs by direct ranking, long runs by prefix keys + counting or by a sort
+    if short_max is not None:
+        monkeypatch.setenv("PO_SHORT_RUN_MAX", short_max)
+    if long_budget is not None:
+        monkeypatch.setenv("PO_LONG_RUN_BUDGET", long_budget)
+    rng = random.Random(77)
+    P = oracle("port")
+    for trial in range(40):
+        n = rng.choice([2, 3, 17, 200, 1500])
+        t, k = _unique_column_table(rng, n, rng.randint(1, 3), rng.choice([0, 3, 40]))
+        m = t.field_count()
+        order = list(range(m))
+        rng.shuffle(order)
+        assert (po.sort_rows_fixed_order(t, order).row_ids.tolist()
+                == P.sort_rows_fixed_order(t, order).tolist()), (trial, n, order)
+        for cfg in (po.GgrConfig(0, 0, 0), po.GgrConfig(1, 1, 0), po.GgrConfig()):
+            assert same_result(po.ggr(t, None, cfg), P.ggr(t, None, cfg)), (trial, n, cfg)
+
+
 def test_error_behaviour():
     t = po.Table(["A", "B"], [["1", "2"]])
     with pytest.raises(po.SchemaError):

@@ -32,6 +32,6 @@ for i in range(reps):
           f"free {torch.cuda.mem_get_info()[0] / 1e9:.1f} GB", flush=True)
     if prof:
         rep = lib.profile_report()
-        top = sorted(rep.items(), key=lambda x: -x[1][1])[:4]
-        print("   kernels %.1f ms; top: %s" % (sum(v[1] for v in rep.values()),
-              ", ".join(f"{k} {v[1]:.1f}" for k, v in top)), flush=True)
+        top = sorted(rep.items(), key=lambda x: -x[1][1])[:int(sys.argv[4]) if sys.argv[4].isdigit() else 4]
+        print("   kernels %.3f ms; top: %s" % (sum(v[1] for v in rep.values()),
+              ", ".join(f"{k} {v[0]}x {v[1]:.3f}" for k, v in top)), flush=True)
