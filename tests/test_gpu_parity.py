@@ -94,6 +94,31 @@ def test_hash_collisions_are_resolved_on_bytes(monkeypatch):
         assert same_result(po.ggr(t, None, cfg), P.ggr(t, None, cfg)), trial
 
 
+@pytest.mark.parametrize("bits", ["3", "64"])
+def test_long_values_collisions_resolved_on_bytes(monkeypatch, bits):
+    # cells of 60-300 bytes (cooperative byte verification) that differ only
+    # in a byte near the end or in length, under forced hash collisions
+    monkeypatch.setenv("PO_DEBUG_HASH_BITS", bits)
+    rng = random.Random(11)
+    P = oracle("port")
+    for trial in range(12):
+        n = rng.choice([33, 100, 700])
+        base = [bytes(rng.choice(b"abc \"\n") for _ in range(rng.randint(60, 300)))
+                for _ in range(3)]
+        vals = []
+        for b in base:
+            k = rng.randrange(len(b))
+            vals += [b, b[:k] + b"z" + b[k + 1:], b + b"x", b[:-1]]
+        rows = [[rng.choice(vals), rng.choice(vals[:4]), bytes([97 + rng.randrange(3)])]
+                for _ in range(n)]
+        t = po.Table(["a", "b", "c"], rows)
+        cfg = rng.choice([po.GgrConfig(), po.exact_config()])
+        assert same_result(po.ggr(t, None, cfg), P.ggr(t, None, cfg)), (trial, bits)
+        st = po.compute_stats(t)
+        card, _ = P.compute_stats(t)
+        assert [f.cardinality for f in st.fields] == card.tolist()
+
+
 def test_phc_hit_random_schedules_vs_oracle():
     rng = random.Random(42)
     P = oracle("port")
