@@ -780,15 +780,30 @@ __global__ void __launch_bounds__(512) k_count(const uint32_t* vid, uint64_t n, 
   extern __shared__ uint32_t h[];
   for (uint32_t b = threadIdx.x; b < nbins; b += blockDim.x) h[b] = 0;
   __syncthreads();
-  const uint64_t total = n * m;
-  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < total;
-       i += uint64_t(gridDim.x) * blockDim.x) {
-    const uint32_t c = uint32_t(i % m);
-    const uint32_t v = vid[i];
-    const uint32_t o = soff[c];
-    if (o == kUniqueCol) count[colbase[c] + v] = 1u;
-    else if (o != kLargeCol) atomicAdd(&h[o + v], 1u);
-    else atomicAdd(&count[colbase[c] + v], 1u);
+  // Warps walk 32 rows column by column; lanes holding the same value (the
+  // frequent values of skewed columns) add once per warp (one atomic per
+  // distinct value in the warp instead of one per cell).
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t ntiles = (n + 31) / 32;
+  for (uint64_t tile = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5; tile < ntiles;
+       tile += (uint64_t(gridDim.x) * blockDim.x) >> 5) {
+    const uint64_t r = tile * 32 + lane;
+    const bool live = r < n;
+    const uint32_t act = __ballot_sync(0xffffffffu, live);
+    for (uint32_t c = 0; c < m; ++c) {
+      const uint32_t o = soff[c];
+      if (o == kUniqueCol) {
+        if (live) count[colbase[c] + vid[r * m + c]] = 1u;
+        continue;
+      }
+      if (!live) continue;
+      const uint32_t v = vid[r * m + c];
+      const uint32_t peers = __match_any_sync(act, v);
+      if (lane != uint32_t(__ffs(peers) - 1)) continue;
+      const uint32_t k = uint32_t(__popc(peers));
+      if (o != kLargeCol) atomicAdd(&h[o + v], k);
+      else atomicAdd(&count[colbase[c] + v], k);
+    }
   }
   __syncthreads();
   // flush: the small column owning bin b is the one with the largest
@@ -1178,7 +1193,7 @@ void encode(const DeviceTable& t, int tok, int scoring, cudaStream_t s, Encoded&
         nbins += uint32_t(e.card[c]);
       }
     auto d_soff = to_device(soff, s);
-    PO_LAUNCH(k_count, grid_for(cells, 512, 2), 512, nbins * sizeof(uint32_t), s, e.vid.get(), n,
+    PO_LAUNCH(k_count, grid_for(((n + 31) / 32) * 32, 512, 2), 512, nbins * sizeof(uint32_t), s, e.vid.get(), n,
               uint32_t(m), d_soff.get(), nbins, e.d_colbase.get(), e.count.get());
   }
   timing_mark("count", s);
