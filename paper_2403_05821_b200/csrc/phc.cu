@@ -245,11 +245,12 @@ uint64_t fixed_order_phc_device(const Encoded& e, const std::vector<int>& order,
     PO_LAUNCH(k_fb_init, grid_for(n, 256), 256, 0, s, e.vid.get(), n, m, uint32_t(f0), gid.get());
     for (size_t p = 1; p < order.size(); ++p) {
       const int f = order[p];
+      // a unique column splits every group into singletons: no hits from here
+      if (e.card[f] == n) break;
       keys.fill_bytes(0xFF);
       PO_LAUNCH(k_fb_depth, grid_for(n, 256, 8), 256, 0, s, e.vid.get(), n, m, uint32_t(f),
                 e.vlen.get() + colbase[f], gid.get(), keys.get(), cap - 1, acc.get(),
                 ng.get() + (p - 1), ng.get() + p);
-      if (e.card[f] == n) break;  // unique column: every group a singleton below
     }
   }
   unsigned long long h = 0;
