@@ -1144,6 +1144,7 @@ void encode(const DeviceTable& t, int tok, int scoring, cudaStream_t s, Encoded&
 
   DevBuf<uint32_t> slot2vid(m * cap, s), col_by_pos(D, s);
   e.rep_row.alloc(D, s);
+  timing_mark("scatter_alloc", s);
   PO_LAUNCH(k_scatter_pos, grid_for(D, 256), 256, 0, s, esc_pos.get(), d_col.get(), d_row.get(),
             sel.get(), e.d_colbase.get(), D, cap, slot2vid.get(), e.rep_row.get(),
             col_by_pos.get());

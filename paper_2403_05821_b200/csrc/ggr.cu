@@ -419,18 +419,25 @@ struct SplitD {
 // Split lookup by binary search over the level's split nodes (ascending
 // node ids), staged in shared memory when they fit.
 constexpr uint32_t kRelabelSmem = 4096;
+constexpr uint32_t kRelabelBlock = 256;  // k_relabel block size (one table slot per thread)
 
-__global__ void k_relabel(uint32_t* node_of_row, uint64_t n, const uint32_t* split_nodes,
-                          uint32_t ns, const SplitD* sp, const uint32_t* vid, uint32_t m,
-                          uint32_t* cursor, const uint64_t* seg_off, uint32_t* blockrows) {
-  extern __shared__ uint32_t s_nodes[];
+__global__ void k_relabel(uint32_t* node_of_row, uint64_t n, const int32_t* split_of_node,
+                          uint32_t node_lo, uint32_t lut_n, const SplitD* sp, const uint32_t* vid,
+                          uint32_t m, uint32_t* cursor, const uint64_t* seg_off,
+                          uint32_t* blockrows) {
+  // split_of_node[node - node_lo]: this level's split index of a node (-1:
+  // not split), staged in shared memory when it fits
+  extern __shared__ int32_t s_lut[];
+  __shared__ int32_t s_key[kRelabelBlock];
+  __shared__ uint32_t s_cnt[kRelabelBlock], s_base[kRelabelBlock];
+  s_key[threadIdx.x] = -1;
+  s_cnt[threadIdx.x] = 0;
   const uint32_t lane = threadIdx.x & 31;
-  const bool staged = ns <= kRelabelSmem;
-  if (staged) {
-    for (uint32_t i = threadIdx.x; i < ns; i += blockDim.x) s_nodes[i] = split_nodes[i];
-    __syncthreads();
-  }
-  const uint32_t* tab = staged ? s_nodes : split_nodes;
+  const bool staged = lut_n <= kRelabelSmem;
+  if (staged)
+    for (uint32_t i = threadIdx.x; i < lut_n; i += blockDim.x) s_lut[i] = split_of_node[i];
+  __syncthreads();
+  const int32_t* tab = staged ? s_lut : split_of_node;
   for (uint64_t base = blockIdx.x * uint64_t(blockDim.x); base < n;
        base += uint64_t(gridDim.x) * blockDim.x) {
     const uint64_t r = base + threadIdx.x;
@@ -438,31 +445,51 @@ __global__ void k_relabel(uint32_t* node_of_row, uint64_t n, const uint32_t* spl
     bool inb = false;
     if (r < n) {
       const uint32_t node = node_of_row[r];
-      uint32_t lo = 0, hi = ns;
-      while (lo < hi) {
-        const uint32_t mid = (lo + hi) >> 1;
-        if (tab[mid] < node) lo = mid + 1;
-        else hi = mid;
-      }
-      if (lo < ns && tab[lo] == node) {
-        j = int32_t(lo);
+      const uint32_t k = node - node_lo;  // wraps for nodes below node_lo
+      if (k < lut_n) j = tab[k];
+      if (j >= 0) {
         const SplitD& d = sp[j];
         inb = vid[r * m + d.col] == d.vid;
         node_of_row[r] = inb ? d.block_id : d.rest_id;
         if (!d.need_rows) inb = false;
       }
     }
-    // warp-aggregated append of block rows to their split's segment
+    // Append of block rows to their split's segment, aggregated per warp
+    // (__match_any_sync) and then per block (a shared table keyed by split):
+    // one global atomic per split per block instead of one per warp — the
+    // rows of a level's large splits otherwise serialise on its cursor.
     const unsigned active = __ballot_sync(0xffffffffu, inb);
+    unsigned peers = 0;
+    int leader = 0;
+    uint32_t slot = 0, off = 0;
     if (inb) {
-      const unsigned peers = __match_any_sync(active, j);
-      const int leader = __ffs(peers) - 1;
-      uint32_t basepos = 0;
-      if (int(lane) == leader) basepos = atomicAdd(&cursor[j], uint32_t(__popc(peers)));
+      peers = __match_any_sync(active, j);
+      leader = __ffs(peers) - 1;
+      if (int(lane) == leader) {
+        slot = uint32_t(j) & (kRelabelBlock - 1);
+        for (;;) {  // at most kRelabelBlock distinct splits per block: never full
+          const int32_t prev = atomicCAS(&s_key[slot], -1, j);
+          if (prev == -1 || prev == j) break;
+          slot = (slot + 1) & (kRelabelBlock - 1);
+        }
+        off = atomicAdd(&s_cnt[slot], uint32_t(__popc(peers)));
+      }
+    }
+    __syncthreads();
+    {
+      const int32_t key = s_key[threadIdx.x];
+      if (key >= 0) s_base[threadIdx.x] = atomicAdd(&cursor[key], s_cnt[threadIdx.x]);
+    }
+    __syncthreads();
+    if (inb) {
+      uint32_t basepos = int(lane) == leader ? s_base[slot] + off : 0u;
       basepos = __shfl_sync(peers, basepos, leader);
       const uint32_t rank = __popc(peers & ((1u << lane) - 1));
       blockrows[seg_off[j] + basepos + rank] = uint32_t(r);
     }
+    __syncthreads();
+    s_key[threadIdx.x] = -1;
+    s_cnt[threadIdx.x] = 0;
   }
 }
 
@@ -1186,19 +1213,25 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
                                     std::min(seg[j + 1], lo + kRowsPerTask)});
         }
       }
+      // dense node -> split index table over this level's node id range
+      const uint32_t node_lo = split_nodes.front();
+      const uint32_t lut_n = split_nodes.back() - node_lo + 1;
+      std::vector<int32_t> lut(lut_n, -1);
+      for (uint32_t j = 0; j < ns; ++j) lut[split_nodes[j] - node_lo] = int32_t(j);
       Pack sp;
-      const size_t o_sp = sp.add(hsp), o_seg = sp.add(seg), o_sn = sp.add(split_nodes);
+      const size_t o_sp = sp.add(hsp), o_seg = sp.add(seg), o_sn = sp.add(lut);
       const size_t o_tasks = sp.add(tasks);
       const size_t o_cursor = sp.add(std::vector<uint32_t>(ns, 0u));
       uint8_t* ds = upload(sp);
       auto* d_sp = reinterpret_cast<SplitD*>(ds + o_sp);
       auto* d_seg = reinterpret_cast<uint64_t*>(ds + o_seg);
-      auto* d_snodes = reinterpret_cast<uint32_t*>(ds + o_sn);
+      auto* d_lut = reinterpret_cast<int32_t*>(ds + o_sn);
       auto* d_cursor = reinterpret_cast<uint32_t*>(ds + o_cursor);
       DevBuf<uint32_t> blockrows(std::max<uint64_t>(1, seg[ns]), s);
-      PO_LAUNCH(k_relabel, grid_for(n, 256), 256, ns <= kRelabelSmem ? ns * 4 : 0, s,
-                node_of_row.get(), n, d_snodes, ns, d_sp, e.vid.get(), m, d_cursor, d_seg,
-                blockrows.get());
+      PO_LAUNCH(k_relabel, grid_for(n, kRelabelBlock), kRelabelBlock,
+                lut_n <= kRelabelSmem ? lut_n * 4 : 0, s,
+                node_of_row.get(), n, d_lut, node_lo, lut_n, d_sp, e.vid.get(), m, d_cursor,
+                d_seg, blockrows.get());
       if (!dist && !tasks.empty())
         PO_LAUNCH(k_aggregate, unsigned(tasks.size()), kAggBlock, 0, s,
                   reinterpret_cast<AggTask*>(ds + o_tasks), blockrows.get(), d_sp, e.vid.get(),
