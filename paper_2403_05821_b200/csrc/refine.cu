@@ -190,6 +190,41 @@ bool two_words_round0() {  // experiment knob: two key words in round 0 too
   return on;
 }
 
+// Round-0 string keys of at most this many items are sorted by one merge
+// sort on the 128-bit (word A, word B) key instead of two 64-bit radix sorts
+// (16 onesweep passes, latency-bound at these sizes). PO_MERGE_ROUND0_MAX.
+uint32_t merge_round0_max() {
+  static const uint32_t v = [] {
+    const char* e = std::getenv("PO_MERGE_ROUND0_MAX");
+    return e && *e ? uint32_t(std::strtoul(e, nullptr, 10)) : (1u << 19);
+  }();
+  return v;
+}
+
+struct Key128 {
+  uint64_t a, b;
+};
+struct Less128 {
+  __device__ __forceinline__ bool operator()(const Key128& x, const Key128& y) const {
+    return x.a < y.a || (x.a == y.a && x.b < y.b);
+  }
+};
+
+__global__ void k_pack128(const uint64_t* a, const uint64_t* b, const uint32_t* items, uint32_t n,
+                          Key128* k, uint32_t* v) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    k[i] = Key128{a[i], b[i]};
+    v[i] = items[i];
+  }
+}
+
+__global__ void k_unpack128(const Key128* k, uint32_t n, uint64_t* a, uint64_t* b) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    a[i] = k[i].a;
+    b[i] = k[i].b;
+  }
+}
+
 bool seg_radix_rows() {  // experiment knob: row-key rounds by radix with segment prefix
   static const bool on = [] {
     const char* v = std::getenv("PO_SEGRADIX_ROWS");
@@ -526,7 +561,25 @@ void refine_sort_multi(const std::vector<RefineJob>& specs, cudaStream_t s) {
                                                           j.seg_begin.get(), j.seg_begin.get() + 1,
                                                           s));
       };
-      if (two) {
+      if (two && !seg && A <= merge_round0_max()) {
+        // one stable merge sort by (word A, word B): the same order as the
+        // two LSD passes below
+        ProfScope ps("cub_merge_sort", s);
+        DevBuf<Key128> k128(A, s);
+        PO_LAUNCH(k_pack128, grid_for(A, 256), 256, 0, s, j.keys.get(), j.kb.get(), j.items.get(),
+                  A, k128.get(), j.items2.get());
+        size_t need = 0;
+        PO_CUDA(cub::DeviceMergeSort::StableSortPairs(nullptr, need, k128.get(), j.items2.get(),
+                                                      int(A), Less128(), s));
+        if (need > j.tb) {
+          j.tmp.alloc(need, s);
+          j.tb = need;
+        }
+        PO_CUDA(cub::DeviceMergeSort::StableSortPairs(j.tmp.get(), need, k128.get(),
+                                                      j.items2.get(), int(A), Less128(), s));
+        PO_LAUNCH(k_unpack128, grid_for(A, 256), 256, 0, s, k128.get(), A, j.keys2.get(),
+                  j.kb.get());
+      } else if (two) {
         // LSD over the two words: by word B, then stably by word A
         sort_pass(j.kb.get(), j.kb2.get(), j.pos_iota.get(), j.perm1.get(), 64);
         PO_LAUNCH(k_gather_kv, grid_for(A, 256), 256, 0, s, j.perm1.get(), A, j.keys.get(),
