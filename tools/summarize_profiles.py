@@ -20,7 +20,7 @@ def launches(path, cmd):
         if len(r) <= vi or r[mi] != "gpu__time_duration.sum":
             continue
         name = r[ki].split("(")[0].replace("void ", "")
-        name = name.split("::")[-1] if "po::" in name else name[:60]
+        name = name.split("::")[-1] if name.startswith("po::") else name[:60]
         v = float(r[vi].replace(",", ""))
         unit = h[vi]
         agg[name][0] += 1
