@@ -249,11 +249,8 @@ struct Prepared {
 // compute_stats): the escaped-order rank job is not started.
 // Unique columns stay unranked (Encoded::unranked) unless PO_RANK_UNIQUE=1.
 bool rank_unique_columns() {
-  static const bool on = [] {
-    const char* v = std::getenv("PO_RANK_UNIQUE");
-    return v && *v == '1';
-  }();
-  return on;
+  const char* v = std::getenv("PO_RANK_UNIQUE");
+  return v && *v == '1';
 }
 
 void prepare(const po_table* tv, int tok, int scoring, cudaStream_t s, Prepared& p,

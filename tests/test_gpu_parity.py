@@ -119,6 +119,22 @@ def test_long_values_collisions_resolved_on_bytes(monkeypatch, bits):
         assert [f.cardinality for f in st.fields] == card.tolist()
 
 
+def test_all_columns_ranked_mode_vs_oracle(monkeypatch):
+    # PO_RANK_UNIQUE=1 ranks unique columns too (no tie-break pass)
+    monkeypatch.setenv("PO_RANK_UNIQUE", "1")
+    rng = random.Random(21)
+    P = oracle("port")
+    for trial in range(60):
+        t = random_table(rng, 14, 4, ALPHABETS[rng.choice(list(ALPHABETS))], max_len=4, min_len=0)
+        cfg = rng.choice([po.GgrConfig(), po.exact_config(), po.GgrConfig(0, 0, 0)])
+        assert same_result(po.ggr(t, None, cfg), P.ggr(t, None, cfg)), trial
+        m = t.field_count()
+        order = list(range(m))
+        rng.shuffle(order)
+        assert (po.sort_rows_fixed_order(t, order).row_ids.tolist()
+                == P.sort_rows_fixed_order(t, order).tolist())
+
+
 def test_phc_hit_random_schedules_vs_oracle():
     rng = random.Random(42)
     P = oracle("port")
