@@ -1476,6 +1476,21 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
   RK.key_kind = d_kk.get();
   RK.key_bits = d_kb.get();
   timing_mark("layout", s);
+  if (debug_timing()) {  // rows per leaf kind and key width of the leaf sort
+    uint64_t rows_by_kind[8] = {0};
+    uint32_t leaves_by_kind[8] = {0};
+    for (uint32_t l = 0; l < nleaves; ++l) {
+      const Node& nd = nodes[leaf_nodes[l]];
+      rows_by_kind[nd.kind] += nd.size;
+      leaves_by_kind[nd.kind]++;
+    }
+    fprintf(stderr, "[po leaves] %u leaves; rows/leaves by kind:", nleaves);
+    const char* kn[] = {"scan", "empty", "rowid", "single", "raw1", "fallback", "split"};
+    for (int k = 0; k < 7; ++k)
+      if (leaves_by_kind[k])
+        fprintf(stderr, " %s %llu/%u", kn[k], (unsigned long long)rows_by_kind[k], leaves_by_kind[k]);
+    fprintf(stderr, "; chunk bits round0 %u later %u\n", ks.widest0, ks.widest);
+  }
   RefineJob leaf_job;
   leaf_job.n_items = uint32_t(n);
   leaf_job.d_grp_init = row_leaf.get();  // round 0: leaf index
