@@ -731,15 +731,23 @@ __global__ void k_row_leaf(const uint32_t* node_of_row, uint64_t n, const uint32
   }
 }
 
-__global__ void k_emit(const uint32_t* pos, uint64_t n, uint32_t m, const uint32_t* row_leaf,
-                       const int32_t* leaf_orders, uint32_t* rows_out, int32_t* orders_out) {
+__global__ void k_emit(const uint32_t* pos, uint64_t n, uint32_t* rows_out) {
   for (uint64_t r = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; r < n;
-       r += uint64_t(gridDim.x) * blockDim.x) {
-    const uint32_t p = pos[r];
-    rows_out[p] = uint32_t(r);
-    const int32_t* src = leaf_orders + uint64_t(row_leaf[r]) * m;
-    int32_t* dst = orders_out + uint64_t(p) * m;
-    for (uint32_t f = 0; f < m; ++f) dst[f] = src[f];
+       r += uint64_t(gridDim.x) * blockDim.x)
+    rows_out[pos[r]] = uint32_t(r);
+}
+
+// Field orders in schedule order, one thread per output entry (coalesced
+// writes; the row's leaf order is a small cached table).
+__global__ void k_emit_orders(const uint32_t* rows, uint64_t n, uint32_t m,
+                              const uint32_t* row_leaf, const int32_t* leaf_orders,
+                              int32_t* orders_out) {
+  const uint64_t total = n * m;
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < total;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t p = i / m;
+    const uint32_t f = uint32_t(i - p * m);
+    orders_out[i] = leaf_orders[uint64_t(row_leaf[rows[p]]) * m + f];
   }
 }
 
@@ -1573,8 +1581,9 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
     sync(s);
     if (hb) fprintf(stderr, "[po debug] leaf sort positions: %llu collisions/out of range\n", hb);
   }
-  PO_LAUNCH(k_emit, grid_for(n, 256), 256, 0, s, pos.get(), n, m, row_leaf.get(),
-            d_leaf_orders.get(), d_rows, d_orders);
+  PO_LAUNCH(k_emit, grid_for(n, 256), 256, 0, s, pos.get(), n, d_rows);
+  PO_LAUNCH(k_emit_orders, grid_for(n * m, 256), 256, 0, s, d_rows, n, m, row_leaf.get(),
+            d_leaf_orders.get(), d_orders);
   out.phc = phc_device(e, n, nullptr, d_rows, nullptr, d_orders, s);
   timing_mark("emit_phc", s);
 
