@@ -159,6 +159,68 @@ struct PinnedArena {
 thread_local PinnedArena g_pin;
 }  // namespace
 
+namespace {
+struct CachedBlock {
+  void* p = nullptr;
+  size_t bytes = 0;
+  int device = 0;
+  bool busy = false;
+  cudaEvent_t released = nullptr;  // recorded on the releasing stream
+  cudaStream_t last = nullptr;
+};
+std::mutex g_blocks_mu;
+std::vector<CachedBlock> g_blocks;
+}  // namespace
+
+void* cached_block_acquire(size_t bytes, cudaStream_t s) {
+  int dev = 0;
+  PO_CUDA(cudaGetDevice(&dev));
+  bytes = (bytes + (2u << 20) - 1) & ~size_t((2u << 20) - 1);
+  std::lock_guard<std::mutex> lk(g_blocks_mu);
+  CachedBlock* best = nullptr;
+  for (auto& b : g_blocks)  // best fit among free blocks of at most twice the size
+    if (!b.busy && b.device == dev && b.bytes >= bytes && b.bytes <= 2 * bytes &&
+        (!best || b.bytes < best->bytes))
+      best = &b;
+  if (best) {
+    if (best->last != s) PO_CUDA(cudaStreamWaitEvent(s, best->released, 0));
+    best->busy = true;
+    return best->p;
+  }
+  CachedBlock b;
+  b.bytes = bytes;
+  b.device = dev;
+  b.busy = true;
+  if (cudaMalloc(&b.p, bytes) != cudaSuccess) {
+    (void)cudaGetLastError();
+    // free the idle cached blocks of this device and retry once
+    PO_CUDA(cudaDeviceSynchronize());
+    for (auto it = g_blocks.begin(); it != g_blocks.end();)
+      if (!it->busy && it->device == dev) {
+        cudaFree(it->p);
+        cudaEventDestroy(it->released);
+        it = g_blocks.erase(it);
+      } else {
+        ++it;
+      }
+    PO_CUDA(cudaMalloc(&b.p, bytes));
+  }
+  PO_CUDA(cudaEventCreateWithFlags(&b.released, cudaEventDisableTiming));
+  g_blocks.push_back(b);
+  return b.p;
+}
+
+void cached_block_release(void* p, cudaStream_t s) {
+  std::lock_guard<std::mutex> lk(g_blocks_mu);
+  for (auto& b : g_blocks)
+    if (b.p == p) {
+      cudaEventRecord(b.released, s);
+      b.last = s;
+      b.busy = false;
+      return;
+    }
+}
+
 void h2d_async(void* dst, const void* src, size_t bytes, cudaStream_t s) {
   if (!bytes) return;
   PinnedArena& a = g_pin;

@@ -83,6 +83,14 @@ inline unsigned grid_for(uint64_t work, unsigned block, unsigned max_waves = 16)
 constexpr size_t kPinnedSmallCopy = 1 << 20;
 void h2d_async(void* dst, const void* src, size_t bytes, cudaStream_t s);
 
+// Large transient buffers (the dictionary tables, per-cell arrays) come from
+// a per-device cache of cudaMalloc'd blocks that are never returned to the
+// driver: a block is reused by the next call that needs one of about its size
+// (the new stream waits on an event recorded where the block was released),
+// so repeated calls map no memory. Returns the block's pointer.
+void* cached_block_acquire(size_t bytes, cudaStream_t s);
+void cached_block_release(void* p, cudaStream_t s);
+
 // ---------------------------------------------------------------------------
 // stream-ordered device buffer (cudaMallocAsync on the call's stream)
 // ---------------------------------------------------------------------------
@@ -101,8 +109,10 @@ class DevBuf {
       p_ = o.p_;
       n_ = o.n_;
       s_ = o.s_;
+      cached_ = o.cached_;
       o.p_ = nullptr;
       o.n_ = 0;
+      o.cached_ = false;
     }
     return *this;
   }
@@ -112,6 +122,16 @@ class DevBuf {
     n_ = n;
     if (n) PO_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p_), n * sizeof(T) + 64, s));
   }
+  // the same from the block cache (cached_block_acquire)
+  void alloc_cached(size_t n, cudaStream_t s) {
+    release();
+    s_ = s;
+    n_ = n;
+    if (n) {
+      p_ = static_cast<T*>(cached_block_acquire(n * sizeof(T) + 64, s));
+      cached_ = true;
+    }
+  }
   void zero() {
     if (n_) PO_CUDA(cudaMemsetAsync(p_, 0, n_ * sizeof(T), s_));
   }
@@ -119,9 +139,13 @@ class DevBuf {
     if (n_) PO_CUDA(cudaMemsetAsync(p_, v, n_ * sizeof(T), s_));
   }
   void release() {
-    if (p_) cudaFreeAsync(p_, s_);
+    if (p_) {
+      if (cached_) cached_block_release(p_, s_);
+      else cudaFreeAsync(p_, s_);
+    }
     p_ = nullptr;
     n_ = 0;
+    cached_ = false;
   }
   T* get() const { return p_; }
   size_t size() const { return n_; }
@@ -136,6 +160,7 @@ class DevBuf {
   T* p_ = nullptr;
   size_t n_ = 0;
   cudaStream_t s_ = nullptr;
+  bool cached_ = false;
 };
 
 template <class T>

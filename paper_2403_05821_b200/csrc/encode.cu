@@ -961,12 +961,17 @@ void encode(const DeviceTable& t, int tok, int scoring, cudaStream_t s, Encoded&
   while (cap < 2 * n) cap <<= 1;
   const uint8_t* arena_end = t.arena + t.arena_bytes;
 
-  DevBuf<unsigned long long> keys(m * cap, s);
+  // the large transient tables come from the block cache (common.cuh)
+  DevBuf<unsigned long long> keys;
+  keys.alloc_cached(m * cap, s);
   keys.zero();
-  DevBuf<uint32_t> reps(m * cap, s);
+  DevBuf<uint32_t> reps;
+  reps.alloc_cached(m * cap, s);
   reps.fill_bytes(0xFF);
-  DevBuf<unsigned long long> repoffs(m * cap, s);
-  DevBuf<uint32_t> slot_of_cell(cells, s);
+  DevBuf<unsigned long long> repoffs;
+  repoffs.alloc_cached(m * cap, s);
+  DevBuf<uint32_t> slot_of_cell;
+  slot_of_cell.alloc_cached(cells, s);
   uint64_t hmask = hash_bits_debug >= 64 ? ~uint64_t(0) : ((uint64_t(1) << hash_bits_debug) - 1);
   {
     // K1: hash every cell. Tiles of whole rows sized so a typical tile uses
@@ -985,7 +990,8 @@ void encode(const DeviceTable& t, int tok, int scoring, cudaStream_t s, Encoded&
                                    int(smem)));
       attr_set = int(smem);
     }
-    DevBuf<unsigned long long> hashes(cells, s);
+    DevBuf<unsigned long long> hashes;
+    hashes.alloc_cached(cells, s);
     // cols (default) | seg (TMA ring, group per cell) | tile (TMA, thread per cell)
     const char* hk = std::getenv("PO_HASH_KERNEL");
     const std::string hsel = hk && *hk ? hk : "cols";
@@ -1036,7 +1042,8 @@ void encode(const DeviceTable& t, int tok, int scoring, cudaStream_t s, Encoded&
     // K2a/K2b: probe + claim, then byte verification of every duplicate
     PO_LAUNCH(k_dict_probe, grid_for(cells, 256, 32), 256, 0, s, hashes.get(), t.offsets, cells,
               uint32_t(m), cap, keys.get(), reps.get(), repoffs.get(), slot_of_cell.get());
-    DevBuf<uint32_t> collided(cells, s), ncol(1, s);
+    DevBuf<uint32_t> collided, ncol(1, s);
+    collided.alloc_cached(cells, s);
     ncol.zero();
     PO_LAUNCH(k_dict_verify, grid_for(((n + 31) / 32) * 32, 256, 8), 256, 0, s, t.arena,
               arena_end, t.offsets, n, uint32_t(m), cap, reps.get(), repoffs.get(), slot_of_cell.get(),
@@ -1051,7 +1058,8 @@ void encode(const DeviceTable& t, int tok, int scoring, cudaStream_t s, Encoded&
   // Distinct values per column (occupied slots): every column is compacted
   // into its own region of `stage` without host round trips, then one D2H of
   // the m counts gives the cardinalities and the packed layout.
-  DevBuf<uint32_t> stage_sel(m * cap, s);
+  DevBuf<uint32_t> stage_sel;
+  stage_sel.alloc_cached(m * cap, s);
   DevBuf<int> nsel(m, s);
   nsel.zero();
   {
@@ -1142,7 +1150,8 @@ void encode(const DeviceTable& t, int tok, int scoring, cudaStream_t s, Encoded&
   }
   timing_mark("rank_sort", s);
 
-  DevBuf<uint32_t> slot2vid(m * cap, s), col_by_pos(D, s);
+  DevBuf<uint32_t> slot2vid, col_by_pos(D, s);
+  slot2vid.alloc_cached(m * cap, s);
   e.rep_row.alloc(D, s);
   timing_mark("scatter_alloc", s);
   PO_LAUNCH(k_scatter_pos, grid_for(D, 256), 256, 0, s, esc_pos.get(), d_col.get(), d_row.get(),
