@@ -122,6 +122,11 @@ class DevBuf {
     n_ = n;
     if (n) PO_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p_), n * sizeof(T) + 64, s));
   }
+  // large buffers (>= 16 MB) from the block cache, others from the pool
+  void alloc_auto(size_t n, cudaStream_t s) {
+    if (n * sizeof(T) >= (16u << 20)) alloc_cached(n, s);
+    else alloc(n, s);
+  }
   // the same from the block cache (cached_block_acquire)
   void alloc_cached(size_t n, cudaStream_t s) {
     release();

@@ -440,31 +440,31 @@ void refine_sort_multi(const std::vector<RefineJob>& specs, cudaStream_t s) {
     j->end_bit = 64;
     if (j->key.kind == 1) ensure_esc_table();
     const uint32_t n = sp.n_items;
-    j->items.alloc(n, s);
-    j->items2.alloc(n, s);
-    j->grp.alloc(n, s);
-    j->keys.alloc(n, s);
-    j->keys2.alloc(n, s);
-    j->pk.alloc(n, s);
-    j->pk2.alloc(n, s);
-    j->starts.alloc(n, s);
-    j->keep.alloc(n, s);
-    j->segflags.alloc(n, s);
-    j->seg_begin.alloc(n + 1, s);
-    j->segidx.alloc(n, s);
+    j->items.alloc_auto(n, s);
+    j->items2.alloc_auto(n, s);
+    j->grp.alloc_auto(n, s);
+    j->keys.alloc_auto(n, s);
+    j->keys2.alloc_auto(n, s);
+    j->pk.alloc_auto(n, s);
+    j->pk2.alloc_auto(n, s);
+    j->starts.alloc_auto(n, s);
+    j->keep.alloc_auto(n, s);
+    j->segflags.alloc_auto(n, s);
+    j->seg_begin.alloc_auto(n + 1, s);
+    j->segidx.alloc_auto(n, s);
     PO_LAUNCH(k_iota, grid_for(n, 256), 256, 0, s, j->items.get(), n);
     if (j->key.kind != 2) {
-      j->kb.alloc(n, s);
-      j->kb2.alloc(n, s);
-      j->k1g.alloc(n, s);
-      j->perm1.alloc(n, s);
-      j->perm2.alloc(n, s);
-      j->pos_iota.alloc(n, s);
-      j->itg.alloc(n, s);
-      j->item_off.alloc(n, s);
+      j->kb.alloc_auto(n, s);
+      j->kb2.alloc_auto(n, s);
+      j->k1g.alloc_auto(n, s);
+      j->perm1.alloc_auto(n, s);
+      j->perm2.alloc_auto(n, s);
+      j->pos_iota.alloc_auto(n, s);
+      j->itg.alloc_auto(n, s);
+      j->item_off.alloc_auto(n, s);
       j->item_off.zero();
-      j->head.alloc(n, s);
-      j->seg_skip.alloc(n, s);
+      j->head.alloc_auto(n, s);
+      j->seg_skip.alloc_auto(n, s);
       j->key.item_off = j->item_off.get();
       PO_LAUNCH(k_iota, grid_for(n, 256), 256, 0, s, j->pos_iota.get(), n);
     }
