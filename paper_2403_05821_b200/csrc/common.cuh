@@ -168,6 +168,14 @@ class DevBuf {
   bool cached_ = false;
 };
 
+// a buffer from alloc_auto (block cache when large)
+template <class T>
+DevBuf<T> dev_auto(size_t n, cudaStream_t s) {
+  DevBuf<T> b;
+  b.alloc_auto(n, s);
+  return b;
+}
+
 template <class T>
 DevBuf<T> to_device(const std::vector<T>& v, cudaStream_t s) {
   DevBuf<T> d(v.size(), s);

@@ -1152,7 +1152,7 @@ void encode(const DeviceTable& t, int tok, int scoring, cudaStream_t s, Encoded&
 
   DevBuf<uint32_t> slot2vid, col_by_pos(D, s);
   slot2vid.alloc_cached(m * cap, s);
-  e.rep_row.alloc(D, s);
+  e.rep_row.alloc_auto(D, s);
   timing_mark("scatter_alloc", s);
   PO_LAUNCH(k_scatter_pos, grid_for(D, 256), 256, 0, s, esc_pos.get(), d_col.get(), d_row.get(),
             sel.get(), e.d_colbase.get(), D, cap, slot2vid.get(), e.rep_row.get(),
@@ -1178,20 +1178,20 @@ void encode(const DeviceTable& t, int tok, int scoring, cudaStream_t s, Encoded&
   }
   (void)word_count_host;
   DevBuf<uint64_t> d_nchar = to_device(nchar, s), d_nword = to_device(nword, s);
-  e.vlen.alloc(D, s);
+  e.vlen.alloc_auto(D, s);
   PO_LAUNCH(k_vlen, grid_for(D, 256), 256, 0, s, t.arena, t.offsets, t.cell_lens,
             e.rep_row.get(), col_by_pos.get(), D, uint32_t(m), tok, scoring, d_nchar.get(),
             d_nword.get(), e.vlen.get());
 
   timing_mark("vlen", s);
   // vid matrix (row-major) and occurrence counts.
-  e.vid.alloc(cells, s);
+  e.vid.alloc_auto(cells, s);
   PO_LAUNCH(k_vid, grid_for(cells, 256), 256, 0, s, slot_of_cell.get(), slot2vid.get(), n,
             uint32_t(m), cap, e.vid.get());
   slot_of_cell.release();
   slot2vid.release();
   timing_mark("vid", s);
-  e.count.alloc(D, s);
+  e.count.alloc_auto(D, s);
   e.count.zero();
   {
     std::vector<uint32_t> soff(m, kLargeCol);

@@ -885,7 +885,7 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
     root.kind = classify(root, cfg);
     nodes.push_back(std::move(root));
   }
-  DevBuf<uint32_t> node_of_row(n, s);
+  DevBuf<uint32_t> node_of_row = dev_auto<uint32_t>(n, s);
   node_of_row.zero();
 
   // Work items over a node's table: dense tables are cut at column
@@ -1467,7 +1467,8 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
   auto d_kf = to_device(key_field, s);
   auto d_kk = to_device(key_kind, s), d_kb = to_device(key_bits, s);
   auto d_leaf_orders = to_device(h_leaf_orders, s);
-  DevBuf<uint32_t> row_leaf(n, s), grp(n, s), pos(n, s);
+  DevBuf<uint32_t> row_leaf = dev_auto<uint32_t>(n, s), grp = dev_auto<uint32_t>(n, s),
+                   pos = dev_auto<uint32_t>(n, s);
   PO_LAUNCH(k_row_leaf, grid_for(n, 256), 256, 0, s, node_of_row.get(), n, d_node_leaf.get(),
             d_leaf_off.get(), row_leaf.get(), grp.get());
   RefineKey RK;

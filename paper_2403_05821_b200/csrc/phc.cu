@@ -236,8 +236,8 @@ uint64_t fixed_order_phc_device(const Encoded& e, const std::vector<int>& order,
     uint64_t cap = 1;
     while (cap < 2 * n) cap <<= 1;
     if (cap > (1ull << 32)) fail(PO_ERR_SIZE, "table too large for the fallback group table");
-    DevBuf<uint32_t> gid(n, s);
-    DevBuf<unsigned long long> keys(cap, s);
+    DevBuf<uint32_t> gid = dev_auto<uint32_t>(n, s);
+    DevBuf<unsigned long long> keys = dev_auto<unsigned long long>(cap, s);
     DevBuf<unsigned long long> ng(order.size(), s);
     ng.zero();
     const unsigned long long c0 = e.card[f0];
@@ -372,7 +372,8 @@ void break_unranked_ties(const Encoded& e, const TieSpec& ts, const uint32_t* ro
   std::vector<int32_t> kf = ts.key_fields;
   if (kf.empty()) kf.push_back(0);
   auto d_kf = to_device(kf, s);
-  DevBuf<uint32_t> perm(n, s), run(n, s), items(n, s);
+  DevBuf<uint32_t> perm = dev_auto<uint32_t>(n, s), run = dev_auto<uint32_t>(n, s),
+                   items = dev_auto<uint32_t>(n, s);
   PO_LAUNCH(k_invert, grid_for(n, 256), 256, 0, s, pos, n, perm.get());
   timing_mark("ties_setup", s);
   PO_LAUNCH(k_tie_heads, grid_for(n, 256), 256, 0, s, perm.get(), n, e.m, e.vid.get(), row_leaf,
@@ -386,7 +387,7 @@ void break_unranked_ties(const Encoded& e, const TieSpec& ts, const uint32_t* ro
   // short runs: each position ranks itself against its run (quadratic, no
   // sort); long runs: a kind-1 string refine job
   const uint32_t max_short = short_run_max();
-  DevBuf<uint32_t> run_len(n, s);
+  DevBuf<uint32_t> run_len = dev_auto<uint32_t>(n, s);
   PO_LAUNCH(k_run_len, grid_for(n, 256), 256, 0, s, run.get(), n, run_len.get());
   timing_mark("ties_runs", s);
   rank_short_runs(e.arena, e.offsets, e.m, perm.get(), run.get(), run_len.get(), row_leaf,
