@@ -415,10 +415,15 @@ __global__ void __launch_bounds__(256) k_cell_hash_cols(
     const uint32_t sh = uint32_t(ad & 7) * 8;
     const uint64_t words = (len + 7) / 8;
     uint64_t sum = 0;
+    // the last aligned word of a step is the first of the next: carried in a
+    // register (four loads per four words)
+    uint64_t carry = (words && p < lim) ? __ldg(p) : 0;
     for (uint64_t k = 0; k < words; k += 4) {
       uint64_t w[5];
+      w[0] = carry;
 #pragma unroll
-      for (int u = 0; u < 5; ++u) w[u] = (p + k + u < lim) ? __ldg(p + k + u) : 0;
+      for (int u = 1; u < 5; ++u) w[u] = (p + k + u < lim) ? __ldg(p + k + u) : 0;
+      carry = w[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const uint64_t kk = k + u;
