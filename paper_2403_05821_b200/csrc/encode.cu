@@ -489,6 +489,36 @@ __global__ void __launch_bounds__(256) k_dict_probe(
 struct Step4 {
   uint64_t w[4];
 };
+// Four words of a byte string from five aligned words, the first passed in
+// (the previous step's last one) and the new last one handed back: four
+// loads per step.
+__device__ __forceinline__ Step4 load_step4_carry(const uint64_t* p, uint32_t sh,
+                                                  const uint64_t* lim, uint64_t& carry) {
+  uint64_t a[5];
+  a[0] = carry;
+#pragma unroll
+  for (int u = 1; u < 5; ++u) a[u] = (p + u < lim) ? __ldg(p + u) : 0;
+  carry = a[4];
+  Step4 r;
+#pragma unroll
+  for (int u = 0; u < 4; ++u) r.w[u] = sh ? ((a[u] >> sh) | (a[u + 1] << (64 - sh))) : a[u];
+  return r;
+}
+// Four words of a byte string from five aligned words, the first passed in
+// (the previous step's last one) and the new last one handed back: four
+// loads per step.
+__device__ __forceinline__ Step4 load_step4_carry(const uint64_t* p, uint32_t sh,
+                                                  const uint64_t* lim, uint64_t& carry) {
+  uint64_t a[5];
+  a[0] = carry;
+#pragma unroll
+  for (int u = 1; u < 5; ++u) a[u] = (p + u < lim) ? __ldg(p + u) : 0;
+  carry = a[4];
+  Step4 r;
+#pragma unroll
+  for (int u = 0; u < 4; ++u) r.w[u] = sh ? ((a[u] >> sh) | (a[u + 1] << (64 - sh))) : a[u];
+  return r;
+}
 __device__ __forceinline__ Step4 load_step4(const uint64_t* p, uint32_t sh, const uint64_t* lim) {
   uint64_t a[5];
 #pragma unroll
@@ -536,9 +566,10 @@ __global__ void __launch_bounds__(256) k_dict_verify(
       const uint64_t* pb = reinterpret_cast<const uint64_t*>(bb & ~uintptr_t(7));
       const uint32_t sa = uint32_t(aa & 7) * 8, sb = uint32_t(bb & 7) * 8;
       const uint64_t words = (len + 7) / 8;
+      uint64_t ca = pa < lim ? __ldg(pa) : 0, cb = pb < lim ? __ldg(pb) : 0;
       for (uint64_t k = 0; k < words && eq; k += 4) {
-        const Step4 x = load_step4(pa + k, sa, lim);
-        const Step4 y = load_step4(pb + k, sb, lim);
+        const Step4 x = load_step4_carry(pa + k, sa, lim, ca);
+        const Step4 y = load_step4_carry(pb + k, sb, lim, cb);
         uint64_t d = 0;
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
