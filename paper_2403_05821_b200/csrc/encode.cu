@@ -485,7 +485,7 @@ __global__ void __launch_bounds__(256) k_dict_probe(
 // step). A mismatch — two different strings with the same 64-bit hash —
 // flags the cell for K2c.
 // ---------------------------------------------------------------------------
-// Unaligned 4-word step of a byte string: 5 independent aligned loads.
+// Unaligned 4-word step of a byte string.
 struct Step4 {
   uint64_t w[4];
 };
@@ -499,30 +499,6 @@ __device__ __forceinline__ Step4 load_step4_carry(const uint64_t* p, uint32_t sh
 #pragma unroll
   for (int u = 1; u < 5; ++u) a[u] = (p + u < lim) ? __ldg(p + u) : 0;
   carry = a[4];
-  Step4 r;
-#pragma unroll
-  for (int u = 0; u < 4; ++u) r.w[u] = sh ? ((a[u] >> sh) | (a[u + 1] << (64 - sh))) : a[u];
-  return r;
-}
-// Four words of a byte string from five aligned words, the first passed in
-// (the previous step's last one) and the new last one handed back: four
-// loads per step.
-__device__ __forceinline__ Step4 load_step4_carry(const uint64_t* p, uint32_t sh,
-                                                  const uint64_t* lim, uint64_t& carry) {
-  uint64_t a[5];
-  a[0] = carry;
-#pragma unroll
-  for (int u = 1; u < 5; ++u) a[u] = (p + u < lim) ? __ldg(p + u) : 0;
-  carry = a[4];
-  Step4 r;
-#pragma unroll
-  for (int u = 0; u < 4; ++u) r.w[u] = sh ? ((a[u] >> sh) | (a[u + 1] << (64 - sh))) : a[u];
-  return r;
-}
-__device__ __forceinline__ Step4 load_step4(const uint64_t* p, uint32_t sh, const uint64_t* lim) {
-  uint64_t a[5];
-#pragma unroll
-  for (int u = 0; u < 5; ++u) a[u] = (p + u < lim) ? __ldg(p + u) : 0;
   Step4 r;
 #pragma unroll
   for (int u = 0; u < 4; ++u) r.w[u] = sh ? ((a[u] >> sh) | (a[u + 1] << (64 - sh))) : a[u];
