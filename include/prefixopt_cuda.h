@@ -251,6 +251,13 @@ const char* po_build_info(void);
  * incremented at each launch site; used by bench.py's gpu_launches). */
 uint64_t po_kernel_launch_count(void);
 
+/* Large transient device buffers are kept in a per-device block cache
+ * between calls (no memory is mapped on repeated calls). po_trim_device_cache
+ * returns the idle blocks of every device to the driver; the returned value
+ * is the number of bytes released. Safe to call at any time; blocks in use by
+ * a running call are kept. */
+uint64_t po_trim_device_cache(void);
+
 /* Per-kernel CUDA-event timing on the launching stream. po_profile_report
  * drains the recorded launches and writes "name count total_ms" lines into
  * buf (NUL-terminated, truncated to cap); returns the full length + 1. */

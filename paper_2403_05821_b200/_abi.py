@@ -189,6 +189,7 @@ class CudaLib:
         self.last_error = _bind(L, "po_last_error", C.c_char_p, [])
         self.build_info = _bind(L, "po_build_info", C.c_char_p, [])
         self.kernel_launch_count = _bind(L, "po_kernel_launch_count", C.c_uint64, [])
+        self.trim_device_cache = _bind(L, "po_trim_device_cache", C.c_uint64, [])
         self.profile_enable = _bind(L, "po_profile_enable", None, [C.c_int])
         self._profile_report = _bind(L, "po_profile_report", C.c_uint64, [C.c_char_p, C.c_uint64])
 

@@ -210,6 +210,26 @@ void* cached_block_acquire(size_t bytes, cudaStream_t s) {
   return b.p;
 }
 
+uint64_t trim_cached_blocks() {
+  std::lock_guard<std::mutex> lk(g_blocks_mu);
+  uint64_t freed = 0;
+  for (auto it = g_blocks.begin(); it != g_blocks.end();)
+    if (!it->busy) {
+      int prev = 0;
+      cudaGetDevice(&prev);
+      cudaSetDevice(it->device);
+      cudaEventSynchronize(it->released);  // its last user is done
+      cudaFree(it->p);
+      cudaEventDestroy(it->released);
+      cudaSetDevice(prev);
+      freed += it->bytes;
+      it = g_blocks.erase(it);
+    } else {
+      ++it;
+    }
+  return freed;
+}
+
 void cached_block_release(void* p, cudaStream_t s) {
   std::lock_guard<std::mutex> lk(g_blocks_mu);
   for (auto& b : g_blocks)
@@ -898,6 +918,8 @@ void po_slice_free(po_slice* slice) { delete slice; }
 const char* po_last_error(void) { return g_err.c_str(); }
 
 const char* po_build_info(void) { return "prefixopt-b200 sm_100a"; }
+
+uint64_t po_trim_device_cache(void) { return po::trim_cached_blocks(); }
 
 uint64_t po_kernel_launch_count(void) { return g_launches.load(); }
 

@@ -135,6 +135,20 @@ def test_all_columns_ranked_mode_vs_oracle(monkeypatch):
                 == P.sort_rows_fixed_order(t, order).tolist())
 
 
+def test_trim_device_cache_then_solve_again():
+    # idle cached blocks go back to the driver; the next call allocates anew
+    from paper_2403_05821_b200._abi import cuda_lib
+    rng = random.Random(8)
+    P = oracle("port")
+    t = skewed_table(rng, 3000, [3, 40, 200, 3000], [6, 12, 20, 10])
+    first = po.ggr(t, None, po.GgrConfig())
+    cuda_lib().trim_device_cache()
+    cuda_lib().trim_device_cache()  # nothing idle left: a no-op
+    again = po.ggr(t, None, po.GgrConfig())
+    assert same_result(first, again)
+    assert same_result(again, P.ggr(t, None, po.GgrConfig()))
+
+
 def test_phc_hit_random_schedules_vs_oracle():
     rng = random.Random(42)
     P = oracle("port")
