@@ -590,10 +590,11 @@ __global__ void k_dict_fixup(const uint8_t* __restrict__ arena, const uint8_t* a
 }
 
 // Occupied dictionary slots of every column, compacted per column into
-// sel[c*cap ..] (any order: the rank sort orders them). A block takes a chunk
-// of kCompactChunk slots of one column (cap is a power of two >= 64; chunks
-// never straddle columns), counts its occupied slots, reserves them with ONE
-// atomic, then writes them in order (the second read of the chunk hits L1/L2).
+// sel[c*cap ..] (any order: the rank sort orders them; unranked and
+// equality-only ids use it only as identity). A block takes a chunk of
+// kCompactChunk slots of one column (cap is a power of two >= 64; chunks never
+// straddle columns), counts its occupied slots and reserves them with ONE
+// atomic.
 constexpr uint32_t kCompactChunk = 4096;
 __global__ void __launch_bounds__(256) k_compact_slots(const unsigned long long* __restrict__ keys,
                                                        uint64_t cap, uint64_t total, uint32_t* sel,
@@ -602,6 +603,29 @@ __global__ void __launch_bounds__(256) k_compact_slots(const unsigned long long*
   __shared__ int s_base;
   const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const uint64_t chunk = cap < kCompactChunk ? cap : kCompactChunk;
+  if (chunk == kCompactChunk) {
+    // one coalesced pass: thread t owns slots c0 + u*256 + t (u < 16) as a
+    // bit mask, a block scan of the per-thread counts places them
+    typedef cub::BlockScan<int, 256> BS;
+    __shared__ typename BS::TempStorage ts;
+    for (uint64_t c0 = blockIdx.x * chunk; c0 < total; c0 += uint64_t(gridDim.x) * chunk) {
+      const uint64_t col = c0 / cap;
+      uint32_t occ = 0;
+#pragma unroll
+      for (int u = 0; u < int(kCompactChunk / 256); ++u)
+        occ |= uint32_t(keys[c0 + u * 256 + threadIdx.x] != 0) << u;
+      int before = 0, tot = 0;
+      BS(ts).ExclusiveSum(__popc(occ), before, tot);
+      if (threadIdx.x == 0) s_base = tot ? atomicAdd(&count[col], tot) : 0;
+      __syncthreads();
+      uint32_t* out = sel + col * cap + s_base + before;
+      const uint32_t rel0 = uint32_t(c0 - col * cap) + threadIdx.x;
+      for (int u = 0; occ; ++u, occ >>= 1)
+        if (occ & 1u) *out++ = rel0 + uint32_t(u) * 256u;
+      __syncthreads();  // s_base and the scan storage are reused
+    }
+    return;
+  }
   for (uint64_t c0 = blockIdx.x * chunk; c0 < total; c0 += uint64_t(gridDim.x) * chunk) {
     const uint64_t col = c0 / cap;
     int mine = 0;
