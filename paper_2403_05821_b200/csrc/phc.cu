@@ -150,12 +150,7 @@ __global__ void k_fb_depth(const uint32_t* vid, uint64_t n, uint32_t m, uint32_t
     return;
   }
   unsigned long long sum = 0, fresh = 0;
-  for (uint64_t r = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; r < n;
-       r += uint64_t(gridDim.x) * blockDim.x) {
-    const uint32_t v = vid[r * m + f];
-    const unsigned long long key = (uint64_t(gid[r]) << 32) | v;
-    const uint64_t l = vlen_col[v];
-    const unsigned long long sq = l * l;
+  auto probe = [&](unsigned long long key, unsigned long long sq) -> uint32_t {
     uint64_t slot = fmix64(key) & mask;
     for (;;) {
       unsigned long long k = keys[slot];
@@ -171,7 +166,21 @@ __global__ void k_fb_depth(const uint32_t* vid, uint64_t n, uint32_t m, uint32_t
       slot = (slot + 1) & mask;
     }
     sum += sq;
-    gid[r] = uint32_t(slot);
+    return uint32_t(slot);
+  };
+  // two rows per iteration: both rows' gathers are in flight before either
+  // probes the table
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  for (uint64_t r = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; r < n; r += 2 * stride) {
+    const uint64_t r2 = r + stride;
+    const bool two = r2 < n;
+    const uint32_t v = vid[r * m + f];
+    const uint32_t v2 = two ? vid[r2 * m + f] : 0u;
+    const unsigned long long key = (uint64_t(gid[r]) << 32) | v;
+    const unsigned long long key2 = two ? ((uint64_t(gid[r2]) << 32) | v2) : 0ull;
+    const uint64_t l = vlen_col[v], l2 = two ? vlen_col[v2] : 0;
+    gid[r] = probe(key, l * l);
+    if (two) gid[r2] = probe(key2, l2 * l2);
   }
   typedef cub::BlockReduce<unsigned long long, 256> BR;
   __shared__ typename BR::TempStorage tmp;
