@@ -390,9 +390,11 @@ __global__ void __launch_bounds__(kSegBlock, 3) k_cell_hash_seg(
 
 // K1 cell_scan (direct): one thread per cell, warps assigned column-major
 // over tiles of 32 rows so the 32 lanes of a warp hash cells of the same
-// column (similar lengths: converged loops). Each step issues 5 independent
-// aligned 8-byte loads (4 words of the cell), so every thread keeps several
-// loads in flight without any shared-memory staging or block barriers.
+// column (similar lengths: converged loops). Each step covers 4 words of the
+// cell with 4 independent aligned 8-byte loads (the fifth aligned word a
+// step needs is the previous step's last, kept in a register), so every
+// thread keeps several loads in flight without shared-memory staging or
+// block barriers.
 __global__ void __launch_bounds__(256) k_cell_hash_cols(
     const uint8_t* __restrict__ arena, const uint8_t* arena_end,
     const uint64_t* __restrict__ offsets, uint64_t n, uint32_t m, uint64_t hash_mask,
@@ -481,9 +483,9 @@ __global__ void __launch_bounds__(256) k_dict_probe(
 
 // ---------------------------------------------------------------------------
 // K2b verify: every cell whose slot is owned by another row is compared
-// byte for byte with the representative (4 independent 8-byte loads per
-// step). A mismatch — two different strings with the same 64-bit hash —
-// flags the cell for K2c.
+// byte for byte with the representative (4 words of each string per step,
+// 4 aligned loads each). A mismatch — two different strings with the same
+// 64-bit hash — flags the cell for K2c.
 // ---------------------------------------------------------------------------
 // Unaligned 4-word step of a byte string.
 struct Step4 {
@@ -511,7 +513,7 @@ __global__ void __launch_bounds__(256) k_dict_verify(
     const uint32_t* __restrict__ reps, const unsigned long long* __restrict__ repoffs,
     const uint32_t* __restrict__ slot_of_cell, uint32_t* collided, uint32_t* n_collided) {
   // Warps take 32 rows of one column (similar lengths); every lane compares
-  // its own cell with the representative, 4 words per step with all 10 loads
+  // its own cell with the representative, 4 words per step with all 8 loads
   // in flight.
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t ntiles = (n + 31) / 32;
