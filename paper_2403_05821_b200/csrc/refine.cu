@@ -412,10 +412,99 @@ void esc_code_table(uint16_t code[257]) {
 
 uint32_t refine_chunk_bits(uint32_t grp_max) { return 64u - uint32_t(bits_for(grp_max)); }
 
+namespace {
+
+// One-pass exact string sort (kinds 0 and 1, small jobs): a stable merge sort
+// of (group, first 14 symbols as two words, item) records whose comparator
+// falls back to the remaining symbols when the words tie, so no refinement
+// rounds are needed. Equal strings keep their item order (stable), exactly as
+// the refinement sort leaves them.
+struct StrRec {
+  uint32_t g, item;
+  uint64_t k0, k1;
+};
+
+__device__ __forceinline__ uint32_t sym_code(const RefineKey& K, const uint8_t* p, uint64_t len,
+                                             uint64_t pos) {
+  if (pos < len) return K.kind == 0 ? uint32_t(p[pos]) + 2 : c_esc_code[p[pos]];
+  return pos == len ? end_code(K) : 0u;
+}
+
+struct StrLess {
+  RefineKey K;
+  __device__ __forceinline__ bool operator()(const StrRec& a, const StrRec& b) const {
+    if (a.g != b.g) return a.g < b.g;
+    if (a.k0 != b.k0) return a.k0 < b.k0;
+    if (a.k1 != b.k1) return a.k1 < b.k1;
+    // symbols [14, ...) of both strings
+    const uint64_t ia = uint64_t(K.item_cell_row[a.item]) * K.m + K.item_col[a.item];
+    const uint64_t ib = uint64_t(K.item_cell_row[b.item]) * K.m + K.item_col[b.item];
+    const uint64_t oa = K.offsets[ia], ob = K.offsets[ib];
+    const uint64_t la = K.offsets[ia + 1] - oa, lb = K.offsets[ib + 1] - ob;
+    const uint8_t* pa = K.arena + oa;
+    const uint8_t* pb = K.arena + ob;
+    for (uint64_t pos = 14 + K.skip;; ++pos) {
+      const uint32_t ca = sym_code(K, pa, la, pos), cb = sym_code(K, pb, lb, pos);
+      if (ca != cb) return ca < cb;
+      if (ca == 0 || pos >= la || pos >= lb) return false;  // equal strings
+    }
+  }
+};
+
+__global__ void k_str_recs(RefineKey K, const uint32_t* grp_init, uint32_t n, StrRec* recs) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    recs[i] = StrRec{grp_init[i], i, string_chunk(K, i, 0, 7), string_chunk(K, i, 7, 7)};
+}
+
+__global__ void k_str_first(const StrRec* recs, uint32_t n, uint32_t* first) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    if (i == 0 || recs[i - 1].g != recs[i].g) first[recs[i].g] = i;
+}
+
+__global__ void k_str_place(const StrRec* recs, uint32_t n, const uint32_t* first,
+                            const uint32_t* grp_start, uint32_t* out_pos) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const uint32_t g = recs[i].g;
+    out_pos[recs[i].item] = (grp_start ? grp_start[g] : g) + (i - first[g]);
+  }
+}
+
+// PO_MERGE_RANK=0 disables the one-pass path
+bool merge_rank_enabled() {
+  const char* e = std::getenv("PO_MERGE_RANK");
+  return !(e && *e == '0');
+}
+
+}  // namespace
+
+// True when the job was sorted here (kinds 0/1 up to merge_round0_max items).
+bool merge_rank_job(const RefineJob& sp, cudaStream_t s) {
+  if (!merge_rank_enabled() || (sp.key.kind != 0 && sp.key.kind != 1) ||
+      sp.n_items > merge_round0_max() || sp.key.item_off)
+    return false;
+  if (sp.key.kind == 1) ensure_esc_table();
+  const uint32_t n = sp.n_items;
+  ProfScope ps("cub_merge_sort", s);
+  DevBuf<StrRec> recs(n, s);
+  PO_LAUNCH(k_str_recs, grid_for(n, 256), 256, 0, s, sp.key, sp.d_grp_init, n, recs.get());
+  size_t need = 0;
+  StrLess less{sp.key};
+  PO_CUDA(cub::DeviceMergeSort::StableSortKeys(nullptr, need, recs.get(), int(n), less, s));
+  DevBuf<uint8_t> tmp(need, s);
+  PO_CUDA(cub::DeviceMergeSort::StableSortKeys(tmp.get(), need, recs.get(), int(n), less, s));
+  const uint32_t ng = sp.d_grp_start ? sp.n_groups : sp.grp_max + 1;
+  DevBuf<uint32_t> first(std::max<uint32_t>(ng, 1), s);
+  PO_LAUNCH(k_str_first, grid_for(n, 256), 256, 0, s, recs.get(), n, first.get());
+  PO_LAUNCH(k_str_place, grid_for(n, 256), 256, 0, s, recs.get(), n, first.get(), sp.d_grp_start,
+            sp.d_out_pos);
+  return true;
+}
+
 void refine_sort_multi(const std::vector<RefineJob>& specs, cudaStream_t s) {
   std::vector<std::unique_ptr<Job>> jobs;
   for (const RefineJob& sp : specs) {
     if (sp.n_items == 0) continue;
+    if (merge_rank_job(sp, s)) continue;
     auto j = std::make_unique<Job>();
     j->spec = sp;
     j->key = sp.key;

@@ -119,9 +119,14 @@ def test_long_values_collisions_resolved_on_bytes(monkeypatch, bits):
         assert [f.cardinality for f in st.fields] == card.tolist()
 
 
-def test_all_columns_ranked_mode_vs_oracle(monkeypatch):
-    # PO_RANK_UNIQUE=1 ranks unique columns too (no tie-break pass)
-    monkeypatch.setenv("PO_RANK_UNIQUE", "1")
+@pytest.mark.parametrize("env", [{"PO_RANK_UNIQUE": "1"}, {"PO_MERGE_RANK": "0"},
+                                 {"PO_MERGE_RANK": "0", "PO_MERGE_ROUND0_MAX": "0"}])
+def test_alternate_sort_paths_vs_oracle(monkeypatch, env):
+    # PO_RANK_UNIQUE=1 ranks unique columns too (no tie-break pass);
+    # PO_MERGE_RANK=0 sorts small string jobs by refinement rounds instead of
+    # the one-pass merge sort (and PO_MERGE_ROUND0_MAX=0 with radix round 0)
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
     rng = random.Random(21)
     P = oracle("port")
     for trial in range(60):
