@@ -691,15 +691,25 @@ __global__ void k_scatter_sub(const uint32_t* sub_d, const uint32_t* sub_pos, ui
 }
 
 
-__global__ void k_distinct_info(const uint32_t* col_sel, uint64_t cnt, uint64_t base, uint32_t c,
-                                uint64_t cap, const uint32_t* reps, uint32_t* sel_slot,
+// Per distinct value d (column-major dictionary order): its column (binary
+// search over colbase), its slot and its representative row; one launch for
+// every column.
+__global__ void k_distinct_info(const uint32_t* stage_sel, uint64_t D, const uint64_t* colbase,
+                                uint32_t m, uint64_t cap, const uint32_t* reps, uint32_t* sel_slot,
                                 uint32_t* d_col, uint32_t* d_row) {
-  for (uint64_t d = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; d < cnt;
+  for (uint64_t d = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; d < D;
        d += uint64_t(gridDim.x) * blockDim.x) {
-    const uint32_t slot = col_sel[d];
-    sel_slot[base + d] = slot;
-    d_col[base + d] = c;
-    d_row[base + d] = reps[uint64_t(c) * cap + slot];
+    uint32_t lo = 0, hi = m;  // last c with colbase[c] <= d
+    while (hi - lo > 1) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (colbase[mid] <= d) lo = mid;
+      else hi = mid;
+    }
+    const uint32_t c = lo;
+    const uint32_t slot = stage_sel[uint64_t(c) * cap + (d - colbase[c])];
+    sel_slot[d] = slot;
+    d_col[d] = c;
+    d_row[d] = reps[uint64_t(c) * cap + slot];
   }
 }
 
@@ -1120,10 +1130,9 @@ void encode(const DeviceTable& t, int tok, int scoring, cudaStream_t s, Encoded&
 
   DevBuf<uint32_t> sel(D, s);  // per distinct (column order): slot within its column
   DevBuf<uint32_t> d_col(D, s), d_row(D, s);
-  for (uint32_t c = 0; c < m; ++c)
-    PO_LAUNCH(k_distinct_info, grid_for(e.card[c], 256), 256, 0, s,
-              stage_sel.get() + uint64_t(c) * cap, e.card[c], e.colbase[c], c, cap, reps.get(),
-              sel.get(), d_col.get(), d_row.get());
+  PO_LAUNCH(k_distinct_info, grid_for(D, 256), 256, 0, s, stage_sel.get(), D,
+            e.d_colbase.get(), uint32_t(m), cap, reps.get(), sel.get(), d_col.get(),
+            d_row.get());
   stage_sel.release();
 
   // Escaped fragment-key order (json_escape(v) + '"') of the distinct values
