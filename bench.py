@@ -159,11 +159,13 @@ def run_reference(args):
         return 0
     from paper_2403_05821_b200 import gen
     cfg_id = args.config
-    sample = args.ref_rows
+    sample = args.ref_rows if args.ref_rows is not None else gen.CONFIGS[cfg_id].rows
     table = gen.generate(cfg_id, n_rows=sample)
     fds = gen.fds(cfg_id)
+    # untimed warm-up steps on a small prefix (page-in, allocator); the timed
+    # steps run the reference on the whole configured table
     for _ in range(args.warmup):
-        cpu_reference_rows_per_s(table, fds, sample, "reference")
+        cpu_reference_rows_per_s(table, fds, min(sample, 20_000), "reference")
     rates, secs_total, kind = [], 0.0, "reference"
     for _ in range(args.steps):
         r, secs, kind, n, _res = cpu_reference_rows_per_s(table, fds, sample, "reference")
@@ -176,11 +178,14 @@ def run_reference(args):
         "ms_per_step": 1e3 * secs_total / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
         "config": {"workload": gen.CONFIGS[cfg_id].name, "rows_per_step": sample,
-                   "sample": f"first {sample} rows of {gen.CONFIGS[cfg_id].name}",
+                   "sample": (f"the whole {gen.CONFIGS[cfg_id].name} table"
+                              if sample >= gen.CONFIGS[cfg_id].rows else
+                              f"first {sample} rows of {gen.CONFIGS[cfg_id].name}"),
                    "parallelism": "single-thread CPU (the reference has no threads)"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": kind,
-                         "sample": f"first {sample} rows of {gen.CONFIGS[cfg_id].name}, "
-                                   "GgrConfig defaults, wall time from SolveStats.wall_ms"},
+                         "sample": f"{sample} rows of {gen.CONFIGS[cfg_id].name} (warm-up: "
+                                   "20K-row prefix), GgrConfig defaults, wall time from "
+                                   "SolveStats.wall_ms"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -254,13 +259,19 @@ def run_ours(args):
         barrier()
         clk.mark_start()
         ev0.record(stream)
+        marks = []
         for _ in range(args.steps):
             phc, st = step_device()
+            e = torch.cuda.Event(enable_timing=True)
+            e.record(stream)
+            marks.append(e)
         ev1.record(stream)
         barrier()
         clk.mark_end()
     launches = (lib.kernel_launch_count() - l0) // max(args.steps, 1)
     ms = ev0.elapsed_time(ev1) / args.steps
+    per = [ev0.elapsed_time(marks[0])] + [a.elapsed_time(b) for a, b in zip(marks, marks[1:])]
+    log(f"[rank {rank}] per-step ms: " + " ".join(f"{x:.2f}" for x in per))
     ms = max_over_ranks(ms)
     value = world * n / (ms / 1e3)
     log(f"[rank {rank}] device-resident: {ms:.3f} ms/step, phc={phc}, stats={st}")
@@ -335,8 +346,8 @@ def run_ours(args):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         try:
-            rate, secs, kind, ns, res = cpu_reference_rows_per_s(table, fds, args.cpu_rows,
-                                                                 "reference")
+            rate, secs, kind, ns, res = cpu_reference_rows_per_s(
+                table, fds, args.cpu_rows if args.cpu_rows is not None else n, "reference")
             cpu = {"value": rate, "unit": UNIT, "cores": 1, "kind": kind,
                    "sample": f"first {ns} rows of {gen.CONFIGS[cfg_id].name}, GgrConfig "
                              f"defaults, {secs:.1f} s single-threaded (SolveStats.wall_ms)"}
@@ -394,8 +405,10 @@ def main():
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--rows", type=int, default=None)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--cpu-rows", type=int, default=300_000)
-    ap.add_argument("--ref-rows", type=int, default=300_000)
+    ap.add_argument("--cpu-rows", type=int, default=None,
+                    help="rows of the CPU baseline sample (default: the whole table)")
+    ap.add_argument("--ref-rows", type=int, default=None,
+                    help="rows per reference step (default: the whole configured table)")
     ap.add_argument("--prof-steps", type=int, default=3)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--sharded", action="store_true",

@@ -20,7 +20,7 @@ BUILD = REPO / "build" / "cuda"
 OUT = PKG / "libprefixopt_cuda.so"
 GEN_OUT = PKG / "libpogen.so"
 CXX = os.environ.get("CXX", shutil.which("g++") or "g++")
-SOURCES = ["abi.cu", "encode.cu", "refine.cu", "phc.cu", "ggr.cu", "comm.cu", "shard.cu", "fd.cu", "render.cu", "replay.cu", "csv.cu"]
+SOURCES = ["abi.cu", "dict.cu", "encode.cu", "refine.cu", "phc.cu", "ggr.cu", "comm.cu", "shard.cu", "fd.cu", "render.cu", "replay.cu", "csv.cu"]
 
 NVCC = os.environ.get("NVCC", shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -131,10 +131,21 @@ std::vector<std::pair<uint8_t*, size_t>> g_pin_free;
 struct PinnedArena {
   uint8_t* base = nullptr;
   size_t cap = 0, used = 0;
+  // the last staged copy: its stream (compared only, never synchronised: the
+  // caller may destroy it) and an event recorded after it, which orders
+  // every earlier copy on that stream
   cudaStream_t last = nullptr;
+  cudaEvent_t done = nullptr;
+  int done_dev = -1;
+  bool pending = false;
+  void wait_copies() {
+    if (pending) cudaEventSynchronize(done);
+    pending = false;
+  }
   ~PinnedArena() {
     if (!base) return;
-    if (last) cudaStreamSynchronize(last);  // copies out of the arena are done
+    wait_copies();  // copies out of the arena are done
+    if (done) cudaEventDestroy(done);
     std::lock_guard<std::mutex> lk(g_pin_mu);
     g_pin_free.push_back({base, cap});
   }
@@ -166,7 +177,6 @@ struct CachedBlock {
   int device = 0;
   bool busy = false;
   cudaEvent_t released = nullptr;  // recorded on the releasing stream
-  cudaStream_t last = nullptr;
 };
 std::mutex g_blocks_mu;
 std::vector<CachedBlock> g_blocks;
@@ -183,7 +193,10 @@ void* cached_block_acquire(size_t bytes, cudaStream_t s) {
         (!best || b.bytes < best->bytes))
       best = &b;
   if (best) {
-    if (best->last != s) PO_CUDA(cudaStreamWaitEvent(s, best->released, 0));
+    // always ordered on the release event: stream handles are not unique
+    // identities (cudaStreamPerThread, reused handles); the wait is a no-op
+    // once the event has completed
+    PO_CUDA(cudaStreamWaitEvent(s, best->released, 0));
     best->busy = true;
     return best->p;
   }
@@ -235,10 +248,25 @@ void cached_block_release(void* p, cudaStream_t s) {
   for (auto& b : g_blocks)
     if (b.p == p) {
       cudaEventRecord(b.released, s);
-      b.last = s;
       b.busy = false;
       return;
     }
+}
+
+cudaStream_t copy_stream() {
+  struct PerDevice {
+    std::vector<cudaStream_t> s;
+    ~PerDevice() {
+      for (cudaStream_t x : s)
+        if (x) cudaStreamDestroy(x);
+    }
+  };
+  static thread_local PerDevice streams;
+  int dev = 0;
+  PO_CUDA(cudaGetDevice(&dev));
+  if (size_t(dev) >= streams.s.size()) streams.s.resize(dev + 1, nullptr);
+  if (!streams.s[dev]) PO_CUDA(cudaStreamCreateWithFlags(&streams.s[dev], cudaStreamNonBlocking));
+  return streams.s[dev];
 }
 
 void h2d_async(void* dst, const void* src, size_t bytes, cudaStream_t s) {
@@ -256,16 +284,25 @@ void h2d_async(void* dst, const void* src, size_t bytes, cudaStream_t s) {
     }
   }
   const size_t need = (bytes + 15) & ~size_t(15);
-  if (a.used + need > a.cap || (a.last && a.last != s)) {
+  int dev = 0;
+  PO_CUDA(cudaGetDevice(&dev));
+  if (a.used + need > a.cap || (a.pending && (a.last != s || a.done_dev != dev))) {
     // recycle: every earlier copy out of the arena must have completed
-    if (a.last) PO_CUDA(cudaStreamSynchronize(a.last));
+    a.wait_copies();
     a.used = 0;
+  }
+  if (a.done_dev != dev) {  // events record only on streams of their device
+    if (a.done) cudaEventDestroy(a.done);
+    PO_CUDA(cudaEventCreateWithFlags(&a.done, cudaEventDisableTiming));
+    a.done_dev = dev;
   }
   uint8_t* p = a.base + a.used;
   a.used += need;
   a.last = s;
   std::memcpy(p, src, bytes);
   PO_CUDA(cudaMemcpyAsync(dst, p, bytes, cudaMemcpyHostToDevice, s));
+  PO_CUDA(cudaEventRecord(a.done, s));
+  a.pending = true;
 }
 
 namespace {
@@ -339,7 +376,9 @@ void prepare(const po_table* tv, int tok, int scoring, cudaStream_t s, Prepared&
              bool ordered = true) {
   check_modes(tok, scoring);
   init_pool_once();
-  make_device_table(tv, tok, s, p.t);
+  // host tables stream through the dictionary pass (row chunks copied while
+  // the previous chunk is encoded); nothing after encode() reads the table
+  make_device_table(tv, tok, s, p.t, /*stream_host=*/true);
   timing_mark("table_h2d", s);
   encode(p.t, tok, scoring, s, p.e, debug_hash_bits(), ordered, rank_unique_columns());
 }

@@ -283,8 +283,7 @@ __global__ void k_collect_ties(const WorkItem* __restrict__ work, const ScanSlot
                                const uint64_t* __restrict__ vlen, uint32_t m, uint32_t K,
                                const Cand* __restrict__ best, const int32_t* __restrict__ tie_group,
                                const uint32_t* __restrict__ tie_off, uint32_t* cursor,
-                               const uint32_t* __restrict__ rep_row, uint32_t* t_row,
-                               uint32_t* t_col, uint32_t* t_vid, uint32_t* t_grp) {
+                               uint32_t* t_ref, uint32_t* t_vid, uint32_t* t_grp) {
   const WorkItem w = work[blockIdx.x];
   const int32_t g = tie_group[w.slot];
   if (g < 0) return;
@@ -303,8 +302,7 @@ __global__ void k_collect_ties(const WorkItem* __restrict__ work, const ScanSlot
       if (wt[c * K + k]) ptot += uint64_t(wt[c * K + k]) * sl.t.psum[e * K + k];
     if ((u128(vl) * vl * cnt + ptot) * u128(cnt - 1) != b.numer) continue;
     const uint32_t at = tie_off[g] + atomicAdd(&cursor[g], 1u);
-    t_row[at] = rep_row[colbase[c] + v];
-    t_col[at] = c;
+    t_ref[at] = uint32_t(colbase[c] + v);
     t_vid[at] = v;
     t_grp[at] = uint32_t(g);
   }
@@ -327,11 +325,14 @@ __global__ void k_raw1_flags(const uint32_t* row_leaf, uint64_t n, const int32_t
 }
 
 __global__ void k_raw1_items(const uint32_t* rows, uint32_t cnt, const uint32_t* row_leaf,
-                             const int32_t* leaf_raw1_col, uint32_t* grp, uint32_t* col) {
+                             const int32_t* leaf_raw1_col, const uint32_t* vid,
+                             const uint64_t* colbase, uint32_t m, uint32_t* grp, uint32_t* ref) {
   for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < cnt; k += gridDim.x * blockDim.x) {
-    const uint32_t l = row_leaf[rows[k]];
+    const uint32_t r = rows[k];
+    const uint32_t l = row_leaf[r];
+    const uint32_t c = uint32_t(leaf_raw1_col[l]);
     grp[k] = l;
-    col[k] = uint32_t(leaf_raw1_col[l]);
+    ref[k] = uint32_t(colbase[c] + vid[uint64_t(r) * m + c]);  // the cell's distinct value
   }
 }
 
@@ -1077,14 +1078,14 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
         const uint32_t ng = uint32_t(tie_slot.size()), total = tie_off.back();
         auto d_tg = to_device(tie_group, s);
         auto d_toff = to_device(tie_off, s);
-        DevBuf<uint32_t> cursor(ng, s), t_row(total, s), t_col(total, s), t_vid(total, s),
-            t_grp(total, s), t_pos(total, s), min_vid(ng, s);
+        DevBuf<uint32_t> cursor(ng, s), t_ref(total, s), t_vid(total, s), t_grp(total, s),
+            t_pos(total, s), min_vid(ng, s);
         cursor.zero();
         PO_LAUNCH(k_collect_ties, unsigned(L.work.size()), kArgBlock, 0, s,
                   reinterpret_cast<WorkItem*>(dp + o_work), reinterpret_cast<ScanSlot*>(dp + o_slots),
                   reinterpret_cast<uint32_t*>(dp + o_masks), reinterpret_cast<uint32_t*>(dp + o_w),
                   colbase, vlen, m, K, d_best, d_tg.get(), d_toff.get(), cursor.get(),
-                  e.rep_row.get(), t_row.get(), t_col.get(), t_vid.get(), t_grp.get());
+                  t_ref.get(), t_vid.get(), t_grp.get());
         RefineJob tj;
         tj.n_items = total;
         tj.d_grp_init = t_grp.get();
@@ -1092,12 +1093,11 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
         tj.n_groups = ng;
         tj.grp_max = total;
         tj.key.kind = 0;  // raw bytes
-        tj.key.arena = e.arena;
-        tj.key.arena_bytes = e.arena_bytes;
-        tj.key.offsets = e.offsets;
-        tj.key.item_cell_row = t_row.get();
-        tj.key.item_col = t_col.get();
-        tj.key.m = m;
+        tj.key.arena = e.val_arena;
+        tj.key.arena_bytes = e.val_bytes;
+        tj.key.str_off = e.val_off.get();
+        tj.key.str_len = e.val_len.get();
+        tj.key.item_ref = t_ref.get();
         tj.d_out_pos = t_pos.get();
         refine_sort_multi({tj}, s);
         PO_LAUNCH(k_pick_min, grid_for(total, 256), 256, 0, s, t_pos.get(), t_grp.get(),
@@ -1545,7 +1545,7 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
     raw_col.alloc(n_raw, s);
     raw_pos.alloc(n_raw, s);
     PO_LAUNCH(k_raw1_items, grid_for(n_raw, 256), 256, 0, s, raw_rows.get(), n_raw, row_leaf.get(),
-              d_lrc.get(), raw_grp.get(), raw_col.get());
+              d_lrc.get(), e.vid.get(), colbase, m, raw_grp.get(), raw_col.get());
     RefineJob rj;
     rj.n_items = n_raw;
     rj.d_grp_init = raw_grp.get();
@@ -1553,12 +1553,11 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
     rj.n_groups = nleaves;
     rj.grp_max = uint32_t(n);
     rj.key.kind = 0;  // raw bytes
-    rj.key.arena = e.arena;
-    rj.key.arena_bytes = e.arena_bytes;
-    rj.key.offsets = e.offsets;
-    rj.key.item_cell_row = raw_rows.get();
-    rj.key.item_col = raw_col.get();
-    rj.key.m = m;
+    rj.key.arena = e.val_arena;
+    rj.key.arena_bytes = e.val_bytes;
+    rj.key.str_off = e.val_off.get();
+    rj.key.str_len = e.val_len.get();
+    rj.key.item_ref = raw_col.get();  // distinct value of each item's cell
     rj.d_out_pos = raw_pos.get();
     sort_jobs.push_back(rj);
   }

@@ -25,14 +25,45 @@ struct DeviceTable {
   uint64_t arena_bytes = 0;
   const uint64_t* offsets = nullptr;  // device, n*m+1
   const uint64_t* cell_lens = nullptr;  // device or null (custom tokenizer)
+  // deferred host table (make_device_table(stream_host = true)): arena and
+  // offsets stay in host memory and the dictionary pass streams row chunks
+  // (arena / offsets above are then null)
+  const uint8_t* h_arena = nullptr;
+  const uint64_t* h_offsets = nullptr;
   // owned copies when the caller passed host buffers
   DevBuf<uint8_t> own_arena;
   DevBuf<uint64_t> own_offsets;
   DevBuf<uint64_t> own_lens;
 };
 
-// Builds a DeviceTable from the ABI view, copying host buffers to HBM.
-void make_device_table(const po_table* t, int tok, cudaStream_t s, DeviceTable& out);
+// Builds a DeviceTable from the ABI view, copying host buffers to HBM (or,
+// with stream_host, leaving arena + offsets on the host for the streamed
+// dictionary pass: only for callers that use the table through encode()).
+void make_device_table(const po_table* t, int tok, cudaStream_t s, DeviceTable& out,
+                       bool stream_host = false);
+
+// A second stream of the calling thread (current device) for copies that
+// overlap work on the call's stream.
+cudaStream_t copy_stream();
+
+void exclusive_scan_u64(const uint64_t* in, uint64_t* out, uint64_t n, cudaStream_t s);
+
+// K1 + K2 (dict.cu): exact per-column dictionaries in one read of the cell
+// bytes. cid_mat[r*m + c] = dense id of cell (r, c)'s value within column c
+// in first-claim order; distinct value d = colbase[c] + id is the string
+// val_arena[val_off[d] .. + val_len[d]) held by row rep_row[d].
+struct DictResult {
+  uint64_t D = 0;
+  std::vector<uint64_t> card, colbase;
+  DevBuf<uint64_t> d_colbase;
+  DevBuf<uint64_t> val_off;
+  DevBuf<uint32_t> val_len, rep_row, d_col;
+  const uint8_t* val_arena = nullptr;  // the table arena, or own_vals (streamed tables)
+  uint64_t val_bytes = 0;
+  DevBuf<uint8_t> own_vals;
+};
+void build_dictionary(const DeviceTable& t, uint32_t hash_bits, cudaStream_t s, uint32_t* cid_mat,
+                      DictResult& out);
 
 // Exact dictionary encoding of every column (K1 cell_scan + K2 dict_encode +
 // K3 rank_sort). After encode():
@@ -47,11 +78,6 @@ void make_device_table(const po_table* t, int tok, cudaStream_t s, DeviceTable& 
 struct Encoded {
   uint64_t n = 0;
   uint32_t m = 0;
-  // the table bytes (non-owning; valid for the call) for on-demand raw-byte
-  // comparisons of a few values
-  const uint8_t* arena = nullptr;
-  const uint64_t* offsets = nullptr;
-  uint64_t arena_bytes = 0;
   uint64_t D = 0;  // total distinct values
   std::vector<uint64_t> card, colbase;  // host (colbase has m+1 entries)
   DevBuf<uint64_t> d_colbase;
@@ -59,6 +85,14 @@ struct Encoded {
   DevBuf<uint64_t> vlen;      // D
   DevBuf<uint32_t> count;     // D
   DevBuf<uint32_t> rep_row;   // D: a row holding the value
+  // bytes of every distinct value (index colbase[c] + vid): the string
+  // val_arena[val_off[d] .. + val_len[d]) — in the caller's table arena, or in
+  // own_vals when the table was streamed from the host
+  const uint8_t* val_arena = nullptr;
+  uint64_t val_bytes = 0;
+  DevBuf<uint64_t> val_off;   // D
+  DevBuf<uint32_t> val_len;   // D
+  DevBuf<uint8_t> own_vals;
   std::vector<uint64_t> total_len;  // host, per column: sum of segment lengths (stats.hpp:38)
   // host, per column (empty = none): ids of a unique column left in
   // compaction order (encode(rank_unique = false)); sorts break ties on it
@@ -89,14 +123,16 @@ struct RefineKey {
   int kind = 0;
   uint64_t skip = 0;  // string kinds: symbols [0, skip) are shared by every item
   uint32_t* item_off = nullptr;  // string kinds (set by refine_sort): symbols consumed per item
-  // string keys
+  // string keys: item i is string r = item_ref ? item_ref[i] : i, at
+  // arena + str_off[r] (in symbols: bytes, or u16 codes for kind 3) of
+  // str_len[r] symbols (str_len null: str_off[r + 1] - str_off[r])
   const uint8_t* arena = nullptr;
   uint64_t arena_bytes = 0;
-  const uint64_t* offsets = nullptr;
-  const uint32_t* item_cell_row = nullptr;  // item -> row of the cell holding the string
-  const uint32_t* item_col = nullptr;       // item -> column
-  uint32_t m = 0;
+  const uint32_t* item_ref = nullptr;
+  const uint64_t* str_off = nullptr;
+  const uint32_t* str_len = nullptr;
   // row keys
+  uint32_t m = 0;
   const uint32_t* vid = nullptr;
   const uint64_t* colbase = nullptr;
   const uint32_t* row_leaf = nullptr;      // row -> leaf index
@@ -236,17 +272,34 @@ struct TieSpec {
 // position of q's run, run_len[start] = its length) by the escaped bytes of
 // col_of_leaf[row_leaf[row]] (distinct within a run): pos[perm[q]] = start +
 // rank. One thread per position; longer runs are left alone (refine.cu).
-void rank_short_runs(const uint8_t* arena, const uint64_t* offsets, uint32_t m,
-                     const uint32_t* perm, const uint32_t* run, const uint32_t* run_len,
-                     const uint32_t* row_leaf, const int32_t* col_of_leaf, uint64_t n,
-                     uint32_t max_len, uint32_t* pos, cudaStream_t s);
+// Bytes of cell (row, col) through its value id (Encoded's value arena).
+struct CellStr {
+  const uint8_t* arena;
+  const uint8_t* lim;
+  const uint64_t* val_off;
+  const uint32_t* val_len;
+  const uint32_t* vid;
+  const uint64_t* colbase;
+  uint32_t m;
+  __device__ __forceinline__ void get(uint64_t row, uint32_t col, const uint8_t*& p,
+                                      uint64_t& len) const {
+    const uint64_t d = colbase[col] + vid[row * m + col];
+    p = arena + val_off[d];
+    len = val_len[d];
+  }
+};
+CellStr cell_str(const Encoded& e);
+
+void rank_short_runs(const CellStr& cs, const uint32_t* perm, const uint32_t* run,
+                     const uint32_t* run_len, const uint32_t* row_leaf, const int32_t* col_of_leaf,
+                     uint64_t n, uint32_t max_len, uint32_t* pos, cudaStream_t s);
 // The same for the positions items[0, nt) of longer runs: 126-bit prefix
 // keys, then a quadratic count per run (work = sum of squared run lengths;
 // max_len = the longest run).
-void rank_long_runs(const uint8_t* arena, const uint64_t* offsets, uint32_t m, const uint32_t* perm,
-                    const uint32_t* run, const uint32_t* run_len, const uint32_t* row_leaf,
-                    const int32_t* col_of_leaf, const uint32_t* items, uint32_t nt, uint64_t n,
-                    uint32_t max_len, uint32_t* pos, cudaStream_t s);
+void rank_long_runs(const CellStr& cs, const uint32_t* perm, const uint32_t* run,
+                    const uint32_t* run_len, const uint32_t* row_leaf, const int32_t* col_of_leaf,
+                    const uint32_t* items, uint32_t nt, uint64_t n, uint32_t max_len, uint32_t* pos,
+                    cudaStream_t s);
 void break_unranked_ties(const Encoded& e, const TieSpec& ts, const uint32_t* row_leaf,
                          const uint32_t* d_leaf_off, uint32_t* pos, cudaStream_t s);
 

@@ -339,12 +339,14 @@ __global__ void k_tie_flags(const uint32_t* run, const uint32_t* run_len, uint64
 
 __global__ void k_tie_items(const uint32_t* items, uint32_t nt, const uint32_t* perm,
                             const uint32_t* run, const uint32_t* row_leaf, const int32_t* tie_col,
-                            uint32_t* t_row, uint32_t* t_grp, uint32_t* t_col) {
+                            const uint32_t* vid, const uint64_t* colbase, uint32_t m,
+                            uint32_t* t_row, uint32_t* t_grp, uint32_t* t_ref) {
   for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < nt; k += gridDim.x * blockDim.x) {
     const uint32_t q = items[k], r = perm[q];
+    const uint32_t c = uint32_t(tie_col[row_leaf[r]]);
     t_row[k] = r;
     t_grp[k] = run[q];
-    t_col[k] = uint32_t(tie_col[row_leaf[r]]);
+    t_ref[k] = uint32_t(colbase[c] + vid[uint64_t(r) * m + c]);  // the cell's distinct value
   }
 }
 
@@ -399,8 +401,9 @@ void break_unranked_ties(const Encoded& e, const TieSpec& ts, const uint32_t* ro
   DevBuf<uint32_t> run_len = dev_auto<uint32_t>(n, s);
   PO_LAUNCH(k_run_len, grid_for(n, 256), 256, 0, s, run.get(), n, run_len.get());
   timing_mark("ties_runs", s);
-  rank_short_runs(e.arena, e.offsets, e.m, perm.get(), run.get(), run_len.get(), row_leaf,
-                  d_tc.get(), n, max_short, pos, s);
+  const CellStr cs = cell_str(e);
+  rank_short_runs(cs, perm.get(), run.get(), run_len.get(), row_leaf, d_tc.get(), n, max_short,
+                  pos, s);
   timing_mark("ties_short", s);
   DevBuf<uint8_t> flag(n, s);
   PO_LAUNCH(k_tie_flags, grid_for(n, 256), 256, 0, s, run.get(), run_len.get(), n, max_short,
@@ -442,24 +445,24 @@ void break_unranked_ties(const Encoded& e, const TieSpec& ts, const uint32_t* ro
   }
   if (nt == 0) return;
   if (hw[0] <= long_run_budget()) {  // quadratic per run, no sort
-    rank_long_runs(e.arena, e.offsets, e.m, perm.get(), run.get(), run_len.get(), row_leaf,
-                   d_tc.get(), items.get(), nt, n, uint32_t(hw[1]), pos, s);
+    rank_long_runs(cs, perm.get(), run.get(), run_len.get(), row_leaf, d_tc.get(), items.get(), nt,
+                   n, uint32_t(hw[1]), pos, s);
     return;
   }
   DevBuf<uint32_t> t_row(nt, s), t_grp(nt, s), t_col(nt, s), t_pos(nt, s);
   PO_LAUNCH(k_tie_items, grid_for(nt, 256), 256, 0, s, items.get(), nt, perm.get(), run.get(),
-            row_leaf, d_tc.get(), t_row.get(), t_grp.get(), t_col.get());
+            row_leaf, d_tc.get(), e.vid.get(), e.d_colbase.get(), e.m, t_row.get(), t_grp.get(),
+            t_col.get());
   RefineJob tj;
   tj.n_items = nt;
   tj.d_grp_init = t_grp.get();  // run start positions
   tj.grp_max = uint32_t(n);
   tj.key.kind = 1;  // escaped bytes: the order of the column's ranks
-  tj.key.arena = e.arena;
-  tj.key.arena_bytes = e.arena_bytes;
-  tj.key.offsets = e.offsets;
-  tj.key.item_cell_row = t_row.get();
-  tj.key.item_col = t_col.get();
-  tj.key.m = e.m;
+  tj.key.arena = e.val_arena;
+  tj.key.arena_bytes = e.val_bytes;
+  tj.key.str_off = e.val_off.get();
+  tj.key.str_len = e.val_len.get();
+  tj.key.item_ref = t_col.get();
   tj.d_out_pos = t_pos.get();
   refine_sort_multi({tj}, s);
   PO_LAUNCH(k_tie_scatter, grid_for(nt, 256), 256, 0, s, t_row.get(), t_pos.get(), nt, pos);

@@ -37,11 +37,18 @@ __device__ __forceinline__ uint32_t end_code(const RefineKey& K) {
 // json_escape expansion and the end marker is the closing '"' (0x22) of the
 // fragment, so comparing code strings == comparing escaped fragment keys (the
 // expansions are prefix-free).
+// Location of item i's string: offset and length in symbols.
+__device__ __forceinline__ void str_at(const RefineKey& K, uint32_t item, uint64_t& o0,
+                                       uint64_t& len) {
+  const uint32_t r = K.item_ref ? K.item_ref[item] : item;
+  o0 = K.str_off[r];
+  len = K.str_len ? uint64_t(K.str_len[r]) : K.str_off[r + 1] - o0;
+}
+
 __device__ __forceinline__ uint64_t string_chunk(const RefineKey& K, uint32_t item, uint64_t base,
                                                  uint32_t nsym) {
-  const uint64_t i = uint64_t(K.item_cell_row[item]) * K.m + K.item_col[item];
-  const uint64_t o0 = K.offsets[i];
-  const uint64_t len = K.offsets[i + 1] - o0;
+  uint64_t o0, len;
+  str_at(K, item, o0, len);
   const uint8_t* p = K.arena + o0;
   const uint16_t* p16 = reinterpret_cast<const uint16_t*>(K.arena) + o0;
   uint64_t chunk = 0;
@@ -137,15 +144,15 @@ __global__ void k_advance(const uint32_t* items, const int* count, uint32_t cons
 // 14 symbols.
 __device__ __forceinline__ uint64_t sym_lcp(const RefineKey& K, uint32_t a, uint32_t b,
                                             uint64_t off) {
-  const uint64_t ia = uint64_t(K.item_cell_row[a]) * K.m + K.item_col[a];
-  const uint64_t ib = uint64_t(K.item_cell_row[b]) * K.m + K.item_col[b];
-  const uint64_t la = K.offsets[ia + 1] - K.offsets[ia], lb = K.offsets[ib + 1] - K.offsets[ib];
+  uint64_t oa, la, ob, lb;
+  str_at(K, a, oa, la);
+  str_at(K, b, ob, lb);
   const uint64_t st = off + K.skip;
   if (st >= la || st >= lb) return 0;
   const uint64_t n = (la < lb ? la : lb) - st;  // symbols to compare
   const uint32_t us = K.kind == 3 ? 2u : 1u;    // bytes per symbol
-  const uint8_t* pa = K.arena + (K.offsets[ia] + st) * us;
-  const uint8_t* pb = K.arena + (K.offsets[ib] + st) * us;
+  const uint8_t* pa = K.arena + (oa + st) * us;
+  const uint8_t* pb = K.arena + (ob + st) * us;
   const uint8_t* lim = K.arena + K.arena_bytes;
   const uint64_t nb = n * us;
   for (uint64_t t = 0; t < nb; t += 8) {
@@ -437,10 +444,9 @@ struct StrLess {
     if (a.k0 != b.k0) return a.k0 < b.k0;
     if (a.k1 != b.k1) return a.k1 < b.k1;
     // symbols [14, ...) of both strings
-    const uint64_t ia = uint64_t(K.item_cell_row[a.item]) * K.m + K.item_col[a.item];
-    const uint64_t ib = uint64_t(K.item_cell_row[b.item]) * K.m + K.item_col[b.item];
-    const uint64_t oa = K.offsets[ia], ob = K.offsets[ib];
-    const uint64_t la = K.offsets[ia + 1] - oa, lb = K.offsets[ib + 1] - ob;
+    uint64_t oa, la, ob, lb;
+    str_at(K, a.item, oa, la);
+    str_at(K, b.item, ob, lb);
     const uint8_t* pa = K.arena + oa;
     const uint8_t* pb = K.arena + ob;
     for (uint64_t pos = 14 + K.skip;; ++pos) {
@@ -774,9 +780,7 @@ __device__ __forceinline__ bool esc_less(const uint8_t* a, uint64_t la, const ui
 
 // Thread per position of a short run (2..max_len rows of one leaf, distinct
 // values of column col_of_leaf[leaf]): its rank among the run's values.
-__global__ void k_rank_short_runs(const uint8_t* __restrict__ arena,
-                                  const uint64_t* __restrict__ offsets, uint32_t m,
-                                  const uint32_t* perm, const uint32_t* run,
+__global__ void k_rank_short_runs(CellStr cs, const uint32_t* perm, const uint32_t* run,
                                   const uint32_t* run_len, const uint32_t* row_leaf,
                                   const int32_t* col_of_leaf, uint64_t n, uint32_t max_len,
                                   uint32_t* pos) {
@@ -786,14 +790,16 @@ __global__ void k_rank_short_runs(const uint8_t* __restrict__ arena,
     if (L < 2 || L > max_len) continue;
     const uint32_t r = perm[q];
     const uint32_t c = uint32_t(col_of_leaf[row_leaf[r]]);
-    const uint64_t ia = uint64_t(r) * m + c;
-    const uint8_t* a = arena + offsets[ia];
-    const uint64_t la = offsets[ia + 1] - offsets[ia];
+    const uint8_t* a;
+    uint64_t la;
+    cs.get(r, c, a, la);
     uint32_t rank = 0;
     for (uint32_t j = st; j < st + L; ++j) {
       if (j == q) continue;
-      const uint64_t ib = uint64_t(perm[j]) * m + c;
-      rank += esc_less(arena + offsets[ib], offsets[ib + 1] - offsets[ib], a, la);
+      const uint8_t* b;
+      uint64_t lb;
+      cs.get(perm[j], c, b, lb);
+      rank += esc_less(b, lb, a, la);
     }
     pos[r] = st + rank;
   }
@@ -812,15 +818,14 @@ __device__ __forceinline__ uint64_t esc_word(const uint8_t* p, uint64_t len, uin
   return chunk;
 }
 
-__global__ void k_long_keys(const uint8_t* __restrict__ arena, const uint64_t* __restrict__ offsets,
-                            uint32_t m, const uint32_t* perm, const uint32_t* row_leaf,
+__global__ void k_long_keys(CellStr cs, const uint32_t* perm, const uint32_t* row_leaf,
                             const int32_t* col_of_leaf, const uint32_t* items, uint32_t nt,
                             uint64_t* k0, uint64_t* k1) {
   for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < nt; k += gridDim.x * blockDim.x) {
     const uint32_t q = items[k], r = perm[q];
-    const uint64_t i = uint64_t(r) * m + uint32_t(col_of_leaf[row_leaf[r]]);
-    const uint8_t* p = arena + offsets[i];
-    const uint64_t len = offsets[i + 1] - offsets[i];
+    const uint8_t* p;
+    uint64_t len;
+    cs.get(r, uint32_t(col_of_leaf[row_leaf[r]]), p, len);
     k0[q] = esc_word(p, len, 0);
     k1[q] = esc_word(p, len, 1);
   }
@@ -834,9 +839,7 @@ __global__ void k_long_keys(const uint8_t* __restrict__ arena, const uint64_t* _
 // coincide.
 constexpr uint32_t kLongPart = 512;
 
-__global__ void k_rank_long_runs(const uint8_t* __restrict__ arena,
-                                 const uint64_t* __restrict__ offsets, uint32_t m,
-                                 const uint32_t* perm, const uint32_t* run, const uint32_t* run_len,
+__global__ void k_rank_long_runs(CellStr cs, const uint32_t* perm, const uint32_t* run, const uint32_t* run_len,
                                  const uint32_t* row_leaf, const int32_t* col_of_leaf,
                                  const uint32_t* items, uint32_t nt, const uint64_t* __restrict__ k0,
                                  const uint64_t* __restrict__ k1, uint32_t gx, uint32_t* rank_out) {
@@ -858,12 +861,15 @@ __global__ void k_rank_long_runs(const uint8_t* __restrict__ arena,
   if (eq > uint32_t(q >= lo && q < hi)) {  // shared 14-symbol prefixes: compare bytes
     const uint32_t r = perm[q];
     const uint32_t c = uint32_t(col_of_leaf[row_leaf[r]]);
-    const uint64_t ia = uint64_t(r) * m + c;
+    const uint8_t* a;
+    uint64_t la;
+    cs.get(r, c, a, la);
     for (uint32_t j = lo; j < hi; ++j) {
       if (j == q || k0[j] != a0 || k1[j] != a1) continue;
-      const uint64_t ib = uint64_t(perm[j]) * m + c;
-      rank += esc_less(arena + offsets[ib], offsets[ib + 1] - offsets[ib], arena + offsets[ia],
-                       offsets[ia + 1] - offsets[ia]);
+      const uint8_t* b;
+      uint64_t lb;
+      cs.get(perm[j], c, b, lb);
+      rank += esc_less(b, lb, a, la);
     }
   }
   if (rank) atomicAdd(rank_out + k, rank);
@@ -879,30 +885,34 @@ __global__ void k_long_place(const uint32_t* items, uint32_t nt, const uint32_t*
 
 }  // namespace
 
-void rank_short_runs(const uint8_t* arena, const uint64_t* offsets, uint32_t m,
-                     const uint32_t* perm, const uint32_t* run, const uint32_t* run_len,
-                     const uint32_t* row_leaf, const int32_t* col_of_leaf, uint64_t n,
-                     uint32_t max_len, uint32_t* pos, cudaStream_t s) {
-  if (n == 0) return;
-  ensure_esc_table();
-  PO_LAUNCH(k_rank_short_runs, grid_for(n, 256), 256, 0, s, arena, offsets, m, perm, run, run_len,
-            row_leaf, col_of_leaf, n, max_len, pos);
+CellStr cell_str(const Encoded& e) {
+  return CellStr{e.val_arena, e.val_arena + e.val_bytes, e.val_off.get(), e.val_len.get(),
+                 e.vid.get(), e.d_colbase.get(), e.m};
 }
 
-void rank_long_runs(const uint8_t* arena, const uint64_t* offsets, uint32_t m, const uint32_t* perm,
-                    const uint32_t* run, const uint32_t* run_len, const uint32_t* row_leaf,
-                    const int32_t* col_of_leaf, const uint32_t* items, uint32_t nt, uint64_t n,
-                    uint32_t max_len, uint32_t* pos, cudaStream_t s) {
+void rank_short_runs(const CellStr& cs, const uint32_t* perm, const uint32_t* run,
+                     const uint32_t* run_len, const uint32_t* row_leaf, const int32_t* col_of_leaf,
+                     uint64_t n, uint32_t max_len, uint32_t* pos, cudaStream_t s) {
+  if (n == 0) return;
+  ensure_esc_table();
+  PO_LAUNCH(k_rank_short_runs, grid_for(n, 256), 256, 0, s, cs, perm, run, run_len, row_leaf,
+            col_of_leaf, n, max_len, pos);
+}
+
+void rank_long_runs(const CellStr& cs, const uint32_t* perm, const uint32_t* run,
+                    const uint32_t* run_len, const uint32_t* row_leaf, const int32_t* col_of_leaf,
+                    const uint32_t* items, uint32_t nt, uint64_t n, uint32_t max_len, uint32_t* pos,
+                    cudaStream_t s) {
   if (nt == 0) return;
   ensure_esc_table();
   DevBuf<uint64_t> k0(n, s), k1(n, s);
-  PO_LAUNCH(k_long_keys, grid_for(nt, 256), 256, 0, s, arena, offsets, m, perm, row_leaf,
-            col_of_leaf, items, nt, k0.get(), k1.get());
+  PO_LAUNCH(k_long_keys, grid_for(nt, 256), 256, 0, s, cs, perm, row_leaf, col_of_leaf, items, nt,
+            k0.get(), k1.get());
   DevBuf<uint32_t> rank(nt, s);
   rank.zero();
   const uint32_t gx = (nt + 255) / 256, parts = (max_len + kLongPart - 1) / kLongPart;
-  PO_LAUNCH(k_rank_long_runs, gx * parts, 256, 0, s, arena, offsets, m, perm, run, run_len,
-            row_leaf, col_of_leaf, items, nt, k0.get(), k1.get(), gx, rank.get());
+  PO_LAUNCH(k_rank_long_runs, gx * parts, 256, 0, s, cs, perm, run, run_len, row_leaf, col_of_leaf,
+            items, nt, k0.get(), k1.get(), gx, rank.get());
   PO_LAUNCH(k_long_place, grid_for(nt, 256), 256, 0, s, items, nt, perm, run, rank.get(), pos);
 }
 

@@ -246,10 +246,7 @@ void replay_unbounded_device(const DeviceTable& pt, int tok, uint64_t* d_input, 
   j.key.kind = word ? 3 : 0;
   j.key.arena = keys;
   j.key.arena_bytes = key_bytes;
-  j.key.offsets = koff;
-  j.key.item_cell_row = iota.get();
-  j.key.item_col = zeros.get();
-  j.key.m = 1;
+  j.key.str_off = koff;  // string i = prompt i (consecutive offsets)
   j.key.skip = skip;
   j.d_out_pos = pos.get();
   refine_sort_multi({j}, s);

@@ -83,15 +83,12 @@ __host__ __device__ __forceinline__ int cmp_bytes(const Code* code, const uint8_
 // (rep_row[i], icol[i]) of the local table.
 struct LocalDict {
   const uint8_t* arena;
-  const uint64_t* offsets;
-  const uint32_t* rep_row;
-  const uint32_t* icol;
-  uint32_t m;
+  const uint64_t* val_off;
+  const uint32_t* val_len;
+  const uint32_t* icol;  // column of each local distinct value
   __device__ __forceinline__ void str(uint32_t i, const uint8_t*& p, uint64_t& len) const {
-    const uint64_t c = uint64_t(rep_row[i]) * m + icol[i];
-    const uint64_t o = offsets[c];
-    p = arena + o;
-    len = offsets[c + 1] - o;
+    p = arena + val_off[i];
+    len = val_len[i];
   }
 };
 
@@ -344,15 +341,6 @@ __global__ void k_scatter_u32(uint64_t D, const uint32_t* icol, const uint32_t* 
     out[gcb[icol[i]] + grank[i]] = val[i];
 }
 
-void exclusive_scan_u64(const uint64_t* in, uint64_t* out, uint64_t n, cudaStream_t s) {
-  if (!n) return;
-  size_t tb = 0;
-  PO_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, in, out, int64_t(n), s));
-  DevBuf<uint8_t> tmp(tb, s);
-  ProfScope ps("cub_scan", s);
-  PO_CUDA(cub::DeviceScan::ExclusiveSum(tmp.get(), tb, in, out, int64_t(n), s));
-}
-
 void inclusive_scan_u32(const uint32_t* in, uint32_t* out, uint64_t n, cudaStream_t s) {
   if (!n) return;
   size_t tb = 0;
@@ -370,7 +358,7 @@ DevBuf<uint32_t> global_ranks(Comm& comm, const Encoded& L, const uint32_t* d_ic
   const int N = comm.size();
   const uint32_t m = L.m;
   const uint64_t D = L.D;
-  LocalDict ld{L.arena, L.offsets, L.rep_row.get(), d_icol, m};
+  LocalDict ld{L.val_arena, L.val_off.get(), L.val_len.get(), d_icol};
 
   // local order of the distinct values in `kind` (escaped: the vid order)
   DevBuf<uint32_t> ord;
@@ -386,12 +374,10 @@ DevBuf<uint32_t> global_ranks(Comm& comm, const Encoded& L, const uint32_t* d_ic
     j.n_groups = m;
     j.grp_max = uint32_t(D);
     j.key.kind = 0;
-    j.key.arena = L.arena;
-    j.key.arena_bytes = L.arena_bytes;
-    j.key.offsets = L.offsets;
-    j.key.item_cell_row = L.rep_row.get();
-    j.key.item_col = d_icol;
-    j.key.m = m;
+    j.key.arena = L.val_arena;
+    j.key.arena_bytes = L.val_bytes;
+    j.key.str_off = L.val_off.get();
+    j.key.str_len = L.val_len.get();
     j.d_out_pos = pos.get();
     refine_sort_multi({j}, s);
     ord.alloc(D, s);
@@ -452,7 +438,7 @@ DevBuf<uint32_t> global_ranks(Comm& comm, const Encoded& L, const uint32_t* d_ic
   DevBuf<uint2> meta(D, s);
   DevBuf<uint8_t> sbytes(bb[N], s);
   PO_LAUNCH(k_pack_values, grid_for(D * 32, 256), 256, 0, s, D, d_ord, ld, boff.get(),
-            L.arena + L.arena_bytes, meta.get(),
+            L.val_arena + L.val_bytes, meta.get(),
             sbytes.get());
   std::vector<uint64_t> s_items(N), s_bytes(N), s_meta(N);
   for (int r = 0; r < N; ++r) {

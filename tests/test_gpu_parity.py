@@ -261,3 +261,20 @@ def test_launches_counted():
     before = po._abi.cuda_lib().kernel_launch_count()
     po.ggr(distinct_first_table(5, 3), None)
     assert po._abi.cuda_lib().kernel_launch_count() > before
+
+
+def test_all_empty_cells_null_arena():
+    # every cell "": the C++ drop-in passes an empty vector's data() (null);
+    # the reference returns a valid schedule with PHC 0
+    t = po.Table(["a", "b", "c"], [["", "", ""]] * 7)
+    P = oracle("port")
+    for cfg in (po.GgrConfig(), po.exact_config()):
+        assert same_result(po.ggr(t, None, cfg), P.ggr(t, None, cfg))
+    view = t.view(arena=0)
+    rows = np.empty(7, np.uint64)
+    orders = np.empty(21, np.int32)
+    phc, st = po.api.ggr_into(view, [], po.GgrConfig(), po.char_tokenizer().kind, 0,
+                              po._abi.PO_LOC_HOST, rows, orders)
+    ref = P.ggr(t, None, po.GgrConfig())
+    assert phc == ref.phc_score == 0
+    assert rows.tolist() == ref.schedule.row_ids.tolist()
