@@ -208,6 +208,30 @@ int po_csv_copy(const po_csv* csv, uint32_t out_location, uint8_t* out_arena,
                 void* stream);
 void po_csv_free(po_csv* csv);
 
+/* prefixopt::load_jsonl (table.hpp:225-269): one JSON object per line (host
+ * text), parsed on the host with the reference's JSON library (nlohmann 3.11.3):
+ * union schema in first-seen key order, absent keys "", strings verbatim,
+ * null "", other values their compact JSON text; blank lines skipped.
+ * PO_ERR_STRUCTURAL: a line that does not parse ("jsonl: line N: ...") or is
+ * not an object; PO_ERR_SCHEMA: an empty key. Handle as po_csv, host outputs. */
+typedef struct po_jsonl po_jsonl;
+int po_load_jsonl(const uint8_t* data, uint64_t len, po_jsonl** out);
+int po_jsonl_info(const po_jsonl* j, uint64_t* out_rows, uint32_t* out_fields,
+                  uint64_t* out_arena_bytes, uint64_t* out_names_bytes);
+int po_jsonl_copy(const po_jsonl* j, uint8_t* out_arena, uint64_t* out_offsets, uint8_t* out_names,
+                  uint64_t* out_name_offsets);
+void po_jsonl_free(po_jsonl* j);
+
+/* prefixopt::load_fd_config (fd.hpp:143-164): the FD config document
+ * {"groups": [["field", ...], ...]} (host text). First call with the three
+ * array pointers NULL for the sizes; then group g = names
+ * [group_offsets[g], group_offsets[g+1]), name k = bytes
+ * [name_offsets[k], name_offsets[k+1]). PO_ERR_STRUCTURAL: not JSON
+ * ("fd config: ..."); PO_ERR_SCHEMA: wrong shape (the reference's messages). */
+int po_load_fd_config(const uint8_t* data, uint64_t len, uint32_t* out_groups, uint64_t* out_names,
+                      uint64_t* out_names_bytes, uint64_t* out_group_offsets,
+                      uint64_t* out_name_offsets, uint8_t* out_bytes);
+
 /* ---- row-sharded solve over several GPUs ---------------
  * No reference counterpart: the reference ggr() (ggr.hpp:367-394) is one
  * process on one table. Here every rank (one per GPU) passes a contiguous

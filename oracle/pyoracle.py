@@ -338,27 +338,36 @@ def _csv_oracle_methods():
                 cell.append(ch)
                 any_content = True
 
+    def ref_loader(self, symbol, data):
+        fn = _bind(C.CDLL(str(self.path)), symbol, C.c_int, [C.c_void_p, C.c_uint64] + [C.c_void_p] * 8)
+        buf = np.frombuffer(data or b"\0", np.uint8)
+        rows, fields = C.c_uint64(0), C.c_uint32(0)
+        ab, nb = C.c_uint64(0), C.c_uint64(0)
+        args = (buf.ctypes.data, len(data), C.byref(rows), C.byref(fields), C.byref(ab),
+                C.byref(nb))
+        self._check(fn(*args, None, None, None, None))
+        n, m = int(rows.value), int(fields.value)
+        arena = np.zeros(max(int(ab.value), 1), np.uint8)
+        offs = np.zeros(n * m + 1, np.uint64)
+        names = np.zeros(max(int(nb.value), 1), np.uint8)
+        noff = np.zeros(m + 1, np.uint64)
+        self._check(fn(*args, arena.ctypes.data, offs.ctypes.data, names.ctypes.data,
+                       noff.ctypes.data))
+        nb_ = names.tobytes()
+        return Table.from_arena([nb_[int(noff[f]):int(noff[f + 1])] for f in range(m)],
+                                arena, offs, n)
+
+    def load_jsonl(self, data):
+        """load_jsonl (table.hpp:225-269): the reference itself only (its
+        behaviour is nlohmann::json's parser and serializer; no restatement)."""
+        if self.kind != "reference":
+            raise NotImplementedError("load_jsonl has no port restatement; use the reference")
+        return ref_loader(self, "ref_load_jsonl", bytes(data))
+
     def load_csv(self, data):
         data = bytes(data)
         if self.kind == "reference":
-            fn = _bind(C.CDLL(str(self.path)), "ref_load_csv", C.c_int,
-                       [C.c_void_p, C.c_uint64] + [C.c_void_p] * 8)
-            buf = np.frombuffer(data or b"\0", np.uint8)
-            rows, fields = C.c_uint64(0), C.c_uint32(0)
-            ab, nb = C.c_uint64(0), C.c_uint64(0)
-            args = (buf.ctypes.data, len(data), C.byref(rows), C.byref(fields), C.byref(ab),
-                    C.byref(nb))
-            self._check(fn(*args, None, None, None, None))
-            n, m = int(rows.value), int(fields.value)
-            arena = np.zeros(max(int(ab.value), 1), np.uint8)
-            offs = np.zeros(n * m + 1, np.uint64)
-            names = np.zeros(max(int(nb.value), 1), np.uint8)
-            noff = np.zeros(m + 1, np.uint64)
-            self._check(fn(*args, arena.ctypes.data, offs.ctypes.data, names.ctypes.data,
-                           noff.ctypes.data))
-            nb_ = names.tobytes()
-            return Table.from_arena([nb_[int(noff[f]):int(noff[f + 1])] for f in range(m)],
-                                    arena, offs, n)
+            return ref_loader(self, "ref_load_csv", data)
         first = read_record(data, 0, 1)
         if first is None:
             raise StructuralError("csv: missing header row")
@@ -386,6 +395,7 @@ def _csv_oracle_methods():
         return Table(header, rows)
 
     OracleLib.load_csv = load_csv
+    OracleLib.load_jsonl = load_jsonl
 
 
 _csv_oracle_methods()

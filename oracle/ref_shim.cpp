@@ -345,40 +345,65 @@ int ref_simulate(uint64_t n, const uint8_t* arena, const uint64_t* offsets, int3
   });
 }
 
+}  // extern "C"
+
+namespace {
+// A loaded table as sizes (out_arena == NULL) or as row-major arena +
+// offsets and names (the layout po_csv_copy / po_jsonl_copy produce).
+void emit_table(const prefixopt::Table& t, uint64_t* out_rows, uint32_t* out_fields,
+                uint64_t* out_arena_bytes, uint64_t* out_names_bytes, uint8_t* out_arena,
+                uint64_t* out_offsets, uint8_t* out_names, uint64_t* out_name_offsets) {
+  uint64_t ab = 0, nb = 0;
+  for (size_t r = 0; r < t.row_count(); ++r)
+    for (size_t f = 0; f < t.field_count(); ++f) ab += t.cell(r, f).size();
+  for (const auto& nm : t.field_names()) nb += nm.size();
+  *out_rows = t.row_count();
+  *out_fields = uint32_t(t.field_count());
+  *out_arena_bytes = ab;
+  *out_names_bytes = nb;
+  if (!out_arena) return;
+  uint64_t pos = 0, k = 0;
+  out_offsets[0] = 0;
+  for (size_t r = 0; r < t.row_count(); ++r)
+    for (size_t f = 0; f < t.field_count(); ++f) {
+      const std::string& c = t.cell(r, f);
+      std::memcpy(out_arena + pos, c.data(), c.size());
+      pos += c.size();
+      out_offsets[++k] = pos;
+    }
+  pos = 0;
+  out_name_offsets[0] = 0;
+  for (size_t f = 0; f < t.field_count(); ++f) {
+    const std::string& nm = t.field_name(f);
+    std::memcpy(out_names + pos, nm.data(), nm.size());
+    pos += nm.size();
+    out_name_offsets[f + 1] = pos;
+  }
+}
+}  // namespace
+
+extern "C" {
+
 // prefixopt::load_csv (table.hpp:188-215) on `len` bytes; sizes first
-// (out_arena == NULL), then the table (row-major arena + offsets, names).
+// (out_arena == NULL), then the table.
 int ref_load_csv(const uint8_t* data, uint64_t len, uint64_t* out_rows, uint32_t* out_fields,
                  uint64_t* out_arena_bytes, uint64_t* out_names_bytes, uint8_t* out_arena,
                  uint64_t* out_offsets, uint8_t* out_names, uint64_t* out_name_offsets) {
   return guarded([&] {
     std::istringstream in(std::string(reinterpret_cast<const char*>(data), len));
-    prefixopt::Table t = prefixopt::load_csv(in);
-    uint64_t ab = 0, nb = 0;
-    for (size_t r = 0; r < t.row_count(); ++r)
-      for (size_t f = 0; f < t.field_count(); ++f) ab += t.cell(r, f).size();
-    for (const auto& nm : t.field_names()) nb += nm.size();
-    *out_rows = t.row_count();
-    *out_fields = uint32_t(t.field_count());
-    *out_arena_bytes = ab;
-    *out_names_bytes = nb;
-    if (!out_arena) return;
-    uint64_t pos = 0, k = 0;
-    out_offsets[0] = 0;
-    for (size_t r = 0; r < t.row_count(); ++r)
-      for (size_t f = 0; f < t.field_count(); ++f) {
-        const std::string& c = t.cell(r, f);
-        std::memcpy(out_arena + pos, c.data(), c.size());
-        pos += c.size();
-        out_offsets[++k] = pos;
-      }
-    pos = 0;
-    out_name_offsets[0] = 0;
-    for (size_t f = 0; f < t.field_count(); ++f) {
-      const std::string& nm = t.field_name(f);
-      std::memcpy(out_names + pos, nm.data(), nm.size());
-      pos += nm.size();
-      out_name_offsets[f + 1] = pos;
-    }
+    emit_table(prefixopt::load_csv(in), out_rows, out_fields, out_arena_bytes, out_names_bytes,
+               out_arena, out_offsets, out_names, out_name_offsets);
+  });
+}
+
+// prefixopt::load_jsonl (table.hpp:225-269), same calling convention.
+int ref_load_jsonl(const uint8_t* data, uint64_t len, uint64_t* out_rows, uint32_t* out_fields,
+                   uint64_t* out_arena_bytes, uint64_t* out_names_bytes, uint8_t* out_arena,
+                   uint64_t* out_offsets, uint8_t* out_names, uint64_t* out_name_offsets) {
+  return guarded([&] {
+    std::istringstream in(std::string(reinterpret_cast<const char*>(data), len));
+    emit_table(prefixopt::load_jsonl(in), out_rows, out_fields, out_arena_bytes, out_names_bytes,
+               out_arena, out_offsets, out_names, out_name_offsets);
   });
 }
 

@@ -175,6 +175,10 @@ class CudaLib:
         self.csv_info = _bind(L, "po_csv_info", C.c_int, [vp, vp, vp, vp, vp])
         self.csv_copy = _bind(L, "po_csv_copy", C.c_int, [vp, C.c_uint32, vp, vp, vp, vp, vp])
         self.csv_free = _bind(L, "po_csv_free", None, [vp])
+        self.load_jsonl = _bind(L, "po_load_jsonl", C.c_int, [vp, C.c_uint64, vp])
+        self.jsonl_info = _bind(L, "po_jsonl_info", C.c_int, [vp, vp, vp, vp, vp])
+        self.jsonl_copy = _bind(L, "po_jsonl_copy", C.c_int, [vp, vp, vp, vp, vp])
+        self.jsonl_free = _bind(L, "po_jsonl_free", None, [vp])
         # row-sharded solve
         self.comm_unique_id = _bind(L, "po_comm_unique_id", C.c_int, [vp])
         self.comm_init_nccl = _bind(L, "po_comm_init_nccl", C.c_int,

@@ -723,6 +723,37 @@ def load_csv(source) -> Table:
     return Table.from_arena(field_names, arena, offs, n)
 
 
+def load_jsonl(source) -> Table:
+    """prefixopt::load_jsonl (table.hpp:225-269): `source` is the JSONL text
+    (bytes) or a path. Parsed on the host behind the C ABI (po_load_jsonl) with
+    the reference's JSON library; same table and same errors as the reference."""
+    if isinstance(source, (bytes, bytearray, memoryview)):
+        data = bytes(source)
+    else:
+        with open(source, "rb") as fh:
+            data = fh.read()
+    lib = cuda_lib()
+    buf = np.frombuffer(data or b"\0", dtype=np.uint8)
+    h = C.c_void_p(0)
+    lib.check(lib.load_jsonl(buf.ctypes.data, len(data), C.byref(h)))
+    try:
+        rows, fields = C.c_uint64(0), C.c_uint32(0)
+        ab, nb = C.c_uint64(0), C.c_uint64(0)
+        lib.check(lib.jsonl_info(h, C.byref(rows), C.byref(fields), C.byref(ab), C.byref(nb)))
+        n, m = int(rows.value), int(fields.value)
+        arena = np.empty(max(int(ab.value), 1), dtype=np.uint8)
+        offs = np.empty(n * m + 1, dtype=np.uint64)
+        names = np.empty(max(int(nb.value), 1), dtype=np.uint8)
+        noff = np.empty(m + 1, dtype=np.uint64)
+        lib.check(lib.jsonl_copy(h, arena.ctypes.data, offs.ctypes.data, names.ctypes.data,
+                                 noff.ctypes.data))
+    finally:
+        lib.jsonl_free(h)
+    nb_ = names.tobytes()
+    field_names = [nb_[int(noff[f]):int(noff[f + 1])] for f in range(m)]
+    return Table.from_arena(field_names, arena, offs, n)
+
+
 # low-level entry for callers holding device buffers (bench.py, multi-GPU)
 def ggr_into(view: TableView, fd_groups: list, cfg: GgrConfig, tok_kind: int, scoring: int,
              out_location: int, out_rows, out_orders, stream: int = 0):
@@ -749,5 +780,5 @@ __all__ = [
     "PO_LOC_HOST", "PO_LOC_DEVICE", "FdWitness", "FdGroupReport", "FdValidationReport",
     "validate_fds", "discover_fds", "render_prompts", "render_prompts_arena", "DedupResult",
     "dedup", "CacheConfig", "RequestSim", "SimReport", "simulate", "validate_schedule",
-    "phr_for_schedule", "load_csv",
+    "phr_for_schedule", "load_csv", "load_jsonl",
 ]

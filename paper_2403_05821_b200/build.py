@@ -20,6 +20,11 @@ BUILD = REPO / "build" / "cuda"
 OUT = PKG / "libprefixopt_cuda.so"
 GEN_OUT = PKG / "libpogen.so"
 CXX = os.environ.get("CXX", shutil.which("g++") or "g++")
+# host-only translation units (g++): JSONL ingest with the reference's JSON library
+CPP_SOURCES = ["jsonl.cpp"]
+JSON_DIR = os.environ.get(
+    "PO_JSON_DIR",
+    "/opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_frontend/thirdparty/nlohmann")
 SOURCES = ["abi.cu", "dict.cu", "encode.cu", "refine.cu", "phc.cu", "ggr.cu", "comm.cu", "shard.cu", "fd.cu", "render.cu", "replay.cu", "csv.cu"]
 
 NVCC = os.environ.get("NVCC", shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc")
@@ -55,6 +60,13 @@ def build(verbose: bool = False, force: bool = False) -> Path:
             raise RuntimeError(f"nvcc failed:\n{' '.join(cmd)}\n{r.stdout}\n{r.stderr}")
         return r
 
+    for src in CPP_SOURCES:
+        c = CSRC / src
+        o = BUILD / (src + ".o")
+        objs.append(o)
+        if force or _stale(o, [c, REPO / "include" / "prefixopt_cuda.h"]):
+            jobs.append([CXX, "-std=c++17", "-O2", "-fPIC", "-I", JSON_DIR, "-I", str(REPO / "include"),
+                         "-c", str(c), "-o", str(o)])
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
         list(ex.map(run, jobs))
     if force or jobs or _stale(OUT, objs):

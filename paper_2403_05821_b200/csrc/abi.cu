@@ -956,6 +956,15 @@ void po_slice_free(po_slice* slice) { delete slice; }
 
 const char* po_last_error(void) { return g_err.c_str(); }
 
+}  // extern "C"
+
+namespace po {
+// for entry points defined in other translation units (jsonl.cpp)
+void set_last_error(const std::string& msg) { g_err = msg; }
+}  // namespace po
+
+extern "C" {
+
 const char* po_build_info(void) { return "prefixopt-b200 sm_100a"; }
 
 uint64_t po_trim_device_cache(void) { return po::trim_cached_blocks(); }

@@ -8,28 +8,13 @@
 #include <vector>
 
 #include "prefixopt_cuda.h"
+#include "prefixopt/detail/check.hpp"
 #include "prefixopt/errors.hpp"
 #include "prefixopt/scoring.hpp"
 #include "prefixopt/table.hpp"
 #include "prefixopt/tokenizer.hpp"
 
 namespace prefixopt::detail {
-
-// Rethrows a PO_ERR_* status as the reference's exception class.
-inline void check(int code) {
-  if (code == PO_OK) return;
-  std::string msg = po_last_error();
-  switch (code) {
-    case PO_ERR_SCHEMA: throw schema_error(msg);
-    case PO_ERR_STRUCTURAL: throw structural_error(msg);
-    case PO_ERR_DOMAIN: throw domain_error(msg);
-    case PO_ERR_SIZE: throw size_error(msg);
-    case PO_ERR_IO: throw io_error(msg);
-    case PO_ERR_OUT_OF_RANGE: throw std::out_of_range(msg);
-    case PO_ERR_INVALID_ARG: throw std::invalid_argument(msg);
-    default: throw error(msg);
-  }
-}
 
 inline int tokenizer_kind(const Tokenizer& tok) {
   if (dynamic_cast<const CharTokenizer*>(&tok)) return PO_TOK_CHAR;

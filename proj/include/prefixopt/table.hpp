@@ -114,3 +114,6 @@ class Table {
 };
 
 }  // namespace prefixopt
+
+// ingest (load_csv / load_jsonl / load_table*) and write_csv
+#include "prefixopt/detail/table_io.hpp"

@@ -1,27 +1,125 @@
-"""The reference's own C++ tests (proj/tests/*.cpp in /root/reference),
-compiled against the drop-in headers in proj/include and linked with
-libprefixopt_cuda.so (proj/tests/Makefile), must pass on the GPU."""
+"""The reference's own C++ tests and demo (proj/tests/*.cpp, demos/
+quickstart.cpp in /root/reference), compiled against the drop-in headers in
+proj/include and linked with libprefixopt_cuda.so (proj/tests/Makefile), must
+pass on the GPU. The demo and the cmd_solve driver (the reference's
+production caller of ggr(), run.hpp:375-480) are also compiled against the
+unmodified reference headers alone (CPU): both builds must print the same
+results and write the same schedule files."""
+import csv
+import io
+import json
 import subprocess
 from pathlib import Path
 
 import pytest
 
+from golden_cases import load_cases
+from paper_2403_05821_b200 import gen
+
 BIN = Path(__file__).resolve().parent.parent / "proj" / "tests" / "bin"
 TESTS = ["test_objective", "test_solver_greedy", "test_solver_exact", "acceptance",
-         "test_b200_ext"]
+         "test_table", "test_b200_ext"]
+
+
+def _exe(name):
+    exe = BIN / name
+    if not exe.exists():
+        pytest.skip(f"{exe} not built (make -C proj/tests needs /root/reference at build time)")
+    return exe
+
+
+def _run(exe, *args, cwd=None):
+    r = subprocess.run([str(exe), *map(str, args)], capture_output=True, timeout=900, cwd=cwd)
+    return r.returncode, r.stdout, r.stderr
 
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("name", TESTS)
 def test_reference_cpp_suite_against_dropin(name):
-    exe = BIN / name
-    if not exe.exists():
-        pytest.skip(f"{exe} not built (make -C proj/tests needs /root/reference at build time)")
-    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=900)
-    print(r.stdout[-4000:], r.stderr[-4000:])
-    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    rc, out, err = _run(_exe(name))
+    out, err = out.decode(errors="replace"), err.decode(errors="replace")
+    print(out[-4000:], err[-4000:])
+    assert rc == 0, out[-2000:] + err[-2000:]
     if name == "acceptance":
-        assert "[FAIL]" not in r.stdout
+        assert "[FAIL]" not in out
         # criterion 8 known answer: 30000x57 synthetic_wide_table, seed
         # 20240008, GgrConfig defaults -> PHC 8,072,240
-        assert "score 8072240" in r.stdout
+        assert "score 8072240" in out
+
+
+def _write_csv(path, names, rows):
+    buf = io.StringIO(newline="")
+    w = csv.writer(buf, lineterminator="\n")
+    w.writerow(names)
+    w.writerows(rows)
+    path.write_bytes(buf.getvalue().encode("latin-1"))
+
+
+def _movie_files(tmp_path):
+    """demos/data/movie_reviews.csv (from the golden cases: the box has no
+    /root/reference) and demos/data/movie_fds.json."""
+    case = next(c for c in load_cases() if c[0] == "movie_reviews_quickstart")
+    t = case[1]
+    names = [n.decode("latin-1") for n in t.field_names]
+    rows = [[c.decode("latin-1") for c in t.row(r)] for r in range(t.row_count())]
+    table = tmp_path / "movie_reviews.csv"
+    _write_csv(table, names, rows)
+    fds = tmp_path / "movie_fds.json"
+    fds.write_text(json.dumps({"groups": [["movie_title", "movie_info"]]}))
+    jl = tmp_path / "movie_reviews.jsonl"
+    jl.write_text("".join(json.dumps(dict(zip(names, r))) + "\n" for r in rows))
+    return table, fds, jl, names, rows
+
+
+@pytest.mark.gpu
+def test_quickstart_demo_matches_reference_build(tmp_path):
+    table, fds, _, _, _ = _movie_files(tmp_path)
+    a = _run(_exe("quickstart"), table, fds)
+    b = _run(_exe("quickstart_ref"), table, fds)
+    print(a[1].decode(), b[1].decode())
+    assert a[0] == b[0] == 0
+    assert a[1] == b[1]
+    ggr_line = next(l for l in a[1].decode().splitlines() if l.startswith("ggr"))
+    assert ggr_line.split()[1] == "254072"  # SURVEY.md §8c known answer
+
+
+def _cmd_solve_cases(tmp_path):
+    table, fds, jl, names, rows = _movie_files(tmp_path)
+    bad_fd = tmp_path / "bad_fds.json"
+    bad_fd.write_text(json.dumps({"groups": [["movie_title", "review_type"]]}))
+    c1 = gen.generate(1, n_rows=3000)
+    c1_csv = tmp_path / "c1.csv"
+    _write_csv(c1_csv, [n.decode() for n in c1.field_names],
+               [[x.decode("latin-1") for x in c1.row(r)] for r in range(c1.row_count())])
+    c3 = gen.generate(3, n_rows=4000)
+    c3_csv = tmp_path / "c3.csv"
+    _write_csv(c3_csv, [n.decode() for n in c3.field_names],
+               [[x.decode("latin-1") for x in c3.row(r)] for r in range(c3.row_count())])
+    c3_fd = tmp_path / "c3_fds.json"
+    c3_fd.write_text(json.dumps({"groups": gen.fds(3)}))
+    return [
+        ("movies_ggr_fds", table, fds, "ggr", None),
+        ("movies_ggr_fds_threshold0", table, fds, "ggr", 0),
+        ("movies_jsonl_ggr", jl, fds, "ggr", 0),
+        ("movies_fixed_stats", table, "-", "fixed-stats", None),
+        ("movies_original", table, "-", "original", None),
+        ("movies_violated_fd", table, bad_fd, "ggr", 0),
+        ("c1_3000_ggr", c1_csv, "-", "ggr", None),
+        ("c3_4000_ggr_fds", c3_csv, c3_fd, "ggr", None),
+    ]
+
+
+@pytest.mark.gpu
+def test_cmd_solve_matches_reference_build(tmp_path):
+    for name, table, fd, solver, thr in _cmd_solve_cases(tmp_path):
+        outs = []
+        for exe in ("cmd_solve_smoke", "cmd_solve_smoke_ref"):
+            sched = tmp_path / f"{name}.jsonl"  # same path: the report echoes it
+            args = [table, fd, solver, sched] + ([thr] if thr is not None else [])
+            rc, out, err = _run(_exe(exe), *args)
+            assert rc == 0, (name, exe, out[-2000:], err[-2000:])
+            outs.append((out, sched.read_bytes()))
+        assert outs[0][0] == outs[1][0], (name, outs[0][0][:3000], outs[1][0][:3000])
+        assert outs[0][1] == outs[1][1], name
+        if name == "movies_violated_fd":
+            assert b"warning: fd group" in outs[0][0]
