@@ -292,14 +292,18 @@ def run_ours(args):
         log(f"   {k:28s} {ms_k:8.3f} ms/step  {cnt:6.1f} launches  "
             f"({100*ms_k/max(total_kernel_ms,1e-9):5.1f}% of kernel time)")
 
-    # roofline of the HBM-streaming kernel (K1 cell_scan, k_cell_hash_seg):
-    # it must read every cell byte and its offset pair once, so its algorithmic
-    # bytes per launch are S + 8*(n*m+1) (the 8-byte hash it writes per cell is
-    # an intermediate of this design and is not counted)
+    # roofline of the dominant kernel: the top kernel by time when its
+    # algorithmic bytes are defined, else the HBM-streaming dictionary kernel.
+    # k_hash_probe (K1 + K2a) must read every cell byte and its offset pair
+    # once: S + 8*(n*m+1) per launch over all its launches of a step (the
+    # 4-byte id it writes per cell is an intermediate of this design and is
+    # not counted)
     peak, peak_kind = peaks()
-    dom = next((k for k in prof if k.startswith("k_cell_hash")), "k_cell_hash_seg")
-    dom_ms = prof.get(dom, (1, 0.0))[1] / max(prof.get(dom, (1, 0.0))[0], 1)
-    dom_bytes = cell_bytes + 8 * (n * m + 1)
+    alg = {"k_hash_probe": cell_bytes + 8 * (n * m + 1)}
+    top = kern[0][1] if kern else "k_hash_probe"
+    dom = top if top in alg else "k_hash_probe"
+    dom_ms = prof.get(dom, (1, 0.0))[1] / prof_steps  # all launches of one step
+    dom_bytes = alg[dom]
     achieved = dom_bytes / (dom_ms / 1e3) / 1e9 if dom_ms > 0 else 0.0
     traffic = None
     tfile = ROOT / "profiles" / "ncu_traffic.json"
@@ -375,13 +379,17 @@ def run_ours(args):
                             "candidates_examined": st.candidates_examined,
                             "max_depth": st.max_depth},
             "e2e": {"value": world * n / (ms_e2e / 1e3), "unit": UNIT,
+                    "cell_bytes_per_s": world * cell_bytes / (ms_e2e / 1e3),
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "ms_per_step": ms_e2e, "host_wall_ms_per_step": wall_e2e},
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
                          "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
-                         "algorithmic_bytes_per_launch": dom_bytes,
-                         "kernel_ms": dom_ms, "peak_source": peak_kind,
+                         "algorithmic_bytes_per_step": dom_bytes,
+                         "kernel_ms_per_step": dom_ms, "peak_source": peak_kind,
+                         "top_kernel": {"name": top, "ms_per_step": kern[0][0] if kern else None,
+                                        "share": (kern[0][0] / total_kernel_ms) if kern else None},
                          "pipeline_b_alg_frac": (b_alg / (ms / 1e3) / 1e9) / peak},
+            "cell_bytes_per_s": value * cell_bytes / n,
             "kernels_ms_per_step": {k: round(v, 4) for v, k, _ in kern[:16]},
             "kernel_ms_total": round(total_kernel_ms, 4),
             "cpu_baseline": cpu,

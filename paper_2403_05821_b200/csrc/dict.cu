@@ -488,22 +488,66 @@ __global__ void __launch_bounds__(kBuildBlock, 3) k_dict_build(BuildArgs A) {
 // ---------------------------------------------------------------------------
 // Default path: three kernels per chunk (the fused group kernel above is
 // slower on C2 and C5: profiles/r2_dict_experiments.md).
-//   K1 k_hash_cells   thread per cell, warps walk 32 rows column by column
+//   K1+K2a k_hash_probe thread per cell, warps walk 32 rows column by column
 //                     (lanes of a warp hash cells of one column: similar
-//                     lengths), 4 aligned 8-byte loads per 4 words
-//   K2a k_probe_cells thread per cell: claim (new value id) or find the slot
-//                     of the cell's hash; found ids are marked pending
+//                     lengths), 4 aligned 8-byte loads per 4 words; then the
+//                     warp probes the column's table in lockstep rounds:
+//                     claim (new value id) or find the slot of the cell's
+//                     hash (id marked pending)
 //   K2b k_verify_cells every pending cell byte-compared with its value's
 //                     representative; a mismatch (64-bit collision) goes to
 //   K2c k_fixup_cells exact re-probe with byte verification at every equal key
 // ---------------------------------------------------------------------------
 constexpr uint32_t kPending = 0x80000000u;  // cid_mat: found, not yet verified
 
-__global__ void __launch_bounds__(256) k_hash_cells(const uint8_t* __restrict__ chunk, uint64_t base,
+// Cell hash of (row r, column c) of the chunk (thread per cell): the last
+// aligned word of a step is the first of the next, carried (four loads per
+// four words).
+__device__ __forceinline__ uint64_t cell_hash(const uint8_t* __restrict__ chunk, uint64_t base,
+                                              const uint64_t* lim, uint64_t o0, uint64_t len,
+                                              uint64_t hash_mask) {
+  const uintptr_t ad = reinterpret_cast<uintptr_t>(chunk + (o0 - base));
+  const uint64_t* p = reinterpret_cast<const uint64_t*>(ad & ~uintptr_t(7));
+  const uint32_t sh = uint32_t(ad & 7) * 8;
+  const uint64_t words = (len + 7) / 8;
+  uint64_t sum = 0;
+  uint64_t carry = (words && p < lim) ? __ldg(p) : 0;
+  for (uint64_t k = 0; k < words; k += 4) {
+    uint64_t w[5];
+    w[0] = carry;
+#pragma unroll
+    for (int u = 1; u < 5; ++u) w[u] = (p + k + u < lim) ? __ldg(p + k + u) : 0;
+    carry = w[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint64_t kk = k + u;
+      if (kk < words) {
+        uint64_t x = funnel(w[u], w[u + 1], sh);
+        const uint64_t rem = len - 8 * kk;
+        if (rem < 8) x = mask_low_bytes(x, uint32_t(rem));
+        sum += word_term(x, kk);
+      }
+    }
+  }
+  const uint64_t h = hash_finish(sum, len) & hash_mask;
+  return h ? h : 1;
+}
+
+// K1 + K2a: warps take 32 rows and walk them column by column (lanes of a
+// warp hash cells of one column: similar lengths; one row's bytes are read
+// by the same lane in consecutive iterations, so boundary sectors hit L1),
+// then probe the column's table with the hashes in lockstep rounds
+// (probe_round: each round's claims reserve their ids with one atomic per
+// warp; a lane meeting its hash in a slot whose id is not yet visible
+// retries it next round). Claimed cells get their new id, found cells the
+// slot's id marked pending (byte verification follows).
+__global__ void __launch_bounds__(256) k_hash_probe(const uint8_t* __restrict__ chunk, uint64_t base,
                                                     const uint8_t* chunk_lim,
                                                     const uint64_t* __restrict__ offs, uint64_t rows,
-                                                    uint32_t m, uint64_t hash_mask,
-                                                    unsigned long long* __restrict__ hashes) {
+                                                    uint64_t r0, uint32_t m, uint64_t hash_mask,
+                                                    const ColDict* __restrict__ cols, uint32_t* ncid,
+                                                    uint32_t* overflow, uint32_t* cid_mat) {
+  constexpr unsigned kFull = 0xffffffffu;
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t ntiles = (rows + 31) / 32;
   const uint64_t* lim =
@@ -511,73 +555,22 @@ __global__ void __launch_bounds__(256) k_hash_cells(const uint8_t* __restrict__ 
   for (uint64_t tile = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5; tile < ntiles;
        tile += (uint64_t(gridDim.x) * blockDim.x) >> 5)
     for (uint32_t c = 0; c < m; ++c) {
-      // the warp walks its 32 rows column by column: one row's bytes are read
-      // by the same lane in consecutive iterations (boundary sectors hit L1)
-      const uint64_t r = tile * 32 + lane;
-      if (r >= rows) continue;
-      const uint64_t i = r * m + c;
-      const uint64_t o0 = offs[i], len = offs[i + 1] - o0;
-      const uintptr_t ad = reinterpret_cast<uintptr_t>(chunk + (o0 - base));
-      const uint64_t* p = reinterpret_cast<const uint64_t*>(ad & ~uintptr_t(7));
-      const uint32_t sh = uint32_t(ad & 7) * 8;
-      const uint64_t words = (len + 7) / 8;
-      uint64_t sum = 0;
-      // the last aligned word of a step is the first of the next: carried
-      // (four loads per four words)
-      uint64_t carry = (words && p < lim) ? __ldg(p) : 0;
-      for (uint64_t k = 0; k < words; k += 4) {
-        uint64_t w[5];
-        w[0] = carry;
-#pragma unroll
-        for (int u = 1; u < 5; ++u) w[u] = (p + k + u < lim) ? __ldg(p + k + u) : 0;
-        carry = w[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const uint64_t kk = k + u;
-          if (kk < words) {
-            uint64_t x = funnel(w[u], w[u + 1], sh);
-            const uint64_t rem = len - 8 * kk;
-            if (rem < 8) x = mask_low_bytes(x, uint32_t(rem));
-            sum += word_term(x, kk);
-          }
-        }
-      }
-      const uint64_t h = hash_finish(sum, len) & hash_mask;
-      hashes[(tile * m + c) * 32 + lane] = h ? h : 1;  // tile-major: coalesced
-    }
-}
-
-// Warps take 32 rows of one column (the layout of k_hash_cells) and probe in
-// lockstep rounds: each lane examines one slot per round; the round's claims
-// of a new value reserve their ids with ONE atomic per warp (a per-column
-// counter would otherwise serialise every new value of a unique column), and
-// a lane that meets its hash in a slot whose id is not yet visible simply
-// retries it next round.
-__global__ void __launch_bounds__(256) k_probe_cells(const ColDict* __restrict__ cols,
-                                                     const unsigned long long* __restrict__ hashes,
-                                                     const uint64_t* __restrict__ offs, uint64_t rows,
-                                                     uint64_t r0, uint32_t m, uint32_t* ncid,
-                                                     uint32_t* overflow, uint32_t* cid_mat) {
-  constexpr unsigned kFull = 0xffffffffu;
-  const uint32_t lane = threadIdx.x & 31;
-  const uint64_t ntiles = (rows + 31) / 32;
-  for (uint64_t tile = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5; tile < ntiles;
-       tile += (uint64_t(gridDim.x) * blockDim.x) >> 5)
-    for (uint32_t c = 0; c < m; ++c) {
-      const ColDict& D = cols[c];
       const uint64_t r = tile * 32 + lane;
       bool search = r < rows;
-      const uint64_t h = search ? hashes[(tile * m + c) * 32 + lane] : 0;
-      uint64_t slot = h & (D.cap - 1);
-      uint64_t tries = 0;
-      uint32_t out = kNoCid;
       const uint64_t i = r * m + c;
-      const uint64_t o0 = search ? offs[i] : 0;
-      const uint32_t len = search ? uint32_t(offs[i + 1] - o0) : 0;
+      uint64_t o0 = 0, len = 0, h = 0;
+      if (search) {
+        o0 = offs[i];
+        len = offs[i + 1] - o0;
+        h = cell_hash(chunk, base, lim, o0, len, hash_mask);
+      }
+      const ColDict& D = cols[c];
+      uint64_t slot = h & (D.cap - 1), tries = 0;
+      uint32_t out = kNoCid;
       while (__any_sync(kFull, search)) {
         uint32_t id = 0;
-        const uint32_t res =
-            probe_round(D, c, h, slot, tries, search, id, o0, len, uint32_t(r0 + r), ncid, overflow);
+        const uint32_t res = probe_round(D, c, h, slot, tries, search, id, o0, uint32_t(len),
+                                         uint32_t(r0 + r), ncid, overflow);
         if (search && res != kSearching) {
           out = res == kClaimed ? id : (res == kFound ? (id | kPending) : kNoCid);
           search = false;
@@ -681,16 +674,17 @@ __global__ void __launch_bounds__(256) k_verify_cells(BuildArgs A, uint32_t* col
 
 // Rare path: a cell whose hash slot holds a different string re-probes its
 // column with byte verification at every slot of its hash.
-__global__ void k_fixup_cells(BuildArgs A, const unsigned long long* __restrict__ hashes,
-                              const uint32_t* collided, const uint32_t* n_collided_dev) {
+__global__ void k_fixup_cells(BuildArgs A, const uint32_t* collided, const uint32_t* n_collided_dev) {
   const uint32_t nc = *n_collided_dev;  // read on the device: no host round trip
   for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < nc; q += gridDim.x * blockDim.x) {
     const uint64_t i = collided[q];
     const uint64_t r = i / A.m;
     const uint32_t c = uint32_t(i - r * A.m);
     const ColDict& D = A.cols[c];
-    const uint64_t h = hashes[((r / 32) * A.m + c) * 32 + (r % 32)];
     const uint64_t o0 = A.offs[i], len = A.offs[i + 1] - o0;
+    const uint64_t* lim = reinterpret_cast<const uint64_t*>(
+        (reinterpret_cast<uintptr_t>(A.chunk_lim) + 7) & ~uintptr_t(7));
+    const uint64_t h = cell_hash(A.chunk, A.base, lim, o0, len, A.hmask);
     const uint8_t* cell = A.chunk + (o0 - A.base);
     uint64_t slot = h & (D.cap - 1);
     uint32_t out = kNoCid;
@@ -948,17 +942,14 @@ class Builder {
         PO_LAUNCH(k_dict_build, grid, kBuildBlock, smem, s_, A);
       } else {
         const uint64_t cells = (r1 - r0) * m_;
-        hashes_.alloc_auto(((r1 - r0 + 31) / 32) * 32 * m_, s_);
         collided_.alloc_auto(cells, s_);
         DevBuf<uint32_t> ncol(1, s_);
         ncol.zero();
         const unsigned gw = grid_for(((r1 - r0 + 31) / 32) * 32, 256, 8);
-        PO_LAUNCH(k_hash_cells, gw, 256, 0, s_, chunk, base, chunk_lim, offs, r1 - r0, m_, hmask_,
-                  hashes_.get());
-        PO_LAUNCH(k_probe_cells, gw, 256, 0, s_, d_cols_.get(), hashes_.get(),
-                  offs, r1 - r0, r0, m_, ncid_.get(), over_.get(), cid_mat);
+        PO_LAUNCH(k_hash_probe, gw, 256, 0, s_, chunk, base, chunk_lim, offs, r1 - r0, r0, m_, hmask_,
+                  d_cols_.get(), ncid_.get(), over_.get(), cid_mat);
         PO_LAUNCH(k_verify_cells, gw, 256, 0, s_, A, collided_.get(), ncol.get());
-        PO_LAUNCH(k_fixup_cells, kSMs, 128, 0, s_, A, hashes_.get(), collided_.get(), ncol.get());
+        PO_LAUNCH(k_fixup_cells, kSMs, 128, 0, s_, A, collided_.get(), ncol.get());
       }
       std::vector<uint32_t> hc(2 * m_);
       ncid_.download(hc.data(), m_);
@@ -1018,7 +1009,6 @@ class Builder {
     const char* v = std::getenv("PO_DICT_KERNEL");
     return v && std::string(v) == "fused";
   }();
-  DevBuf<unsigned long long> hashes_;
   DevBuf<uint32_t> collided_;
   bool dirty_ = true;
   std::vector<uint32_t> count_;
@@ -1076,10 +1066,13 @@ void build_dictionary(const DeviceTable& t, uint32_t hash_bits, cudaStream_t s, 
   // budget (about 48 B per cell), one chunk with exact worst-case tables;
   // otherwise a first chunk with room for all its rows to be new, then
   // tables sized from its distinct counts.
-  size_t free_b = 0, total_b = 0;
-  PO_CUDA(cudaMemGetInfo(&free_b, &total_b));
   const double worst = 48.0 * double(n) * double(m);
-  const bool exact_caps = worst <= std::min(4e9, 0.1 * double(free_b));
+  bool exact_caps = worst <= 1e9;  // no driver query on the common path
+  if (!exact_caps && worst <= 4e9) {
+    size_t free_b = 0, total_b = 0;
+    PO_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    exact_caps = worst <= 0.1 * double(free_b);
+  }
   const uint64_t R0 = (exact_caps || n <= 131072) ? n : std::max<uint64_t>(65536, n / 16);
   for (uint32_t c = 0; c < m; ++c) B.reserve(c, exact_caps ? n : R0);
 
