@@ -32,6 +32,8 @@ GOLD = json.loads((Path(__file__).resolve().parent / "golden" / "full_digests.js
 def _solve_device(t, cfg_id):
     fd_idx = [[t.require_field(x) for x in g] for g in gen.fds(cfg_id)]
     n, m = t.row_count(), t.field_count()
+    po._abi.cuda_lib().trim_device_cache()  # idle cached blocks of earlier large solves
+    torch.cuda.empty_cache()
     d_arena = torch.from_numpy(t.arena).to("cuda")
     d_offs = torch.from_numpy(t.offsets.view(np.int64)).to("cuda")
     dv = t.view(PO_LOC_DEVICE, arena=d_arena, offsets=d_offs)

@@ -77,6 +77,8 @@ def main():
     for path in paths:
         res, seen = None, set()
         if path == "device":
+            po._abi.cuda_lib().trim_device_cache()
+            torch.cuda.empty_cache()
             s = torch.cuda.current_stream()
             d_arena = torch.from_numpy(t.arena).to("cuda")
             d_offs = torch.from_numpy(t.offsets.view(np.int64)).to("cuda")
