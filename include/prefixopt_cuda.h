@@ -250,6 +250,24 @@ int po_comm_init_nccl(const uint8_t* id128, int32_t nranks, int32_t rank, po_com
 /* In-process transport: nranks communicators for nranks host threads of one
  * process (any devices, several ranks may share one GPU). */
 int po_comm_init_local(int32_t nranks, po_comm** out_array);
+/* Host-staged transport over caller-provided collectives on HOST buffers
+ * (e.g. MPI, or torch.distributed with the gloo backend): every device
+ * collective is staged D2H, handed to the callbacks, and staged back H2D.
+ * Callbacks return 0 on success. Ranks are processes (or threads) of any
+ * layout, including several ranks on one GPU. */
+typedef struct po_host_collectives {
+  void* ctx;
+  /* recv = every rank's `bytes` bytes, back to back in rank order */
+  int (*allgather)(void* ctx, const void* send, void* recv, uint64_t bytes);
+  /* rank r contributes recv_bytes[r] bytes (send holds recv_bytes[rank]);
+   * recv gets them back to back in rank order */
+  int (*allgatherv)(void* ctx, const void* send, void* recv, const uint64_t* recv_bytes);
+  /* send_bytes[r] bytes to rank r and recv_bytes[r] from rank r, both
+   * contiguous in rank order */
+  int (*alltoallv)(void* ctx, const void* send, const uint64_t* send_bytes, void* recv,
+                   const uint64_t* recv_bytes);
+} po_host_collectives;
+int po_comm_init_host(const po_host_collectives* ops, int32_t nranks, int32_t rank, po_comm** out);
 int po_comm_destroy(po_comm* comm);
 
 /* Sharded prefixopt::ggr. `t` holds this rank's rows (same fields on every

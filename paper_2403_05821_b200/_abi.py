@@ -185,6 +185,8 @@ class CudaLib:
                                     [vp, C.c_int32, C.c_int32, C.POINTER(vp)])
         self.comm_init_local = _bind(L, "po_comm_init_local", C.c_int, [C.c_int32, vp])
         self.comm_destroy = _bind(L, "po_comm_destroy", C.c_int, [vp])
+        self.comm_init_host = _bind(L, "po_comm_init_host", C.c_int,
+                                    [vp, C.c_int32, C.c_int32, vp])
         self.ggr_sharded = _bind(L, "po_ggr_sharded", C.c_int,
                                  [vp, vp, vp, vp, C.c_int32, C.c_int32, C.POINTER(vp), vp, vp, vp])
         self.slice_info = _bind(L, "po_slice_info", C.c_int, [vp, vp, vp])

@@ -883,6 +883,15 @@ int po_comm_init_local(int32_t nranks, po_comm** out_array) {
   });
 }
 
+int po_comm_init_host(const po_host_collectives* ops, int32_t nranks, int32_t rank, po_comm** out) {
+  return guarded([&] {
+    if (!ops || !out) fail(PO_ERR_INVALID_ARG, "null argument");
+    auto h = std::make_unique<po_comm>();
+    h->c.reset(make_host_comm(*ops, nranks, rank));
+    *out = h.release();
+  });
+}
+
 int po_comm_destroy(po_comm* comm) {
   return guarded([&] { delete comm; });
 }

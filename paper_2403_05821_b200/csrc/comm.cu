@@ -278,7 +278,87 @@ class LocalComm final : public Comm {
   std::shared_ptr<LocalGroup> g_;
 };
 
+// ---------------------------------------------------------------------------
+// host-staged transport over caller-provided host collectives
+// ---------------------------------------------------------------------------
+class HostComm final : public Comm {
+ public:
+  HostComm(const po_host_collectives& ops, int nranks, int rank) : ops_(ops) {
+    rank_ = rank;
+    size_ = nranks;
+  }
+  void allreduce(void* d, size_t n, CDtype t, COp op, cudaStream_t s) override {
+    if (!n || size_ == 1) return;
+    const size_t es = t == CDtype::U32 ? 4 : 8;
+    std::vector<uint8_t> mine(n * es), all(n * es * size_);
+    down(d, mine.data(), n * es, s);
+    call(ops_.allgather(ops_.ctx, mine.data(), all.data(), n * es), "allgather");
+    DevBuf<uint8_t> d_all(all.size(), s);
+    d_all.upload(all.data(), all.size());
+    if (t == CDtype::U32)
+      PO_LAUNCH(k_reduce_ranks<uint32_t>, grid_for(n, 256), 256, 0, s,
+                reinterpret_cast<const uint32_t*>(d_all.get()), n, size_, op == COp::Max ? 1 : 0,
+                static_cast<uint32_t*>(d));
+    else
+      PO_LAUNCH(k_reduce_ranks<unsigned long long>, grid_for(n, 256), 256, 0, s,
+                reinterpret_cast<const unsigned long long*>(d_all.get()), n, size_,
+                op == COp::Max ? 1 : 0, static_cast<unsigned long long*>(d));
+    sync(s);
+  }
+  void allgather(const void* send, void* recv, size_t bytes, cudaStream_t s) override {
+    if (!bytes) return;
+    std::vector<uint8_t> mine(bytes), all(bytes * size_);
+    down(send, mine.data(), bytes, s);
+    call(ops_.allgather(ops_.ctx, mine.data(), all.data(), bytes), "allgather");
+    up(all.data(), recv, all.size(), s);
+  }
+  void allgatherv(const void* send, void* recv, const std::vector<uint64_t>& rb,
+                  cudaStream_t s) override {
+    uint64_t tot = 0;
+    for (uint64_t b : rb) tot += b;
+    std::vector<uint8_t> mine(rb[rank_] ? rb[rank_] : 1), all(tot ? tot : 1);
+    down(send, mine.data(), rb[rank_], s);
+    call(ops_.allgatherv(ops_.ctx, mine.data(), all.data(), rb.data()), "allgatherv");
+    up(all.data(), recv, tot, s);
+  }
+  void alltoallv(const void* send, const std::vector<uint64_t>& sb, void* recv,
+                 const std::vector<uint64_t>& rb, cudaStream_t s) override {
+    uint64_t st = 0, rt = 0;
+    for (int r = 0; r < size_; ++r) {
+      st += sb[r];
+      rt += rb[r];
+    }
+    std::vector<uint8_t> hs(st ? st : 1), hr(rt ? rt : 1);
+    down(send, hs.data(), st, s);
+    call(ops_.alltoallv(ops_.ctx, hs.data(), sb.data(), hr.data(), rb.data()), "alltoallv");
+    up(hr.data(), recv, rt, s);
+  }
+
+ private:
+  static void call(int rc, const char* what) {
+    if (rc != 0) fail(PO_ERR_ERROR, std::string("host collective ") + what + " failed");
+  }
+  static void down(const void* d, void* h, size_t bytes, cudaStream_t s) {
+    if (!bytes) return;
+    PO_CUDA(cudaMemcpyAsync(h, d, bytes, cudaMemcpyDeviceToHost, s));
+    sync(s);
+  }
+  static void up(const void* h, void* d, size_t bytes, cudaStream_t s) {
+    if (!bytes) return;
+    PO_CUDA(cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, s));
+    sync(s);  // the host staging buffer is freed on return
+  }
+  po_host_collectives ops_;
+};
+
 }  // namespace
+
+Comm* make_host_comm(const po_host_collectives& ops, int nranks, int rank) {
+  if (nranks < 1 || rank < 0 || rank >= nranks) fail(PO_ERR_INVALID_ARG, "bad rank/world size");
+  if (!ops.allgather || !ops.allgatherv || !ops.alltoallv)
+    fail(PO_ERR_INVALID_ARG, "null host collective");
+  return new HostComm(ops, nranks, rank);
+}
 
 void nccl_unique_id(uint8_t out[128]) {
   ncclUniqueId uid;

@@ -1,9 +1,12 @@
 // Collectives of the row-sharded solver.
 //
-// One rank per GPU. Two transports behind one interface:
+// One rank per GPU. Three transports behind one interface:
 //   * NcclComm  — production: NCCL over NVLink/NVSwitch, one process per GPU
 //                 (libnccl.so.2 is opened lazily, so single-GPU users of the
 //                 library never need it);
+//   * HostComm  — caller-provided collectives on host buffers (MPI, gloo):
+//                 device buffers staged through host memory; any process
+//                 layout, several ranks per GPU included (tests);
 //   * LocalComm — N ranks as host threads of ONE process (any devices,
 //                 including N ranks on one GPU): collectives are peer
 //                 cudaMemcpyAsync between the ranks' buffers behind a host
@@ -58,5 +61,7 @@ void nccl_unique_id(uint8_t out[128]);
 Comm* make_nccl_comm(const uint8_t id[128], int nranks, int rank);
 // nranks communicators sharing one in-process group (rank i = out[i]).
 std::vector<Comm*> make_local_group(int nranks);
+// host-staged collectives provided by the caller (po_host_collectives)
+Comm* make_host_comm(const po_host_collectives& ops, int nranks, int rank);
 
 }  // namespace po

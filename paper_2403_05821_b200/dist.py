@@ -5,7 +5,9 @@
   and gets back one contiguous slice of the schedule; the slices in rank
   order are bit-identical to ggr() on the whole table. Collectives run over a
   `ShardComm`: NCCL between B200s (`nccl_comm`, one process per GPU, the
-  unique id shipped over torch.distributed) or an in-process thread group
+  unique id shipped over torch.distributed), host-staged collectives over any
+  torch.distributed backend (`host_comm`, e.g. gloo: processes sharing a
+  GPU) or an in-process thread group
   (`local_comms`, several ranks on one GPU — how the parity tests exercise
   the sharded path on a 1-GPU box).
 * `sharded_phc` — the row-range-sharded PHC over torch.distributed with the
@@ -143,6 +145,92 @@ def nccl_comm(rank: int | None = None, world: int | None = None, group=None) -> 
     h = C.c_void_p(0)
     lib.check(lib.comm_init_nccl(uid.ctypes.data, world, rank, C.byref(h)))
     return ShardComm(h.value, rank, world)
+
+
+# host-staged transport: po_host_collectives implemented with torch.distributed
+_ALLGATHER = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64)
+_ALLGATHERV = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(C.c_uint64))
+_ALLTOALLV = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.POINTER(C.c_uint64), C.c_void_p,
+                         C.POINTER(C.c_uint64))
+
+
+class _HostCollectives(C.Structure):
+    _fields_ = [("ctx", C.c_void_p), ("allgather", _ALLGATHER), ("allgatherv", _ALLGATHERV),
+                ("alltoallv", _ALLTOALLV)]
+
+
+def _host_bytes(ptr: int, n: int) -> torch.Tensor:
+    return torch.from_numpy(np.ctypeslib.as_array((C.c_uint8 * max(n, 1)).from_address(ptr))[:n].copy())
+
+
+def _gather_padded(mine: torch.Tensor, world: int, group) -> list:
+    """Every rank's byte tensor (different sizes allowed), via equal-size
+    all_gather (the gloo backend has no variable-size collectives)."""
+    n = torch.tensor([mine.numel()], dtype=torch.int64)
+    ns = [torch.zeros(1, dtype=torch.int64) for _ in range(world)]
+    dist.all_gather(ns, n, group=group)
+    mx = max(int(x.item()) for x in ns)
+    pad = torch.zeros(max(mx, 1), dtype=torch.uint8)
+    pad[:mine.numel()] = mine
+    outs = [torch.zeros(max(mx, 1), dtype=torch.uint8) for _ in range(world)]
+    dist.all_gather(outs, pad, group=group)
+    return [o[:int(k.item())] for o, k in zip(outs, ns)]
+
+
+def host_comm(group=None) -> ShardComm:
+    """Communicator over the ranks of an initialised torch.distributed group
+    of ANY backend (gloo on CPU included) through po_comm_init_host: device
+    buffers are staged through host memory and exchanged with
+    torch.distributed collectives. Slower than NCCL; it lets the sharded
+    solver run across processes where NCCL cannot (several ranks on one GPU)."""
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+
+    def allgather(ctx, send, recv, nbytes):
+        try:
+            parts = _gather_padded(_host_bytes(send, nbytes), world, group)
+            out = torch.cat(parts).numpy()
+            C.memmove(recv, out.ctypes.data, out.nbytes)
+            return 0
+        except Exception:  # pragma: no cover - reported as PO_ERR_ERROR
+            return 1
+
+    def allgatherv(ctx, send, recv, recv_bytes):
+        try:
+            parts = _gather_padded(_host_bytes(send, int(recv_bytes[rank])), world, group)
+            out = torch.cat(parts).numpy()
+            if out.nbytes:
+                C.memmove(recv, out.ctypes.data, out.nbytes)
+            return 0
+        except Exception:  # pragma: no cover
+            return 1
+
+    def alltoallv(ctx, send, send_bytes, recv, recv_bytes):
+        try:
+            sb = [int(send_bytes[r]) for r in range(world)]
+            mine = _host_bytes(send, sum(sb))
+            counts = _gather_padded(torch.tensor(sb, dtype=torch.int64).view(torch.uint8), world, group)
+            datas = _gather_padded(mine, world, group)
+            pieces = []
+            for r in range(world):
+                c = counts[r].view(torch.int64).tolist()
+                off = sum(c[:rank])
+                pieces.append(datas[r][off:off + c[rank]])
+                assert c[rank] == int(recv_bytes[r])
+            out = torch.cat(pieces).numpy()
+            if out.nbytes:
+                C.memmove(recv, out.ctypes.data, out.nbytes)
+            return 0
+        except Exception:  # pragma: no cover
+            return 1
+
+    ops = _HostCollectives(None, _ALLGATHER(allgather), _ALLGATHERV(allgatherv),
+                           _ALLTOALLV(alltoallv))
+    lib = cuda_lib()
+    h = C.c_void_p(0)
+    lib.check(lib.comm_init_host(C.byref(ops), world, rank, C.byref(h)))
+    comm = ShardComm(h.value, rank, world)
+    comm._keep = ops  # the callbacks must outlive the communicator
+    return comm
 
 
 @dataclass
