@@ -1,31 +1,34 @@
 #!/usr/bin/env python
 """Benchmark: rows/s reordered + PHC-scored by prefixopt::ggr on B200.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl ours|reference]
 
 A step is one full `ggr()` (GgrConfig defaults: dictionary encoding, greedy
 group recursion, leaf fallbacks, whole-table fallback competition and the
-PHC of the emitted schedule) over one synthetic table of BASELINE config C2
-(Amazon-products shape, 1M rows x 6 columns, ~0.75 GB of cell bytes; the
-configuration BASELINE.json's metric is quoted on). Inputs (0.75 GB) are
-larger than L2 (126 MB), so no explicit flush is needed between steps.
+PHC of the emitted schedule) over one synthetic table.
+
+N = 1: BASELINE config C2 (Amazon-products shape, 1M rows x 6 columns,
+~0.75 GB of cell bytes; the configuration BASELINE.json's metric is quoted
+on), po_ggr on one GPU. Inputs are larger than L2 (126 MB): no flush.
+
+N > 1 (torchrun, one rank per GPU): config C4, the north star's 100M-row x
+8 table, split N ways (strong scaling): rank r generates and holds its
+contiguous row range and the ranks solve ONE table together through
+po_ggr_sharded over NCCL (global dictionary sample sort, replicated
+value-group tables from exchanged contributions, distributed leaf sort;
+csrc/shard.cu); value = total rows / max-over-ranks time. --config / --rows
+override the table, --sharded forces the sharded path at N=1, --transport
+host runs the collectives host-staged over gloo (ranks may share a GPU).
 
   value   whole-job rows/s with the table resident in HBM (device buffers)
   e2e     the same call through the C ABI with pinned HOST buffers: the
           arena+offsets H2D copy and the schedule D2H copy are inside every
           step
-Under torchrun (N>1) the table is N times larger (1M rows per GPU: weak
-scaling) and row-range sharded: rank r generates and holds rows
-[r*1M, (r+1)*1M) and the ranks solve ONE table together through
-po_ggr_sharded over NCCL (global dictionary sample sort, replicated
-value-group tables from exchanged contributions, distributed leaf sort;
-csrc/shard.cu). value = N * rows / max-over-ranks time; each rank's slice of
-the schedule stays in HBM. --sharded forces that path at N=1 as well.
 
 --impl reference times the reference C++ implementation (oracle/_ref, the
 unmodified prefixopt headers compiled from /root/reference; the CPU port in
-oracle/ when _ref is absent) on the host cores, one bounded row-prefix sample
-of the same table per step.
+oracle/ when _ref is absent) on the host cores: the whole C2 table per step
+(a 200K-row prefix of C4 under N > 1).
 """
 from __future__ import annotations
 
@@ -158,8 +161,11 @@ def run_reference(args):
     if rank != 0:
         return 0
     from paper_2403_05821_b200 import gen
-    cfg_id = args.config
-    sample = args.ref_rows if args.ref_rows is not None else gen.CONFIGS[cfg_id].rows
+    cfg_id = args.config if args.config is not None else (4 if world > 1 else 2)
+    # the whole table when one core finishes it in well under a minute (C2),
+    # else a bounded row prefix of it (C4's 100M rows: 200K rows per step)
+    full = gen.CONFIGS[cfg_id].rows
+    sample = args.ref_rows if args.ref_rows is not None else (full if full <= 1_000_000 else 200_000)
     table = gen.generate(cfg_id, n_rows=sample)
     fds = gen.fds(cfg_id)
     # untimed warm-up steps on a small prefix (page-in, allocator); the timed
@@ -195,24 +201,32 @@ def run_reference(args):
 def run_ours(args):
     import torch
     rank, world, local = dist_env()
-    torch.cuda.set_device(local)
+    # one GPU per rank (the host transport may put several ranks on one GPU)
+    torch.cuda.set_device(local % max(torch.cuda.device_count(), 1))
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.transport == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
     import paper_2403_05821_b200 as po
     from paper_2403_05821_b200 import gen
     from paper_2403_05821_b200._abi import PO_LOC_DEVICE, PO_LOC_HOST, cuda_lib
+    from paper_2403_05821_b200.dist import shard_range
 
     lib = cuda_lib()
-    cfg_id = args.config
     sharded = world > 1 or args.sharded
+    # N = 1: C2 (the headline metric's config); N > 1: C4, the north star's
+    # 100M-row table, split N ways (strong scaling)
+    cfg_id = args.config if args.config is not None else (4 if world > 1 else 2)
     t0 = time.time()
-    n_per = args.rows if args.rows is not None else gen.CONFIGS[cfg_id].rows
-    table = gen.generate(cfg_id, n_rows=n_per, row_begin=rank * n_per if sharded else 0)
+    n_total = args.rows if args.rows is not None else gen.CONFIGS[cfg_id].rows
+    lo, hi = shard_range(n_total, world, rank) if sharded else (0, n_total)
+    table = gen.generate(cfg_id, n_rows=hi - lo, row_begin=lo)
     n, m = table.row_count(), table.field_count()
     cell_bytes = table.cell_bytes
-    log(f"[rank {rank}] generated {gen.CONFIGS[cfg_id].name}: {n} rows, {cell_bytes/1e9:.3f} GB "
-        f"in {time.time()-t0:.1f}s")
+    log(f"[rank {rank}] generated {gen.CONFIGS[cfg_id].name} rows [{lo}, {hi}): "
+        f"{cell_bytes/1e9:.3f} GB in {time.time()-t0:.1f}s")
     fds = gen.fds(cfg_id)
     fd_idx = [[table.require_field(x) for x in g] for g in fds]
     cfg = po.GgrConfig()
@@ -227,8 +241,8 @@ def run_ours(args):
 
     comm = None
     if sharded:
-        from paper_2403_05821_b200.dist import ggr_sharded_into, nccl_comm
-        comm = nccl_comm(rank, world)
+        from paper_2403_05821_b200.dist import ggr_sharded_into, host_comm, nccl_comm
+        comm = nccl_comm(rank, world) if args.transport == "nccl" else host_comm()
 
     def step_device():
         if sharded:
@@ -242,11 +256,21 @@ def run_ours(args):
             dist.barrier()
         torch.cuda.synchronize()
 
+    def sum_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        import torch.distributed as dist
+        t = torch.tensor([x], dtype=torch.float64,
+                         device="cuda" if args.transport == "nccl" else "cpu")
+        dist.all_reduce(t)
+        return float(t.item())
+
     def max_over_ranks(x: float) -> float:
         if world == 1:
             return x
         import torch.distributed as dist
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        t = torch.tensor([x], dtype=torch.float64,
+                         device="cuda" if args.transport == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -273,7 +297,8 @@ def run_ours(args):
     per = [ev0.elapsed_time(marks[0])] + [a.elapsed_time(b) for a, b in zip(marks, marks[1:])]
     log(f"[rank {rank}] per-step ms: " + " ".join(f"{x:.2f}" for x in per))
     ms = max_over_ranks(ms)
-    value = world * n / (ms / 1e3)
+    value = n_total / (ms / 1e3)
+    total_cell_bytes = int(sum_over_ranks(cell_bytes))
     log(f"[rank {rank}] device-resident: {ms:.3f} ms/step, phc={phc}, stats={st}")
 
     # per-kernel CUDA-event profile of the same step (separate pass)
@@ -317,9 +342,18 @@ def run_ours(args):
     # whole-pipeline figure on SURVEY.md §8d's B_alg = S_row + 8m + 4 + m per row
     b_alg = cell_bytes + n * (8 * m + 4 + m)
 
-    # e2e: pinned host inputs and outputs through the C ABI every step
-    h_arena = torch.from_numpy(table.arena).pin_memory()
-    h_offs = torch.from_numpy(table.offsets.view(np.int64)).pin_memory()
+    # e2e: pinned host inputs and outputs through the C ABI every step (large
+    # shards are page-locked in place instead of copied)
+    registered = []
+    if cell_bytes > (4 << 30):
+        from cuda.bindings import runtime as rt
+        for arr in (table.arena, table.offsets):
+            rt.cudaHostRegister(arr.ctypes.data, arr.nbytes, 0)
+            registered.append(arr.ctypes.data)
+        h_arena, h_offs = table.arena, table.offsets
+    else:
+        h_arena = torch.from_numpy(table.arena).pin_memory()
+        h_offs = torch.from_numpy(table.offsets.view(np.int64)).pin_memory()
     hview = table.view(PO_LOC_HOST, arena=h_arena, offsets=h_offs)
     h_rows = torch.empty(n, dtype=torch.int64).pin_memory()
     h_orders = torch.empty(n * m, dtype=torch.int32).pin_memory()
@@ -342,8 +376,12 @@ def run_ours(args):
     barrier()
     ms_e2e = max_over_ranks(e0.elapsed_time(e1) / args.steps)
     wall_e2e = (time.perf_counter() - t_e) * 1e3 / args.steps
-    h2d = int(table.arena.nbytes + table.offsets.nbytes)
-    d2h = int(n * 8 + n * m * 4 + 8)
+    h2d = int(sum_over_ranks(table.arena.nbytes + table.offsets.nbytes))
+    d2h = int(n_total * 8 + n_total * m * 4 + 8 * world)
+    if registered:
+        from cuda.bindings import runtime as rt
+        for ptr in registered:
+            rt.cudaHostUnregister(ptr)
     if phc_e2e != phc:
         raise RuntimeError(f"e2e PHC {phc_e2e} != device-resident PHC {phc}")
 
@@ -364,22 +402,25 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u8",
             "data": "synthetic",
             "config": {"workload": gen.CONFIGS[cfg_id].name if not sharded else
-                       f"{gen.CONFIGS[cfg_id].name} x{world} (rows {world * n}, {n} per GPU)",
-                       "rows": world * n, "rows_per_gpu": n, "fields": m,
-                       "cell_bytes": cell_bytes, "ggr_config": "defaults (4/2/100000, fds on)",
+                       f"{gen.CONFIGS[cfg_id].name} split {world} ways "
+                       f"({n_total} rows, ~{n_total // world} per GPU)",
+                       "rows": n_total, "rows_per_gpu": n_total // world, "fields": m,
+                       "cell_bytes": total_cell_bytes,
+                       "ggr_config": "defaults (4/2/100000, fds on)",
                        "tokenizer": "char", "scoring": "value_only",
                        "l2": "inputs (arena+offsets) larger than the 126 MB L2; no flush",
-                       "parallelism": (f"dp{world}: one table row-range sharded, NCCL "
-                                       "(po_ggr_sharded)") if sharded else "single GPU"},
+                       "parallelism": (f"dp{world}: one table row-range sharded, "
+                                       f"{'NCCL' if args.transport == 'nccl' else 'host-staged gloo'}"
+                                       " (po_ggr_sharded)") if sharded else "single GPU"},
             "phc": int(phc),
             "solve_stats": {"recursive_calls": st.recursive_calls,
                             "candidates_examined": st.candidates_examined,
                             "max_depth": st.max_depth},
-            "e2e": {"value": world * n / (ms_e2e / 1e3), "unit": UNIT,
-                    "cell_bytes_per_s": world * cell_bytes / (ms_e2e / 1e3),
+            "e2e": {"value": n_total / (ms_e2e / 1e3), "unit": UNIT,
+                    "cell_bytes_per_s": total_cell_bytes / (ms_e2e / 1e3),
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "ms_per_step": ms_e2e, "host_wall_ms_per_step": wall_e2e},
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
@@ -389,7 +430,7 @@ def run_ours(args):
                          "top_kernel": {"name": top, "ms_per_step": kern[0][0] if kern else None,
                                         "share": (kern[0][0] / total_kernel_ms) if kern else None},
                          "pipeline_b_alg_frac": (b_alg / (ms / 1e3) / 1e9) / peak},
-            "cell_bytes_per_s": value * cell_bytes / n,
+            "cell_bytes_per_s": value * total_cell_bytes / n_total,
             "kernels_ms_per_step": {k: round(v, 4) for v, k, _ in kern[:16]},
             "kernel_ms_total": round(total_kernel_ms, 4),
             "cpu_baseline": cpu,
@@ -410,7 +451,11 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--config", type=int, default=None,
+                    help="BASELINE config (default: 2 at N=1, 4 split N ways at N>1)")
+    ap.add_argument("--transport", choices=["nccl", "host"], default="nccl",
+                    help="collectives of the sharded solver: NCCL (one GPU per rank) or "
+                         "host-staged over gloo (ranks may share a GPU; for testing)")
     ap.add_argument("--rows", type=int, default=None)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--cpu-rows", type=int, default=None,
