@@ -101,11 +101,28 @@ typedef struct po_solve_stats {
 
 /* prefixopt::ggr (ggr.hpp:367-394). Emits the schedule (row ids in request
  * order, and a full field permutation per request: n_rows*n_fields ints),
- * its PHC and the solver counters. Outputs live at `out_location`. */
+ * its PHC and the solver counters. Outputs live at `out_location`. FD
+ * groups sharing two members: PO_ERR_SIZE, see po_ggr_schedule. */
 int po_ggr(const po_table* t, const po_fd_groups* fds, const po_ggr_config* cfg,
            int32_t tokenizer, int32_t scoring, uint32_t out_location,
            uint64_t* out_row_ids, int32_t* out_field_orders, uint64_t* out_phc,
            po_solve_stats* out_stats, void* stream);
+
+/* prefixopt::ggr returning the schedule as a handle with CSR field orders.
+ * Needed when FD groups share members: the reference then emits a partner
+ * once per group holding it, so field orders can be longer than n_fields
+ * (ggr.hpp:154-164, 280-282; po_ggr fails with PO_ERR_SIZE in that case).
+ * Same results as po_ggr otherwise. Device memory is owned by the handle. */
+typedef struct po_schedule po_schedule;
+int po_ggr_schedule(const po_table* t, const po_fd_groups* fds, const po_ggr_config* cfg,
+                    int32_t tokenizer, int32_t scoring, po_schedule** out_schedule,
+                    uint64_t* out_phc, po_solve_stats* out_stats, void* stream);
+int po_schedule_info(const po_schedule* schedule, uint64_t* out_entries,
+                     uint64_t* out_fields_total);
+/* row ids (entries), CSR offsets (entries + 1) and fields (fields_total). */
+int po_schedule_copy(const po_schedule* schedule, uint32_t out_location, uint64_t* out_row_ids,
+                     uint64_t* out_order_offsets, int32_t* out_order_fields, void* stream);
+void po_schedule_free(po_schedule* schedule);
 
 /* prefixopt::phc (objective.hpp:94-99) over an arbitrary schedule: entry i is
  * row row_ids[i] rendered with fields order_fields[order_offsets[i] ..

@@ -432,8 +432,8 @@ int guarded(F&& fn) {
 extern "C" {
 
 int oracle_ggr(const po_table* tv, const po_fd_groups* fds, const po_ggr_config* cfg,
-               int32_t tok, int32_t scoring, uint64_t* out_rows, int32_t* out_orders,
-               uint64_t* out_phc, po_solve_stats* out_stats) {
+               int32_t tok, int32_t scoring, uint64_t* out_rows, uint64_t* out_offsets,
+               int32_t* out_fields, uint64_t cap, uint64_t* out_phc, po_solve_stats* out_stats) {
   return guarded([&] {
     auto t0 = std::chrono::steady_clock::now();
     check_modes(tok, scoring);
@@ -462,10 +462,15 @@ int oracle_ggr(const po_table* tv, const po_fd_groups* fds, const po_ggr_config*
         score = fscore;
       }
     }
+    uint64_t at = 0;
+    for (const auto& e : sched) at += e.fields.size();
+    if (at > cap) fail(PO_ERR_SIZE, "oracle: field capacity too small");
+    at = 0;
+    out_offsets[0] = 0;
     for (uint64_t i = 0; i < sched.size(); ++i) {
       out_rows[i] = sched[i].row;
-      for (uint32_t p = 0; p < t.m; ++p)
-        out_orders[i * t.m + p] = p < sched[i].fields.size() ? sched[i].fields[p] : -1;
+      for (int f : sched[i].fields) out_fields[at++] = f;
+      out_offsets[i + 1] = at;
     }
     *out_phc = score;
     if (out_stats) {

@@ -23,9 +23,12 @@ extern "C" {
 #endif
 
 #define PO_ORACLE_DECLARE(prefix)                                                        \
+  /* schedule in CSR form: fields of entry i at [out_order_offsets[i],         \
+     out_order_offsets[i+1]); PO_ERR_SIZE when more than fields_capacity */    \
   int prefix##ggr(const po_table* t, const po_fd_groups* fds, const po_ggr_config* cfg,  \
                   int32_t tokenizer, int32_t scoring, uint64_t* out_row_ids,             \
-                  int32_t* out_field_orders, uint64_t* out_phc, po_solve_stats* out_stats); \
+                  uint64_t* out_order_offsets, int32_t* out_order_fields,                \
+                  uint64_t fields_capacity, uint64_t* out_phc, po_solve_stats* out_stats); \
   int prefix##phc(const po_table* t, int32_t tokenizer, int32_t scoring,                \
                   uint64_t n_entries, const uint64_t* row_ids,                           \
                   const uint64_t* order_offsets, const int32_t* order_fields,            \

@@ -38,7 +38,8 @@ class OracleLib:
         L = C.CDLL(str(path))
         p = PREFIX[kind]
         vp = C.c_void_p
-        self._ggr = _bind(L, p + "ggr", C.c_int, [vp, vp, vp, C.c_int32, C.c_int32, vp, vp, vp, vp])
+        self._ggr = _bind(L, p + "ggr", C.c_int,
+                          [vp, vp, vp, C.c_int32, C.c_int32, vp, vp, vp, C.c_uint64, vp, vp])
         self._phc = _bind(L, p + "phc", C.c_int, [vp, C.c_int32, C.c_int32, C.c_uint64, vp, vp, vp, vp])
         self._sort = _bind(L, p + "sort_rows_fixed_order", C.c_int, [vp, vp, vp])
         self._stats = _bind(L, p + "compute_stats", C.c_int, [vp, C.c_int32, C.c_int32, vp, vp])
@@ -63,16 +64,22 @@ class OracleLib:
         cfg = cfg or GgrConfig()
         tok = tok or char_tokenizer()
         n, m = t.row_count(), t.field_count()
-        fdv = FdView(_fd_indices(t, fds, cfg))
+        groups = _fd_indices(t, fds, cfg)
+        fdv = FdView(groups)
         view = t.view(cell_lens=_cell_lens(t, tok, scoring))
+        # a row's order holds every field plus repeated FD partners (groups
+        # sharing members, ggr.hpp:280-282): m + sum of group sizes bounds it
+        cap = max(n * (m + sum(len(g) for g in groups)), 1)
         rows = np.empty(max(n, 1), dtype=np.uint64)
-        orders = np.empty(max(n * m, 1), dtype=np.int32)
+        offs = np.zeros(n + 1, dtype=np.uint64)
+        fields = np.empty(cap, dtype=np.int32)
         score = C.c_uint64(0)
         st = po_solve_stats()
         c = cfg.abi()
         self._check(self._ggr(view.ref(), fdv.ref(), C.byref(c), tok.kind, int(scoring),
-                              rows.ctypes.data, orders.ctypes.data, C.byref(score), C.byref(st)))
-        sched = RequestSchedule.full(rows[:n], orders[:n * m].reshape(n, m))
+                              rows.ctypes.data, offs.ctypes.data, fields.ctypes.data, cap,
+                              C.byref(score), C.byref(st)))
+        sched = RequestSchedule(rows[:n], offs, fields[:int(offs[-1])])
         return SolveResult(int(score.value), sched,
                            SolveStats(st.recursive_calls, st.candidates_examined, st.max_depth,
                                       st.wall_ms))

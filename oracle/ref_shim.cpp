@@ -137,8 +137,8 @@ extern "C" {
 
 // prefixopt::ggr (ggr.hpp:367-394)
 int ref_ggr(const po_table* tv, const po_fd_groups* fds, const po_ggr_config* cfg, int32_t tok,
-            int32_t scoring, uint64_t* out_rows, int32_t* out_orders, uint64_t* out_phc,
-            po_solve_stats* out_stats) {
+            int32_t scoring, uint64_t* out_rows, uint64_t* out_offsets, int32_t* out_fields,
+            uint64_t cap, uint64_t* out_phc, po_solve_stats* out_stats) {
   return guarded([&] {
     prefixopt::Table t = to_table(tv);
     auto sc = scoring_of(scoring);
@@ -158,12 +158,16 @@ int ref_ggr(const po_table* tv, const po_fd_groups* fds, const po_ggr_config* cf
     c.use_fds = cfg->use_fds != 0;
     c.stats_variant = variant_of(cfg->stats_variant);
     prefixopt::SolveResult res = prefixopt::ggr(t, set, c, *tk.tok, sc);
-    uint32_t m = tv->n_fields;
+    uint64_t at = 0;
+    for (const auto& e : res.schedule.entries) at += e.field_order.size();
+    if (at > cap) throw prefixopt::size_error("ref shim: field capacity too small");
+    at = 0;
+    out_offsets[0] = 0;
     for (size_t i = 0; i < res.schedule.entries.size(); ++i) {
       const auto& e = res.schedule.entries[i];
       out_rows[i] = e.row_id;
-      for (uint32_t p = 0; p < m; ++p)
-        out_orders[i * m + p] = p < e.field_order.size() ? e.field_order[p] : -1;
+      for (int f : e.field_order) out_fields[at++] = f;
+      out_offsets[i + 1] = at;
     }
     *out_phc = res.phc_score;
     if (out_stats) {

@@ -185,6 +185,11 @@ class CudaLib:
                                     [vp, C.c_int32, C.c_int32, C.POINTER(vp)])
         self.comm_init_local = _bind(L, "po_comm_init_local", C.c_int, [C.c_int32, vp])
         self.comm_destroy = _bind(L, "po_comm_destroy", C.c_int, [vp])
+        self.ggr_schedule = _bind(L, "po_ggr_schedule", C.c_int,
+                                  [vp, vp, vp, C.c_int32, C.c_int32, vp, vp, vp, vp])
+        self.schedule_info = _bind(L, "po_schedule_info", C.c_int, [vp, vp, vp])
+        self.schedule_copy = _bind(L, "po_schedule_copy", C.c_int, [vp, C.c_uint32, vp, vp, vp, vp])
+        self.schedule_free = _bind(L, "po_schedule_free", None, [vp])
         self.comm_init_host = _bind(L, "po_comm_init_host", C.c_int,
                                     [vp, C.c_int32, C.c_int32, vp])
         self.ggr_sharded = _bind(L, "po_ggr_sharded", C.c_int,

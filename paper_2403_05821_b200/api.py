@@ -284,17 +284,28 @@ def ggr(t: Table, fds=None, cfg: GgrConfig | None = None, tok: Tokenizer = _CHAR
     """prefixopt::ggr (ggr.hpp:367-394) on the GPU."""
     cfg = cfg or GgrConfig()
     lib = cuda_lib()
-    n, m = t.row_count(), t.field_count()
     fdv = FdView(_fd_indices(t, fds, cfg))
     view = _view(t, tok, scoring)
-    rows = np.empty(max(n, 1), dtype=np.uint64)
-    orders = np.empty(max(n * m, 1), dtype=np.int32)
     score = C.c_uint64(0)
     st = po_solve_stats()
     c = cfg.abi()
-    lib.check(lib.ggr(view.ref(), fdv.ref(), C.byref(c), tok.kind, int(scoring), PO_LOC_HOST,
-                      rows.ctypes.data, orders.ctypes.data, C.byref(score), C.byref(st), stream))
-    sched = RequestSchedule.full(rows[:n], orders[:n * m].reshape(n, m))
+    # schedule handle with CSR field orders (FD groups sharing members make
+    # some orders longer than the schema, ggr.hpp:280-282)
+    h = C.c_void_p(0)
+    lib.check(lib.ggr_schedule(view.ref(), fdv.ref(), C.byref(c), tok.kind, int(scoring),
+                               C.byref(h), C.byref(score), C.byref(st), stream))
+    try:
+        ne, tot = C.c_uint64(0), C.c_uint64(0)
+        lib.check(lib.schedule_info(h, C.byref(ne), C.byref(tot)))
+        n, total = int(ne.value), int(tot.value)
+        rows = np.empty(max(n, 1), dtype=np.uint64)
+        offs = np.empty(n + 1, dtype=np.uint64)
+        fields = np.empty(max(total, 1), dtype=np.int32)
+        lib.check(lib.schedule_copy(h, PO_LOC_HOST, rows.ctypes.data, offs.ctypes.data,
+                                    fields.ctypes.data, stream))
+    finally:
+        lib.schedule_free(h)
+    sched = RequestSchedule(rows[:n], offs, fields[:total])
     return SolveResult(int(score.value), sched,
                        SolveStats(st.recursive_calls, st.candidates_examined, st.max_depth,
                                   st.wall_ms))

@@ -462,6 +462,13 @@ struct po_csv {
   po::CsvParsed parsed;
 };
 
+struct po_schedule {
+  uint64_t n = 0, m = 0, total = 0;
+  po::DevBuf<uint32_t> rows;
+  po::DevBuf<uint64_t> offsets;  // empty: uniform (entry i at i*m)
+  po::DevBuf<int32_t> fields;
+};
+
 struct po_slice {
   uint64_t offset = 0, count = 0;
   uint32_t m = 0;
@@ -503,6 +510,10 @@ int po_ggr(const po_table* t, const po_fd_groups* fds, const po_ggr_config* cfg,
     }
     GgrOutput go;
     ggr_device(p.e, groups, *cfg, rows.get(), d_orders, go, s);
+    if (go.csr)
+      fail(PO_ERR_SIZE,
+           "FD groups repeat a field pair: some field orders are longer than n_fields; "
+           "use po_ggr_schedule");
     deliver_rows(rows.get(), n, out_location, out_row_ids, s);
     if (out_location == PO_LOC_HOST) own_orders.download(out_field_orders, n * m);
     sync(s);
@@ -516,6 +527,88 @@ int po_ggr(const po_table* t, const po_fd_groups* fds, const po_ggr_config* cfg,
     }
   });
 }
+
+int po_ggr_schedule(const po_table* t, const po_fd_groups* fds, const po_ggr_config* cfg,
+                    int32_t tok, int32_t scoring, po_schedule** out_schedule, uint64_t* out_phc,
+                    po_solve_stats* out_stats, void* stream) {
+  return guarded([&] {
+    auto t0 = std::chrono::steady_clock::now();
+    if (!cfg || !out_phc || !out_schedule) fail(PO_ERR_INVALID_ARG, "null config or output");
+    if (cfg->stats_variant < 0 || cfg->stats_variant > 2)
+      fail(PO_ERR_INVALID_ARG, "unknown stats variant");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    std::vector<std::vector<int>> groups;
+    if (fds && cfg->use_fds)
+      for (uint32_t g = 0; g < fds->n_groups; ++g)
+        groups.emplace_back(fds->members + fds->group_offsets[g],
+                            fds->members + fds->group_offsets[g + 1]);
+    Prepared p;
+    prepare(t, tok, scoring, s, p);
+    const uint64_t n = p.e.n, m = p.e.m;
+    auto sc = std::make_unique<po_schedule>();
+    sc->n = n;
+    sc->m = m;
+    sc->rows.alloc(n, s);
+    DevBuf<int32_t> orders(n * m, s);
+    GgrOutput go;
+    ggr_device(p.e, groups, *cfg, sc->rows.get(), orders.get(), go, s);
+    if (go.csr) {
+      sc->offsets = std::move(go.csr_offsets);
+      sc->fields = std::move(go.csr_fields);
+      sc->total = go.csr_total;
+    } else {
+      sc->fields = std::move(orders);
+      sc->total = n * m;
+    }
+    sync(s);
+    *out_phc = go.phc;
+    if (out_stats) {
+      *out_stats = go.stats;
+      out_stats->wall_ms =
+          std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    }
+    *out_schedule = sc.release();
+  });
+}
+
+int po_schedule_info(const po_schedule* sc, uint64_t* out_entries, uint64_t* out_fields_total) {
+  return guarded([&] {
+    if (!sc) fail(PO_ERR_INVALID_ARG, "null schedule");
+    if (out_entries) *out_entries = sc->n;
+    if (out_fields_total) *out_fields_total = sc->total;
+  });
+}
+
+int po_schedule_copy(const po_schedule* sc, uint32_t out_location, uint64_t* out_row_ids,
+                     uint64_t* out_order_offsets, int32_t* out_order_fields, void* stream) {
+  return guarded([&] {
+    if (!sc) fail(PO_ERR_INVALID_ARG, "null schedule");
+    if (out_location != PO_LOC_HOST && out_location != PO_LOC_DEVICE)
+      fail(PO_ERR_INVALID_ARG, "bad output location");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const uint64_t n = sc->n;
+    if (n && (!out_row_ids || !out_order_offsets || (sc->total && !out_order_fields)))
+      fail(PO_ERR_INVALID_ARG, "null output");
+    deliver_rows(sc->rows.get(), n, out_location, out_row_ids, s);
+    const cudaMemcpyKind k = out_location == PO_LOC_HOST ? cudaMemcpyDeviceToHost
+                                                         : cudaMemcpyDeviceToDevice;
+    if (sc->offsets.get()) {
+      PO_CUDA(cudaMemcpyAsync(out_order_offsets, sc->offsets.get(), (n + 1) * 8, k, s));
+    } else if (out_order_offsets) {  // uniform: entry i at i*m
+      std::vector<uint64_t> h(n + 1);
+      for (uint64_t i = 0; i <= n; ++i) h[i] = i * sc->m;
+      PO_CUDA(cudaMemcpyAsync(out_order_offsets, h.data(), (n + 1) * 8,
+                              out_location == PO_LOC_HOST ? cudaMemcpyHostToHost
+                                                          : cudaMemcpyHostToDevice, s));
+      sync(s);
+    }
+    if (sc->total)
+      PO_CUDA(cudaMemcpyAsync(out_order_fields, sc->fields.get(), sc->total * 4, k, s));
+    sync(s);
+  });
+}
+
+void po_schedule_free(po_schedule* sc) { delete sc; }
 
 int po_phc(const po_table* t, int32_t tok, int32_t scoring, uint64_t n_entries,
            const uint64_t* row_ids, const uint64_t* order_offsets, const int32_t* order_fields,

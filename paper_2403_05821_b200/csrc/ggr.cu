@@ -752,6 +752,23 @@ __global__ void k_emit_orders(const uint32_t* rows, uint64_t n, uint32_t m,
   }
 }
 
+// CSR field orders (repeated FD pairs): thread per schedule position.
+__global__ void k_emit_orders_csr(const uint32_t* rows, uint64_t n, const uint32_t* row_leaf,
+                                  const int32_t* leaf_fields, const uint32_t* leaf_fields_off,
+                                  const uint32_t* leaf_width, const uint64_t* leaf_base,
+                                  const uint32_t* leaf_pos, uint64_t total, uint64_t* offsets,
+                                  int32_t* fields) {
+  for (uint64_t p = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; p < n;
+       p += uint64_t(gridDim.x) * blockDim.x) {
+    const uint32_t l = row_leaf[rows[p]];
+    const uint32_t w = leaf_width[l];
+    const uint64_t at = leaf_base[l] + (p - leaf_pos[l]) * uint64_t(w);
+    offsets[p] = at;
+    for (uint32_t j = 0; j < w; ++j) fields[at + j] = leaf_fields[leaf_fields_off[l] + j];
+    if (p + 1 == n) offsets[n] = total;
+  }
+}
+
 __global__ void k_tile_order(const int32_t* order, uint64_t n, uint32_t m, int32_t* out) {
   for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n * m;
        i += uint64_t(gridDim.x) * blockDim.x)
@@ -851,17 +868,25 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
           if (o != f) partners[f].push_back(o);
     }
   }
+  // Groups may share members: a partner then appears several times in
+  // partners_[f] and the reference counts its length once per appearance
+  // (ggr.hpp:252-255) and emits it once per appearance in the block prefix
+  // (ggr.hpp:280-282, 303-309). Partner sums are kept per distinct partner
+  // (dpart) and weighted by the multiplicity (dmult).
   uint32_t K = 0;
   std::vector<std::vector<int>> dpart(m);
+  std::vector<std::vector<uint32_t>> dmult(m);
   for (uint32_t c = 0; c < m; ++c) {
     std::vector<int> u = partners[c];
     std::sort(u.begin(), u.end());
-    if (std::adjacent_find(u.begin(), u.end()) != u.end())
-      fail(PO_ERR_SCHEMA,
-           "FD groups repeat a field pair (a field would appear twice in a field order); "
-           "groups must not share two members");
-    dpart[c] = u;
-    K = std::max<uint32_t>(K, uint32_t(u.size()));
+    for (size_t i = 0; i < u.size();) {
+      size_t j = i;
+      while (j < u.size() && u[j] == u[i]) ++j;
+      dpart[c].push_back(u[i]);
+      dmult[c].push_back(uint32_t(j - i));
+      i = j;
+    }
+    K = std::max<uint32_t>(K, uint32_t(dpart[c].size()));
   }
   std::vector<int32_t> h_dpart(std::max<size_t>(1, size_t(m) * K), 0);
   std::vector<uint32_t> h_npart(m, 0);
@@ -992,7 +1017,7 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
       for (int c : nd.cols) act[c] = 1;
       for (uint32_t c = 0; c < m; ++c)
         for (size_t k = 0; k < dpart[c].size(); ++k)
-          if (act[dpart[c][k]]) L.weights[sl.w_off + c * K + k] = 1;
+          if (act[dpart[c][k]]) L.weights[sl.w_off + c * K + k] = dmult[c][k];
       L.slots.push_back(sl);
       add_work(L.work, uint32_t(i), *nd.table, scan_cols);
       L.slot_work_off.push_back(uint32_t(L.work.size()));
@@ -1360,7 +1385,7 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
       std::vector<int> full = f.prefix;
       if (nd.kind == FALLBACK) full.insert(full.end(), nd.leaf_order.begin(), nd.leaf_order.end());
       else full.insert(full.end(), nd.cols.begin(), nd.cols.end());
-      if (full.size() != m) fail(PO_ERR_ERROR, "internal: leaf field order is not a permutation");
+      if (full.size() < m) fail(PO_ERR_ERROR, "internal: leaf field order misses fields");
       node_leaf[f.id] = uint32_t(leaf_nodes.size());
       leaf_nodes.push_back(f.id);
       leaf_full_order.push_back(std::move(full));
@@ -1368,7 +1393,12 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
   }
   const uint32_t nleaves = uint32_t(leaf_nodes.size());
   std::vector<uint32_t> leaf_off(nleaves, 0), leaf_chunk_off(nleaves), leaf_nchunks(nleaves);
-  std::vector<int32_t> h_leaf_orders(size_t(nleaves) * m);
+  // repeated FD pairs make some field orders longer than m: CSR output
+  bool csr = false;
+  for (const auto& fo : leaf_full_order) csr |= fo.size() != m;
+  if (csr && dist)
+    fail(PO_ERR_SCHEMA, "sharded ggr: FD groups repeating a field pair are not supported");
+  std::vector<int32_t> h_leaf_orders(csr ? 0 : size_t(nleaves) * m);
   KeySchedule ks;
   TieSpec ties;
   // round 0 groups the rows by leaf index; later rounds by start position
@@ -1379,8 +1409,9 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
     const Node& nd = nodes[leaf_nodes[l]];
     leaf_off[l] = uint32_t(off);
     off += nd.size;
-    std::copy(leaf_full_order[l].begin(), leaf_full_order[l].end(),
-              h_leaf_orders.begin() + size_t(l) * m);
+    if (!csr)
+      std::copy(leaf_full_order[l].begin(), leaf_full_order[l].end(),
+                h_leaf_orders.begin() + size_t(l) * m);
     // sort keys of the leaf
     std::vector<std::pair<int, uint8_t>> keys;  // (field, kind)
     // single-column leaves are ordered by raw bytes in a separate string job
@@ -1582,9 +1613,38 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
     if (hb) fprintf(stderr, "[po debug] leaf sort positions: %llu collisions/out of range\n", hb);
   }
   PO_LAUNCH(k_emit, grid_for(n, 256), 256, 0, s, pos.get(), n, d_rows);
-  PO_LAUNCH(k_emit_orders, grid_for(n * m, 256), 256, 0, s, d_rows, n, m, row_leaf.get(),
-            d_leaf_orders.get(), d_orders);
-  out.phc = phc_device(e, n, nullptr, d_rows, nullptr, d_orders, s);
+  if (!csr) {
+    PO_LAUNCH(k_emit_orders, grid_for(n * m, 256), 256, 0, s, d_rows, n, m, row_leaf.get(),
+              d_leaf_orders.get(), d_orders);
+    out.phc = phc_device(e, n, nullptr, d_rows, nullptr, d_orders, s);
+  } else {
+    // leaf l's rows hold positions [leaf_off[l], + size) and each takes
+    // |full order of l| fields: CSR offsets per position
+    std::vector<int32_t> lf;
+    std::vector<uint32_t> lf_off(nleaves + 1, 0), lw(nleaves);
+    std::vector<uint64_t> lbase(nleaves);
+    uint64_t total = 0;
+    for (uint32_t l = 0; l < nleaves; ++l) {
+      lf.insert(lf.end(), leaf_full_order[l].begin(), leaf_full_order[l].end());
+      lf_off[l + 1] = uint32_t(lf.size());
+      lw[l] = uint32_t(leaf_full_order[l].size());
+      lbase[l] = total;
+      total += nodes[leaf_nodes[l]].size * lw[l];
+    }
+    auto d_lf = to_device(lf, s);
+    auto d_lf_off = to_device(lf_off, s);
+    auto d_lw = to_device(lw, s);
+    auto d_lbase = to_device(lbase, s);
+    auto d_loff = to_device(leaf_off, s);
+    out.csr = true;
+    out.csr_total = total;
+    out.csr_offsets.alloc(n + 1, s);
+    out.csr_fields.alloc(std::max<uint64_t>(total, 1), s);
+    PO_LAUNCH(k_emit_orders_csr, grid_for(n, 256), 256, 0, s, d_rows, n, row_leaf.get(), d_lf.get(),
+              d_lf_off.get(), d_lw.get(), d_lbase.get(), d_loff.get(), total,
+              out.csr_offsets.get(), out.csr_fields.get());
+    out.phc = phc_device(e, n, nullptr, d_rows, out.csr_offsets.get(), out.csr_fields.get(), s);
+  }
   timing_mark("emit_phc", s);
 
   // ---- whole-table fallback competition (ggr.hpp:379-387) ----
@@ -1612,6 +1672,9 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
     sort_all_rows(e, fb_order, d_rows, s);
     PO_LAUNCH(k_tile_order, grid_for(n * m, 256), 256, 0, s, d_fo.get(), n, m, d_orders);
     out.phc = fb_phc;
+    out.csr = false;  // every order is the fallback's m fields
+    out.csr_offsets.release();
+    out.csr_fields.release();
   }
   sync(s);
 }

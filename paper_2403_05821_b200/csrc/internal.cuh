@@ -323,6 +323,13 @@ class FixedOrderSort {
 struct GgrOutput {
   uint64_t phc = 0;
   po_solve_stats stats{};
+  // FD groups repeating a field pair lengthen some field orders past m
+  // (ggr.hpp:280-282): the schedule's orders are then these CSR arrays
+  // instead of d_orders
+  bool csr = false;
+  uint64_t csr_total = 0;
+  DevBuf<uint64_t> csr_offsets;  // n + 1
+  DevBuf<int32_t> csr_fields;    // csr_total
 };
 
 // FD checks (fd.cu): for every field pair (pa[k], pb[k]) the first row where

@@ -121,19 +121,26 @@ inline SolveResult ggr(const Table& t, const FunctionalDependencySet& fds, const
                   cfg.hitcount_stop_threshold, cfg.use_fds ? 1 : 0,
                   static_cast<std::int32_t>(cfg.stats_variant)};
   detail::TableAbi tv(t, tok, scoring);
-  const std::size_t n = t.row_count(), m = t.field_count();
-  std::vector<std::uint64_t> rows(n ? n : 1);
-  std::vector<std::int32_t> orders(n * m != 0 ? n * m : 1);
   std::uint64_t score = 0;
   po_solve_stats st{};
-  detail::check(po_ggr(&tv.view, &fv, &c, tv.tok_kind, tv.scoring, PO_LOC_HOST, rows.data(),
-                       orders.data(), &score, &st, nullptr));
+  // the schedule handle carries CSR field orders: FD groups sharing members
+  // make some orders longer than the schema (ggr.hpp:280-282)
+  po_schedule* h = nullptr;
+  detail::check(po_ggr_schedule(&tv.view, &fv, &c, tv.tok_kind, tv.scoring, &h, &score, &st,
+                                nullptr));
+  std::uint64_t n = 0, total = 0;
+  po_schedule_info(h, &n, &total);
+  std::vector<std::uint64_t> rows(n ? n : 1), offs(n + 1);
+  std::vector<std::int32_t> fields(total ? total : 1);
+  const int rc = po_schedule_copy(h, PO_LOC_HOST, rows.data(), offs.data(), fields.data(), nullptr);
+  po_schedule_free(h);
+  detail::check(rc);
   SolveResult res;
   res.phc_score = score;
   res.schedule.entries.reserve(n);
   for (std::size_t i = 0; i < n; ++i)
     res.schedule.entries.push_back(
-        {rows[i], std::vector<int>(orders.begin() + i * m, orders.begin() + (i + 1) * m)});
+        {rows[i], std::vector<int>(fields.begin() + offs[i], fields.begin() + offs[i + 1])});
   res.stats.recursive_calls = st.recursive_calls;
   res.stats.candidates_examined = st.candidates_examined;
   res.stats.max_depth = st.max_depth;

@@ -10,7 +10,7 @@ import pytest
 
 import paper_2403_05821_b200 as po
 from golden_cases import check_result, load_cases, same_result
-from oracle.pyoracle import oracle
+from oracle.pyoracle import available, oracle
 from tables import (ALPHABETS, distinct_first_table, fd_covered_table, group_per_field_table,
                     random_table, skewed_table)
 
@@ -278,3 +278,29 @@ def test_all_empty_cells_null_arena():
     ref = P.ggr(t, None, po.GgrConfig())
     assert phc == ref.phc_score == 0
     assert rows.tolist() == ref.schedule.row_ids.tolist()
+
+
+def test_fd_groups_sharing_members_vs_reference():
+    # groups that share two members: the reference emits a partner once per
+    # group holding it and counts its length as often (ggr.hpp:154-164,
+    # 252-255, 280-282), so field orders get longer than the schema
+    rng = random.Random(77)
+    R = oracle("reference") if available("reference") else oracle("port")
+    shapes = [[["f0", "f1", "f2"], ["f0", "f1"]], [["f0", "f1"], ["f0", "f1"]],
+              [["f0", "f1", "f2"], ["f1", "f2", "f3"]], [["f1", "f0"], ["f0", "f1", "f2"], ["f2", "f1"]]]
+    seen_long = False
+    for trial in range(160):
+        alpha = ALPHABETS[rng.choice(list(ALPHABETS))]
+        t = random_table(rng, 40, 5, alpha, max_len=3, min_len=0, min_rows=2)
+        m = t.field_count()
+        fds = [g for g in rng.choice(shapes) if all(int(x[1:]) < m for x in g)]
+        cfg = rng.choice([po.GgrConfig(), po.exact_config(), po.GgrConfig(1, 1, 0),
+                          po.GgrConfig(2, 2, 0, True, po.StatsScoreVariant(rng.randint(0, 2)))])
+        tok, sc = rng.choice(TOKS), rng.choice(SCS)
+        a = po.ggr(t, fds, cfg, tok, sc)
+        b = R.ggr(t, fds, cfg, tok, sc)
+        assert same_result(a, b), (trial, fds, cfg)
+        assert a.schedule.order_offsets.tolist() == b.schedule.order_offsets.tolist()
+        assert po.phc(a.schedule, t, tok, sc) == a.phc_score
+        seen_long |= a.schedule.order_fields.size > t.row_count() * m
+    assert seen_long  # some schedule did carry repeated partners
