@@ -206,7 +206,8 @@ void* cached_block_acquire(size_t bytes, cudaStream_t s) {
   b.busy = true;
   if (cudaMalloc(&b.p, bytes) != cudaSuccess) {
     (void)cudaGetLastError();
-    // free the idle cached blocks of this device and retry once
+    // free the idle cached blocks of this device and the stream-ordered
+    // pool's unused reservation, then retry once
     PO_CUDA(cudaDeviceSynchronize());
     for (auto it = g_blocks.begin(); it != g_blocks.end();)
       if (!it->busy && it->device == dev) {
@@ -216,6 +217,8 @@ void* cached_block_acquire(size_t bytes, cudaStream_t s) {
       } else {
         ++it;
       }
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
     PO_CUDA(cudaMalloc(&b.p, bytes));
   }
   PO_CUDA(cudaEventCreateWithFlags(&b.released, cudaEventDisableTiming));

@@ -116,17 +116,21 @@ class DevBuf {
     }
     return *this;
   }
+  // Buffers of 16 MB and more come from the block cache (identical sizes
+  // recur call after call, so steady-state calls map no memory and the two
+  // allocators never compete for the same GBs), smaller ones from the
+  // stream-ordered pool.
   void alloc(size_t n, cudaStream_t s) {
+    if (n * sizeof(T) >= (16u << 20)) {
+      alloc_cached(n, s);
+      return;
+    }
     release();
     s_ = s;
     n_ = n;
     if (n) PO_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p_), n * sizeof(T) + 64, s));
   }
-  // large buffers (>= 16 MB) from the block cache, others from the pool
-  void alloc_auto(size_t n, cudaStream_t s) {
-    if (n * sizeof(T) >= (16u << 20)) alloc_cached(n, s);
-    else alloc(n, s);
-  }
+  void alloc_auto(size_t n, cudaStream_t s) { alloc(n, s); }
   // the same from the block cache (cached_block_acquire)
   void alloc_cached(size_t n, cudaStream_t s) {
     release();
