@@ -533,6 +533,46 @@ __device__ __forceinline__ uint64_t cell_hash(const uint8_t* __restrict__ chunk,
   return h ? h : 1;
 }
 
+// Whole-warp hash of one long cell (same value as cell_hash): lane l takes
+// words 2l, 2l+1, 2l+64, ... with three aligned 8-byte loads per word pair
+// (consecutive lanes read consecutive 16 bytes: coalesced), then the warp
+// reduces the word terms. (A variant loading aligned 16-byte chunks and
+// shifting them through shuffles was slower on C5: 12.2 vs 8.8 ms per 3M rows.)
+__device__ __forceinline__ uint64_t warp_cell_hash(const uint8_t* p, uint64_t len, const uint8_t* lim,
+                                                   uint64_t hash_mask, uint32_t lane) {
+  const uint64_t nwords = (len + 7) / 8;
+  const uint64_t lastmask = (len & 7) ? ((uint64_t(1) << (8 * (len & 7))) - 1) : ~0ull;
+  unsigned long long sum = 0;
+  for (uint64_t k0 = 2 * lane; k0 < nwords; k0 += 64) {
+    uint64_t x0, x1;
+    rep_words(p, int64_t(k0), lim, x0, x1);
+    if (k0 + 1 == nwords) x0 &= lastmask;
+    sum += word_term(x0, k0);
+    if (k0 + 1 < nwords) {
+      if (k0 + 2 == nwords) x1 &= lastmask;
+      sum += word_term(x1, k0 + 1);
+    }
+  }
+  const uint64_t h = hash_finish(warp_sum_u64(sum), len) & hash_mask;
+  return h ? h : 1;
+}
+
+// Whole-warp byte equality of two strings of length len (same lane layout).
+__device__ __forceinline__ bool warp_equal(const uint8_t* a, const uint8_t* a_lim, const uint8_t* b,
+                                           const uint8_t* b_lim, uint64_t len, uint32_t lane) {
+  const uint64_t nwords = (len + 7) / 8;
+  const uint64_t lastmask = (len & 7) ? ((uint64_t(1) << (8 * (len & 7))) - 1) : ~0ull;
+  uint64_t diff = 0;
+  for (uint64_t k0 = 2 * lane; k0 < nwords; k0 += 64) {
+    uint64_t x0, x1, y0, y1;
+    rep_words(a, int64_t(k0), a_lim, x0, x1);
+    rep_words(b, int64_t(k0), b_lim, y0, y1);
+    diff |= (x0 ^ y0) & (k0 + 1 == nwords ? lastmask : ~0ull);
+    if (k0 + 1 < nwords) diff |= (x1 ^ y1) & (k0 + 2 == nwords ? lastmask : ~0ull);
+  }
+  return !__any_sync(0xffffffffu, diff != 0);
+}
+
 // K1 + K2a: warps take 32 rows and walk them column by column (lanes of a
 // warp hash cells of one column: similar lengths; one row's bytes are read
 // by the same lane in consecutive iterations, so boundary sectors hit L1),
@@ -546,7 +586,8 @@ __global__ void __launch_bounds__(256) k_hash_probe(const uint8_t* __restrict__ 
                                                     const uint64_t* __restrict__ offs, uint64_t rows,
                                                     uint64_t r0, uint32_t m, uint64_t hash_mask,
                                                     const ColDict* __restrict__ cols, uint32_t* ncid,
-                                                    uint32_t* overflow, uint32_t* cid_mat) {
+                                                    uint32_t* overflow, uint32_t* cid_mat,
+                                                    uint64_t long_min) {
   constexpr unsigned kFull = 0xffffffffu;
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t ntiles = (rows + 31) / 32;
@@ -562,7 +603,16 @@ __global__ void __launch_bounds__(256) k_hash_probe(const uint8_t* __restrict__ 
       if (search) {
         o0 = offs[i];
         len = offs[i + 1] - o0;
-        h = cell_hash(chunk, base, lim, o0, len, hash_mask);
+      }
+      // cells of at least long_min bytes are hashed by the whole warp
+      // (coalesced), the others by their own lane
+      const bool coop = search && len >= long_min;
+      if (search && !coop) h = cell_hash(chunk, base, lim, o0, len, hash_mask);
+      for (unsigned lm = __ballot_sync(kFull, coop); lm; lm &= lm - 1) {
+        const int src = __ffs(lm) - 1;
+        const uint64_t so = __shfl_sync(kFull, o0, src), sl = __shfl_sync(kFull, len, src);
+        const uint64_t sh = warp_cell_hash(chunk + (so - base), sl, chunk_lim, hash_mask, lane);
+        if (int(lane) == src) h = sh;
       }
       const ColDict& D = cols[c];
       uint64_t slot = h & (D.cap - 1), tries = 0;
@@ -644,9 +694,11 @@ __device__ __forceinline__ void rep_loc(const ColDict& D, uint32_t id, const Bui
 }
 
 __global__ void __launch_bounds__(256) k_verify_cells(BuildArgs A, uint32_t* collided,
-                                                      uint32_t* n_collided) {
-  // warps take 32 rows of one column (similar lengths); every lane compares
-  // its own cell with its value's representative
+                                                      uint32_t* n_collided, uint64_t long_min) {
+  // warps take 32 rows of one column (similar lengths); a lane compares its
+  // own cell with its value's representative, cells of at least long_min
+  // bytes are compared by the whole warp (coalesced)
+  constexpr unsigned kFull = 0xffffffffu;
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t rows = A.r1 - A.r0;
   const uint64_t ntiles = (rows + 31) / 32;
@@ -654,21 +706,39 @@ __global__ void __launch_bounds__(256) k_verify_cells(BuildArgs A, uint32_t* col
        tile += (uint64_t(gridDim.x) * blockDim.x) >> 5)
     for (uint32_t c = 0; c < A.m; ++c) {
       const uint64_t r = tile * 32 + lane;
-      if (r >= rows) continue;
       const uint64_t gi = (A.r0 + r) * A.m + c;
-      const uint32_t v = A.cid_mat[gi];
-      if (!(v & kPending) || v == kNoCid) continue;
+      const uint32_t v = r < rows ? A.cid_mat[gi] : kNoCid;
+      const bool pending = (v & kPending) && v != kNoCid;
       const uint32_t id = v & ~kPending;
-      const ColDict& D = A.cols[c];
       const uint64_t i = r * A.m + c;
-      const uint64_t o0 = A.offs[i], len = A.offs[i + 1] - o0;
-      const uint8_t* rep;
-      const uint8_t* rlim;
-      uint64_t rlen;
-      rep_loc(D, id, A, rep, rlim, rlen);
-      const bool eq = rlen == len && equal_bytes4(A.chunk + (o0 - A.base), A.chunk_lim, rep, rlim, len);
-      if (eq) A.cid_mat[gi] = id;
-      else collided[atomicAdd(n_collided, 1u)] = uint32_t(i);
+      uint64_t o0 = 0, len = 0, rlen = 0;
+      const uint8_t* rep = nullptr;
+      const uint8_t* rlim = nullptr;
+      if (pending) {
+        o0 = A.offs[i];
+        len = A.offs[i + 1] - o0;
+        rep_loc(A.cols[c], id, A, rep, rlim, rlen);
+      }
+      const uint8_t* cell = A.chunk + (o0 - A.base);
+      const bool coop = pending && rlen == len && len >= long_min;
+      bool eq = false;
+      if (pending && !coop) eq = rlen == len && equal_bytes4(cell, A.chunk_lim, rep, rlim, len);
+      for (unsigned lm = __ballot_sync(kFull, coop); lm; lm &= lm - 1) {
+        const int src = __ffs(lm) - 1;
+        const uint8_t* sc = reinterpret_cast<const uint8_t*>(
+            __shfl_sync(kFull, reinterpret_cast<uintptr_t>(cell), src));
+        const uint8_t* sr = reinterpret_cast<const uint8_t*>(
+            __shfl_sync(kFull, reinterpret_cast<uintptr_t>(rep), src));
+        const uint8_t* srl = reinterpret_cast<const uint8_t*>(
+            __shfl_sync(kFull, reinterpret_cast<uintptr_t>(rlim), src));
+        const uint64_t sl = __shfl_sync(kFull, len, src);
+        const bool e = warp_equal(sc, A.chunk_lim, sr, srl, sl, lane);
+        if (int(lane) == src) eq = e;
+      }
+      if (pending) {
+        if (eq) A.cid_mat[gi] = id;
+        else collided[atomicAdd(n_collided, 1u)] = uint32_t(i);
+      }
     }
 }
 
@@ -946,9 +1016,16 @@ class Builder {
         DevBuf<uint32_t> ncol(1, s_);
         ncol.zero();
         const unsigned gw = grid_for(((r1 - r0 + 31) / 32) * 32, 256, 8);
+        // PO_LONG_CELL: cells of at least this many bytes are hashed and
+        // verified by a whole warp (C5's ~2 KB cells: verify 15.7 -> 10.9 ms
+        // per 3M rows; C2's cells stay below it)
+        static const uint64_t long_min = [] {
+          const char* v = std::getenv("PO_LONG_CELL");
+          return v && *v ? uint64_t(std::strtoull(v, nullptr, 10)) : uint64_t(1024);
+        }();
         PO_LAUNCH(k_hash_probe, gw, 256, 0, s_, chunk, base, chunk_lim, offs, r1 - r0, r0, m_, hmask_,
-                  d_cols_.get(), ncid_.get(), over_.get(), cid_mat);
-        PO_LAUNCH(k_verify_cells, gw, 256, 0, s_, A, collided_.get(), ncol.get());
+                  d_cols_.get(), ncid_.get(), over_.get(), cid_mat, long_min);
+        PO_LAUNCH(k_verify_cells, gw, 256, 0, s_, A, collided_.get(), ncol.get(), long_min);
         PO_LAUNCH(k_fixup_cells, kSMs, 128, 0, s_, A, collided_.get(), ncol.get());
       }
       std::vector<uint32_t> hc(2 * m_);
