@@ -159,7 +159,7 @@ struct Cand {
 // is resolved afterwards on the tied values only (vids are ranks in the
 // escaped order, not in raw-byte order). The merge is associative and
 // commutative, so any reduction order gives the same result.
-__device__ __forceinline__ Cand merge(const Cand& a, const Cand& b) {
+__host__ __device__ __forceinline__ Cand merge(const Cand& a, const Cand& b) {
   if (a.count == 0) return b;
   if (b.count == 0) return a;
   const u128 l = a.numer * u128(b.count), r = b.numer * u128(a.count);
@@ -217,13 +217,37 @@ __device__ __forceinline__ bool decode_work(const WorkItem& w, const TDesc& t,
 
 constexpr int kArgBlock = 256;
 
+// Sharded solve: which rank scans an entry of a replicated table. Dense
+// tables have the same layout on every rank: whole work items are dealt out
+// (item i to rank i % nparts, the others skip it without reading it). A
+// hashed table holds the same keys on every rank but at slot positions that
+// depend on the insertion order, so its entries are dealt out by identity:
+// (colbase[c] + vid) % nparts.
+__device__ __forceinline__ bool item_skipped(const TDesc& t, uint32_t part, uint32_t nparts) {
+  return nparts > 1 && t.dense && blockIdx.x % nparts != part;
+}
+__device__ __forceinline__ bool entry_skipped(const TDesc& t, const uint64_t* colbase, uint32_t c,
+                                              uint32_t v, uint32_t part, uint32_t nparts) {
+  return nparts > 1 && !t.dense && (colbase[c] + v) % nparts != part;
+}
+
 __global__ void __launch_bounds__(kArgBlock) k_argmax(
     const WorkItem* __restrict__ work, const ScanSlot* __restrict__ slots,
     const uint32_t* __restrict__ masks, const uint32_t* __restrict__ weights,
     const uint64_t* __restrict__ colbase, const uint64_t* __restrict__ vlen, uint32_t m,
-    uint32_t K, Cand* partial, unsigned long long* partial_cands) {
+    uint32_t K, Cand* partial, unsigned long long* partial_cands, uint32_t part, uint32_t nparts) {
+  // sharded solve: the replicated tables' work items are split over the
+  // ranks (item i on rank i % nparts); the per-slot results are merged
+  // across ranks afterwards (merge is associative and commutative)
   const WorkItem w = work[blockIdx.x];
   const ScanSlot sl = slots[w.slot];
+  if (item_skipped(sl.t, part, nparts)) {
+    if (threadIdx.x == 0) {
+      partial[blockIdx.x] = Cand{};
+      partial_cands[blockIdx.x] = 0;
+    }
+    return;
+  }
   const uint32_t* mask = masks + sl.mask_off;
   const uint32_t* wt = weights + sl.w_off;
   Cand best{};
@@ -232,7 +256,7 @@ __global__ void __launch_bounds__(kArgBlock) k_argmax(
     uint32_t c, v;
     if (!decode_work(w, sl.t, colbase, m, e, c, v)) continue;
     const uint32_t cnt = sl.t.cnt[e];
-    if (cnt == 0 || !mask_has(mask, c)) continue;
+    if (cnt == 0 || !mask_has(mask, c) || entry_skipped(sl.t, colbase, c, v, part, nparts)) continue;
     ++ncand;
     const uint64_t vl = vlen[colbase[c] + v];
     uint64_t ptot = 0;
@@ -350,11 +374,13 @@ __global__ void k_tie_min_raw(const WorkItem* __restrict__ work, const ScanSlot*
                               const uint64_t* __restrict__ colbase,
                               const uint64_t* __restrict__ vlen, uint32_t m, uint32_t K,
                               const Cand* __restrict__ best, const int32_t* __restrict__ tie_group,
-                              const uint32_t* __restrict__ rv, unsigned long long* minkey) {
+                              const uint32_t* __restrict__ rv, unsigned long long* minkey,
+                              uint32_t part, uint32_t nparts) {
   const WorkItem w = work[blockIdx.x];
   const int32_t g = tie_group[w.slot];
   if (g < 0) return;
   const ScanSlot sl = slots[w.slot];
+  if (item_skipped(sl.t, part, nparts)) return;
   const uint32_t* mask = masks + sl.mask_off;
   const uint32_t* wt = weights + sl.w_off;
   const Cand b = best[w.slot];
@@ -362,7 +388,9 @@ __global__ void k_tie_min_raw(const WorkItem* __restrict__ work, const ScanSlot*
     uint32_t c, v;
     if (!decode_work(w, sl.t, colbase, m, e, c, v)) continue;
     const uint32_t cnt = sl.t.cnt[e];
-    if (cnt != b.count || c != b.col || !mask_has(mask, c)) continue;
+    if (cnt != b.count || c != b.col || !mask_has(mask, c) ||
+        entry_skipped(sl.t, colbase, c, v, part, nparts))
+      continue;
     const uint64_t vl = vlen[colbase[c] + v];
     uint64_t ptot = 0;
     for (uint32_t k = 0; k < K; ++k)
@@ -403,6 +431,26 @@ __global__ void __launch_bounds__(kArgBlock) k_argmax_final(
     out[s] = sb[0];
     out_cands[s] = sc[0];
   }
+}
+
+// Per-slot results of every rank ([rank][slot] Cands then [rank][slot]
+// candidate counts) merged into the first rank's rows.
+__global__ void k_merge_ranks(Cand* all_best, unsigned long long* all_cands, uint32_t nslots,
+                              uint32_t nranks) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nslots; i += gridDim.x * blockDim.x) {
+    Cand b = all_best[i];
+    unsigned long long n = all_cands[i];
+    for (uint32_t r = 1; r < nranks; ++r) {
+      b = merge(b, all_best[size_t(r) * nslots + i]);
+      n += all_cands[size_t(r) * nslots + i];
+    }
+    all_best[i] = b;
+    all_cands[i] = n;
+  }
+}
+
+__global__ void k_complement_u64(unsigned long long* x, uint32_t n) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) x[i] = ~x[i];
 }
 
 // ---------------------------------------------------------------------------
@@ -652,10 +700,12 @@ __global__ void k_root_psum(const uint32_t* vid, uint64_t n, uint32_t m, uint32_
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_leaf_stats(
     const WorkItem* work, const ScanSlot* slots, const uint32_t* masks, const uint64_t* colbase,
-    const uint64_t* vlen, uint32_t m, unsigned long long* card, unsigned long long* tot) {
+    const uint64_t* vlen, uint32_t m, unsigned long long* card, unsigned long long* tot,
+    uint32_t part, uint32_t nparts) {
   extern __shared__ unsigned long long sh[];  // [2*m] for hashed tables with small m
   const WorkItem w = work[blockIdx.x];
   const ScanSlot sl = slots[w.slot];
+  if (item_skipped(sl.t, part, nparts)) return;  // sharded: dealt to another rank
   const uint32_t* mask = masks + sl.mask_off;
   if (w.col != kAnyCol) {
     // dense table, one column: per-thread sums, one atomic pair per block
@@ -690,7 +740,8 @@ __global__ void __launch_bounds__(256) k_leaf_stats(
     unsigned long long l = 0;
     if (e < w.hi && decode_entry(sl.t, colbase, m, e, c, v)) {
       const uint32_t cnt = sl.t.cnt[e];
-      if (cnt == 0 || !mask_has(mask, c)) c = 0xFFFFFFFFu;
+      if (cnt == 0 || !mask_has(mask, c) || entry_skipped(sl.t, colbase, c, v, part, nparts))
+        c = 0xFFFFFFFFu;
       else l = uint64_t(cnt) * vlen[colbase[c] + v];
     } else {
       c = 0xFFFFFFFFu;
@@ -1048,18 +1099,39 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
     auto* d_card = d_ncand + nslots;
     auto* d_tot = d_card + nleaf * m;
     if (nleaf) PO_CUDA(cudaMemsetAsync(d_card, 0, 2 * nleaf * m * 8, s));
+    // sharded solve: every rank scans its share of the replicated tables'
+    // work items; results merged across ranks below
+    static const bool partition = [] {  // PO_DIST_PARTITION=0: every rank scans everything
+      const char* v = std::getenv("PO_DIST_PARTITION");
+      return !(v && *v == '0');
+    }();
+    const uint32_t nparts = dist && partition ? uint32_t(dist->comm->size()) : 1u;
+    const uint32_t part = dist && partition ? uint32_t(dist->comm->rank()) : 0u;
     if (nslots) {
       PO_LAUNCH(k_argmax, unsigned(L.work.size()), kArgBlock, 0, s,
                 reinterpret_cast<WorkItem*>(dp + o_work), reinterpret_cast<ScanSlot*>(dp + o_slots),
                 reinterpret_cast<uint32_t*>(dp + o_masks), reinterpret_cast<uint32_t*>(dp + o_w),
-                colbase, vlen, m, K, partial.get(), pcands.get());
+                colbase, vlen, m, K, partial.get(), pcands.get(), part, nparts);
       PO_LAUNCH(k_argmax_final, nslots, kArgBlock, 0, s, partial.get(), pcands.get(),
                 reinterpret_cast<uint32_t*>(dp + o_swo), d_best, d_ncand);
     }
     if (nleaf)
       PO_LAUNCH(k_leaf_stats, unsigned(S.work.size()), 256, m <= 2048 ? 16 * m : 0, s,
                 reinterpret_cast<WorkItem*>(dp + o_swork), reinterpret_cast<ScanSlot*>(dp + o_sslots),
-                reinterpret_cast<uint32_t*>(dp + o_smasks), colbase, vlen, m, d_card, d_tot);
+                reinterpret_cast<uint32_t*>(dp + o_smasks), colbase, vlen, m, d_card, d_tot, part,
+                nparts);
+    if (nparts > 1) {
+      if (nslots) {
+        DevBuf<Cand> ab(size_t(nslots) * nparts, s);
+        DevBuf<unsigned long long> ac(size_t(nslots) * nparts, s);
+        dist->comm->allgather(d_best, ab.get(), nslots * sizeof(Cand), s);
+        dist->comm->allgather(d_ncand, ac.get(), nslots * 8, s);
+        PO_LAUNCH(k_merge_ranks, grid_for(nslots, 128), 128, 0, s, ab.get(), ac.get(), nslots, nparts);
+        PO_CUDA(cudaMemcpyAsync(d_best, ab.get(), nslots * sizeof(Cand), cudaMemcpyDeviceToDevice, s));
+        PO_CUDA(cudaMemcpyAsync(d_ncand, ac.get(), nslots * 8, cudaMemcpyDeviceToDevice, s));
+      }
+      if (nleaf) dist->comm->allreduce(d_card, 2 * nleaf * m, CDtype::U64, COp::Sum, s);
+    }
     std::vector<uint8_t> hres(std::max<size_t>(16, res_bytes));
     res.download(hres.data(), res_bytes);  // pageable D2H: returns when complete
     sync(s);
@@ -1094,7 +1166,12 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
         PO_LAUNCH(k_tie_min_raw, unsigned(L.work.size()), kArgBlock, 0, s,
                   reinterpret_cast<WorkItem*>(dp + o_work), reinterpret_cast<ScanSlot*>(dp + o_slots),
                   reinterpret_cast<uint32_t*>(dp + o_masks), reinterpret_cast<uint32_t*>(dp + o_w),
-                  colbase, vlen, m, K, d_best, d_tg.get(), rv, mk.get());
+                  colbase, vlen, m, K, d_best, d_tg.get(), rv, mk.get(), part, nparts);
+        if (nparts > 1) {  // min over the ranks' shares = ~max(~x)
+          PO_LAUNCH(k_complement_u64, grid_for(nt, 128), 128, 0, s, mk.get(), nt);
+          dist->comm->allreduce(mk.get(), nt, CDtype::U64, COp::Max, s);
+          PO_LAUNCH(k_complement_u64, grid_for(nt, 128), 128, 0, s, mk.get(), nt);
+        }
         std::vector<unsigned long long> hm(nt);
         mk.download(hm.data(), nt);
         sync(s);
@@ -1142,6 +1219,15 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
     };
     std::vector<SplitH> splits;
     std::vector<HTable*> new_tables;  // block children's tables of this level
+    if (debug_timing()) {
+      unsigned long long sh = 0, st = 0;
+      for (uint32_t i = 0; i < nslots; ++i) {
+        sh += hn[i];
+        st += hbest[i].ties;
+      }
+      fprintf(stderr, "[po level] rank %d slots %u work %zu cands %llu ties %llu\n",
+              dist ? dist->comm->rank() : 0, nslots, L.work.size(), sh, st);
+    }
     for (uint32_t i = 0; i < nslots; ++i) {
       const int id = frontier[i];
       out.stats.candidates_examined += hn[i] + unique_groups[i];
