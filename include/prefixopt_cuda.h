@@ -300,6 +300,12 @@ int po_slice_copy(const po_slice* slice, uint32_t out_location, uint64_t* out_ro
                   int32_t* out_field_orders, void* stream);
 void po_slice_free(po_slice* slice);
 
+/* Test hook (not a reference function): the stable radix sort of the K8
+ * row-key sorts, (u64 key, u32 value) pairs by key bits [begin, end), host
+ * arrays in and out. */
+int po_debug_radix_sort(const uint64_t* keys, const uint32_t* vals, uint64_t n, int32_t begin_bit,
+                        int32_t end_bit, uint64_t* out_keys, uint32_t* out_vals);
+
 /* Thread-local message of the last failing call on this thread. */
 const char* po_last_error(void);
 

@@ -25,7 +25,7 @@ CPP_SOURCES = ["jsonl.cpp"]
 JSON_DIR = os.environ.get(
     "PO_JSON_DIR",
     "/opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_frontend/thirdparty/nlohmann")
-SOURCES = ["abi.cu", "dict.cu", "encode.cu", "refine.cu", "phc.cu", "ggr.cu", "comm.cu", "shard.cu", "fd.cu", "render.cu", "replay.cu", "csv.cu"]
+SOURCES = ["abi.cu", "dict.cu", "radix.cu", "encode.cu", "refine.cu", "phc.cu", "ggr.cu", "comm.cu", "shard.cu", "fd.cu", "render.cu", "replay.cu", "csv.cu"]
 
 NVCC = os.environ.get("NVCC", shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -613,6 +613,28 @@ int po_schedule_copy(const po_schedule* sc, uint32_t out_location, uint64_t* out
 
 void po_schedule_free(po_schedule* sc) { delete sc; }
 
+// Test hook: the K8 radix sort on host arrays (tests/test_gpu_radix.py).
+int po_debug_radix_sort(const uint64_t* keys, const uint32_t* vals, uint64_t n, int32_t begin_bit,
+                        int32_t end_bit, uint64_t* out_keys, uint32_t* out_vals) {
+  return guarded([&] {
+    if (n >= (uint64_t(1) << 32)) fail(PO_ERR_SIZE, "too many items");
+    if (begin_bit < 0 || end_bit > 64 || begin_bit > end_bit) fail(PO_ERR_INVALID_ARG, "bad bit range");
+    cudaStream_t s = nullptr;
+    DevBuf<uint64_t> k(n, s), k2(n, s);
+    DevBuf<uint32_t> v(n, s), v2(n, s);
+    if (n) {
+      PO_CUDA(cudaMemcpyAsync(k.get(), keys, n * 8, cudaMemcpyHostToDevice, s));
+      PO_CUDA(cudaMemcpyAsync(v.get(), vals, n * 4, cudaMemcpyHostToDevice, s));
+    }
+    radix_sort_pairs(k.get(), k2.get(), v.get(), v2.get(), uint32_t(n), begin_bit, end_bit, s);
+    if (n) {
+      PO_CUDA(cudaMemcpyAsync(out_keys, k2.get(), n * 8, cudaMemcpyDeviceToHost, s));
+      PO_CUDA(cudaMemcpyAsync(out_vals, v2.get(), n * 4, cudaMemcpyDeviceToHost, s));
+    }
+    sync(s);
+  });
+}
+
 int po_phc(const po_table* t, int32_t tok, int32_t scoring, uint64_t n_entries,
            const uint64_t* row_ids, const uint64_t* order_offsets, const int32_t* order_fields,
            uint32_t sched_location, uint64_t* out_phc, void* stream) {

@@ -48,6 +48,13 @@ cudaStream_t copy_stream();
 
 void exclusive_scan_u64(const uint64_t* in, uint64_t* out, uint64_t n, cudaStream_t s);
 
+// Stable LSD radix sort of (u64 key, u32 value) pairs by key bits
+// [begin_bit, end_bit) (radix.cu: hand-written onesweep). kin/vin and
+// kout/vout must not overlap. PO_RADIX=cub routes to cub::DeviceRadixSort
+// (comparison runs).
+void radix_sort_pairs(const uint64_t* kin, uint64_t* kout, const uint32_t* vin, uint32_t* vout,
+                      uint32_t n, int begin_bit, int end_bit, cudaStream_t s);
+
 // K1 + K2 (dict.cu): exact per-column dictionaries in one read of the cell
 // bytes. cid_mat[r*m + c] = dense id of cell (r, c)'s value within column c
 // in first-claim order; distinct value d = colbase[c] + id is the string

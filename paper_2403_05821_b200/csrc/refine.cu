@@ -636,10 +636,7 @@ void refine_sort_multi(const std::vector<RefineJob>& specs, cudaStream_t s) {
       auto sort_pass = [&](const uint64_t* kin, uint64_t* kout, const uint32_t* vin, uint32_t* vout,
                            int end_bit) {
         if (!seg || segradix) {
-          ProfScope ps("cub_radix_sort", s);
-          b = j.tb;
-          PO_CUDA(cub::DeviceRadixSort::SortPairs(j.tmp.get(), b, kin, kout, vin, vout, A, 0,
-                                                  end_bit, s));
+          radix_sort_pairs(kin, kout, vin, vout, A, 0, end_bit, s);
           return;
         }
         ProfScope ps("cub_segmented_sort", s);

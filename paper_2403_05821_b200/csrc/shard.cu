@@ -670,18 +670,12 @@ void sort_recs(const uint64_t* recs, uint64_t n, const RecFmt& f, uint32_t key_b
   DevBuf<uint64_t> k0(n, s), k1(n, s);
   DevBuf<uint32_t> p0(n, s), p1(n, s);
   PO_LAUNCH(k_iota32, grid_for(n, 256), 256, 0, s, p0.get(), n);
-  size_t tb = 0;
-  PO_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, k0.get(), k1.get(), p0.get(), p1.get(),
-                                          int(n), 0, 64, s));
-  DevBuf<uint8_t> tmp(tb, s);
   for (int w = int(f.W) - 1; w >= 0; --w) {
     PO_LAUNCH(k_key_word, grid_for(n, 256), 256, 0, s, n, recs, f.stride, uint32_t(w), p0.get(),
               k0.get());
     // keys are packed from the top: the last word's low bits are padding
     const int begin = w == int(f.W) - 1 ? int(64 * f.W - key_bits) : 0;
-    ProfScope ps("cub_radix_sort", s);
-    PO_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(), tb, k0.get(), k1.get(), p0.get(), p1.get(),
-                                            int(n), begin, 64, s));
+    radix_sort_pairs(k0.get(), k1.get(), p0.get(), p1.get(), uint32_t(n), begin, 64, s);
     std::swap(p0, p1);
   }
   PO_LAUNCH(k_gather_recs, grid_for(n * f.stride, 256), 256, 0, s, n, recs, f.stride, p0.get(),
