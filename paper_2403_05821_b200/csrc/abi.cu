@@ -2,6 +2,7 @@
 // Each call runs synchronously on the caller's stream; exceptions become
 // PO_ERR_* codes with a thread-local message.
 
+#include <algorithm>
 #include <chrono>
 #include <cstdlib>
 #include <cstring>
@@ -43,13 +44,36 @@ cudaEvent_t prof_event() {
 }
 
 void prof_drain() {  // caller holds g_prof_mu
+  // device idle time between the recorded launches (sweep over the scopes'
+  // [start, end) intervals in start order), charged to the launch that ends
+  // the gap as "gap:<name>": the host work between two launches
+  struct Iv {
+    float a, b;
+    const char* name;
+  };
+  std::vector<Iv> iv;
+  iv.reserve(g_prof_pending.size());
   for (auto& r : g_prof_pending) {
-    float ms = 0;
+    float ms = 0, a = 0;
     PO_CUDA(cudaEventSynchronize(r.b));
     PO_CUDA(cudaEventElapsedTime(&ms, r.a, r.b));
+    PO_CUDA(cudaEventElapsedTime(&a, g_prof_pending.front().a, r.a));
+    iv.push_back({a, a + ms, r.name});
     auto& acc = g_prof_acc[r.name];
     acc.first += 1;
     acc.second += ms;
+  }
+  std::stable_sort(iv.begin(), iv.end(), [](const Iv& x, const Iv& y) { return x.a < y.a; });
+  float covered = iv.empty() ? 0.f : iv.front().a;
+  for (const Iv& x : iv) {
+    if (x.a > covered + 0.002f) {
+      auto& acc = g_prof_acc[std::string("gap:") + x.name];
+      acc.first += 1;
+      acc.second += x.a - covered;
+    }
+    covered = std::max(covered, x.b);
+  }
+  for (auto& r : g_prof_pending) {
     g_prof_free.push_back(r.a);
     g_prof_free.push_back(r.b);
   }
@@ -65,6 +89,13 @@ void profile_begin(const char* name, cudaStream_t s, void** token) {
   PO_CUDA(cudaEventRecord(r.a, s));
   g_prof_pending.push_back(r);
   *token = reinterpret_cast<void*>(g_prof_pending.size());
+}
+
+void profile_host(const char* name, double ms) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  auto& acc = g_prof_acc[std::string("host:") + name];
+  acc.first += 1;
+  acc.second += ms;
 }
 
 void profile_end(void* token, cudaStream_t s) {
@@ -270,6 +301,36 @@ cudaStream_t copy_stream() {
   if (size_t(dev) >= streams.s.size()) streams.s.resize(dev + 1, nullptr);
   if (!streams.s[dev]) PO_CUDA(cudaStreamCreateWithFlags(&streams.s[dev], cudaStreamNonBlocking));
   return streams.s[dev];
+}
+
+// Small device -> host reads that the host waits for (level results): through
+// a per-thread pinned buffer, which completes sooner than a pageable copy.
+void d2h_sync(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+  struct Pinned {
+    uint8_t* p = nullptr;
+    size_t cap = 0;
+    ~Pinned() {
+      if (p) cudaFreeHost(p);
+    }
+  };
+  static thread_local Pinned buf;
+  constexpr size_t kMax = 4u << 20;
+  if (bytes > kMax) {
+    PO_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s));
+    sync(s);
+    return;
+  }
+  if (buf.cap < bytes) {
+    if (buf.p) PO_CUDA(cudaFreeHost(buf.p));
+    buf.p = nullptr;
+    buf.cap = 0;
+    const size_t cap = std::max<size_t>(bytes, 64u << 10);
+    PO_CUDA(cudaMallocHost(reinterpret_cast<void**>(&buf.p), cap));
+    buf.cap = cap;
+  }
+  if (bytes) PO_CUDA(cudaMemcpyAsync(buf.p, src, bytes, cudaMemcpyDeviceToHost, s));
+  sync(s);
+  if (bytes) std::memcpy(dst, buf.p, bytes);
 }
 
 void h2d_async(void* dst, const void* src, size_t bytes, cudaStream_t s) {

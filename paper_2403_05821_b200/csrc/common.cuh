@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <cstring>
 #include <cstdint>
 #include <stdexcept>
@@ -52,6 +53,22 @@ struct ProfScope {
   }
 };
 
+// Host wall time of a section (profile mode only, no synchronisation):
+// reported as "host:<name>" next to the kernels.
+void profile_host(const char* name, double ms);
+struct HostScope {
+  const char* name;
+  std::chrono::steady_clock::time_point t0;
+  bool on;
+  explicit HostScope(const char* n) : name(n), on(g_profile.load(std::memory_order_relaxed)) {
+    if (on) t0 = std::chrono::steady_clock::now();
+  }
+  ~HostScope() {
+    if (on)
+      profile_host(name, std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+  }
+};
+
 // Every kernel of this library is launched through PO_LAUNCH so bench.py can
 // report how many of OUR kernels ran (po_kernel_launch_count) and time them.
 #define PO_LAUNCH(kernel, grid, block, smem, stream, ...)                    \
@@ -82,6 +99,8 @@ inline unsigned grid_for(uint64_t work, unsigned block, unsigned max_waves = 16)
 // stream and stall the launch queue). Larger copies (caller data) go direct.
 constexpr size_t kPinnedSmallCopy = 1 << 20;
 void h2d_async(void* dst, const void* src, size_t bytes, cudaStream_t s);
+// device -> host copy, then the stream synchronised (pinned bounce buffer)
+void d2h_sync(void* dst, const void* src, size_t bytes, cudaStream_t s);
 
 // Large transient buffers (the dictionary tables, per-cell arrays) come from
 // a per-device cache of cudaMalloc'd blocks that are never returned to the
@@ -189,6 +208,7 @@ DevBuf<T> to_device(const std::vector<T>& v, cudaStream_t s) {
 
 extern thread_local uint64_t g_syncs;  // host synchronisations of this thread (debug timing)
 inline void sync(cudaStream_t s) {
+  HostScope hs("sync");
   ++g_syncs;
   PO_CUDA(cudaStreamSynchronize(s));
 }

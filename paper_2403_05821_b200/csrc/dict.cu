@@ -902,10 +902,9 @@ struct ColBufs {
 class Builder {
  public:
   Builder(uint64_t n, uint32_t m, uint64_t hmask, cudaStream_t s)
-      : n_(n), m_(m), hmask_(hmask), s_(s), bufs_(m), h_(m), ncid_(m, s), over_(m, s),
+      : n_(n), m_(m), hmask_(hmask), s_(s), bufs_(m), h_(m), cnt2_(2 * size_t(m), s),
         d_cols_(m, s) {
-    ncid_.zero();
-    over_.zero();
+    cnt2_.zero();
   }
 
   // lanes per cell from the columns' average lengths
@@ -939,6 +938,8 @@ class Builder {
     const uint32_t keep = D.keys ? std::min<uint32_t>(count_[c], D.cidcap) : 0;
     const uint32_t cidcap = uint32_t(want);
     const uint64_t cap = pow2_at_least(2 * want);
+    HostScope hs("dict_reserve");
+    ProfScope ps("dict_reserve", s_);
     ColBufs nb;
     nb.keys.alloc_auto(cap, s_);
     nb.cids.alloc_auto(cap, s_);
@@ -951,11 +952,10 @@ class Builder {
     nb.voff.fill_bytes(0xFF);  // kUnsetOff / kUnsetLen
     nb.vlen.fill_bytes(0xFF);
     if (keep) {
-      ColBufs& ob = bufs_[c];
-      PO_CUDA(cudaMemcpyAsync(nb.vhash.get(), ob.vhash.get(), keep * 8ull, cudaMemcpyDeviceToDevice, s_));
-      PO_CUDA(cudaMemcpyAsync(nb.voff.get(), ob.voff.get(), keep * 8ull, cudaMemcpyDeviceToDevice, s_));
-      PO_CUDA(cudaMemcpyAsync(nb.vlen.get(), ob.vlen.get(), keep * 4ull, cudaMemcpyDeviceToDevice, s_));
-      PO_CUDA(cudaMemcpyAsync(nb.vrow.get(), ob.vrow.get(), keep * 4ull, cudaMemcpyDeviceToDevice, s_));
+      PO_CUDA(cudaMemcpyAsync(nb.vhash.get(), D.vhash, keep * 8ull, cudaMemcpyDeviceToDevice, s_));
+      PO_CUDA(cudaMemcpyAsync(nb.voff.get(), D.voff, keep * 8ull, cudaMemcpyDeviceToDevice, s_));
+      PO_CUDA(cudaMemcpyAsync(nb.vlen.get(), D.vlen, keep * 4ull, cudaMemcpyDeviceToDevice, s_));
+      PO_CUDA(cudaMemcpyAsync(nb.vrow.get(), D.vrow, keep * 4ull, cudaMemcpyDeviceToDevice, s_));
       PO_LAUNCH(k_rehash, grid_for(keep, 256), 256, 0, s_, nb.vhash.get(), keep, nb.keys.get(),
                 nb.cids.get(), cap);
     }
@@ -968,6 +968,40 @@ class Builder {
     D.vrow = bufs_[c].vrow.get();
     D.cap = cap;
     D.cidcap = cidcap;
+    dirty_ = true;
+  }
+
+  // First reservation of every column at once: one allocation holding all
+  // columns' arrays, grouped so that two memsets initialise them (slot keys
+  // zero; cids and the value offsets / lengths all-ones).
+  void reserve_all(uint64_t want_each) {
+    HostScope hs("dict_reserve_all");
+    ProfScope ps("dict_reserve_all", s_);
+    const uint64_t want = std::max<uint64_t>(1, std::min<uint64_t>(want_each, n_));
+    const uint64_t cap = pow2_at_least(2 * want);
+    auto al = [](uint64_t b) { return (b + 255) & ~uint64_t(255); };
+    const uint64_t zb = al(cap * 8), fb = al(cap * 4) + al(want * 8) + al(want * 4),
+                   ub = al(want * 8) + al(want * 4);
+    shared_.alloc_auto(m_ * (zb + fb + ub), s_);
+    uint8_t* z = shared_.get();
+    uint8_t* f = z + m_ * zb;
+    uint8_t* u = f + m_ * fb;
+    PO_CUDA(cudaMemsetAsync(z, 0, m_ * zb, s_));
+    PO_CUDA(cudaMemsetAsync(f, 0xFF, m_ * fb, s_));
+    for (uint32_t c = 0; c < m_; ++c) {
+      ColDict& D = h_[c];
+      bufs_[c] = ColBufs{};
+      D.keys = reinterpret_cast<unsigned long long*>(z + c * zb);
+      uint8_t* fc = f + c * fb;
+      D.cids = reinterpret_cast<uint32_t*>(fc);
+      D.voff = reinterpret_cast<unsigned long long*>(fc + al(cap * 4));
+      D.vlen = reinterpret_cast<uint32_t*>(fc + al(cap * 4) + al(want * 8));
+      uint8_t* uc = u + c * ub;
+      D.vhash = reinterpret_cast<unsigned long long*>(uc);
+      D.vrow = reinterpret_cast<uint32_t*>(uc + al(want * 8));
+      D.cap = cap;
+      D.cidcap = uint32_t(want);
+    }
     dirty_ = true;
   }
 
@@ -994,8 +1028,8 @@ class Builder {
       A.items = items_;
       A.hmask = hmask_;
       A.cols = d_cols_.get();
-      A.ncid = ncid_.get();
-      A.overflow = over_.get();
+      A.ncid = ncid();
+      A.overflow = over();
       A.cid_mat = cid_mat;
       const uint64_t work = ((r1 - r0 + kTileRows - 1) / kTileRows) * items_;
       const uint64_t tiles = (r1 - r0 + kTileRows - 1) / kTileRows;
@@ -1028,14 +1062,12 @@ class Builder {
           return v && *v ? uint64_t(std::strtoull(v, nullptr, 10)) : uint64_t(1024);
         }();
         PO_LAUNCH(k_hash_probe, gw, 256, 0, s_, chunk, base, chunk_lim, offs, r1 - r0, r0, m_, hmask_,
-                  d_cols_.get(), ncid_.get(), over_.get(), cid_mat, long_min);
+                  d_cols_.get(), ncid(), over(), cid_mat, long_min);
         PO_LAUNCH(k_verify_cells, gw, 256, 0, s_, A, collided_.get(), ncol.get(), long_min);
         PO_LAUNCH(k_fixup_cells, kSMs, 128, 0, s_, A, collided_.get(), ncol.get());
       }
       std::vector<uint32_t> hc(2 * m_);
-      ncid_.download(hc.data(), m_);
-      over_.download(hc.data() + m_, m_);
-      sync(s_);
+      d2h_sync(hc.data(), cnt2_.get(), 2 * size_t(m_) * sizeof(uint32_t), s_);
       bool any = false;
       for (uint32_t c = 0; c < m_; ++c) {
         count_[c] = hc[c];
@@ -1054,8 +1086,8 @@ class Builder {
           reserve(c, want);
           hc[c] = keep;
         }
-      ncid_.upload(hc.data(), m_);
-      over_.zero();
+      std::fill(hc.begin() + m_, hc.end(), 0u);
+      cnt2_.upload(hc.data(), 2 * size_t(m_));
     }
   }
 
@@ -1081,7 +1113,10 @@ class Builder {
   cudaStream_t s_;
   std::vector<ColBufs> bufs_;
   std::vector<ColDict> h_;
-  DevBuf<uint32_t> ncid_, over_;
+  DevBuf<uint32_t> cnt2_;  // [new ids per column][overflow flags per column]
+  DevBuf<uint8_t> shared_;  // reserve_all's arrays of every column
+  uint32_t* ncid() { return cnt2_.get(); }
+  uint32_t* over() { return cnt2_.get() + m_; }
   DevBuf<ColDict> d_cols_;
   uint32_t items_ = 0;
   double row_bytes_ = 0;
@@ -1215,8 +1250,7 @@ void build_dictionary(const DeviceTable& t, uint32_t hash_bits, cudaStream_t s, 
       d_sums.zero();
       PO_LAUNCH(k_sample_col_bytes, grid_for(uint64_t(ns) * m, 256, 4), 256, 0, s, t.offsets, n,
                 uint32_t(m), ns, d_sums.get());
-      d_sums.download(sums.data(), m);
-      sync(s);
+      d2h_sync(sums.data(), d_sums.get(), (m) * sizeof(*d_sums.get()), s);
     }
     for (uint64_t c = 0; c < m; ++c) avg[c] = double(sums[c]) / double(std::max<uint32_t>(ns, 1));
   }
@@ -1234,7 +1268,7 @@ void build_dictionary(const DeviceTable& t, uint32_t hash_bits, cudaStream_t s, 
     exact_caps = worst <= 0.1 * double(free_b);
   }
   const uint64_t R0 = (exact_caps || n <= 131072) ? n : std::max<uint64_t>(65536, n / 16);
-  for (uint32_t c = 0; c < m; ++c) B.reserve(c, exact_caps ? n : R0);
+  B.reserve_all(exact_caps ? n : R0);
 
   if (!streamed) {
     const uint8_t* lim = t.arena + t.arena_bytes;

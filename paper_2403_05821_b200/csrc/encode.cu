@@ -495,8 +495,7 @@ void encode(const DeviceTable& t, int tok, int scoring, cudaStream_t s, Encoded&
   PO_LAUNCH(k_total_len, grid_for((D + kTotRun - 1) / kTotRun, 256, 2), 256, m <= 4096 ? m * 8 : 0, s, e.count.get(),
             e.vlen.get(), col_by_pos.get(), D, uint32_t(m), tot.get());
   std::vector<unsigned long long> htot(m);
-  tot.download(htot.data(), m);
-  sync(s);
+  d2h_sync(htot.data(), tot.get(), (m) * sizeof(*tot.get()), s);
   for (uint32_t c = 0; c < m; ++c) e.total_len[c] = htot[c];
   timing_mark("encode_tail", s);
 }

@@ -20,6 +20,7 @@
 // every leaf's rows at once; K10 emits the schedule and K9 scores it. The
 // whole-table statistics fallback competes last (ggr.hpp:379-387).
 
+#include <optional>
 #include <cub/cub.cuh>
 #include <cooperative_groups.h>
 #include <cooperative_groups/reduce.h>
@@ -72,7 +73,10 @@ void alloc_tables(const std::vector<HTable*>& ts, uint32_t K, cudaStream_t s) {
   size_t total = 0;
   for (const HTable* t : ts) total += al(t->cap * 8) + al(t->cap * 4) + (K ? al(t->cap * K * 8) : 0);
   auto mem = std::make_shared<DevBuf<uint8_t>>(total, s);
-  mem->zero();
+  {
+    ProfScope ps("memset_tables", s);
+    mem->zero();
+  }
   uint8_t* p = mem->get();
   for (HTable* t : ts) {
     t->keys = reinterpret_cast<unsigned long long*>(p);
@@ -204,6 +208,28 @@ struct WorkItem {
 
 constexpr uint32_t kAnyCol = 0xFFFFFFFFu;
 
+// A slot's scan of one table (or one dense column) as consecutive work items
+// of kWorkChunk entries; first = the item number of its first item.
+struct WorkSeg {
+  uint32_t slot, col;
+  uint64_t lo, hi;
+  uint32_t first, pad;
+};
+constexpr uint64_t kWorkChunk = 2048;
+
+// This block's work item: the last segment with first <= blockIdx.x.
+__device__ __forceinline__ WorkItem work_at(const WorkSeg* __restrict__ segs, uint32_t nseg) {
+  uint32_t lo = 0, hi = nseg - 1;
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi + 1) / 2;
+    if (segs[mid].first <= blockIdx.x) lo = mid;
+    else hi = mid - 1;
+  }
+  const WorkSeg& g = segs[lo];
+  const uint64_t a = g.lo + uint64_t(blockIdx.x - g.first) * kWorkChunk;
+  return WorkItem{g.slot, g.col, a, a + kWorkChunk < g.hi ? a + kWorkChunk : g.hi};
+}
+
 __device__ __forceinline__ bool decode_work(const WorkItem& w, const TDesc& t,
                                             const uint64_t* colbase, uint32_t m, uint64_t e,
                                             uint32_t& c, uint32_t& v) {
@@ -232,14 +258,14 @@ __device__ __forceinline__ bool entry_skipped(const TDesc& t, const uint64_t* co
 }
 
 __global__ void __launch_bounds__(kArgBlock) k_argmax(
-    const WorkItem* __restrict__ work, const ScanSlot* __restrict__ slots,
+    const WorkSeg* __restrict__ work, uint32_t nwseg, const ScanSlot* __restrict__ slots,
     const uint32_t* __restrict__ masks, const uint32_t* __restrict__ weights,
     const uint64_t* __restrict__ colbase, const uint64_t* __restrict__ vlen, uint32_t m,
     uint32_t K, Cand* partial, unsigned long long* partial_cands, uint32_t part, uint32_t nparts) {
   // sharded solve: the replicated tables' work items are split over the
   // ranks (item i on rank i % nparts); the per-slot results are merged
   // across ranks afterwards (merge is associative and commutative)
-  const WorkItem w = work[blockIdx.x];
+  const WorkItem w = work_at(work, nwseg);
   const ScanSlot sl = slots[w.slot];
   if (item_skipped(sl.t, part, nparts)) {
     if (threadIdx.x == 0) {
@@ -300,7 +326,7 @@ __global__ void __launch_bounds__(kArgBlock) k_argmax(
 // Every entry of a tied slot whose (score, count, column) key equals the
 // slot's best: its value is appended to the slot's segment for the raw-byte
 // tie-break (ggr.hpp:196).
-__global__ void k_collect_ties(const WorkItem* __restrict__ work, const ScanSlot* __restrict__ slots,
+__global__ void k_collect_ties(const WorkSeg* __restrict__ work, uint32_t nwseg, const ScanSlot* __restrict__ slots,
                                const uint32_t* __restrict__ masks,
                                const uint32_t* __restrict__ weights,
                                const uint64_t* __restrict__ colbase,
@@ -308,7 +334,7 @@ __global__ void k_collect_ties(const WorkItem* __restrict__ work, const ScanSlot
                                const Cand* __restrict__ best, const int32_t* __restrict__ tie_group,
                                const uint32_t* __restrict__ tie_off, uint32_t* cursor,
                                uint32_t* t_ref, uint32_t* t_vid, uint32_t* t_grp) {
-  const WorkItem w = work[blockIdx.x];
+  const WorkItem w = work_at(work, nwseg);
   const int32_t g = tie_group[w.slot];
   if (g < 0) return;
   const ScanSlot sl = slots[w.slot];
@@ -368,7 +394,7 @@ __global__ void k_raw1_scatter(const uint32_t* rows, const uint32_t* raw_pos, ui
 
 // Sharded solve: tie-break by the global raw-byte rank (rv, per global dense
 // index): per tie group the entry with the smallest (raw rank, vid).
-__global__ void k_tie_min_raw(const WorkItem* __restrict__ work, const ScanSlot* __restrict__ slots,
+__global__ void k_tie_min_raw(const WorkSeg* __restrict__ work, uint32_t nwseg, const ScanSlot* __restrict__ slots,
                               const uint32_t* __restrict__ masks,
                               const uint32_t* __restrict__ weights,
                               const uint64_t* __restrict__ colbase,
@@ -376,7 +402,7 @@ __global__ void k_tie_min_raw(const WorkItem* __restrict__ work, const ScanSlot*
                               const Cand* __restrict__ best, const int32_t* __restrict__ tie_group,
                               const uint32_t* __restrict__ rv, unsigned long long* minkey,
                               uint32_t part, uint32_t nparts) {
-  const WorkItem w = work[blockIdx.x];
+  const WorkItem w = work_at(work, nwseg);
   const int32_t g = tie_group[w.slot];
   if (g < 0) return;
   const ScanSlot sl = slots[w.slot];
@@ -546,15 +572,30 @@ __global__ void k_relabel(uint32_t* node_of_row, uint64_t n, const int32_t* spli
 // K4 group_hist: block-row aggregation into the block child's table and
 // decrement of the parent's table (inherited by the rest child)
 // ---------------------------------------------------------------------------
-struct AggTask {
+// One (split, column) pair of a level's aggregation: the block rows [lo, hi)
+// of the split's segment, cut into kAggRows-row tasks; first = the task
+// number of its first task (exclusive prefix over the level's segments).
+struct AggSeg {
   uint32_t split;  // index into this level's SplitD array
   uint32_t col;
   uint32_t to_b;   // add into the block child's table (col is one of its columns)
   uint32_t to_p;   // subtract from the parent's table (kept by the rest child)
-  uint64_t lo, hi; // block-row range [lo, hi) of the split's segment
+  uint64_t lo, hi;
+  uint32_t first, pad;
 };
 
 constexpr int kAggBlock = 256;
+constexpr uint64_t kAggRows = 2 * kAggBlock;
+
+// Host: append (split, col) over rows [lo, hi); returns the tasks added.
+inline uint32_t add_agg_seg(std::vector<AggSeg>& v, uint32_t& ntask, uint32_t split, uint32_t col,
+                            uint32_t to_b, uint32_t to_p, uint64_t lo, uint64_t hi) {
+  if (hi <= lo) return 0;
+  const uint32_t t = uint32_t((hi - lo + kAggRows - 1) / kAggRows);
+  v.push_back(AggSeg{split, col, to_b, to_p, lo, hi, ntask, 0});
+  ntask += t;
+  return t;
+}
 
 // One block per (split, column, row range). Lanes of a warp hold consecutive
 // block rows of ONE column, so equal values inside a warp are merged with
@@ -562,11 +603,35 @@ constexpr int kAggBlock = 256;
 // (low-cardinality columns and the split column itself collapse to one
 // atomic per warp).
 __global__ void __launch_bounds__(kAggBlock) k_aggregate(
-    const AggTask* __restrict__ tasks, const uint32_t* __restrict__ blockrows,
+    const AggSeg* __restrict__ segs, uint32_t nseg, const uint32_t* __restrict__ blockrows,
     const SplitD* __restrict__ sp, const uint32_t* __restrict__ vid,
     const uint64_t* __restrict__ vlen, const uint64_t* __restrict__ colbase, uint32_t m,
     uint32_t K, const int32_t* __restrict__ dpart, const uint32_t* __restrict__ npart) {
-  const AggTask tk = tasks[blockIdx.x];
+  // this block's task: the last segment with first <= blockIdx.x
+  __shared__ uint32_t s_seg;
+  if (threadIdx.x == 0) {
+    uint32_t lo = 0, hi = nseg - 1;
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi + 1) / 2;
+      if (segs[mid].first <= blockIdx.x) lo = mid;
+      else hi = mid - 1;
+    }
+    s_seg = lo;
+  }
+  __syncthreads();
+  struct {
+    uint32_t split, col, to_b, to_p;
+    uint64_t lo, hi;
+  } tk;
+  {
+    const AggSeg& g = segs[s_seg];
+    tk.split = g.split;
+    tk.col = g.col;
+    tk.to_b = g.to_b;
+    tk.to_p = g.to_p;
+    tk.lo = g.lo + uint64_t(blockIdx.x - g.first) * kAggRows;
+    tk.hi = tk.lo + kAggRows < g.hi ? tk.lo + kAggRows : g.hi;
+  }
   const SplitD& d = sp[tk.split];
   const uint32_t c = tk.col;
   const uint32_t np = npart[c];
@@ -699,11 +764,11 @@ __global__ void k_root_psum(const uint32_t* vid, uint64_t n, uint32_t m, uint32_
 // K7 leaf_stats: per (leaf, column) distinct count and length sum
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_leaf_stats(
-    const WorkItem* work, const ScanSlot* slots, const uint32_t* masks, const uint64_t* colbase,
+    const WorkSeg* work, uint32_t nwseg, const ScanSlot* slots, const uint32_t* masks, const uint64_t* colbase,
     const uint64_t* vlen, uint32_t m, unsigned long long* card, unsigned long long* tot,
     uint32_t part, uint32_t nparts) {
   extern __shared__ unsigned long long sh[];  // [2*m] for hashed tables with small m
-  const WorkItem w = work[blockIdx.x];
+  const WorkItem w = work_at(work, nwseg);
   const ScanSlot sl = slots[w.slot];
   if (item_skipped(sl.t, part, nparts)) return;  // sharded: dealt to another rank
   const uint32_t* mask = masks + sl.mask_off;
@@ -858,7 +923,6 @@ int classify(const Node& nd, const po_ggr_config& cfg) {
   return SCAN;
 }
 
-constexpr uint64_t kWorkChunk = 2048;
 
 bool debug_checks() {
   static const bool on = [] {
@@ -872,7 +936,8 @@ struct Level {
   std::vector<ScanSlot> slots;
   std::vector<uint32_t> masks;
   std::vector<uint32_t> weights;
-  std::vector<WorkItem> work;
+  std::vector<WorkSeg> work;
+  uint32_t nitems = 0;  // work items (blocks) over all segments
   std::vector<uint32_t> slot_work_off{0};
 };
 
@@ -967,15 +1032,16 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
 
   // Work items over a node's table: dense tables are cut at column
   // boundaries (only the node's active columns), hashed ones in plain chunks.
-  auto add_work = [&](std::vector<WorkItem>& work, uint32_t slot, const HTable& t,
-                      const std::vector<int>& cols) {
+  auto add_work = [&](Level& lv, uint32_t slot, const HTable& t, const std::vector<int>& cols) {
+    auto seg = [&](uint32_t col, uint64_t lo, uint64_t hi) {
+      if (hi <= lo) return;
+      lv.work.push_back(WorkSeg{slot, col, lo, hi, lv.nitems, 0});
+      lv.nitems += uint32_t((hi - lo + kWorkChunk - 1) / kWorkChunk);
+    };
     if (t.dense) {
-      for (int c : cols)
-        for (uint64_t lo = e.colbase[c]; lo < e.colbase[c + 1]; lo += kWorkChunk)
-          work.push_back(WorkItem{slot, uint32_t(c), lo, std::min(e.colbase[c + 1], lo + kWorkChunk)});
+      for (int c : cols) seg(uint32_t(c), e.colbase[c], e.colbase[c + 1]);
     } else {
-      for (uint64_t lo = 0; lo < t.cap; lo += kWorkChunk)
-        work.push_back(WorkItem{slot, kAnyCol, lo, std::min(t.cap, lo + kWorkChunk)});
+      seg(kAnyCol, 0, t.cap);
     }
   };
   auto col_mask = [&](const std::vector<int>& cols, std::vector<uint32_t>& dst) {
@@ -1047,6 +1113,7 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
   while (!frontier.empty() || !pending.empty()) {
     // ---- one GPU pass per level: K5 argmax over the frontier, K7 leaf
     // statistics of the leaves created by the previous level, one D2H ----
+    std::optional<HostScope> hs_build(std::in_place, "lvl_build");
     Level L, S;
     std::vector<uint64_t> unique_groups(frontier.size(), 0);
     for (size_t i = 0; i < frontier.size(); ++i) {
@@ -1070,8 +1137,8 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
         for (size_t k = 0; k < dpart[c].size(); ++k)
           if (act[dpart[c][k]]) L.weights[sl.w_off + c * K + k] = dmult[c][k];
       L.slots.push_back(sl);
-      add_work(L.work, uint32_t(i), *nd.table, scan_cols);
-      L.slot_work_off.push_back(uint32_t(L.work.size()));
+      add_work(L, uint32_t(i), *nd.table, scan_cols);
+      L.slot_work_off.push_back(L.nitems);
     }
     for (size_t i = 0; i < pending.size(); ++i) {
       const Node& nd = nodes[pending[i]];
@@ -1080,7 +1147,7 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
       sl.mask_off = col_mask(nd.cols, S.masks);
       sl.w_off = 0;
       S.slots.push_back(sl);
-      add_work(S.work, uint32_t(i), *nd.table, nd.cols);
+      add_work(S, uint32_t(i), *nd.table, nd.cols);
     }
     const uint32_t nslots = uint32_t(L.slots.size());
     const size_t nleaf = pending.size();
@@ -1089,8 +1156,8 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
     const size_t o_work = pk.add(L.work), o_swo = pk.add(L.slot_work_off);
     const size_t o_sslots = pk.add(S.slots), o_smasks = pk.add(S.masks), o_swork = pk.add(S.work);
     uint8_t* dp = upload(pk);
-    grow(partial, std::max<size_t>(1, L.work.size()));
-    grow(pcands, std::max<size_t>(1, L.work.size()));
+    grow(partial, std::max<size_t>(1, L.nitems));
+    grow(pcands, std::max<size_t>(1, L.nitems));
     // results: [best Cand x nslots][ncand u64 x nslots][card u64 x nleaf*m][tot u64 x nleaf*m]
     const size_t res_bytes = nslots * (sizeof(Cand) + 8) + 2 * nleaf * m * 8;
     grow(res, std::max<size_t>(16, res_bytes));
@@ -1099,6 +1166,7 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
     auto* d_card = d_ncand + nslots;
     auto* d_tot = d_card + nleaf * m;
     if (nleaf) PO_CUDA(cudaMemsetAsync(d_card, 0, 2 * nleaf * m * 8, s));
+    hs_build.reset();
     // sharded solve: every rank scans its share of the replicated tables'
     // work items; results merged across ranks below
     static const bool partition = [] {  // PO_DIST_PARTITION=0: every rank scans everything
@@ -1108,16 +1176,16 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
     const uint32_t nparts = dist && partition ? uint32_t(dist->comm->size()) : 1u;
     const uint32_t part = dist && partition ? uint32_t(dist->comm->rank()) : 0u;
     if (nslots) {
-      PO_LAUNCH(k_argmax, unsigned(L.work.size()), kArgBlock, 0, s,
-                reinterpret_cast<WorkItem*>(dp + o_work), reinterpret_cast<ScanSlot*>(dp + o_slots),
+      PO_LAUNCH(k_argmax, L.nitems, kArgBlock, 0, s,
+                reinterpret_cast<WorkSeg*>(dp + o_work), uint32_t(L.work.size()), reinterpret_cast<ScanSlot*>(dp + o_slots),
                 reinterpret_cast<uint32_t*>(dp + o_masks), reinterpret_cast<uint32_t*>(dp + o_w),
                 colbase, vlen, m, K, partial.get(), pcands.get(), part, nparts);
       PO_LAUNCH(k_argmax_final, nslots, kArgBlock, 0, s, partial.get(), pcands.get(),
                 reinterpret_cast<uint32_t*>(dp + o_swo), d_best, d_ncand);
     }
     if (nleaf)
-      PO_LAUNCH(k_leaf_stats, unsigned(S.work.size()), 256, m <= 2048 ? 16 * m : 0, s,
-                reinterpret_cast<WorkItem*>(dp + o_swork), reinterpret_cast<ScanSlot*>(dp + o_sslots),
+      PO_LAUNCH(k_leaf_stats, S.nitems, 256, m <= 2048 ? 16 * m : 0, s,
+                reinterpret_cast<WorkSeg*>(dp + o_swork), uint32_t(S.work.size()), reinterpret_cast<ScanSlot*>(dp + o_sslots),
                 reinterpret_cast<uint32_t*>(dp + o_smasks), colbase, vlen, m, d_card, d_tot, part,
                 nparts);
     if (nparts > 1) {
@@ -1133,8 +1201,7 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
       if (nleaf) dist->comm->allreduce(d_card, 2 * nleaf * m, CDtype::U64, COp::Sum, s);
     }
     std::vector<uint8_t> hres(std::max<size_t>(16, res_bytes));
-    res.download(hres.data(), res_bytes);  // pageable D2H: returns when complete
-    sync(s);
+    d2h_sync(hres.data(), res.get(), res_bytes, s);
     std::vector<Cand> hbest(nslots);
     if (nslots) std::memcpy(hbest.data(), hres.data(), nslots * sizeof(Cand));
     const unsigned long long* hn =
@@ -1163,8 +1230,8 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
         auto d_tg = to_device(tie_group, s);
         DevBuf<unsigned long long> mk(nt, s);
         mk.fill_bytes(0xFF);
-        PO_LAUNCH(k_tie_min_raw, unsigned(L.work.size()), kArgBlock, 0, s,
-                  reinterpret_cast<WorkItem*>(dp + o_work), reinterpret_cast<ScanSlot*>(dp + o_slots),
+        PO_LAUNCH(k_tie_min_raw, L.nitems, kArgBlock, 0, s,
+                  reinterpret_cast<WorkSeg*>(dp + o_work), uint32_t(L.work.size()), reinterpret_cast<ScanSlot*>(dp + o_slots),
                   reinterpret_cast<uint32_t*>(dp + o_masks), reinterpret_cast<uint32_t*>(dp + o_w),
                   colbase, vlen, m, K, d_best, d_tg.get(), rv, mk.get(), part, nparts);
         if (nparts > 1) {  // min over the ranks' shares = ~max(~x)
@@ -1173,8 +1240,7 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
           PO_LAUNCH(k_complement_u64, grid_for(nt, 128), 128, 0, s, mk.get(), nt);
         }
         std::vector<unsigned long long> hm(nt);
-        mk.download(hm.data(), nt);
-        sync(s);
+        d2h_sync(hm.data(), mk.get(), (nt) * sizeof(*mk.get()), s);
         for (uint32_t g = 0; g < nt; ++g) hbest[tie_slot[g]].vid = uint32_t(hm[g]);
       } else if (!tie_slot.empty()) {
         const uint32_t ng = uint32_t(tie_slot.size()), total = tie_off.back();
@@ -1183,8 +1249,8 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
         DevBuf<uint32_t> cursor(ng, s), t_ref(total, s), t_vid(total, s), t_grp(total, s),
             t_pos(total, s), min_vid(ng, s);
         cursor.zero();
-        PO_LAUNCH(k_collect_ties, unsigned(L.work.size()), kArgBlock, 0, s,
-                  reinterpret_cast<WorkItem*>(dp + o_work), reinterpret_cast<ScanSlot*>(dp + o_slots),
+        PO_LAUNCH(k_collect_ties, L.nitems, kArgBlock, 0, s,
+                  reinterpret_cast<WorkSeg*>(dp + o_work), uint32_t(L.work.size()), reinterpret_cast<ScanSlot*>(dp + o_slots),
                   reinterpret_cast<uint32_t*>(dp + o_masks), reinterpret_cast<uint32_t*>(dp + o_w),
                   colbase, vlen, m, K, d_best, d_tg.get(), d_toff.get(), cursor.get(),
                   t_ref.get(), t_vid.get(), t_grp.get());
@@ -1205,13 +1271,13 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
         PO_LAUNCH(k_pick_min, grid_for(total, 256), 256, 0, s, t_pos.get(), t_grp.get(),
                   t_vid.get(), d_toff.get(), total, min_vid.get());
         std::vector<uint32_t> hmin(ng);
-        min_vid.download(hmin.data(), ng);
-        sync(s);
+        d2h_sync(hmin.data(), min_vid.get(), (ng) * sizeof(*min_vid.get()), s);
         for (uint32_t g = 0; g < ng; ++g) hbest[tie_slot[g]].vid = hmin[g];
       }
     }
 
     // ---- host decisions (ggr.hpp:276-301) ----
+    std::optional<HostScope> hs_dec(std::in_place, "lvl_decide");
     std::vector<int> next;
     struct SplitH {
       int node;
@@ -1226,7 +1292,7 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
         st += hbest[i].ties;
       }
       fprintf(stderr, "[po level] rank %d slots %u work %zu cands %llu ties %llu\n",
-              dist ? dist->comm->rank() : 0, nslots, L.work.size(), sh, st);
+              dist ? dist->comm->rank() : 0, nslots, size_t(L.nitems), sh, st);
     }
     for (uint32_t i = 0; i < nslots; ++i) {
       const int id = frontier[i];
@@ -1299,7 +1365,9 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
       }
     }
 
+    hs_dec.reset();
     alloc_tables(new_tables, K, s);
+    HostScope hs_split("lvl_split");
     for (SplitH& sh : splits)
       if (nodes[sh.d.block_id].table) sh.d.tB = nodes[sh.d.block_id].table->desc();
 
@@ -1311,8 +1379,8 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
       std::vector<SplitD> hsp(ns);
       std::vector<uint64_t> seg(ns + 1, 0);
       std::vector<uint32_t> split_nodes(ns);
-      std::vector<AggTask> tasks;
-      constexpr uint64_t kRowsPerTask = 2 * kAggBlock;
+      std::vector<AggSeg> tasks;
+      uint32_t ntask = 0;
       for (uint32_t j = 0; j < ns; ++j) {
         hsp[j] = splits[j].d;
         split_nodes[j] = uint32_t(splits[j].node);
@@ -1327,9 +1395,7 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
           const uint32_t to_b = (hsp[j].tB.keys && inB[c]) ? 1u : 0u;
           const uint32_t to_p = hsp[j].tP.cnt ? 1u : 0u;
           if (!to_b && !to_p) continue;
-          for (uint64_t lo = seg[j]; lo < seg[j + 1]; lo += kRowsPerTask)
-            tasks.push_back(AggTask{j, uint32_t(c), to_b, to_p, lo,
-                                    std::min(seg[j + 1], lo + kRowsPerTask)});
+          add_agg_seg(tasks, ntask, j, uint32_t(c), to_b, to_p, seg[j], seg[j + 1]);
         }
       }
       // dense node -> split index table over this level's node id range
@@ -1352,8 +1418,8 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
                 node_of_row.get(), n, d_lut, node_lo, lut_n, d_sp, e.vid.get(), m, d_cursor,
                 d_seg, blockrows.get());
       if (!dist && !tasks.empty())
-        PO_LAUNCH(k_aggregate, unsigned(tasks.size()), kAggBlock, 0, s,
-                  reinterpret_cast<AggTask*>(ds + o_tasks), blockrows.get(), d_sp, e.vid.get(),
+        PO_LAUNCH(k_aggregate, ntask, kAggBlock, 0, s, reinterpret_cast<AggSeg*>(ds + o_tasks),
+                  uint32_t(tasks.size()), blockrows.get(), d_sp, e.vid.get(),
                   vlen, colbase, m, K, d_dpart.get(), d_npart.get());
       if (dist) {
         // this rank's block rows -> private tables -> contributions, all-gathered
@@ -1363,7 +1429,8 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
         sync(s);
         std::vector<std::unique_ptr<HTable>> priv(ns);
         std::vector<SplitD> hsp2(hsp);
-        std::vector<AggTask> tasks2;
+        std::vector<AggSeg> tasks2;
+        uint32_t ntask2 = 0;
         std::vector<uint32_t> bmask(size_t(ns) * W, 0);
         uint64_t max_entries = 0;
         for (uint32_t j = 0; j < ns; ++j) {
@@ -1382,17 +1449,16 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
           priv[j] = std::move(t);
           max_entries += bound;
           for (int c : P.cols)
-            for (uint64_t lo = seg[j]; lo < seg[j] + lcnt[j]; lo += kRowsPerTask)
-              tasks2.push_back(AggTask{j, uint32_t(c), 1u, 0u, lo,
-                                       std::min<uint64_t>(seg[j] + lcnt[j], lo + kRowsPerTask)});
+            add_agg_seg(tasks2, ntask2, j, uint32_t(c), 1u, 0u, seg[j], seg[j] + lcnt[j]);
         }
         Pack p2;
         const size_t o_sp2 = p2.add(hsp2), o_t2 = p2.add(tasks2), o_bm = p2.add(bmask);
         DevBuf<uint8_t> dev2(p2.host.size(), s);
         dev2.upload(p2.host.data(), p2.host.size());
         if (!tasks2.empty())
-          PO_LAUNCH(k_aggregate, unsigned(tasks2.size()), kAggBlock, 0, s,
-                    reinterpret_cast<AggTask*>(dev2.get() + o_t2), blockrows.get(),
+          PO_LAUNCH(k_aggregate, ntask2, kAggBlock, 0, s,
+                    reinterpret_cast<AggSeg*>(dev2.get() + o_t2), uint32_t(tasks2.size()),
+                    blockrows.get(),
                     reinterpret_cast<SplitD*>(dev2.get() + o_sp2), e.vid.get(), vlen, colbase, m,
                     K, d_dpart.get(), d_npart.get());
         const uint32_t RW = 2 + K;
@@ -1404,8 +1470,7 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
             PO_LAUNCH(k_compact_contrib, grid_for(priv[j]->cap, 256), 256, 0, s, priv[j]->desc(), j,
                       K, contrib.get(), ccur.get());
         unsigned long long El = 0;
-        ccur.download(&El, 1);
-        sync(s);
+        d2h_sync(&El, ccur.get(), (1) * sizeof(*ccur.get()), s);
         priv.clear();
         const std::vector<uint64_t> Es = dist->comm->allgather_host({uint64_t(El)}, s);
         std::vector<uint64_t> rbytes(Es.size());
@@ -1427,8 +1492,7 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
       PO_LAUNCH(k_dbg_node_hist, grid_for(n, 256), 256, 0, s, node_of_row.get(), n,
                 uint32_t(nodes.size()), hist.get());
       std::vector<unsigned long long> hh(nodes.size() + 1);
-      hist.download(hh.data(), hh.size());
-      sync(s);
+      d2h_sync(hh.data(), hist.get(), (hh.size()) * sizeof(*hist.get()), s);
       for (size_t id = 0; id < nodes.size(); ++id) {
         const Node& nd = nodes[id];
         const bool live = nd.kind != SPLIT;
@@ -1655,8 +1719,7 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
     PO_CUDA(cub::DeviceSelect::Flagged(tmp.get(), tb, it, flags.get(), raw_rows.get(), nsel.get(),
                                        int(n), s));
     int hn1 = 0;
-    nsel.download(&hn1, 1);
-    sync(s);
+    d2h_sync(&hn1, nsel.get(), (1) * sizeof(*nsel.get()), s);
     n_raw = uint32_t(hn1);
     raw_grp.alloc(n_raw, s);
     raw_col.alloc(n_raw, s);
@@ -1694,8 +1757,7 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
     bad.zero();
     PO_LAUNCH(k_dbg_perm, grid_for(n, 256), 256, 0, s, pos.get(), n, seen.get(), bad.get());
     unsigned long long hb = 0;
-    bad.download(&hb, 1);
-    sync(s);
+    d2h_sync(&hb, bad.get(), (1) * sizeof(*bad.get()), s);
     if (hb) fprintf(stderr, "[po debug] leaf sort positions: %llu collisions/out of range\n", hb);
   }
   PO_LAUNCH(k_emit, grid_for(n, 256), 256, 0, s, pos.get(), n, d_rows);

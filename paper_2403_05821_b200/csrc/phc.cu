@@ -92,8 +92,7 @@ uint64_t phc_device_raw(const uint32_t* vid, const uint64_t* vlen, const uint64_
   unsigned long long h = 0;
   int herr = 0;
   tot.download(&h, 1);
-  err.download(&herr, 1);
-  sync(s);
+  d2h_sync(&herr, err.get(), (1) * sizeof(*err.get()), s);
   if (herr) fail(PO_ERR_OUT_OF_RANGE, "schedule references a row or field outside the table");
   return h;
 }
@@ -225,8 +224,7 @@ bool fallback_cannot_win(const Encoded& e, uint64_t phc, cudaStream_t s) {
   PO_LAUNCH(k_fb_bound, grid_for(e.D, 256, 4), 256, 0, s, e.count.get(), e.vlen.get(), e.D,
             acc.get());
   double ub = 0;
-  acc.download(&ub, 1);
-  sync(s);
+  d2h_sync(&ub, acc.get(), (1) * sizeof(*acc.get()), s);
   const double ub_hi = ub * (1.0 + 1e-9) + 1.0;
   return ub_hi < 1.8e19 && ub_hi < double(phc) * (1.0 - 1e-15);
 }
@@ -263,8 +261,7 @@ uint64_t fixed_order_phc_device(const Encoded& e, const std::vector<int>& order,
     }
   }
   unsigned long long h = 0;
-  acc.download(&h, 1);
-  sync(s);
+  d2h_sync(&h, acc.get(), (1) * sizeof(*acc.get()), s);
   return h;
 }
 
