@@ -11,6 +11,7 @@ from this package.
 from __future__ import annotations
 
 import ctypes as C
+import re
 import os
 from pathlib import Path
 
@@ -206,14 +207,22 @@ class CudaLib:
         self.profile_enable = _bind(L, "po_profile_enable", None, [C.c_int])
         self._profile_report = _bind(L, "po_profile_report", C.c_uint64, [C.c_char_p, C.c_uint64])
 
-    def profile_report(self) -> dict:
-        """{kernel name: (launches, total ms)} since the last report."""
+    def profile_report(self, raw: bool = False) -> dict:
+        """{kernel name: (launches, total ms)} since the last report. Template
+        launches are reported under the kernel's name ("(k<6, 4>)" -> "k").
+        raw=True keeps the names as recorded and adds the "gap:<launch>"
+        (device idle before a launch) and "host:<section>" entries."""
         buf = C.create_string_buffer(1 << 16)
         self._profile_report(buf, len(buf))
         out = {}
         for line in buf.value.decode().splitlines():
             name, cnt, ms = line.rsplit(" ", 2)
-            out[name] = (int(cnt), float(ms))
+            if not raw:
+                if name.startswith(("gap:", "host:")):
+                    continue
+                name = re.sub(r"^\((\w+)<.*>\)$", r"\1", name)
+            c0, m0 = out.get(name, (0, 0.0))
+            out[name] = (c0 + int(cnt), m0 + float(ms))
         return out
 
     def check(self, code: int) -> None:

@@ -507,6 +507,7 @@ constexpr uint32_t kPending = 0x80000000u;  // cid_mat: found, not yet verified
 // Cell hash of (row r, column c) of the chunk (thread per cell): the last
 // aligned word of a step is the first of the next, carried (four loads per
 // four words).
+template <int STEP = 4>
 __device__ __forceinline__ uint64_t cell_hash(const uint8_t* __restrict__ chunk, uint64_t base,
                                               const uint64_t* lim, uint64_t o0, uint64_t len,
                                               uint64_t hash_mask) {
@@ -516,14 +517,14 @@ __device__ __forceinline__ uint64_t cell_hash(const uint8_t* __restrict__ chunk,
   const uint64_t words = (len + 7) / 8;
   uint64_t sum = 0;
   uint64_t carry = (words && p < lim) ? __ldg(p) : 0;
-  for (uint64_t k = 0; k < words; k += 4) {
-    uint64_t w[5];
+  for (uint64_t k = 0; k < words; k += STEP) {
+    uint64_t w[STEP + 1];
     w[0] = carry;
 #pragma unroll
-    for (int u = 1; u < 5; ++u) w[u] = (p + k + u < lim) ? __ldg(p + k + u) : 0;
-    carry = w[4];
+    for (int u = 1; u < STEP + 1; ++u) w[u] = (p + k + u < lim) ? __ldg(p + k + u) : 0;
+    carry = w[STEP];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < STEP; ++u) {
       const uint64_t kk = k + u;
       if (kk < words) {
         uint64_t x = funnel(w[u], w[u + 1], sh);
@@ -585,7 +586,8 @@ __device__ __forceinline__ bool warp_equal(const uint8_t* a, const uint8_t* a_li
 // warp; a lane meeting its hash in a slot whose id is not yet visible
 // retries it next round). Claimed cells get their new id, found cells the
 // slot's id marked pending (byte verification follows).
-__global__ void __launch_bounds__(256) k_hash_probe(const uint8_t* __restrict__ chunk, uint64_t base,
+template <int MINB, int STEP>
+__global__ void __launch_bounds__(256, MINB) k_hash_probe(const uint8_t* __restrict__ chunk, uint64_t base,
                                                     const uint8_t* chunk_lim,
                                                     const uint64_t* __restrict__ offs, uint64_t rows,
                                                     uint64_t r0, uint32_t m, uint64_t hash_mask,
@@ -611,7 +613,7 @@ __global__ void __launch_bounds__(256) k_hash_probe(const uint8_t* __restrict__ 
       // cells of at least long_min bytes are hashed by the whole warp
       // (coalesced), the others by their own lane
       const bool coop = search && len >= long_min;
-      if (search && !coop) h = cell_hash(chunk, base, lim, o0, len, hash_mask);
+      if (search && !coop) h = cell_hash<STEP>(chunk, base, lim, o0, len, hash_mask);
       for (unsigned lm = __ballot_sync(kFull, coop); lm; lm &= lm - 1) {
         const int src = __ffs(lm) - 1;
         const uint64_t so = __shfl_sync(kFull, o0, src), sl = __shfl_sync(kFull, len, src);
@@ -697,7 +699,8 @@ __device__ __forceinline__ void rep_loc(const ColDict& D, uint32_t id, const Bui
   rlim = in_vals ? A.vals_lim : A.chunk_lim;
 }
 
-__global__ void __launch_bounds__(256) k_verify_cells(BuildArgs A, uint32_t* collided,
+template <int MINB>
+__global__ void __launch_bounds__(256, MINB) k_verify_cells(BuildArgs A, uint32_t* collided,
                                                       uint32_t* n_collided, uint64_t long_min) {
   // warps take 32 rows of one column (similar lengths); a lane compares its
   // own cell with its value's representative, cells of at least long_min
@@ -1006,6 +1009,7 @@ class Builder {
   }
 
   void init_counts() { count_.assign(m_, 0); }
+  void set_avg_cell_bytes(double v) { avg_cell_bytes_ = v; }
 
   // one chunk of rows [r0, r1), retried with grown tables until no column
   // overflows; leaves count_ = the per-column distinct counts
@@ -1061,9 +1065,16 @@ class Builder {
           const char* v = std::getenv("PO_LONG_CELL");
           return v && *v ? uint64_t(std::strtoull(v, nullptr, 10)) : uint64_t(1024);
         }();
-        PO_LAUNCH(k_hash_probe, gw, 256, 0, s_, chunk, base, chunk_lim, offs, r1 - r0, r0, m_, hmask_,
-                  d_cols_.get(), ncid(), over(), cid_mat, long_min);
-        PO_LAUNCH(k_verify_cells, gw, 256, 0, s_, A, collided_.get(), ncol.get(), long_min);
+        // occupancy (measured, tools/probe_shape_sweep.sh): the probe at 6
+        // blocks per SM (40 registers); the verify at 4, or at 8 when the cells
+        // average at least long_min bytes (they take the whole-warp compare,
+        // which needs few registers: C5 verify 10.8 -> 8.1 ms per 3M rows)
+        PO_LAUNCH((k_hash_probe<6, 4>), gw, 256, 0, s_, chunk, base, chunk_lim, offs, r1 - r0, r0, m_,
+                  hmask_, d_cols_.get(), ncid(), over(), cid_mat, long_min);
+        if (avg_cell_bytes_ >= double(long_min))
+          PO_LAUNCH((k_verify_cells<8>), gw, 256, 0, s_, A, collided_.get(), ncol.get(), long_min);
+        else
+          PO_LAUNCH((k_verify_cells<4>), gw, 256, 0, s_, A, collided_.get(), ncol.get(), long_min);
         PO_LAUNCH(k_fixup_cells, kSMs, 128, 0, s_, A, collided_.get(), ncol.get());
       }
       std::vector<uint32_t> hc(2 * m_);
@@ -1115,6 +1126,7 @@ class Builder {
   std::vector<ColDict> h_;
   DevBuf<uint32_t> cnt2_;  // [new ids per column][overflow flags per column]
   DevBuf<uint8_t> shared_;  // reserve_all's arrays of every column
+  double avg_cell_bytes_ = 0;
   uint32_t* ncid() { return cnt2_.get(); }
   uint32_t* over() { return cnt2_.get() + m_; }
   DevBuf<ColDict> d_cols_;
@@ -1231,6 +1243,7 @@ void build_dictionary(const DeviceTable& t, uint32_t hash_bits, cudaStream_t s, 
   const uint64_t hmask = hash_bits >= 64 ? ~uint64_t(0) : ((uint64_t(1) << hash_bits) - 1);
   Builder B(n, uint32_t(m), hmask, s);
   B.init_counts();
+  B.set_avg_cell_bytes(double(t.arena_bytes) / double(cells));
   const bool streamed = t.h_arena != nullptr;
   const uint64_t* h_offs = streamed ? t.h_offsets : nullptr;
 

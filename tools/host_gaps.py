@@ -35,7 +35,7 @@ for i in range(reps):
     torch.cuda.synchronize()
     po.ggr_into(dv, fd, po.GgrConfig(), 0, 0, PO_LOC_DEVICE, r_, o_, 0)
     torch.cuda.synchronize()
-rep = lib.profile_report()
+rep = lib.profile_report(raw=True)
 lib.profile_enable(0)
 gaps = {k[4:]: v for k, v in rep.items() if k.startswith("gap:")}
 tot = sum(v[1] for v in gaps.values()) / reps

@@ -31,7 +31,7 @@ for i in range(reps):
     print(f"call {i}: {(time.perf_counter() - t0) * 1e3:.1f} ms (wall_ms {st.wall_ms:.1f}) "
           f"free {torch.cuda.mem_get_info()[0] / 1e9:.1f} GB", flush=True)
     if prof:
-        rep = lib.profile_report()
+        rep = {k: v for k, v in lib.profile_report().items() if not k.startswith(("gap:", "host:"))}
         top = sorted(rep.items(), key=lambda x: -x[1][1])[:int(sys.argv[4]) if sys.argv[4].isdigit() else 4]
         print("   kernels %.3f ms; top: %s" % (sum(v[1] for v in rep.values()),
-              ", ".join(f"{k} {v[0]}x {v[1]:.3f}" for k, v in top)), flush=True)
+              " | ".join(f"{k} {v[0]}x {v[1]:.3f}" for k, v in top)), flush=True)
