@@ -311,9 +311,11 @@ def run_ours(args):
     prof = lib.profile_report()
     lib.profile_enable(0)
     prof_steps = max(args.prof_steps, 1)
-    kern = sorted(((v[1] / prof_steps, k, v[0] / prof_steps) for k, v in prof.items()),
-                  reverse=True)
-    total_kernel_ms = sum(x[0] for x in kern)
+    # leaf launches only ("scope:" entries wrap other launches); the total is
+    # the device time under any launch ("busy:", the union of the intervals)
+    kern = sorted(((v[1] / prof_steps, k, v[0] / prof_steps) for k, v in prof.items()
+                   if not k.startswith(("scope:", "busy:"))), reverse=True)
+    total_kernel_ms = prof.get("busy:", (1, sum(x[0] for x in kern) * prof_steps))[1] / prof_steps
     for ms_k, k, cnt in kern[:12]:
         log(f"   {k:28s} {ms_k:8.3f} ms/step  {cnt:6.1f} launches  "
             f"({100*ms_k/max(total_kernel_ms,1e-9):5.1f}% of kernel time)")

@@ -210,8 +210,10 @@ class CudaLib:
     def profile_report(self, raw: bool = False) -> dict:
         """{kernel name: (launches, total ms)} since the last report. Template
         launches are reported under the kernel's name ("(k<6, 4>)" -> "k").
-        raw=True keeps the names as recorded and adds the "gap:<launch>"
-        (device idle before a launch) and "host:<section>" entries."""
+        "scope:<name>" entries wrap other launches (a sort, a library call);
+        "busy:" is the device time under any launch (their union). raw=True
+        keeps the names as recorded and adds the "gap:<launch>" (device idle
+        before a launch) and "host:<section>" entries."""
         buf = C.create_string_buffer(1 << 16)
         self._profile_report(buf, len(buf))
         out = {}

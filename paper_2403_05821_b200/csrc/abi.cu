@@ -59,19 +59,31 @@ void prof_drain() {  // caller holds g_prof_mu
     PO_CUDA(cudaEventElapsedTime(&ms, r.a, r.b));
     PO_CUDA(cudaEventElapsedTime(&a, g_prof_pending.front().a, r.a));
     iv.push_back({a, a + ms, r.name});
-    auto& acc = g_prof_acc[r.name];
-    acc.first += 1;
-    acc.second += ms;
   }
   std::stable_sort(iv.begin(), iv.end(), [](const Iv& x, const Iv& y) { return x.a < y.a; });
-  float covered = iv.empty() ? 0.f : iv.front().a;
+  // a scope whose interval holds the next launch wraps other launches (a
+  // library call or a multi-kernel sort): reported as "scope:<name>" so that
+  // sums over kernels do not count its children twice
+  for (size_t i = 0; i < iv.size(); ++i) {
+    const bool outer = i + 1 < iv.size() && iv[i + 1].a < iv[i].b - 0.0005f;
+    auto& acc = g_prof_acc[outer ? std::string("scope:") + iv[i].name : std::string(iv[i].name)];
+    acc.first += 1;
+    acc.second += iv[i].b - iv[i].a;
+  }
+  float covered = iv.empty() ? 0.f : iv.front().a, busy = 0.f;
   for (const Iv& x : iv) {
     if (x.a > covered + 0.002f) {
       auto& acc = g_prof_acc[std::string("gap:") + x.name];
       acc.first += 1;
       acc.second += x.a - covered;
     }
+    if (x.b > covered) busy += x.b - std::max(x.a, covered);
     covered = std::max(covered, x.b);
+  }
+  if (!iv.empty()) {  // device time under any recorded launch (union of the intervals)
+    auto& acc = g_prof_acc["busy:"];
+    acc.first += 1;
+    acc.second += busy;
   }
   for (auto& r : g_prof_pending) {
     g_prof_free.push_back(r.a);

@@ -1,0 +1,15 @@
+# Round evidence on one B200: GPU suite, smoke, bench line, launch list and
+# the --set full capture of the two dictionary kernels (outputs in gpurun_out/).
+set -u
+TAG=${TAG:-r2b}
+timeout 2400 python -m pytest tests -q -m gpu > gpurun_out/${TAG}_gputest.log 2>&1
+echo "pytest rc=$?" >> gpurun_out/${TAG}_gputest.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" >> gpurun_out/${TAG}_gputest.log 2>&1
+timeout 1200 python bench.py > gpurun_out/${TAG}_bench.json 2> gpurun_out/${TAG}_bench.err
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+  --log-file gpurun_out/${TAG}_launches.csv python bench.py --steps 2 --warmup 1 --no-cpu --prof-steps 0 \
+  > /dev/null 2>&1
+timeout 900 ncu --set full --import-source on --clock-control none \
+  -k 'regex:k_hash_probe|k_verify_cells' -s 2 -c 2 -o gpurun_out/${TAG}_dict \
+  python tools/one_ggr.py 2 2 > /dev/null 2>&1
+echo done

@@ -33,5 +33,6 @@ for i in range(reps):
     if prof:
         rep = {k: v for k, v in lib.profile_report().items() if not k.startswith(("gap:", "host:"))}
         top = sorted(rep.items(), key=lambda x: -x[1][1])[:int(sys.argv[4]) if sys.argv[4].isdigit() else 4]
-        print("   kernels %.3f ms; top: %s" % (sum(v[1] for v in rep.values()),
+        busy = rep.pop("busy:", (0, 0.0))[1]
+        print("   busy %.3f ms; top: %s" % (busy,
               " | ".join(f"{k} {v[0]}x {v[1]:.3f}" for k, v in top)), flush=True)
