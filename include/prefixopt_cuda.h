@@ -306,6 +306,11 @@ void po_slice_free(po_slice* slice);
 int po_debug_radix_sort(const uint64_t* keys, const uint32_t* vals, uint64_t n, int32_t begin_bit,
                         int32_t end_bit, uint64_t* out_keys, uint32_t* out_vals);
 
+/* Test hook (not a reference function): the stable merge sort of the K3
+ * small-job sorts on (a, b, value) records, ordered by (a, b); host arrays. */
+int po_debug_merge_sort(const uint64_t* a, const uint64_t* b, const uint32_t* vals, uint64_t n,
+                        uint64_t* out_a, uint64_t* out_b, uint32_t* out_vals);
+
 /* Thread-local message of the last failing call on this thread. */
 const char* po_last_error(void);
 

@@ -193,6 +193,8 @@ class CudaLib:
         self.schedule_free = _bind(L, "po_schedule_free", None, [vp])
         self.debug_radix_sort = _bind(L, "po_debug_radix_sort", C.c_int,
                                       [vp, vp, C.c_uint64, C.c_int32, C.c_int32, vp, vp])
+        self.debug_merge_sort = _bind(L, "po_debug_merge_sort", C.c_int,
+                                      [vp, vp, vp, C.c_uint64, vp, vp, vp])
         self.comm_init_host = _bind(L, "po_comm_init_host", C.c_int,
                                     [vp, C.c_int32, C.c_int32, vp])
         self.ggr_sharded = _bind(L, "po_ggr_sharded", C.c_int,

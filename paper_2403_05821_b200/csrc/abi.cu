@@ -708,6 +708,15 @@ int po_debug_radix_sort(const uint64_t* keys, const uint32_t* vals, uint64_t n, 
   });
 }
 
+int po_debug_merge_sort(const uint64_t* a, const uint64_t* b, const uint32_t* vals, uint64_t n,
+                        uint64_t* out_a, uint64_t* out_b, uint32_t* out_vals) {
+  return guarded([&] {
+    if (n >= (uint64_t(1) << 32)) fail(PO_ERR_SIZE, "too many items");
+    if (n && (!a || !b || !vals || !out_a || !out_b || !out_vals)) fail(PO_ERR_INVALID_ARG, "null argument");
+    debug_merge_sort(a, b, vals, uint32_t(n), out_a, out_b, out_vals, nullptr);
+  });
+}
+
 int po_phc(const po_table* t, int32_t tok, int32_t scoring, uint64_t n_entries,
            const uint64_t* row_ids, const uint64_t* order_offsets, const int32_t* order_fields,
            uint32_t sched_location, uint64_t* out_phc, void* stream) {

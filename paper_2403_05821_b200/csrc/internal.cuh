@@ -52,6 +52,8 @@ void exclusive_scan_u64(const uint64_t* in, uint64_t* out, uint64_t n, cudaStrea
 // [begin_bit, end_bit) (radix.cu: hand-written onesweep). kin/vin and
 // kout/vout must not overlap. PO_RADIX=cub routes to cub::DeviceRadixSort
 // (comparison runs).
+void debug_merge_sort(const uint64_t* a, const uint64_t* b, const uint32_t* v, uint32_t n,
+                      uint64_t* oa, uint64_t* ob, uint32_t* ov, cudaStream_t s);
 void radix_sort_pairs(const uint64_t* kin, uint64_t* kout, const uint32_t* vin, uint32_t* vout,
                       uint32_t n, int begin_bit, int end_bit, cudaStream_t s);
 

@@ -18,6 +18,7 @@
 #include <mutex>
 
 #include "internal.cuh"
+#include "msort.cuh"
 
 namespace po {
 
@@ -208,28 +209,38 @@ uint32_t merge_round0_max() {
   return v;
 }
 
-struct Key128 {
+// round-0 record of the two-word merge path: (word A, word B) key + item
+struct Rec128 {
   uint64_t a, b;
+  uint32_t v, pad;
 };
 struct Less128 {
-  __device__ __forceinline__ bool operator()(const Key128& x, const Key128& y) const {
+  __device__ __forceinline__ bool operator()(const Rec128& x, const Rec128& y) const {
     return x.a < y.a || (x.a == y.a && x.b < y.b);
   }
 };
 
 __global__ void k_pack128(const uint64_t* a, const uint64_t* b, const uint32_t* items, uint32_t n,
-                          Key128* k, uint32_t* v) {
+                          Rec128* r) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    r[i] = Rec128{a[i], b[i], items[i], 0u};
+}
+
+__global__ void k_unpack128(const Rec128* r, uint32_t n, uint64_t* a, uint64_t* b, uint32_t* v) {
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    k[i] = Key128{a[i], b[i]};
-    v[i] = items[i];
+    a[i] = r[i].a;
+    b[i] = r[i].b;
+    v[i] = r[i].v;
   }
 }
 
-__global__ void k_unpack128(const Key128* k, uint32_t n, uint64_t* a, uint64_t* b) {
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    a[i] = k[i].a;
-    b[i] = k[i].b;
-  }
+// PO_MSORT=cub: the library merge sort on the small-job paths (comparison runs)
+bool msort_cub() {
+  static const bool v = [] {
+    const char* e = std::getenv("PO_MSORT");
+    return e && std::string(e) == "cub";
+  }();
+  return v;
 }
 
 bool seg_radix_rows() {  // experiment knob: row-key rounds by radix with segment prefix
@@ -490,14 +501,19 @@ bool merge_rank_job(const RefineJob& sp, cudaStream_t s) {
     return false;
   if (sp.key.kind == 1) ensure_esc_table();
   const uint32_t n = sp.n_items;
-  ProfScope ps("cub_merge_sort", s);
+  ProfScope ps(msort_cub() ? "cub_merge_sort" : "merge_sort", s);
   DevBuf<StrRec> recs(n, s);
   PO_LAUNCH(k_str_recs, grid_for(n, 256), 256, 0, s, sp.key, sp.d_grp_init, n, recs.get());
-  size_t need = 0;
   StrLess less{sp.key};
-  PO_CUDA(cub::DeviceMergeSort::StableSortKeys(nullptr, need, recs.get(), int(n), less, s));
-  DevBuf<uint8_t> tmp(need, s);
-  PO_CUDA(cub::DeviceMergeSort::StableSortKeys(tmp.get(), need, recs.get(), int(n), less, s));
+  if (msort_cub()) {
+    size_t need = 0;
+    PO_CUDA(cub::DeviceMergeSort::StableSortKeys(nullptr, need, recs.get(), int(n), less, s));
+    DevBuf<uint8_t> tmp(need, s);
+    PO_CUDA(cub::DeviceMergeSort::StableSortKeys(tmp.get(), need, recs.get(), int(n), less, s));
+  } else {
+    DevBuf<StrRec> tmp(n, s);
+    stable_merge_sort(recs.get(), tmp.get(), n, less, s);
+  }
   const uint32_t ng = sp.d_grp_start ? sp.n_groups : sp.grp_max + 1;
   DevBuf<uint32_t> first(std::max<uint32_t>(ng, 1), s);
   PO_LAUNCH(k_str_first, grid_for(n, 256), 256, 0, s, recs.get(), n, first.get());
@@ -656,21 +672,24 @@ void refine_sort_multi(const std::vector<RefineJob>& specs, cudaStream_t s) {
       if (two && !seg && A <= merge_round0_max()) {
         // one stable merge sort by (word A, word B): the same order as the
         // two LSD passes below
-        ProfScope ps("cub_merge_sort", s);
-        DevBuf<Key128> k128(A, s);
+        ProfScope ps(msort_cub() ? "cub_merge_sort" : "merge_sort", s);
+        DevBuf<Rec128> r128(A, s), t128(A, s);
         PO_LAUNCH(k_pack128, grid_for(A, 256), 256, 0, s, j.keys.get(), j.kb.get(), j.items.get(),
-                  A, k128.get(), j.items2.get());
-        size_t need = 0;
-        PO_CUDA(cub::DeviceMergeSort::StableSortPairs(nullptr, need, k128.get(), j.items2.get(),
-                                                      int(A), Less128(), s));
-        if (need > j.tb) {
-          j.tmp.alloc(need, s);
-          j.tb = need;
+                  A, r128.get());
+        if (msort_cub()) {
+          size_t need = 0;
+          PO_CUDA(cub::DeviceMergeSort::StableSortKeys(nullptr, need, r128.get(), int(A), Less128(), s));
+          if (need > j.tb) {
+            j.tmp.alloc(need, s);
+            j.tb = need;
+          }
+          PO_CUDA(cub::DeviceMergeSort::StableSortKeys(j.tmp.get(), need, r128.get(), int(A),
+                                                       Less128(), s));
+        } else {
+          stable_merge_sort(r128.get(), t128.get(), A, Less128(), s);
         }
-        PO_CUDA(cub::DeviceMergeSort::StableSortPairs(j.tmp.get(), need, k128.get(),
-                                                      j.items2.get(), int(A), Less128(), s));
-        PO_LAUNCH(k_unpack128, grid_for(A, 256), 256, 0, s, k128.get(), A, j.keys2.get(),
-                  j.kb.get());
+        PO_LAUNCH(k_unpack128, grid_for(A, 256), 256, 0, s, r128.get(), A, j.keys2.get(), j.kb.get(),
+                  j.items2.get());
       } else if (two) {
         // LSD over the two words: by word B, then stably by word A
         sort_pass(j.kb.get(), j.kb2.get(), j.pos_iota.get(), j.perm1.get(), 64);
@@ -923,6 +942,25 @@ void refine_sort(uint32_t n_items, const uint32_t* d_grp_init, uint32_t grp_max,
   j.d_out_pos = d_out_pos;
   j.row_chunk_bits = row_chunk_bits;
   refine_sort_multi({j}, s);
+}
+
+// po_debug_merge_sort: stable_merge_sort on (a, b, value) records (test hook)
+void debug_merge_sort(const uint64_t* a, const uint64_t* b, const uint32_t* v, uint32_t n,
+                      uint64_t* oa, uint64_t* ob, uint32_t* ov, cudaStream_t s) {
+  DevBuf<uint64_t> da(n, s), db(n, s);
+  DevBuf<uint32_t> dv(n, s);
+  DevBuf<Rec128> r(n, s), t(n, s);
+  if (!n) return;
+  PO_CUDA(cudaMemcpyAsync(da.get(), a, n * 8ull, cudaMemcpyHostToDevice, s));
+  PO_CUDA(cudaMemcpyAsync(db.get(), b, n * 8ull, cudaMemcpyHostToDevice, s));
+  PO_CUDA(cudaMemcpyAsync(dv.get(), v, n * 4ull, cudaMemcpyHostToDevice, s));
+  PO_LAUNCH(k_pack128, grid_for(n, 256), 256, 0, s, da.get(), db.get(), dv.get(), n, r.get());
+  stable_merge_sort(r.get(), t.get(), n, Less128(), s);
+  PO_LAUNCH(k_unpack128, grid_for(n, 256), 256, 0, s, r.get(), n, da.get(), db.get(), dv.get());
+  PO_CUDA(cudaMemcpyAsync(oa, da.get(), n * 8ull, cudaMemcpyDeviceToHost, s));
+  PO_CUDA(cudaMemcpyAsync(ob, db.get(), n * 8ull, cudaMemcpyDeviceToHost, s));
+  PO_CUDA(cudaMemcpyAsync(ov, dv.get(), n * 4ull, cudaMemcpyDeviceToHost, s));
+  sync(s);
 }
 
 }  // namespace po
