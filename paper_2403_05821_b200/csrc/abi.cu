@@ -315,9 +315,33 @@ cudaStream_t copy_stream() {
   return streams.s[dev];
 }
 
+cudaStream_t aux_stream() {
+  struct PerDevice {
+    std::vector<cudaStream_t> s;
+    ~PerDevice() {
+      for (cudaStream_t x : s)
+        if (x) cudaStreamDestroy(x);
+    }
+  };
+  static thread_local PerDevice streams;
+  int dev = 0;
+  PO_CUDA(cudaGetDevice(&dev));
+  if (size_t(dev) >= streams.s.size()) streams.s.resize(dev + 1, nullptr);
+  if (!streams.s[dev]) PO_CUDA(cudaStreamCreateWithFlags(&streams.s[dev], cudaStreamNonBlocking));
+  return streams.s[dev];
+}
+
 // Small device -> host reads that the host waits for (level results): through
 // a per-thread pinned buffer, which completes sooner than a pageable copy.
-void d2h_sync(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+bool debug_syncs() {
+  static const bool on = [] {
+    const char* v = std::getenv("PO_DEBUG_SYNCS");
+    return v && *v && *v != '0';
+  }();
+  return on;
+}
+
+void d2h_sync(void* dst, const void* src, size_t bytes, cudaStream_t s, const char* file, int line) {
   struct Pinned {
     uint8_t* p = nullptr;
     size_t cap = 0;
@@ -329,7 +353,7 @@ void d2h_sync(void* dst, const void* src, size_t bytes, cudaStream_t s) {
   constexpr size_t kMax = 4u << 20;
   if (bytes > kMax) {
     PO_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s));
-    sync(s);
+    sync(s, file, line);
     return;
   }
   if (buf.cap < bytes) {
@@ -341,7 +365,7 @@ void d2h_sync(void* dst, const void* src, size_t bytes, cudaStream_t s) {
     buf.cap = cap;
   }
   if (bytes) PO_CUDA(cudaMemcpyAsync(buf.p, src, bytes, cudaMemcpyDeviceToHost, s));
-  sync(s);
+  sync(s, file, line);
   if (bytes) std::memcpy(dst, buf.p, bytes);
 }
 

@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <cstdio>
 #include <chrono>
 #include <cstring>
 #include <cstdint>
@@ -100,7 +101,8 @@ inline unsigned grid_for(uint64_t work, unsigned block, unsigned max_waves = 16)
 constexpr size_t kPinnedSmallCopy = 1 << 20;
 void h2d_async(void* dst, const void* src, size_t bytes, cudaStream_t s);
 // device -> host copy, then the stream synchronised (pinned bounce buffer)
-void d2h_sync(void* dst, const void* src, size_t bytes, cudaStream_t s);
+void d2h_sync(void* dst, const void* src, size_t bytes, cudaStream_t s,
+              const char* file = __builtin_FILE(), int line = __builtin_LINE());
 
 // Large transient buffers (the dictionary tables, per-cell arrays) come from
 // a per-device cache of cudaMalloc'd blocks that are never returned to the
@@ -207,9 +209,11 @@ DevBuf<T> to_device(const std::vector<T>& v, cudaStream_t s) {
 }
 
 extern thread_local uint64_t g_syncs;  // host synchronisations of this thread (debug timing)
-inline void sync(cudaStream_t s) {
+bool debug_syncs();  // PO_DEBUG_SYNCS=1: print the call site of every stream sync
+inline void sync(cudaStream_t s, const char* file = __builtin_FILE(), int line = __builtin_LINE()) {
   HostScope hs("sync");
   ++g_syncs;
+  if (debug_syncs()) fprintf(stderr, "[po sync] %s:%d\n", file, line);
   PO_CUDA(cudaStreamSynchronize(s));
 }
 

@@ -970,6 +970,42 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
     return;
   }
 
+  // Whole-table fallback competitor (ggr.hpp:379-387), single GPU: its order
+  // comes from the global stats and its PHC and pruning bound need only the
+  // dictionary, so both are queued now on a side stream and run while the
+  // level loop's host round trips leave the device idle; the end of the call
+  // reads them together with the recursion's PHC in one transfer.
+  const bool early_fb = !dist && !debug_checks();
+  std::vector<int> fb_order;
+  DevBuf<unsigned long long> fbres;  // [fallback phc][bound (double)][phc][out-of-range flag]
+  struct FbJoin {  // the call's stream waits for the side stream on every exit
+    cudaStream_t s;
+    cudaEvent_t ev = nullptr;
+    ~FbJoin() {
+      if (ev) {
+        cudaStreamWaitEvent(s, ev, 0);
+        cudaEventDestroy(ev);
+      }
+    }
+  } fb_join{s};
+  if (early_fb) {
+    std::vector<double> avg(m);
+    for (uint32_t c = 0; c < m; ++c)
+      avg[c] = static_cast<double>(e.total_len[c]) / static_cast<double>(ng);
+    fb_order = hitcount_order(ng, e.card, avg, cfg.stats_variant);
+    fbres.alloc(4, s);
+    cudaStream_t a = aux_stream();
+    cudaEvent_t ready;
+    PO_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+    PO_CUDA(cudaEventRecord(ready, s));
+    PO_CUDA(cudaStreamWaitEvent(a, ready, 0));
+    PO_CUDA(cudaEventDestroy(ready));
+    fallback_ub_async(e, a, reinterpret_cast<double*>(fbres.get() + 1));
+    fixed_order_phc_async(e, fb_order, a, fbres.get());
+    PO_CUDA(cudaEventCreateWithFlags(&fb_join.ev, cudaEventDisableTiming));
+    PO_CUDA(cudaEventRecord(fb_join.ev, a));
+  }
+
   // FD partners (ggr.hpp:154-164): per field, the other members of every
   // group holding it, each group's members in ascending order.
   std::vector<std::vector<int>> partners(m);
@@ -1764,7 +1800,12 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
   if (!csr) {
     PO_LAUNCH(k_emit_orders, grid_for(n * m, 256), 256, 0, s, d_rows, n, m, row_leaf.get(),
               d_leaf_orders.get(), d_orders);
-    out.phc = phc_device(e, n, nullptr, d_rows, nullptr, d_orders, s);
+    if (early_fb)
+      phc_device_raw_async(e.vid.get(), e.vlen.get(), e.d_colbase.get(), e.n, e.m, n, nullptr, d_rows,
+                           nullptr, d_orders, s, fbres.get() + 2,
+                           reinterpret_cast<int*>(fbres.get() + 3));
+    else
+      out.phc = phc_device(e, n, nullptr, d_rows, nullptr, d_orders, s);
   } else {
     // leaf l's rows hold positions [leaf_off[l], + size) and each takes
     // |full order of l| fields: CSR offsets per position
@@ -1791,20 +1832,40 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
     PO_LAUNCH(k_emit_orders_csr, grid_for(n, 256), 256, 0, s, d_rows, n, row_leaf.get(), d_lf.get(),
               d_lf_off.get(), d_lw.get(), d_lbase.get(), d_loff.get(), total,
               out.csr_offsets.get(), out.csr_fields.get());
-    out.phc = phc_device(e, n, nullptr, d_rows, out.csr_offsets.get(), out.csr_fields.get(), s);
+    if (early_fb)
+      phc_device_raw_async(e.vid.get(), e.vlen.get(), e.d_colbase.get(), e.n, e.m, n, nullptr, d_rows,
+                           out.csr_offsets.get(), out.csr_fields.get(), s, fbres.get() + 2,
+                           reinterpret_cast<int*>(fbres.get() + 3));
+    else
+      out.phc = phc_device(e, n, nullptr, d_rows, out.csr_offsets.get(), out.csr_fields.get(), s);
   }
   timing_mark("emit_phc", s);
 
   // ---- whole-table fallback competition (ggr.hpp:379-387) ----
-  if (!debug_checks() && fallback_cannot_win(e, out.phc, s)) {
-    timing_mark("fallback_bound", s);
-    return;
+  uint64_t fb_phc = 0;
+  if (early_fb) {
+    PO_CUDA(cudaStreamWaitEvent(s, fb_join.ev, 0));
+    unsigned long long h[4];
+    d2h_sync(h, fbres.get(), sizeof(h), s);
+    int err = 0;
+    std::memcpy(&err, &h[3], sizeof(err));
+    if (err) fail(PO_ERR_OUT_OF_RANGE, "schedule references a row or field outside the table");
+    out.phc = n > 1 ? h[2] : 0;
+    double ub = 0;
+    std::memcpy(&ub, &h[1], sizeof(ub));
+    if (fallback_bound_prunes(e, ub, out.phc)) return;
+    fb_phc = n > 1 ? h[0] : 0;
+  } else {
+    if (!debug_checks() && fallback_cannot_win(e, out.phc, s)) {
+      timing_mark("fallback_bound", s);
+      return;
+    }
+    std::vector<double> avg(m);
+    for (uint32_t c = 0; c < m; ++c)
+      avg[c] = static_cast<double>(e.total_len[c]) / static_cast<double>(ng);
+    fb_order = hitcount_order(ng, e.card, avg, cfg.stats_variant);
+    fb_phc = fixed_order_phc_device(e, fb_order, s);  // prefix groups, no sort
   }
-  std::vector<double> avg(m);
-  for (uint32_t c = 0; c < m; ++c)
-    avg[c] = static_cast<double>(e.total_len[c]) / static_cast<double>(ng);
-  const std::vector<int> fb_order = hitcount_order(ng, e.card, avg, cfg.stats_variant);
-  const uint64_t fb_phc = fixed_order_phc_device(e, fb_order, s);  // prefix groups, no sort
   timing_mark("fallback_phc", s);
   std::vector<int32_t> fo(fb_order.begin(), fb_order.end());
   auto d_fo = to_device(fo, s);
@@ -1824,7 +1885,8 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
     out.csr_offsets.release();
     out.csr_fields.release();
   }
-  sync(s);
+  // no sync: the outputs are stream-ordered on s and every caller
+  // synchronises after delivering them
 }
 
 }  // namespace po

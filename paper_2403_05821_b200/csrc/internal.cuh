@@ -45,6 +45,7 @@ void make_device_table(const po_table* t, int tok, cudaStream_t s, DeviceTable& 
 // A second stream of the calling thread (current device) for copies that
 // overlap work on the call's stream.
 cudaStream_t copy_stream();
+cudaStream_t aux_stream();  // per-thread, per-device side stream for overlapped work
 
 void exclusive_scan_u64(const uint64_t* in, uint64_t* out, uint64_t n, cudaStream_t s);
 
@@ -240,6 +241,14 @@ uint64_t phc_device_raw(const uint32_t* vid, const uint64_t* vlen, const uint64_
                         const int32_t* fields, cudaStream_t s, uint64_t first_entry = 1,
                         bool uniform_order = false);
 
+// The same, queued only: the sum and an out-of-range flag land in d_tot /
+// d_err (both zeroed first).
+void phc_device_raw_async(const uint32_t* vid, const uint64_t* vlen, const uint64_t* colbase,
+                          uint64_t n_rows, uint32_t m, uint64_t n_entries, const uint64_t* rows64,
+                          const uint32_t* rows32, const uint64_t* order_offsets,
+                          const int32_t* fields, cudaStream_t s, unsigned long long* d_tot,
+                          int* d_err, uint64_t first_entry = 1, bool uniform_order = false);
+
 __global__ void k_invert(const uint32_t* pos, uint64_t n, uint32_t* perm);
 
 // Stats-ranked field order (ggr.hpp:59-84) — host IEEE double, no FMA.
@@ -259,9 +268,16 @@ void sort_all_rows(const Encoded& e, const std::vector<int>& order, uint32_t* d_
 // groups without materialising the sort.
 uint64_t fixed_order_phc_device(const Encoded& e, const std::vector<int>& order, cudaStream_t s);
 
+// Queued variant: the PHC lands in d_acc.
+void fixed_order_phc_async(const Encoded& e, const std::vector<int>& order, cudaStream_t s,
+                           unsigned long long* d_acc);
+
 // True when the whole-table fallback's PHC provably cannot exceed `phc`
 // (an upper bound from the dictionary counts and lengths, phc.cu).
 bool fallback_cannot_win(const Encoded& e, uint64_t phc, cudaStream_t s);
+// The bound queued into d_ub, and the decision from its value.
+void fallback_ub_async(const Encoded& e, cudaStream_t s, double* d_ub);
+bool fallback_bound_prunes(const Encoded& e, double ub, uint64_t phc);
 
 // Leaves whose key list stops before an unranked column (Encoded::unranked):
 // per leaf that column (-1: none) and the ranked key fields sorted before it

@@ -76,25 +76,36 @@ __global__ void k_invert(const uint32_t* pos, uint64_t n, uint32_t* perm) {
     perm[pos[r]] = uint32_t(r);
 }
 
+void phc_device_raw_async(const uint32_t* vid, const uint64_t* vlen, const uint64_t* colbase,
+                          uint64_t n_rows, uint32_t m, uint64_t n_entries, const uint64_t* rows64,
+                          const uint32_t* rows32, const uint64_t* order_offsets,
+                          const int32_t* fields, cudaStream_t s, unsigned long long* d_tot,
+                          int* d_err, uint64_t first_entry, bool uniform_order) {
+  PO_CUDA(cudaMemsetAsync(d_tot, 0, sizeof(unsigned long long), s));
+  PO_CUDA(cudaMemsetAsync(d_err, 0, sizeof(int), s));
+  if (n_entries <= first_entry) return;
+  PO_LAUNCH(k_phc, grid_for(n_entries, 256, 8), 256, 0, s, vid, vlen, colbase, n_rows, m,
+            n_entries, first_entry, rows64, rows32, order_offsets, fields, uniform_order ? 1 : 0,
+            d_tot, d_err);
+}
+
 uint64_t phc_device_raw(const uint32_t* vid, const uint64_t* vlen, const uint64_t* colbase,
                         uint64_t n_rows, uint32_t m, uint64_t n_entries, const uint64_t* rows64,
                         const uint32_t* rows32, const uint64_t* order_offsets,
                         const int32_t* fields, cudaStream_t s, uint64_t first_entry,
                         bool uniform_order) {
   if (n_entries <= first_entry) return 0;
-  DevBuf<unsigned long long> tot(1, s);
-  DevBuf<int> err(1, s);
-  tot.zero();
-  err.zero();
-  PO_LAUNCH(k_phc, grid_for(n_entries, 256, 8), 256, 0, s, vid, vlen, colbase, n_rows, m,
-            n_entries, first_entry, rows64, rows32, order_offsets, fields, uniform_order ? 1 : 0,
-            tot.get(), err.get());
-  unsigned long long h = 0;
-  int herr = 0;
-  tot.download(&h, 1);
-  d2h_sync(&herr, err.get(), (1) * sizeof(*err.get()), s);
-  if (herr) fail(PO_ERR_OUT_OF_RANGE, "schedule references a row or field outside the table");
-  return h;
+  struct R {
+    unsigned long long tot;
+    int err, pad;
+  };
+  DevBuf<R> res(1, s);
+  phc_device_raw_async(vid, vlen, colbase, n_rows, m, n_entries, rows64, rows32, order_offsets,
+                       fields, s, &res.get()->tot, &res.get()->err, first_entry, uniform_order);
+  R h{};
+  d2h_sync(&h, res.get(), sizeof(R), s);
+  if (h.err) fail(PO_ERR_OUT_OF_RANGE, "schedule references a row or field outside the table");
+  return h.tot;
 }
 
 uint64_t phc_device(const Encoded& e, uint64_t n_entries, const uint64_t* rows64,
@@ -217,28 +228,37 @@ __global__ void k_fb_bound(const uint32_t* __restrict__ count, const uint64_t* _
 // 2^64 (no wraparound) and not above the recursion's PHC, the fallback cannot
 // be strictly better (ggr.hpp:383) and its PHC / sort are skipped. Every term
 // is computed in double; the relative error of the sum is below 1e-9.
-bool fallback_cannot_win(const Encoded& e, uint64_t phc, cudaStream_t s) {
+void fallback_ub_async(const Encoded& e, cudaStream_t s, double* d_ub) {
+  PO_CUDA(cudaMemsetAsync(d_ub, 0, sizeof(double), s));
+  if (e.D == 0) return;
+  PO_LAUNCH(k_fb_bound, grid_for(e.D, 256, 4), 256, 0, s, e.count.get(), e.vlen.get(), e.D, d_ub);
+}
+
+bool fallback_bound_prunes(const Encoded& e, double ub, uint64_t phc) {
   if (e.D == 0) return true;
-  DevBuf<double> acc(1, s);
-  acc.zero();
-  PO_LAUNCH(k_fb_bound, grid_for(e.D, 256, 4), 256, 0, s, e.count.get(), e.vlen.get(), e.D,
-            acc.get());
-  double ub = 0;
-  d2h_sync(&ub, acc.get(), (1) * sizeof(*acc.get()), s);
   const double ub_hi = ub * (1.0 + 1e-9) + 1.0;
   return ub_hi < 1.8e19 && ub_hi < double(phc) * (1.0 - 1e-15);
 }
 
-uint64_t fixed_order_phc_device(const Encoded& e, const std::vector<int>& order, cudaStream_t s) {
+bool fallback_cannot_win(const Encoded& e, uint64_t phc, cudaStream_t s) {
+  if (e.D == 0) return true;
+  DevBuf<double> acc(1, s);
+  fallback_ub_async(e, s, acc.get());
+  double ub = 0;
+  d2h_sync(&ub, acc.get(), sizeof(double), s);
+  return fallback_bound_prunes(e, ub, phc);
+}
+
+void fixed_order_phc_async(const Encoded& e, const std::vector<int>& order, cudaStream_t s,
+                           unsigned long long* d_acc) {
   const uint64_t n = e.n;
   const uint32_t m = e.m;
-  if (n < 2 || order.empty()) return 0;
+  PO_CUDA(cudaMemsetAsync(d_acc, 0, sizeof(unsigned long long), s));
+  if (n < 2 || order.empty()) return;
   const std::vector<uint64_t>& colbase = e.colbase;
-  DevBuf<unsigned long long> acc(1, s);
-  acc.zero();
   const int f0 = order[0];
   PO_LAUNCH(k_fb_first, grid_for(e.card[f0], 256, 4), 256, 0, s, e.count.get() + colbase[f0],
-            e.vlen.get() + colbase[f0], uint64_t(e.card[f0]), acc.get());
+            e.vlen.get() + colbase[f0], uint64_t(e.card[f0]), d_acc);
   if (order.size() > 1 && e.card[f0] < n) {
     uint64_t cap = 1;
     while (cap < 2 * n) cap <<= 1;
@@ -256,12 +276,18 @@ uint64_t fixed_order_phc_device(const Encoded& e, const std::vector<int>& order,
       if (e.card[f] == n) break;
       keys.fill_bytes(0xFF);
       PO_LAUNCH(k_fb_depth, grid_for(n, 256, 8), 256, 0, s, e.vid.get(), n, m, uint32_t(f),
-                e.vlen.get() + colbase[f], gid.get(), keys.get(), cap - 1, acc.get(),
+                e.vlen.get() + colbase[f], gid.get(), keys.get(), cap - 1, d_acc,
                 ng.get() + (p - 1), ng.get() + p);
     }
   }
+}
+
+uint64_t fixed_order_phc_device(const Encoded& e, const std::vector<int>& order, cudaStream_t s) {
+  if (e.n < 2 || order.empty()) return 0;
+  DevBuf<unsigned long long> acc(1, s);
+  fixed_order_phc_async(e, order, s, acc.get());
   unsigned long long h = 0;
-  d2h_sync(&h, acc.get(), (1) * sizeof(*acc.get()), s);
+  d2h_sync(&h, acc.get(), sizeof(h), s);
   return h;
 }
 
