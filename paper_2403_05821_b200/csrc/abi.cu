@@ -299,37 +299,45 @@ void cached_block_release(void* p, cudaStream_t s) {
     }
 }
 
-cudaStream_t copy_stream() {
-  struct PerDevice {
-    std::vector<cudaStream_t> s;
-    ~PerDevice() {
-      for (cudaStream_t x : s)
-        if (x) cudaStreamDestroy(x);
-    }
-  };
-  static thread_local PerDevice streams;
-  int dev = 0;
-  PO_CUDA(cudaGetDevice(&dev));
-  if (size_t(dev) >= streams.s.size()) streams.s.resize(dev + 1, nullptr);
-  if (!streams.s[dev]) PO_CUDA(cudaStreamCreateWithFlags(&streams.s[dev], cudaStreamNonBlocking));
-  return streams.s[dev];
-}
+// Side streams are per thread and device, taken from a process-wide pool and
+// returned when the thread exits: callers that run every call on a fresh
+// host thread (pipelined e2e, thread ranks) neither create nor destroy
+// streams per call.
+namespace {
+std::mutex g_stream_mu;
+std::map<std::pair<int, int>, std::vector<cudaStream_t>> g_stream_free;  // (kind, device)
 
-cudaStream_t aux_stream() {
-  struct PerDevice {
-    std::vector<cudaStream_t> s;
-    ~PerDevice() {
-      for (cudaStream_t x : s)
-        if (x) cudaStreamDestroy(x);
+cudaStream_t pooled_stream(int kind) {
+  struct Held {
+    std::vector<std::pair<std::pair<int, int>, cudaStream_t>> s;
+    ~Held() {
+      std::lock_guard<std::mutex> lk(g_stream_mu);
+      for (auto& [key, st] : s) g_stream_free[key].push_back(st);
     }
   };
-  static thread_local PerDevice streams;
+  static thread_local Held held;
   int dev = 0;
   PO_CUDA(cudaGetDevice(&dev));
-  if (size_t(dev) >= streams.s.size()) streams.s.resize(dev + 1, nullptr);
-  if (!streams.s[dev]) PO_CUDA(cudaStreamCreateWithFlags(&streams.s[dev], cudaStreamNonBlocking));
-  return streams.s[dev];
+  const std::pair<int, int> key{kind, dev};
+  for (auto& [k, st] : held.s)
+    if (k == key) return st;
+  cudaStream_t st = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(g_stream_mu);
+    auto& f = g_stream_free[key];
+    if (!f.empty()) {
+      st = f.back();
+      f.pop_back();
+    }
+  }
+  if (!st) PO_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  held.s.push_back({key, st});
+  return st;
 }
+}  // namespace
+
+cudaStream_t copy_stream() { return pooled_stream(0); }
+cudaStream_t aux_stream() { return pooled_stream(1); }
 
 // Small device -> host reads that the host waits for (level results): through
 // a per-thread pinned buffer, which completes sooner than a pageable copy.
@@ -342,11 +350,18 @@ bool debug_syncs() {
 }
 
 void d2h_sync(void* dst, const void* src, size_t bytes, cudaStream_t s, const char* file, int line) {
+  // per-thread bounce buffer from a process-wide list (returned at thread
+  // exit, never freed: cudaFreeHost synchronises the device)
+  static std::mutex mu;
+  static std::vector<std::pair<uint8_t*, size_t>> free_bufs;
   struct Pinned {
     uint8_t* p = nullptr;
     size_t cap = 0;
     ~Pinned() {
-      if (p) cudaFreeHost(p);
+      if (p) {
+        std::lock_guard<std::mutex> lk(mu);
+        free_bufs.push_back({p, cap});
+      }
     }
   };
   static thread_local Pinned buf;
@@ -357,12 +372,22 @@ void d2h_sync(void* dst, const void* src, size_t bytes, cudaStream_t s, const ch
     return;
   }
   if (buf.cap < bytes) {
-    if (buf.p) PO_CUDA(cudaFreeHost(buf.p));
+    std::lock_guard<std::mutex> lk(mu);
+    if (buf.p) free_bufs.push_back({buf.p, buf.cap});
     buf.p = nullptr;
     buf.cap = 0;
-    const size_t cap = std::max<size_t>(bytes, 64u << 10);
-    PO_CUDA(cudaMallocHost(reinterpret_cast<void**>(&buf.p), cap));
-    buf.cap = cap;
+    for (size_t i = 0; i < free_bufs.size(); ++i)
+      if (free_bufs[i].second >= bytes) {
+        buf.p = free_bufs[i].first;
+        buf.cap = free_bufs[i].second;
+        free_bufs.erase(free_bufs.begin() + i);
+        break;
+      }
+    if (!buf.p) {
+      const size_t cap = std::max<size_t>(bytes, 64u << 10);
+      PO_CUDA(cudaMallocHost(reinterpret_cast<void**>(&buf.p), cap));
+      buf.cap = cap;
+    }
   }
   if (bytes) PO_CUDA(cudaMemcpyAsync(buf.p, src, bytes, cudaMemcpyDeviceToHost, s));
   sync(s, file, line);

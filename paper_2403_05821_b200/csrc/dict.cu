@@ -1168,13 +1168,20 @@ struct PinnedSlot {
   int dev = -1;
   bool pending = false;
 };
+// A thread's slots go back to a process-wide list when it exits (buffers
+// are never freed: pinning is slow and cudaFreeHost synchronises the
+// device), so a caller that runs each call on a fresh thread reuses them.
+std::mutex g_slot_mu;
+std::vector<std::pair<uint8_t*, size_t>> g_slot_free;
+
 struct PinnedSlots {
   PinnedSlot slot[2];
   ~PinnedSlots() {
+    std::lock_guard<std::mutex> lk(g_slot_mu);
     for (auto& x : slot) {
       if (x.pending) cudaEventSynchronize(x.done);
       if (x.done) cudaEventDestroy(x.done);
-      if (x.p) cudaFreeHost(x.p);
+      if (x.p) g_slot_free.push_back({x.p, x.cap});
     }
   }
 };
@@ -1189,11 +1196,23 @@ PinnedSlot& pinned_slot(int i, size_t bytes) {
     x.pending = false;
   }
   if (x.cap < bytes) {
-    if (x.p) cudaFreeHost(x.p);
+    std::lock_guard<std::mutex> lk(g_slot_mu);
+    if (x.p) g_slot_free.push_back({x.p, x.cap});
     x.p = nullptr;
     x.cap = 0;
-    PO_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&x.p), bytes, cudaHostAllocPortable));
-    x.cap = bytes;
+    size_t best = g_slot_free.size();
+    for (size_t k = 0; k < g_slot_free.size(); ++k)  // smallest free buffer that fits
+      if (g_slot_free[k].second >= bytes &&
+          (best == g_slot_free.size() || g_slot_free[k].second < g_slot_free[best].second))
+        best = k;
+    if (best < g_slot_free.size()) {
+      x.p = g_slot_free[best].first;
+      x.cap = g_slot_free[best].second;
+      g_slot_free.erase(g_slot_free.begin() + best);
+    } else {
+      PO_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&x.p), bytes, cudaHostAllocPortable));
+      x.cap = bytes;
+    }
   }
   if (x.dev != dev) {
     if (x.done) cudaEventDestroy(x.done);

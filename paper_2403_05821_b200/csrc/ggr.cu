@@ -257,7 +257,8 @@ __device__ __forceinline__ bool entry_skipped(const TDesc& t, const uint64_t* co
   return nparts > 1 && !t.dense && (colbase[c] + v) % nparts != part;
 }
 
-__global__ void __launch_bounds__(kArgBlock) k_argmax(
+template <int MINB>
+__global__ void __launch_bounds__(kArgBlock, MINB) k_argmax(
     const WorkSeg* __restrict__ work, uint32_t nwseg, const ScanSlot* __restrict__ slots,
     const uint32_t* __restrict__ masks, const uint32_t* __restrict__ weights,
     const uint64_t* __restrict__ colbase, const uint64_t* __restrict__ vlen, uint32_t m,
@@ -602,7 +603,8 @@ inline uint32_t add_agg_seg(std::vector<AggSeg>& v, uint32_t& ntask, uint32_t sp
 // __match_any_sync / a labeled-partition reduction before the table atomics
 // (low-cardinality columns and the split column itself collapse to one
 // atomic per warp).
-__global__ void __launch_bounds__(kAggBlock) k_aggregate(
+template <int MINB>
+__global__ void __launch_bounds__(kAggBlock, MINB) k_aggregate(
     const AggSeg* __restrict__ segs, uint32_t nseg, const uint32_t* __restrict__ blockrows,
     const SplitD* __restrict__ sp, const uint32_t* __restrict__ vid,
     const uint64_t* __restrict__ vlen, const uint64_t* __restrict__ colbase, uint32_t m,
@@ -763,7 +765,8 @@ __global__ void k_root_psum(const uint32_t* vid, uint64_t n, uint32_t m, uint32_
 // ---------------------------------------------------------------------------
 // K7 leaf_stats: per (leaf, column) distinct count and length sum
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_leaf_stats(
+template <int MINB>
+__global__ void __launch_bounds__(256, MINB) k_leaf_stats(
     const WorkSeg* work, uint32_t nwseg, const ScanSlot* slots, const uint32_t* masks, const uint64_t* colbase,
     const uint64_t* vlen, uint32_t m, unsigned long long* card, unsigned long long* tot,
     uint32_t part, uint32_t nparts) {
@@ -955,6 +958,32 @@ struct Pack {
 
 }  // namespace
 
+// Occupancy of the level kernels: min blocks per SM of k_argmax (8: 32
+// registers), k_aggregate (6: 40) and k_leaf_stats (1), measured with
+// tools/level_minb_sweep.sh (C4 20M-row argmax 2.07 -> 1.29 ms per call,
+// C3 0.30 -> 0.27); PO_LEVEL_MINB=a,b,c picks others (experiments).
+static int level_minb(int which) {
+  static const std::vector<int> v = [] {
+    std::vector<int> r{8, 6, 1};
+    const char* e = std::getenv("PO_LEVEL_MINB");
+    if (e && *e) sscanf(e, "%d,%d,%d", &r[0], &r[1], &r[2]);
+    return r;
+  }();
+  return v[which];
+}
+#define PO_MINB_SWITCH(which, K, grid, block, smem, s, ...)                  \
+  do {                                                                     \
+    switch (level_minb(which)) {                                           \
+      case 4: PO_LAUNCH((K<4>), grid, block, smem, s, __VA_ARGS__); break; \
+      case 6: PO_LAUNCH((K<6>), grid, block, smem, s, __VA_ARGS__); break; \
+      case 8: PO_LAUNCH((K<8>), grid, block, smem, s, __VA_ARGS__); break; \
+      default: PO_LAUNCH((K<1>), grid, block, smem, s, __VA_ARGS__); break; \
+    }                                                                      \
+  } while (0)
+#define PO_ARGMAX(grid, ...) PO_MINB_SWITCH(0, k_argmax, grid, __VA_ARGS__)
+#define PO_AGG(grid, ...) PO_MINB_SWITCH(1, k_aggregate, grid, __VA_ARGS__)
+#define PO_LEAFSTATS(grid, ...) PO_MINB_SWITCH(2, k_leaf_stats, grid, __VA_ARGS__)
+
 void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups,
                 const po_ggr_config& cfg, uint32_t* d_rows, int32_t* d_orders, GgrOutput& out,
                 cudaStream_t s, DistCtx* dist) {
@@ -975,7 +1004,11 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
   // dictionary, so both are queued now on a side stream and run while the
   // level loop's host round trips leave the device idle; the end of the call
   // reads them together with the recursion's PHC in one transfer.
-  const bool early_fb = !dist && !debug_checks();
+  static const bool early_fb_on = [] {  // PO_EARLY_FALLBACK=0: at the end, on s
+    const char* v = std::getenv("PO_EARLY_FALLBACK");
+    return !(v && *v == '0');
+  }();
+  const bool early_fb = early_fb_on && !dist && !debug_checks();
   std::vector<int> fb_order;
   DevBuf<unsigned long long> fbres;  // [fallback phc][bound (double)][phc][out-of-range flag]
   struct FbJoin {  // the call's stream waits for the side stream on every exit
@@ -1212,7 +1245,7 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
     const uint32_t nparts = dist && partition ? uint32_t(dist->comm->size()) : 1u;
     const uint32_t part = dist && partition ? uint32_t(dist->comm->rank()) : 0u;
     if (nslots) {
-      PO_LAUNCH(k_argmax, L.nitems, kArgBlock, 0, s,
+      PO_ARGMAX(L.nitems, kArgBlock, 0, s,
                 reinterpret_cast<WorkSeg*>(dp + o_work), uint32_t(L.work.size()), reinterpret_cast<ScanSlot*>(dp + o_slots),
                 reinterpret_cast<uint32_t*>(dp + o_masks), reinterpret_cast<uint32_t*>(dp + o_w),
                 colbase, vlen, m, K, partial.get(), pcands.get(), part, nparts);
@@ -1220,7 +1253,7 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
                 reinterpret_cast<uint32_t*>(dp + o_swo), d_best, d_ncand);
     }
     if (nleaf)
-      PO_LAUNCH(k_leaf_stats, S.nitems, 256, m <= 2048 ? 16 * m : 0, s,
+      PO_LEAFSTATS(S.nitems, 256, m <= 2048 ? 16 * m : 0, s,
                 reinterpret_cast<WorkSeg*>(dp + o_swork), uint32_t(S.work.size()), reinterpret_cast<ScanSlot*>(dp + o_sslots),
                 reinterpret_cast<uint32_t*>(dp + o_smasks), colbase, vlen, m, d_card, d_tot, part,
                 nparts);
@@ -1454,7 +1487,7 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
                 node_of_row.get(), n, d_lut, node_lo, lut_n, d_sp, e.vid.get(), m, d_cursor,
                 d_seg, blockrows.get());
       if (!dist && !tasks.empty())
-        PO_LAUNCH(k_aggregate, ntask, kAggBlock, 0, s, reinterpret_cast<AggSeg*>(ds + o_tasks),
+        PO_AGG(ntask, kAggBlock, 0, s, reinterpret_cast<AggSeg*>(ds + o_tasks),
                   uint32_t(tasks.size()), blockrows.get(), d_sp, e.vid.get(),
                   vlen, colbase, m, K, d_dpart.get(), d_npart.get());
       if (dist) {
@@ -1492,7 +1525,7 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
         DevBuf<uint8_t> dev2(p2.host.size(), s);
         dev2.upload(p2.host.data(), p2.host.size());
         if (!tasks2.empty())
-          PO_LAUNCH(k_aggregate, ntask2, kAggBlock, 0, s,
+          PO_AGG(ntask2, kAggBlock, 0, s,
                     reinterpret_cast<AggSeg*>(dev2.get() + o_t2), uint32_t(tasks2.size()),
                     blockrows.get(),
                     reinterpret_cast<SplitD*>(dev2.get() + o_sp2), e.vid.get(), vlen, colbase, m,
