@@ -964,27 +964,21 @@ int po_replay_unbounded(uint64_t n, const uint8_t* arena, const uint64_t* offset
     po_table tv{n, 1u, loc, &name, &name_len, arena, offsets, nullptr};
     DeviceTable dt;
     make_device_table(&tv, PO_TOK_CHAR, s, dt);
-    DevBuf<uint64_t> in(n, s), raw(n, s);
+    DevBuf<uint64_t> in(n, s), raw(n, s), hit(n, s), miss(n, s);
+    DevBuf<unsigned long long> tot(3, s);
     replay_unbounded_device(dt, tok, in.get(), raw.get(), s);
-    std::vector<uint64_t> hin(n), hraw(n);
-    in.download(hin.data(), n);
-    raw.download(hraw.data(), n);
-    sync(s);
-    uint64_t ti = 0, th = 0, tm = 0;
-    for (uint64_t i = 0; i < n; ++i) {  // cache_sim.hpp:266-279
-      const uint64_t hit = hraw[i] >= min_cacheable ? hraw[i] : 0;
-      if (out_input) out_input[i] = hin[i];
-      if (out_hit) out_hit[i] = hit;
-      if (out_miss) out_miss[i] = hin[i] - hit;
-      if (out_written) out_written[i] = hin[i] - hraw[i];
-      ti += hin[i];
-      th += hit;
-      tm += hin[i] - hit;
-    }
+    // the report on the device (cache_sim.hpp:266-279): raw becomes written
+    replay_report_device(in.get(), raw.get(), n, min_cacheable, hit.get(), miss.get(), tot.get(), s);
+    if (out_input) in.download(out_input, n);
+    if (out_hit) hit.download(out_hit, n);
+    if (out_miss) miss.download(out_miss, n);
+    if (out_written) raw.download(out_written, n);
+    unsigned long long ht[3];
+    d2h_sync(ht, tot.get(), sizeof(ht), s);
     if (out_totals) {
-      out_totals[0] = ti;
-      out_totals[1] = th;
-      out_totals[2] = tm;
+      out_totals[0] = ht[0];
+      out_totals[1] = ht[1];
+      out_totals[2] = ht[2];
     }
   });
 }

@@ -379,6 +379,10 @@ void dedup_device(const DeviceTable& t, uint64_t* d_expansion, uint64_t* d_uniqu
 // simulate() under an unbounded cache (replay.cu, cache_sim.hpp:223-285):
 // per prompt of the one-column table pt, its input tokens and raw hit (the
 // longest token prefix shared with any earlier prompt); device outputs.
+// The per-request report (hit, miss; d_raw becomes written) and totals.
+void replay_report_device(const uint64_t* d_input, uint64_t* d_raw, uint64_t n, uint64_t min_cacheable,
+                          uint64_t* d_hit, uint64_t* d_miss, unsigned long long* d_totals,
+                          cudaStream_t s);
 void replay_unbounded_device(const DeviceTable& pt, int tok, uint64_t* d_input, uint64_t* d_raw,
                              cudaStream_t s);
 

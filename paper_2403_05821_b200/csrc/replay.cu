@@ -268,4 +268,40 @@ void replay_unbounded_device(const DeviceTable& pt, int tok, uint64_t* d_input, 
             reinterpret_cast<unsigned long long*>(d_raw));
 }
 
+// simulate()'s per-request report from the replay (cache_sim.hpp:266-279):
+// hit = raw LCP when it reaches min_cacheable, else 0; miss = input - hit;
+// written = input - raw; totals of input, hit and miss (atomics per warp).
+__global__ void k_replay_report(const uint64_t* __restrict__ in, uint64_t* raw_to_written, uint64_t n,
+                                uint64_t min_cacheable, uint64_t* hit, uint64_t* miss,
+                                unsigned long long* totals) {
+  unsigned long long ti = 0, th = 0, tm = 0;
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t a = in[i], r = raw_to_written[i];
+    const uint64_t h = r >= min_cacheable ? r : 0;
+    hit[i] = h;
+    miss[i] = a - h;
+    raw_to_written[i] = a - r;
+    ti += a;
+    th += h;
+    tm += a - h;
+  }
+  ti = warp_sum_u64(ti);
+  th = warp_sum_u64(th);
+  tm = warp_sum_u64(tm);
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(&totals[0], ti);
+    atomicAdd(&totals[1], th);
+    atomicAdd(&totals[2], tm);
+  }
+}
+
+void replay_report_device(const uint64_t* d_input, uint64_t* d_raw, uint64_t n, uint64_t min_cacheable,
+                          uint64_t* d_hit, uint64_t* d_miss, unsigned long long* d_totals,
+                          cudaStream_t s) {
+  PO_CUDA(cudaMemsetAsync(d_totals, 0, 3 * sizeof(unsigned long long), s));
+  PO_LAUNCH(k_replay_report, grid_for(n, 256), 256, 0, s, d_input, d_raw, n, min_cacheable, d_hit,
+            d_miss, d_totals);
+}
+
 }  // namespace po
