@@ -460,11 +460,25 @@ struct StrLess {
     str_at(K, b.item, ob, lb);
     const uint8_t* pa = K.arena + oa;
     const uint8_t* pb = K.arena + ob;
-    for (uint64_t pos = 14 + K.skip;; ++pos) {
-      const uint32_t ca = sym_code(K, pa, la, pos), cb = sym_code(K, pb, lb, pos);
-      if (ca != cb) return ca < cb;
-      if (ca == 0 || pos >= la || pos >= lb) return false;  // equal strings
+    const uint8_t* lim = K.arena + K.arena_bytes;
+    // eight bytes at a time while both strings last: symbol codes are a
+    // one-to-one function of the byte, so the first differing byte decides
+    uint64_t pos = 14 + K.skip;
+    while (pos < la && pos < lb) {
+      const uint64_t ra = la - pos, rb = lb - pos;
+      const uint32_t w = uint32_t(ra < rb ? (ra < 8 ? ra : 8) : (rb < 8 ? rb : 8));
+      const uint64_t x = load8_unaligned(pa + pos, lim), y = load8_unaligned(pb + pos, lim);
+      const uint64_t d = mask_low_bytes(x ^ y, w);
+      if (d) {
+        const uint32_t sh = uint32_t(__ffsll(static_cast<long long>(d)) - 1) & ~7u;
+        const uint32_t bx = uint32_t(x >> sh) & 0xFF, by = uint32_t(y >> sh) & 0xFF;
+        return K.kind == 0 ? bx < by : c_esc_code[bx] < c_esc_code[by];
+      }
+      pos += w;
     }
+    // one string ends here: end code against a byte code (or both ended)
+    const uint32_t ca = sym_code(K, pa, la, pos), cb = sym_code(K, pb, lb, pos);
+    return ca < cb;
   }
 };
 
