@@ -1,7 +1,7 @@
 # Round evidence on one B200: GPU suite, smoke, bench line, launch list and
 # the --set full capture of the two dictionary kernels (outputs in gpurun_out/).
 set -u
-TAG=${TAG:-r2b}
+TAG=${TAG:-r2c}
 timeout 2400 python -m pytest tests -q -m gpu > gpurun_out/${TAG}_gputest.log 2>&1
 echo "pytest rc=$?" >> gpurun_out/${TAG}_gputest.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" >> gpurun_out/${TAG}_gputest.log 2>&1
@@ -13,3 +13,6 @@ timeout 900 ncu --set full --import-source on --clock-control none \
   -k 'regex:k_hash_probe|k_verify_cells' -s 2 -c 2 -o gpurun_out/${TAG}_dict \
   python tools/one_ggr.py 2 2 > /dev/null 2>&1
 echo done
+for c in 3 4 5; do
+  timeout 700 python tools/full_size.py $c --paths=device --reps=3 >> gpurun_out/${TAG}_full.jsonl 2>> gpurun_out/${TAG}_full.err
+done

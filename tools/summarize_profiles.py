@@ -20,7 +20,9 @@ def launches(path, cmd):
         if len(r) <= vi or r[mi] != "gpu__time_duration.sum":
             continue
         name = r[ki].split("(")[0].replace("void ", "")
-        name = name.split("::")[-1] if name.startswith("po::") else name[:60]
+        if name.startswith("po::"):
+            name = name.replace("po::", "").replace("<unnamed>::", "")
+        name = name[:60]
         v = float(r[vi].replace(",", ""))
         unit = h[vi]
         agg[name][0] += 1
