@@ -125,10 +125,32 @@ __global__ void k_csv_emit(const uint8_t* __restrict__ d, uint64_t len, uint64_t
     uint32_t st = pre[ch].v & 7;
     ulonglong4 p = base[ch];  // running: content byte, cell, record, line increments
     const uint64_t a = ch * kChunk, b = a + kChunk < len ? a + kChunk : len;
+    // a chunk's content bytes form one contiguous run of the arena: bytes up
+    // to the first 16-byte boundary are stored one by one, then gathered in
+    // registers and stored 16 at a time (a sixteenth of the byte stores)
+    uint32_t acc[4] = {0u, 0u, 0u, 0u};
     for_bytes(d, a, b, [&](uint8_t c) {
       const uint8_t t = c_csv[st][cls(c)];
       st = t & 7;
-      if (t & kEmit) arena[p.x++] = c;
+      if (t & kEmit) {
+        const uint32_t k = uint32_t(p.x & 15);
+        if (p.x - k < base[ch].x) {  // before the chunk's first full 16-byte slot
+          arena[p.x] = c;
+        } else {
+          const uint32_t v = uint32_t(c) << (8 * (k & 3));
+          switch (k >> 2) {
+            case 0: acc[0] |= v; break;
+            case 1: acc[1] |= v; break;
+            case 2: acc[2] |= v; break;
+            default: acc[3] |= v; break;
+          }
+          if (k == 15) {
+            *reinterpret_cast<uint4*>(arena + (p.x - 15)) = make_uint4(acc[0], acc[1], acc[2], acc[3]);
+            acc[0] = acc[1] = acc[2] = acc[3] = 0u;
+          }
+        }
+        ++p.x;
+      }
       if (t & kLine) ++p.w;
       if (t & kCell) cell_end[p.y++] = p.x;
       if (t & kRec) {
@@ -138,6 +160,10 @@ __global__ void k_csv_emit(const uint8_t* __restrict__ d, uint64_t len, uint64_t
         ++p.z;
       }
     });
+    // the partial last slot
+    const uint32_t k = uint32_t(p.x & 15);
+    if (k && p.x - k >= base[ch].x)
+      for (uint32_t q = 0; q < k; ++q) arena[p.x - k + q] = uint8_t(acc[q >> 2] >> (8 * (q & 3)));
   }
 }
 
