@@ -675,6 +675,70 @@ __global__ void __launch_bounds__(kAggBlock, MINB) k_aggregate(
   }
 }
 
+// Unique columns (one distinct value per row, single GPU) are never scanned
+// and get no table entries; a node keeps only its length sum per unique
+// column (usum[node * U + u]) for the leaf statistics. k_unique_sums adds
+// the block rows' lengths of split j (one task per AggSeg chunk), then
+// k_unique_children sets block = that sum and rest = parent - block.
+__global__ void k_unique_sums(const AggSeg* __restrict__ segs, uint32_t nseg,
+                              const uint32_t* __restrict__ blockrows,
+                              const uint32_t* __restrict__ vid, const uint64_t* __restrict__ vlen,
+                              const uint64_t* __restrict__ colbase, uint32_t m,
+                              const int32_t* __restrict__ uidx, uint32_t U, unsigned long long* ublk,
+                              const SplitD* __restrict__ sp, const uint32_t* __restrict__ parent,
+                              uint32_t ns, unsigned long long* usum, uint32_t* done) {
+  __shared__ bool s_last;
+  if (nseg) {
+    uint32_t lo = 0, hi = nseg - 1;
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi + 1) / 2;
+      if (segs[mid].first <= blockIdx.x) lo = mid;
+      else hi = mid - 1;
+    }
+    const AggSeg& g = segs[lo];
+    const uint64_t a = g.lo + uint64_t(blockIdx.x - g.first) * kAggRows;
+    const uint64_t b = a + kAggRows < g.hi ? a + kAggRows : g.hi;
+    const uint32_t c = g.col;
+    unsigned long long sum = 0;
+    for (uint64_t q = a + threadIdx.x; q < b; q += blockDim.x) {
+      const uint32_t r = blockrows[q];
+      sum += vlen[colbase[c] + vid[uint64_t(r) * m + c]];
+    }
+    sum = warp_sum_u64(sum);
+    if ((threadIdx.x & 31) == 0 && sum)
+      atomicAdd(&ublk[uint64_t(g.split) * U + uint32_t(uidx[c])], sum);
+  }
+  // the last block to finish sets the children's sums: block = the block
+  // rows' sum, rest = parent - block
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(done, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  for (uint32_t t = threadIdx.x; t < ns * U; t += blockDim.x) {
+    const uint32_t j = t / U, u = t - j * U;
+    const unsigned long long blk = __ldcg(&ublk[t]);
+    usum[uint64_t(sp[j].block_id) * U + u] = blk;
+    usum[uint64_t(sp[j].rest_id) * U + u] = usum[uint64_t(parent[j]) * U + u] - blk;
+  }
+}
+
+// Leaf statistics of the unique columns: distinct count = leaf size, length
+// sum from usum (k_leaf_stats leaves these (leaf, column) slots at zero).
+__global__ void k_unique_leaf_stats(const uint32_t* __restrict__ leaf_node,
+                                    const unsigned long long* __restrict__ leaf_size, uint32_t nleaf,
+                                    const int32_t* __restrict__ ucol, uint32_t U, uint32_t m,
+                                    const unsigned long long* __restrict__ usum,
+                                    unsigned long long* card, unsigned long long* tot) {
+  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < nleaf * U; t += gridDim.x * blockDim.x) {
+    const uint32_t i = t / U, u = t - i * U;
+    const uint32_t c = uint32_t(ucol[u]);
+    card[uint64_t(i) * m + c] = leaf_size[i];
+    tot[uint64_t(i) * m + c] = usum[uint64_t(leaf_node[i]) * U + u];
+  }
+}
+
 // Sharded solve: this rank's block-row aggregate of split j (a private
 // table) as records [key][split<<32 | count][K partner sums].
 __global__ void k_compact_contrib(TDesc t, uint32_t j, uint32_t K, uint64_t* out,
@@ -1139,6 +1203,35 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
     nodes[0].table = t;
   }
 
+  // Unique columns (single GPU): no table entries, length sums per node
+  // (k_unique_sums / k_unique_children / k_unique_leaf_stats)
+  std::vector<int> ucols;
+  std::vector<int32_t> uidx(m, -1);
+  if (!dist)
+    for (uint32_t c = 0; c < m; ++c)
+      if (e.card[c] == ng && ng > 1) {
+        uidx[c] = int32_t(ucols.size());
+        ucols.push_back(int(c));
+      }
+  const uint32_t U = uint32_t(ucols.size());
+  DevBuf<int32_t> d_uidx, d_ucol;
+  DevBuf<unsigned long long> usum;  // [node][U]
+  if (U) {
+    d_uidx = to_device(uidx, s);
+    d_ucol = to_device(std::vector<int32_t>(ucols.begin(), ucols.end()), s);
+    usum.alloc(size_t(64) * U, s);
+    std::vector<unsigned long long> root(U);
+    for (uint32_t u = 0; u < U; ++u) root[u] = e.total_len[ucols[u]];
+    usum.upload(root.data(), U);
+  }
+  auto grow_usum = [&](size_t nodes_n) {  // keeps the sums of existing nodes
+    if (!U || usum.size() >= nodes_n * U) return;
+    DevBuf<unsigned long long> nb(std::max(nodes_n, usum.size() / U * 2) * U, s);
+    PO_CUDA(cudaMemcpyAsync(nb.get(), usum.get(), usum.size() * sizeof(unsigned long long),
+                            cudaMemcpyDeviceToDevice, s));
+    usum = std::move(nb);
+  };
+
 
   // per-level scratch, grown only (stream order makes the reuse safe: a
   // level's copies and kernels queue behind the previous level's kernels)
@@ -1224,6 +1317,14 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
     const size_t o_slots = pk.add(L.slots), o_masks = pk.add(L.masks), o_w = pk.add(L.weights);
     const size_t o_work = pk.add(L.work), o_swo = pk.add(L.slot_work_off);
     const size_t o_sslots = pk.add(S.slots), o_smasks = pk.add(S.masks), o_swork = pk.add(S.work);
+    std::vector<uint32_t> uln;
+    std::vector<unsigned long long> ulsz;
+    if (U)
+      for (int id : pending) {
+        uln.push_back(uint32_t(id));
+        ulsz.push_back(nodes[id].size);
+      }
+    const size_t o_uln = pk.add(uln), o_ulsz = pk.add(ulsz);
     uint8_t* dp = upload(pk);
     grow(partial, std::max<size_t>(1, L.nitems));
     grow(pcands, std::max<size_t>(1, L.nitems));
@@ -1257,6 +1358,10 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
                 reinterpret_cast<WorkSeg*>(dp + o_swork), uint32_t(S.work.size()), reinterpret_cast<ScanSlot*>(dp + o_sslots),
                 reinterpret_cast<uint32_t*>(dp + o_smasks), colbase, vlen, m, d_card, d_tot, part,
                 nparts);
+    if (nleaf && U)
+      PO_LAUNCH(k_unique_leaf_stats, grid_for(nleaf * U, 128), 128, 0, s,
+                reinterpret_cast<uint32_t*>(dp + o_uln), reinterpret_cast<unsigned long long*>(dp + o_ulsz),
+                uint32_t(nleaf), d_ucol.get(), U, m, usum.get(), d_card, d_tot);
     if (nparts > 1) {
       if (nslots) {
         DevBuf<Cand> ab(size_t(nslots) * nparts, s);
@@ -1406,7 +1511,8 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
       if (needB) {
         // entries <= sum over the parent's columns of min(card, |B|)
         uint64_t bound = 0;
-        for (int c : P.cols) bound += std::min<uint64_t>(e.card[c], B.size);
+        for (int c : P.cols)
+          if (uidx[c] < 0) bound += std::min<uint64_t>(e.card[c], B.size);
         uint64_t cap = 64;
         while (cap < bound + bound / 2) cap <<= 1;
         auto t = std::make_shared<HTable>();
@@ -1448,8 +1554,8 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
       std::vector<SplitD> hsp(ns);
       std::vector<uint64_t> seg(ns + 1, 0);
       std::vector<uint32_t> split_nodes(ns);
-      std::vector<AggSeg> tasks;
-      uint32_t ntask = 0;
+      std::vector<AggSeg> tasks, usegs;
+      uint32_t ntask = 0, nutask = 0;
       for (uint32_t j = 0; j < ns; ++j) {
         hsp[j] = splits[j].d;
         split_nodes[j] = uint32_t(splits[j].node);
@@ -1461,6 +1567,10 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
         std::vector<char> inB(m, 0);
         for (int c : B.cols) inB[c] = 1;
         for (int c : P.cols) {
+          if (uidx[c] >= 0) {  // length sum of the block rows only
+            add_agg_seg(usegs, nutask, j, uint32_t(c), 0u, 0u, seg[j], seg[j + 1]);
+            continue;
+          }
           const uint32_t to_b = (hsp[j].tB.keys && inB[c]) ? 1u : 0u;
           const uint32_t to_p = hsp[j].tP.cnt ? 1u : 0u;
           if (!to_b && !to_p) continue;
@@ -1476,6 +1586,9 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
       const size_t o_sp = sp.add(hsp), o_seg = sp.add(seg), o_sn = sp.add(lut);
       const size_t o_tasks = sp.add(tasks);
       const size_t o_cursor = sp.add(std::vector<uint32_t>(ns, 0u));
+      const size_t o_usegs = sp.add(usegs), o_parent = sp.add(split_nodes);
+      const size_t o_ublk = sp.add(std::vector<unsigned long long>(size_t(ns) * U, 0ull));
+      const size_t o_udone = sp.add(std::vector<uint32_t>(1, 0u));
       uint8_t* ds = upload(sp);
       auto* d_sp = reinterpret_cast<SplitD*>(ds + o_sp);
       auto* d_seg = reinterpret_cast<uint64_t*>(ds + o_seg);
@@ -1490,6 +1603,15 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
         PO_AGG(ntask, kAggBlock, 0, s, reinterpret_cast<AggSeg*>(ds + o_tasks),
                   uint32_t(tasks.size()), blockrows.get(), d_sp, e.vid.get(),
                   vlen, colbase, m, K, d_dpart.get(), d_npart.get());
+      if (U) {
+        grow_usum(nodes.size());
+        auto* d_ublk = reinterpret_cast<unsigned long long*>(ds + o_ublk);
+        PO_LAUNCH(k_unique_sums, std::max<uint32_t>(nutask, 1), kAggBlock, 0, s,
+                  reinterpret_cast<AggSeg*>(ds + o_usegs), uint32_t(usegs.size()), blockrows.get(),
+                  e.vid.get(), vlen, colbase, m, d_uidx.get(), U, d_ublk, d_sp,
+                  reinterpret_cast<uint32_t*>(ds + o_parent), ns, usum.get(),
+                  reinterpret_cast<uint32_t*>(ds + o_udone));
+      }
       if (dist) {
         // this rank's block rows -> private tables -> contributions, all-gathered
         // and applied to the replicated child / parent tables
