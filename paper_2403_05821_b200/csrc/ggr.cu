@@ -678,8 +678,8 @@ __global__ void __launch_bounds__(kAggBlock, MINB) k_aggregate(
 // Unique columns (one distinct value per row, single GPU) are never scanned
 // and get no table entries; a node keeps only its length sum per unique
 // column (usum[node * U + u]) for the leaf statistics. k_unique_sums adds
-// the block rows' lengths of split j (one task per AggSeg chunk), then
-// k_unique_children sets block = that sum and rest = parent - block.
+// the block rows' lengths of split j (one task per AggSeg chunk); its last
+// block sets block = that sum and rest = parent - block.
 __global__ void k_unique_sums(const AggSeg* __restrict__ segs, uint32_t nseg,
                               const uint32_t* __restrict__ blockrows,
                               const uint32_t* __restrict__ vid, const uint64_t* __restrict__ vlen,
@@ -1204,7 +1204,7 @@ void ggr_device(const Encoded& e, const std::vector<std::vector<int>>& fd_groups
   }
 
   // Unique columns (single GPU): no table entries, length sums per node
-  // (k_unique_sums / k_unique_children / k_unique_leaf_stats)
+  // (k_unique_sums / k_unique_leaf_stats)
   std::vector<int> ucols;
   std::vector<int32_t> uidx(m, -1);
   if (!dist)
