@@ -293,7 +293,8 @@ def run_ours(args):
         ev1.record(stream)
         barrier()
         clk.mark_end()
-    launches = (lib.kernel_launch_count() - l0) // max(args.steps, 1)
+    launches_total = lib.kernel_launch_count() - l0  # our kernels inside the timed region
+    launches = launches_total // max(args.steps, 1)
     ms = ev0.elapsed_time(ev1) / args.steps
     per = [ev0.elapsed_time(marks[0])] + [a.elapsed_time(b) for a, b in zip(marks, marks[1:])]
     log(f"[rank {rank}] per-step ms: " + " ".join(f"{x:.2f}" for x in per))
@@ -489,7 +490,8 @@ def run_ours(args):
             "kernels_ms_per_step": {k: round(v, 4) for v, k, _ in kern[:16]},
             "kernel_ms_total": round(total_kernel_ms, 4),
             "cpu_baseline": cpu,
-            "gpu_launches": int(launches),
+            "gpu_launches": int(launches_total),
+            "gpu_launches_per_step": int(launches),
             "clocks": clocks,
         }
         print(json.dumps(line), flush=True)
