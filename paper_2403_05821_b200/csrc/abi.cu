@@ -910,17 +910,24 @@ int po_render_prompts(const po_table* t, uint64_t n_entries, const uint64_t* row
     DevBuf<uint64_t> o;
     DevBuf<uint8_t> b;
     uint64_t total = 0;
-    render_prompts_device(dt, n_entries, d_rows, d_offs, d_fields,
+    // the bytes go straight into a device destination; a host destination
+    // gets them through a device buffer
+    auto dst_for = [&](uint64_t tot) -> uint8_t* {
+      if (!out_bytes) return nullptr;
+      if (out_capacity < tot) fail(PO_ERR_SIZE, "render: output buffer too small");
+      if (out_loc == PO_LOC_DEVICE) return out_bytes;
+      b.alloc(std::max<uint64_t>(tot, 1), s);
+      return b.get();
+    };
+    render_prompts_device(dt, n_entries, d_rows, d_offs, d_fields, nfields,
                           std::string(reinterpret_cast<const char*>(sp), sp ? sp_len : 0),
-                          std::string(reinterpret_cast<const char*>(q), q ? q_len : 0), o, b,
-                          total, s);
+                          std::string(reinterpret_cast<const char*>(q), q ? q_len : 0), o, total,
+                          dst_for, s);
     const cudaMemcpyKind k = out_loc == PO_LOC_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
     PO_CUDA(cudaMemcpyAsync(out_offsets, o.get(), (n_entries + 1) * 8, k, s));
     *out_total = total;
-    if (out_bytes) {
-      if (out_capacity < total) fail(PO_ERR_SIZE, "render: output buffer too small");
-      if (total) PO_CUDA(cudaMemcpyAsync(out_bytes, b.get(), total, k, s));
-    }
+    if (out_bytes && out_loc == PO_LOC_HOST && total)
+      PO_CUDA(cudaMemcpyAsync(out_bytes, b.get(), total, k, s));
     sync(s);
   });
 }

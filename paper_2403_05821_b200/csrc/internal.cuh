@@ -367,10 +367,10 @@ void fd_compare_device(const Encoded& e, const std::vector<int32_t>& pa,
 // render_prompt over a schedule (render.cu, objective.hpp:102-131): prompt i
 // at out_bytes[out_off[i] .. out_off[i+1]); schedule arrays on the device.
 void render_prompts_device(const DeviceTable& t, uint64_t n_entries, const uint64_t* rows,
-                           const uint64_t* order_offsets, const int32_t* fields,
+                           const uint64_t* order_offsets, const int32_t* fields, uint64_t n_fields,
                            const std::string& system_prompt, const std::string& question,
-                           DevBuf<uint64_t>& out_off, DevBuf<uint8_t>& out_bytes,
-                           uint64_t& total, cudaStream_t s);
+                           DevBuf<uint64_t>& out_off, uint64_t& total,
+                           const std::function<uint8_t*(uint64_t)>& dst_for, cudaStream_t s);
 // dedup (cost.hpp:171-186) of the one-column table t's strings: expansion
 // map and, per unique in first-occurrence order, its first index.
 void dedup_device(const DeviceTable& t, uint64_t* d_expansion, uint64_t* d_unique_first,
