@@ -1009,12 +1009,16 @@ int po_load_csv(const uint8_t* data, uint64_t len, uint32_t loc, po_csv** out, v
     const uint64_t R = P.n_records;
     auto unterminated = [&](uint64_t r) {
       fail(PO_ERR_STRUCTURAL, "csv: unterminated quoted field starting near line " +
-                                  std::to_string(P.rec_start_line[r]));
+                                  std::to_string(P.start_line(r, s)));
+    };
+    auto wrong_width = [&](uint64_t r, uint64_t cells, uint64_t h) {
+      fail(PO_ERR_STRUCTURAL, "csv: line " + std::to_string(P.start_line(r, s)) + " has " +
+                                  std::to_string(cells) + " cells, expected " + std::to_string(h));
     };
     // load_csv's order of checks (table.hpp:190-214)
     if (R == 0) fail(PO_ERR_STRUCTURAL, "csv: missing header row");
     if (R == 1 && P.unterminated) unterminated(0);
-    const uint64_t H = P.rec_end_cell[0];
+    const uint64_t H = P.end_cell(0, s);
     std::vector<uint64_t> hend(H);
     P.cell_end.download(hend.data(), H);
     uint64_t hbytes = H ? hend[H - 1] : 0;
@@ -1029,17 +1033,22 @@ int po_load_csv(const uint8_t* data, uint64_t len, uint32_t loc, po_csv** out, v
         if (!seen.insert(nm).second) fail(PO_ERR_SCHEMA, "csv: duplicate header field: " + nm);
     }
     uint64_t rows_end = R;  // records [1, rows_end) are data rows
-    for (uint64_t r = 1; r < R; ++r) {
-      const bool last = r + 1 == R;
-      if (last && P.unterminated) unterminated(r);
-      if (last && P.rec_blank[r]) {  // trailing blank line
-        rows_end = r;
-        break;
+    if (R >= 2) {
+      // records before the last: widths checked on the device, the first
+      // wrong one reported
+      const uint64_t bad = P.first_wrong_width(H, s);
+      if (bad < R - 1) {
+        const uint64_t cells = P.end_cell(bad, s) - P.end_cell(bad - 1, s);
+        wrong_width(bad, cells, H);
       }
-      const uint64_t cells = P.rec_end_cell[r] - P.rec_end_cell[r - 1];
-      if (cells != H)
-        fail(PO_ERR_STRUCTURAL, "csv: line " + std::to_string(P.rec_start_line[r]) + " has " +
-                                    std::to_string(cells) + " cells, expected " + std::to_string(H));
+      const uint64_t r = R - 1;  // the last record
+      if (P.unterminated) unterminated(r);
+      if (P.blank(r, s)) {  // trailing blank line
+        rows_end = r;
+      } else {
+        const uint64_t cells = P.end_cell(r, s) - P.end_cell(r - 1, s);
+        if (cells != H) wrong_width(r, cells, H);
+      }
     }
     for (uint64_t i = 0; i < H; ++i)  // Table's constructor (table.hpp:28-33)
       if (names[i].empty())

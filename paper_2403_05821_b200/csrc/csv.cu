@@ -30,7 +30,7 @@ enum : uint8_t { kR = 0, kC, kU, kQ, kP, kA };
 enum : uint8_t { kEmit = 8, kCell = 16, kRec = 32, kBlank = 64, kLine = 128 };
 
 // [state][class]: class 0 '"', 1 ',', 2 '\n', 3 '\r', 4 other
-__constant__ uint8_t c_csv[6][5] = {
+constexpr uint8_t kCsv[6][5] = {
     /* R */ {kQ, kC | kCell, kR | kCell | kRec | kBlank | kLine, kA | kCell | kRec | kBlank | kLine, kU | kEmit},
     /* C */ {kQ, kC | kCell, kR | kCell | kRec | kLine, kA | kCell | kRec | kLine, kU | kEmit},
     /* U */ {kU | kEmit, kC | kCell, kR | kCell | kRec | kLine, kA | kCell | kRec | kLine, kU | kEmit},
@@ -39,11 +39,27 @@ __constant__ uint8_t c_csv[6][5] = {
     /* A */ {kQ, kC | kCell, kR, kA | kCell | kRec | kBlank | kLine, kU | kEmit},
 };
 
-constexpr uint64_t kChunk = 4096;
-
-__device__ __forceinline__ uint32_t cls(uint8_t c) {
-  return c == '"' ? 0u : c == ',' ? 1u : c == '\n' ? 2u : c == '\r' ? 3u : 4u;
+// The table held in registers (a per-lane __constant__ lookup with divergent
+// indices is serialised): per class, byte s of kT8 is the transition from
+// state s; nibble s of kT4 is its next state.
+__host__ __device__ constexpr uint64_t t8_of(int c) {
+  uint64_t v = 0;
+  for (int s = 0; s < 6; ++s) v |= uint64_t(kCsv[s][c]) << (8 * s);
+  return v;
 }
+__host__ __device__ constexpr uint32_t t4_of(int c) {
+  uint32_t v = 0;
+  for (int s = 0; s < 6; ++s) v |= uint32_t(kCsv[s][c] & 7) << (4 * s);
+  return v;
+}
+__device__ __forceinline__ uint64_t t8(uint8_t b) {
+  return b == '"' ? t8_of(0) : b == ',' ? t8_of(1) : b == '\n' ? t8_of(2) : b == '\r' ? t8_of(3) : t8_of(4);
+}
+__device__ __forceinline__ uint32_t t4(uint8_t b) {
+  return b == '"' ? t4_of(0) : b == ',' ? t4_of(1) : b == '\n' ? t4_of(2) : b == '\r' ? t4_of(3) : t4_of(4);
+}
+
+constexpr uint64_t kChunk = 4096;
 
 // Calls f on bytes d[a..b) in order, reading 16 bytes per load (a is
 // kChunk-aligned; the arena base is at least 16-byte aligned: cudaMalloc /
@@ -66,6 +82,54 @@ __device__ __forceinline__ void for_bytes(const uint8_t* __restrict__ d, uint64_
   for (; i < b; ++i) f(d[i]);
 }
 
+// Per 16-byte block, high-bit byte masks (two words) of quotes or CRs, commas
+// and newlines (exact per byte).
+struct BlockMasks {
+  uint64_t qr[2], sep[2], nl[2];
+};
+__device__ __forceinline__ uint64_t eq_mask(uint64_t x, uint64_t c8) {
+  const uint64_t y = x ^ c8;
+  return ~(((y & 0x7F7F7F7F7F7F7F7Full) + 0x7F7F7F7F7F7F7F7Full) | y) & 0x8080808080808080ull;
+}
+__device__ __forceinline__ BlockMasks block_masks(const uint4& w) {
+  BlockMasks m;
+  const uint64_t x[2] = {uint64_t(w.x) | (uint64_t(w.y) << 32), uint64_t(w.z) | (uint64_t(w.w) << 32)};
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    m.qr[h] = eq_mask(x[h], 0x2222222222222222ull) | eq_mask(x[h], 0x0D0D0D0D0D0D0D0Dull);
+    m.sep[h] = eq_mask(x[h], 0x2C2C2C2C2C2C2C2Cull);
+    m.nl[h] = eq_mask(x[h], 0x0A0A0A0A0A0A0A0Aull);
+  }
+  return m;
+}
+
+// Like for_bytes, but a whole aligned 16-byte block is first offered to
+// fast(w, masks), which returns false to have its bytes walked one by one.
+template <class Fast, class F>
+__device__ __forceinline__ void for_blocks(const uint8_t* __restrict__ d, uint64_t a, uint64_t b,
+                                           Fast&& fast, F&& f) {
+  const bool aligned = (reinterpret_cast<uintptr_t>(d) & 15) == 0;
+  uint64_t i = a;
+  if (aligned)
+    for (; i + 16 <= b; i += 16) {
+      const uint4 w = __ldg(reinterpret_cast<const uint4*>(d + i));
+      if (fast(w, block_masks(w))) continue;
+      const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) f(uint8_t(ws[q] >> (8 * k)));
+    }
+  for (; i < b; ++i) f(d[i]);
+}
+
+// state after a block without quotes or CRs from any state but Q: its last
+// byte decides (',' -> C, '\n' -> R, anything else -> U)
+__device__ __forceinline__ uint32_t plain_block_end(const uint4& w) {
+  const uint8_t last = uint8_t(w.w >> 24);
+  return last == ',' ? uint32_t(kC) : last == '\n' ? uint32_t(kR) : uint32_t(kU);
+}
+
 struct Fn {  // transition function of a chunk: 6 x 3-bit end states
   uint32_t v;
 };
@@ -83,15 +147,24 @@ __host__ __device__ constexpr uint32_t fn_identity() {
 __global__ void k_csv_trans(const uint8_t* __restrict__ d, uint64_t len, uint64_t nch, Fn* out) {
   for (uint64_t ch = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; ch < nch;
        ch += uint64_t(gridDim.x) * blockDim.x) {
-    uint8_t st[6] = {0, 1, 2, 3, 4, 5};
+    uint32_t st4[6] = {0, 4, 8, 12, 16, 20};  // 4 x the state of each run
     const uint64_t a = ch * kChunk, b = a + kChunk < len ? a + kChunk : len;
-    for_bytes(d, a, b, [&](uint8_t byte) {
-      const uint32_t c = cls(byte);
+    for_blocks(
+        d, a, b,
+        [&](const uint4& w, const BlockMasks& mk) {
+          if (mk.qr[0] | mk.qr[1]) return false;
+          const uint32_t g = plain_block_end(w) << 2;
 #pragma unroll
-      for (int s = 0; s < 6; ++s) st[s] = c_csv[st[s]][c] & 7;
-    });
+          for (int s = 0; s < 6; ++s) st4[s] = st4[s] == 4u * kQ ? st4[s] : g;
+          return true;
+        },
+        [&](uint8_t byte) {
+          const uint32_t tb = t4(byte);
+#pragma unroll
+          for (int s = 0; s < 6; ++s) st4[s] = ((tb >> st4[s]) & 7u) << 2;
+        });
     uint32_t v = 0;
-    for (int s = 0; s < 6; ++s) v |= uint32_t(st[s]) << (3 * s);
+    for (int s = 0; s < 6; ++s) v |= (st4[s] >> 2) << (3 * s);
     out[ch] = Fn{v};
   }
 }
@@ -101,17 +174,32 @@ __global__ void k_csv_count(const uint8_t* __restrict__ d, uint64_t len, uint64_
                             const Fn* __restrict__ pre, ulonglong4* cnt) {
   for (uint64_t ch = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; ch < nch;
        ch += uint64_t(gridDim.x) * blockDim.x) {
-    uint32_t st = pre[ch].v & 7;  // state at the chunk start (file starts in R)
-    unsigned long long e = 0, cells = 0, recs = 0, lines = 0;
+    uint32_t st8 = (pre[ch].v & 7) << 3;  // 8 x the state at the chunk start (file starts in R)
+    uint32_t e = 0, cells = 0, recs = 0, lines = 0;
     const uint64_t a = ch * kChunk, b = a + kChunk < len ? a + kChunk : len;
-    for_bytes(d, a, b, [&](uint8_t byte) {
-      const uint8_t t = c_csv[st][cls(byte)];
-      st = t & 7;
-      e += (t & kEmit) != 0;
-      cells += (t & kCell) != 0;
-      recs += (t & kRec) != 0;
-      lines += (t & kLine) != 0;
-    });
+    for_blocks(
+        d, a, b,
+        [&](const uint4& w, const BlockMasks& mk) {
+          // outside quotes and not right after a CR: ',' and '\n' end a cell
+          // ('\n' also a record and a line), every other byte is content
+          if ((mk.qr[0] | mk.qr[1]) || st8 == 8u * kQ || st8 == 8u * kA) return false;
+          const uint32_t nn = __popcll(mk.nl[0]) + __popcll(mk.nl[1]);
+          const uint32_t ns = __popcll(mk.sep[0]) + __popcll(mk.sep[1]) + nn;
+          e += 16 - ns;
+          cells += ns;
+          recs += nn;
+          lines += nn;
+          st8 = plain_block_end(w) << 3;
+          return true;
+        },
+        [&](uint8_t byte) {
+          const uint32_t t = uint32_t(t8(byte) >> st8) & 0xFFu;
+          st8 = (t & 7u) << 3;
+          e += (t >> 3) & 1u;  // kEmit
+          cells += (t >> 4) & 1u;
+          recs += (t >> 5) & 1u;
+          lines += t >> 7;
+        });
     cnt[ch] = make_ulonglong4(e, cells, recs, lines);
   }
 }
@@ -122,19 +210,61 @@ __global__ void k_csv_emit(const uint8_t* __restrict__ d, uint64_t len, uint64_t
                            uint64_t* rec_next_line, uint8_t* rec_blank) {
   for (uint64_t ch = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; ch < nch;
        ch += uint64_t(gridDim.x) * blockDim.x) {
-    uint32_t st = pre[ch].v & 7;
+    uint32_t st8 = (pre[ch].v & 7) << 3;
     ulonglong4 p = base[ch];  // running: content byte, cell, record, line increments
     const uint64_t a = ch * kChunk, b = a + kChunk < len ? a + kChunk : len;
     // a chunk's content bytes form one contiguous run of the arena: bytes up
     // to the first 16-byte boundary are stored one by one, then gathered in
     // registers and stored 16 at a time (a sixteenth of the byte stores)
     uint32_t acc[4] = {0u, 0u, 0u, 0u};
-    for_bytes(d, a, b, [&](uint8_t c) {
-      const uint8_t t = c_csv[st][cls(c)];
-      st = t & 7;
+    const uint64_t x0 = p.x;  // the chunk's first content byte
+    for_blocks(d, a, b,
+    [&](const uint4& w, const BlockMasks& mk) {
+      // 16 content bytes (no quote, CR, comma or newline) appended at once
+      // once the output slot is the chunk's own: the slot's tail is filled
+      // and stored, the rest starts the next slot
+      if (mk.qr[0] | mk.qr[1] | mk.sep[0] | mk.sep[1] | mk.nl[0] | mk.nl[1]) return false;
+      const uint32_t k = uint32_t(p.x & 15);
+      if (p.x - k < x0) return false;
+      const uint64_t X0 = uint64_t(w.x) | (uint64_t(w.y) << 32), X1 = uint64_t(w.z) | (uint64_t(w.w) << 32);
+      if (k == 0) {
+        *reinterpret_cast<uint4*>(arena + p.x) = w;
+      } else {
+        const uint32_t sh = 8 * k;  // 8..120
+        uint64_t lo = uint64_t(acc[0]) | (uint64_t(acc[1]) << 32);
+        uint64_t hi = uint64_t(acc[2]) | (uint64_t(acc[3]) << 32);
+        if (sh < 64) {
+          lo |= X0 << sh;
+          hi |= (X1 << sh) | (X0 >> (64 - sh));
+        } else {
+          hi |= sh == 64 ? X0 : (X0 << (sh - 64));
+        }
+        *reinterpret_cast<uint4*>(arena + (p.x - k)) =
+            make_uint4(uint32_t(lo), uint32_t(lo >> 32), uint32_t(hi), uint32_t(hi >> 32));
+        const uint32_t r = 128 - sh;  // bytes k.. of X start the next slot
+        uint64_t nlo, nhi;
+        if (r >= 64) {
+          nlo = r == 64 ? X1 : (X1 >> (r - 64));
+          nhi = 0;
+        } else {
+          nlo = (X0 >> r) | (X1 << (64 - r));
+          nhi = X1 >> r;
+        }
+        acc[0] = uint32_t(nlo);
+        acc[1] = uint32_t(nlo >> 32);
+        acc[2] = uint32_t(nhi);
+        acc[3] = uint32_t(nhi >> 32);
+      }
+      p.x += 16;
+      st8 = st8 == 8u * kQ ? st8 : 8u * kU;
+      return true;
+    },
+    [&](uint8_t c) {
+      const uint32_t t = uint32_t(t8(c) >> st8) & 0xFFu;
+      st8 = (t & 7u) << 3;
       if (t & kEmit) {
         const uint32_t k = uint32_t(p.x & 15);
-        if (p.x - k < base[ch].x) {  // before the chunk's first full 16-byte slot
+        if (p.x - k < x0) {  // before the chunk's first full 16-byte slot
           arena[p.x] = c;
         } else {
           const uint32_t v = uint32_t(c) << (8 * (k & 3));
@@ -162,9 +292,18 @@ __global__ void k_csv_emit(const uint8_t* __restrict__ d, uint64_t len, uint64_t
     });
     // the partial last slot
     const uint32_t k = uint32_t(p.x & 15);
-    if (k && p.x - k >= base[ch].x)
+    if (k && p.x - k >= x0)
       for (uint32_t q = 0; q < k; ++q) arena[p.x - k + q] = uint8_t(acc[q >> 2] >> (8 * (q & 3)));
   }
+}
+
+// first record r in [1, hi) whose cell count (rec_end[r] - rec_end[r - 1])
+// is not h
+__global__ void k_csv_widths(const uint64_t* __restrict__ rec_end, uint64_t hi, uint64_t h,
+                             unsigned long long* first) {
+  for (uint64_t r = 1 + blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; r < hi;
+       r += uint64_t(gridDim.x) * blockDim.x)
+    if (rec_end[r] - rec_end[r - 1] != h) atomicMin(first, (unsigned long long)r);
 }
 
 struct AddU4 {
@@ -225,22 +364,52 @@ void load_csv_device(const uint8_t* d, uint64_t len, CsvParsed& out, cudaStream_
   if (nch)
     PO_LAUNCH(k_csv_emit, grid_for(nch, 128), 128, 0, s, d, len, nch, pre.get(), base.get(),
               out.arena.get(), out.cell_end.get(), rec_end.get(), rec_line.get(), rec_blank.get());
-  out.rec_end_cell.assign(out.n_records, 0);
-  out.rec_start_line.assign(out.n_records, 1);
-  out.rec_blank.assign(out.n_records, 0);
-  std::vector<uint64_t> nl(out.n_records);
-  if (tot.z) {
-    rec_end.download(out.rec_end_cell.data(), tot.z);
-    rec_line.download(nl.data(), tot.z);
-    rec_blank.download(out.rec_blank.data(), tot.z);
-  }
+  out.n_closed = tot.z;
+  out.rec_end = std::move(rec_end);
+  out.rec_line = std::move(rec_line);
+  out.rec_blank = std::move(rec_blank);
   if (pending) {
     const uint64_t ce = tot.x;
     h2d_async(out.cell_end.get() + tot.y, &ce, 8, s);
   }
   sync(s);
-  if (pending) out.rec_end_cell[out.n_records - 1] = out.n_cells;
-  for (uint64_t r = 1; r < out.n_records; ++r) out.rec_start_line[r] = nl[r - 1];
+}
+
+uint64_t CsvParsed::end_cell(uint64_t r, cudaStream_t s) const {
+  if (r >= n_closed) return n_cells;  // the record pending at EOF
+  uint64_t v = 0;
+  PO_CUDA(cudaMemcpyAsync(&v, rec_end.get() + r, 8, cudaMemcpyDeviceToHost, s));
+  sync(s);
+  return v;
+}
+
+uint64_t CsvParsed::start_line(uint64_t r, cudaStream_t s) const {
+  if (r == 0) return 1;
+  uint64_t v = 1;
+  PO_CUDA(cudaMemcpyAsync(&v, rec_line.get() + (r - 1), 8, cudaMemcpyDeviceToHost, s));
+  sync(s);
+  return v;
+}
+
+bool CsvParsed::blank(uint64_t r, cudaStream_t s) const {
+  if (r >= n_closed) return false;
+  uint8_t v = 0;
+  PO_CUDA(cudaMemcpyAsync(&v, rec_blank.get() + r, 1, cudaMemcpyDeviceToHost, s));
+  sync(s);
+  return v != 0;
+}
+
+uint64_t CsvParsed::first_wrong_width(uint64_t h, cudaStream_t s) const {
+  if (n_records < 3) return n_records;
+  DevBuf<unsigned long long> first(1, s);
+  first.fill_bytes(0xFF);
+  // records [1, n_records - 1) all closed inside the text (r < n_closed)
+  const uint64_t hi = n_records - 1;
+  PO_LAUNCH(k_csv_widths, grid_for(hi, 256), 256, 0, s, rec_end.get(), hi, h, first.get());
+  unsigned long long v = 0;
+  first.download(&v, 1);
+  sync(s);
+  return v == ~0ull ? n_records : uint64_t(v);
 }
 
 }  // namespace po

@@ -392,11 +392,19 @@ void replay_unbounded_device(const DeviceTable& pt, int tok, uint64_t* d_input, 
 // line; unterminated: EOF inside quotes (the last record).
 struct CsvParsed {
   uint64_t content_bytes = 0, n_cells = 0, n_records = 0;
+  uint64_t n_closed = 0;  // records closed inside the text (a pending one follows at EOF)
   bool unterminated = false;
   DevBuf<uint8_t> arena;
   DevBuf<uint64_t> cell_end;
-  std::vector<uint64_t> rec_end_cell, rec_start_line;
-  std::vector<uint8_t> rec_blank;
+  DevBuf<uint64_t> rec_end, rec_line;  // [n_closed]: end cell, line after the record
+  DevBuf<uint8_t> rec_blank;           // [n_closed]
+  // host reads of single records (a small copy each; the per-record checks
+  // run on the device: first_wrong_width)
+  uint64_t end_cell(uint64_t r, cudaStream_t s) const;
+  uint64_t start_line(uint64_t r, cudaStream_t s) const;
+  bool blank(uint64_t r, cudaStream_t s) const;
+  // first record in [1, n_records - 1) whose cell count is not h, else n_records
+  uint64_t first_wrong_width(uint64_t h, cudaStream_t s) const;
 };
 void load_csv_device(const uint8_t* d, uint64_t len, CsvParsed& out, cudaStream_t s);
 
