@@ -110,9 +110,12 @@ __device__ __forceinline__ void for_blocks(const uint8_t* __restrict__ d, uint64
                                            Fast&& fast, F&& f) {
   const bool aligned = (reinterpret_cast<uintptr_t>(d) & 15) == 0;
   uint64_t i = a;
-  if (aligned)
+  if (aligned && i + 16 <= b) {
+    // the next block's load is issued before this one is processed
+    uint4 nx = __ldg(reinterpret_cast<const uint4*>(d + i));
     for (; i + 16 <= b; i += 16) {
-      const uint4 w = __ldg(reinterpret_cast<const uint4*>(d + i));
+      const uint4 w = nx;
+      if (i + 32 <= b) nx = __ldg(reinterpret_cast<const uint4*>(d + i + 16));
       if (fast(w, block_masks(w))) continue;
       const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
@@ -120,6 +123,7 @@ __device__ __forceinline__ void for_blocks(const uint8_t* __restrict__ d, uint64
 #pragma unroll
         for (int k = 0; k < 4; ++k) f(uint8_t(ws[q] >> (8 * k)));
     }
+  }
   for (; i < b; ++i) f(d[i]);
 }
 
@@ -204,6 +208,80 @@ __global__ void k_csv_count(const uint8_t* __restrict__ d, uint64_t len, uint64_
   }
 }
 
+__device__ __forceinline__ void shl128(uint64_t& lo, uint64_t& hi, uint32_t s) {  // s < 128
+  if (s == 0) return;
+  if (s < 64) {
+    hi = (hi << s) | (lo >> (64 - s));
+    lo <<= s;
+  } else {
+    hi = lo << (s - 64);
+    lo = 0;
+  }
+}
+__device__ __forceinline__ void shr128(uint64_t& lo, uint64_t& hi, uint32_t s) {  // s < 128
+  if (s == 0) return;
+  if (s < 64) {
+    lo = (lo >> s) | (hi << (64 - s));
+    hi >>= s;
+  } else {
+    lo = hi >> (s - 64);
+    hi = 0;
+  }
+}
+__device__ __forceinline__ void keep_low_bytes128(uint64_t& lo, uint64_t& hi, uint32_t n) {  // n <= 16
+  if (n < 8) {
+    lo &= n ? (~0ull >> (64 - 8 * n)) : 0ull;
+    hi = 0;
+  } else if (n < 16) {
+    hi &= n > 8 ? (~0ull >> (64 - 8 * (n - 8))) : 0ull;
+  }
+}
+
+// Writes a chunk's content bytes: one contiguous run of the arena starting at
+// x0. Bytes up to the first 16-byte boundary at or after x0 are stored one by
+// one; after that they gather in a 16-byte register slot (lo, hi) stored
+// whole when full.
+struct EmitRun {
+  uint8_t* arena;
+  uint64_t x0;
+  uint64_t x;  // next content byte
+  uint64_t lo = 0, hi = 0;
+  // the low n (<= 16) bytes of (a, b)
+  __device__ __forceinline__ void append(uint64_t a, uint64_t b, uint32_t n) {
+    while (n && (x & ~uint64_t(15)) < x0) {  // the slot is shared with the previous chunk
+      arena[x++] = uint8_t(a);
+      shr128(a, b, 8);
+      --n;
+    }
+    if (!n) return;
+    keep_low_bytes128(a, b, n);
+    const uint32_t k = uint32_t(x & 15);
+    uint64_t sa = a, sb = b;
+    shl128(sa, sb, 8 * k);
+    lo |= sa;
+    hi |= sb;
+    if (k + n >= 16) {
+      *reinterpret_cast<uint4*>(arena + (x - k)) =
+          make_uint4(uint32_t(lo), uint32_t(lo >> 32), uint32_t(hi), uint32_t(hi >> 32));
+      // what did not fit starts the next slot (nothing when k == 0: n == 16)
+      lo = hi = 0;
+      if (k) {
+        lo = a;
+        hi = b;
+        shr128(lo, hi, 8 * (16 - k));
+      }
+    }
+    x += n;
+  }
+  __device__ __forceinline__ void put(uint8_t c) { append(c, 0, 1); }
+  // the partial last slot
+  __device__ __forceinline__ void finish() {
+    const uint32_t k = uint32_t(x & 15);
+    if (k && x - k >= x0)
+      for (uint32_t q = 0; q < k; ++q) arena[x - k + q] = uint8_t((q < 8 ? lo : hi) >> (8 * (q & 7)));
+  }
+};
+
 __global__ void k_csv_emit(const uint8_t* __restrict__ d, uint64_t len, uint64_t nch,
                            const Fn* __restrict__ pre, const ulonglong4* __restrict__ base,
                            uint8_t* arena, uint64_t* cell_end, uint64_t* rec_end_cell,
@@ -212,88 +290,66 @@ __global__ void k_csv_emit(const uint8_t* __restrict__ d, uint64_t len, uint64_t
        ch += uint64_t(gridDim.x) * blockDim.x) {
     uint32_t st8 = (pre[ch].v & 7) << 3;
     ulonglong4 p = base[ch];  // running: content byte, cell, record, line increments
+    EmitRun run{arena, p.x, p.x};
     const uint64_t a = ch * kChunk, b = a + kChunk < len ? a + kChunk : len;
-    // a chunk's content bytes form one contiguous run of the arena: bytes up
-    // to the first 16-byte boundary are stored one by one, then gathered in
-    // registers and stored 16 at a time (a sixteenth of the byte stores)
-    uint32_t acc[4] = {0u, 0u, 0u, 0u};
-    const uint64_t x0 = p.x;  // the chunk's first content byte
-    for_blocks(d, a, b,
-    [&](const uint4& w, const BlockMasks& mk) {
-      // 16 content bytes (no quote, CR, comma or newline) appended at once
-      // once the output slot is the chunk's own: the slot's tail is filled
-      // and stored, the rest starts the next slot
-      if (mk.qr[0] | mk.qr[1] | mk.sep[0] | mk.sep[1] | mk.nl[0] | mk.nl[1]) return false;
-      const uint32_t k = uint32_t(p.x & 15);
-      if (p.x - k < x0) return false;
-      const uint64_t X0 = uint64_t(w.x) | (uint64_t(w.y) << 32), X1 = uint64_t(w.z) | (uint64_t(w.w) << 32);
-      if (k == 0) {
-        *reinterpret_cast<uint4*>(arena + p.x) = w;
-      } else {
-        const uint32_t sh = 8 * k;  // 8..120
-        uint64_t lo = uint64_t(acc[0]) | (uint64_t(acc[1]) << 32);
-        uint64_t hi = uint64_t(acc[2]) | (uint64_t(acc[3]) << 32);
-        if (sh < 64) {
-          lo |= X0 << sh;
-          hi |= (X1 << sh) | (X0 >> (64 - sh));
-        } else {
-          hi |= sh == 64 ? X0 : (X0 << (sh - 64));
-        }
-        *reinterpret_cast<uint4*>(arena + (p.x - k)) =
-            make_uint4(uint32_t(lo), uint32_t(lo >> 32), uint32_t(hi), uint32_t(hi >> 32));
-        const uint32_t r = 128 - sh;  // bytes k.. of X start the next slot
-        uint64_t nlo, nhi;
-        if (r >= 64) {
-          nlo = r == 64 ? X1 : (X1 >> (r - 64));
-          nhi = 0;
-        } else {
-          nlo = (X0 >> r) | (X1 << (64 - r));
-          nhi = X1 >> r;
-        }
-        acc[0] = uint32_t(nlo);
-        acc[1] = uint32_t(nlo >> 32);
-        acc[2] = uint32_t(nhi);
-        acc[3] = uint32_t(nhi >> 32);
-      }
-      p.x += 16;
-      st8 = st8 == 8u * kQ ? st8 : 8u * kU;
-      return true;
-    },
-    [&](uint8_t c) {
-      const uint32_t t = uint32_t(t8(c) >> st8) & 0xFFu;
-      st8 = (t & 7u) << 3;
-      if (t & kEmit) {
-        const uint32_t k = uint32_t(p.x & 15);
-        if (p.x - k < x0) {  // before the chunk's first full 16-byte slot
-          arena[p.x] = c;
-        } else {
-          const uint32_t v = uint32_t(c) << (8 * (k & 3));
-          switch (k >> 2) {
-            case 0: acc[0] |= v; break;
-            case 1: acc[1] |= v; break;
-            case 2: acc[2] |= v; break;
-            default: acc[3] |= v; break;
+    auto end_cell = [&]() { cell_end[p.y++] = run.x; };
+    auto end_record = [&](bool blank) {
+      rec_end_cell[p.z] = p.y;
+      rec_next_line[p.z] = 1 + p.w;  // start line of the record that follows
+      rec_blank[p.z] = blank ? 1 : 0;
+      ++p.z;
+    };
+    for_blocks(
+        d, a, b,
+        [&](const uint4& w, const BlockMasks& mk) {
+          // a block without quotes or CRs, outside quotes and not right after
+          // a CR: ',' ends a cell, '\n' a cell, a record and a line, every
+          // other byte is content; the runs between separators are appended
+          // 16 bytes at a time
+          if ((mk.qr[0] | mk.qr[1]) || st8 == 8u * kQ || st8 == 8u * kA) return false;
+          const uint64_t X0 = uint64_t(w.x) | (uint64_t(w.y) << 32), X1 = uint64_t(w.z) | (uint64_t(w.w) << 32);
+          bool rec_start = st8 == 8u * kR;  // no content since the record began
+          uint32_t used = 0;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            uint64_t sm = mk.sep[h] | mk.nl[h];
+            while (sm) {
+              const uint32_t bit = uint32_t(__ffsll((long long)sm) - 1);
+              sm &= sm - 1;
+              const uint32_t j = 8 * h + (bit >> 3);
+              if (j > used) {
+                uint64_t s0 = X0, s1 = X1;
+                shr128(s0, s1, 8 * used);
+                run.append(s0, s1, j - used);
+                rec_start = false;
+              }
+              const bool nl = (mk.nl[h] >> bit) & 1;
+              end_cell();
+              if (nl) {
+                ++p.w;
+                end_record(rec_start);
+              }
+              rec_start = nl;
+              used = j + 1;
+            }
           }
-          if (k == 15) {
-            *reinterpret_cast<uint4*>(arena + (p.x - 15)) = make_uint4(acc[0], acc[1], acc[2], acc[3]);
-            acc[0] = acc[1] = acc[2] = acc[3] = 0u;
+          if (used < 16) {
+            uint64_t s0 = X0, s1 = X1;
+            shr128(s0, s1, 8 * used);
+            run.append(s0, s1, 16 - used);
           }
-        }
-        ++p.x;
-      }
-      if (t & kLine) ++p.w;
-      if (t & kCell) cell_end[p.y++] = p.x;
-      if (t & kRec) {
-        rec_end_cell[p.z] = p.y;
-        rec_next_line[p.z] = 1 + p.w;  // start line of the record that follows
-        rec_blank[p.z] = (t & kBlank) ? 1 : 0;
-        ++p.z;
-      }
-    });
-    // the partial last slot
-    const uint32_t k = uint32_t(p.x & 15);
-    if (k && p.x - k >= x0)
-      for (uint32_t q = 0; q < k; ++q) arena[p.x - k + q] = uint8_t(acc[q >> 2] >> (8 * (q & 3)));
+          st8 = plain_block_end(w) << 3;
+          return true;
+        },
+        [&](uint8_t c) {
+          const uint32_t t = uint32_t(t8(c) >> st8) & 0xFFu;
+          st8 = (t & 7u) << 3;
+          if (t & kEmit) run.put(c);
+          if (t & kLine) ++p.w;
+          if (t & kCell) end_cell();
+          if (t & kRec) end_record((t & kBlank) != 0);
+        });
+    run.finish();
   }
 }
 
