@@ -326,6 +326,31 @@ __device__ __forceinline__ uint64_t load8_unaligned(const uint8_t* a, const uint
   return (w0 >> sh) | (w1 << (64 - sh));
 }
 
+// Index of the first byte where a[0, n) and b[0, n) differ, or n. 32 bytes
+// per step with every load of the step issued before the first compare (a
+// per-8-byte loop waits a full load latency per step on long common
+// prefixes).
+__device__ __forceinline__ uint64_t first_diff(const uint8_t* a, const uint8_t* b, uint64_t n,
+                                               const uint8_t* limit) {
+  for (uint64_t t = 0; t < n; t += 32) {
+    uint64_t x[4], y[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const bool in = t + 8 * u < n;
+      x[u] = in ? load8_unaligned(a + t + 8 * u, limit) : 0;
+      y[u] = in ? load8_unaligned(b + t + 8 * u, limit) : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint64_t tt = t + 8 * u;
+      if (tt >= n) return n;
+      const uint64_t d = mask_low_bytes(x[u] ^ y[u], n - tt >= 8 ? 8u : uint32_t(n - tt));
+      if (d) return tt + uint64_t(__ffsll((long long)d) - 1) / 8;
+    }
+  }
+  return n;
+}
+
 __device__ __forceinline__ uint64_t warp_sum_u64(uint64_t v) {
   for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
   return v;

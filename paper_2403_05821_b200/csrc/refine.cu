@@ -155,13 +155,7 @@ __device__ __forceinline__ uint64_t sym_lcp(const RefineKey& K, uint32_t a, uint
   const uint8_t* pa = K.arena + (oa + st) * us;
   const uint8_t* pb = K.arena + (ob + st) * us;
   const uint8_t* lim = K.arena + K.arena_bytes;
-  const uint64_t nb = n * us;
-  for (uint64_t t = 0; t < nb; t += 8) {
-    const uint64_t d = mask_low_bytes(load8_unaligned(pa + t, lim) ^ load8_unaligned(pb + t, lim),
-                                      nb - t >= 8 ? 8u : uint32_t(nb - t));
-    if (d) return (t + uint64_t(__ffsll((long long)d) - 1) / 8) / us;
-  }
-  return n;
+  return first_diff(pa, pb, n * us, lim) / us;
 }
 
 __global__ void k_skip_init(const uint8_t* flags, const int* count, uint32_t* seg_skip) {
@@ -172,12 +166,26 @@ __global__ void k_skip_init(const uint8_t* flags, const int* count, uint32_t* se
 
 __global__ void k_skip_lcp(const uint32_t* items, const uint32_t* head, const int* count,
                            RefineKey K, uint32_t* seg_skip) {
+  // items of a segment are contiguous: the lanes of a warp that share a head
+  // take their minimum first (one atomic per segment per warp; a segment
+  // holding most items would otherwise serialise on one address)
   const uint32_t A = uint32_t(*count);
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < A; i += gridDim.x * blockDim.x) {
-    const uint32_t h = head[i];
-    if (h == i) continue;
-    const uint64_t l = sym_lcp(K, items[i], items[h], K.item_off[items[i]]);
-    atomicMin(&seg_skip[h], uint32_t(l < 0xFFFFFFFEull ? l : 0xFFFFFFFEull));
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t stride = gridDim.x * blockDim.x;
+  for (uint32_t base = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); base < A; base += stride) {
+    const uint32_t i = base + lane;
+    uint32_t h = 0xFFFFFFFFu, v = 0xFFFFFFFFu;
+    if (i < A) {
+      h = head[i];
+      if (h == i) h = 0xFFFFFFFFu;
+      else {
+        const uint64_t l = sym_lcp(K, items[i], items[h], K.item_off[items[i]]);
+        v = uint32_t(l < 0xFFFFFFFEull ? l : 0xFFFFFFFEull);
+      }
+    }
+    const unsigned peers = __match_any_sync(0xffffffffu, h);
+    v = __reduce_min_sync(peers, v);
+    if (h != 0xFFFFFFFFu && int(lane) == __ffs(peers) - 1) atomicMin(&seg_skip[h], v);
   }
 }
 

@@ -98,8 +98,8 @@ __global__ void k_word_syms(const uint8_t* __restrict__ arena, const uint64_t* _
   }
 }
 
-// Common prefix (in key units: bytes or symbols) of two keys, 8 bytes per
-// step; word mode also counts the separators (= whole tokens) inside it.
+// Common prefix (in key units: bytes or symbols) of two keys (first_diff);
+// word mode also counts the separators (= whole tokens) inside it.
 struct Lcp {
   uint64_t units, tokens;
 };
@@ -107,28 +107,38 @@ __device__ __forceinline__ Lcp key_lcp(const uint8_t* a, uint64_t la, const uint
                                        const uint8_t* lim, int word) {
   const uint32_t us = word ? 2 : 1;  // bytes per key unit
   const uint64_t n = (la < lb ? la : lb) * us;
+  const uint64_t units = first_diff(a, b, n, lim) / us;
   uint64_t tokens = 0;
-  for (uint64_t i = 0; i < n; i += 8) {
-    const uint64_t x = load8_unaligned(a + i, lim), y = load8_unaligned(b + i, lim);
-    const uint32_t take = n - i >= 8 ? 8u : uint32_t(n - i);
-    const uint64_t d = mask_low_bytes(x ^ y, take);
-    const uint32_t same = d ? uint32_t(__ffsll((long long)d) - 1) / 8 : take;  // equal bytes
-    if (word)
-      for (uint32_t k = 0; k + 2 <= same; k += 2) tokens += ((x >> (8 * k)) & 0xFFFF) == kSymSep;
-    if (d) return {(i + same) / us, tokens};
-  }
-  return {n / us, tokens};
+  if (word)  // separators among the common prefix's symbols (bytes just read: cache hits)
+    for (uint64_t i = 0; i < 2 * units; i += 8) {
+      const uint64_t x = load8_unaligned(a + i, lim);
+      const uint64_t take = 2 * units - i < 8 ? 2 * units - i : 8;
+      for (uint32_t k = 0; k + 2 <= take; k += 2) tokens += ((x >> (8 * k)) & 0xFFFF) == kSymSep;
+    }
+  return {units, tokens};
 }
 
 __global__ void k_lcp_first(const uint8_t* __restrict__ keys, const uint64_t* __restrict__ off,
                             uint64_t n, const uint8_t* lim, int word, unsigned long long* out) {
+  // one atomic per block: a million atomics on one address serialise
   const uint32_t us = word ? 2 : 1;
+  unsigned long long mn = ~0ull;
   for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
        i += uint64_t(gridDim.x) * blockDim.x) {
     const Lcp l = key_lcp(keys + off[0] * us, off[1] - off[0], keys + off[i] * us,
                           off[i + 1] - off[i], lim, word);
-    atomicMin(out, (unsigned long long)l.units);
+    mn = l.units < mn ? l.units : mn;
   }
+  for (int d = 16; d > 0; d >>= 1) {
+    const unsigned long long o = __shfl_xor_sync(0xffffffffu, mn, d);
+    mn = o < mn ? o : mn;
+  }
+  __shared__ unsigned long long s_min;
+  if (threadIdx.x == 0) s_min = ~0ull;
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0 && mn != ~0ull) atomicMin(&s_min, mn);
+  __syncthreads();
+  if (threadIdx.x == 0 && s_min != ~0ull) atomicMin(out, s_min);
 }
 
 // lcp[p] = LCP in tokens of sorted positions p-1 and p (lcp[0] = 0)
