@@ -118,6 +118,16 @@ __device__ __forceinline__ uint32_t esc_flags32(uint32_t x) {
   return ctrl | z1 | z2;
 }
 
+constexpr uint32_t kExtraBig = 0xFFFFFFFFu;
+
+// extra bytes json_escape adds to arena[o, e), one thread (cells too long for
+// k_cell_esc_extra's 32-bit counts)
+__device__ uint64_t esc_extra_serial(const uint8_t* arena, uint64_t o, uint64_t e) {
+  uint64_t x = 0;
+  for (uint64_t i = o; i < e; ++i) x += esc_len_b(arena[i]) - 1;
+  return x;
+}
+
 // Escaped-length extras of every cell (escaped length = len + extra). A
 // warp takes 32 consecutive cells — one contiguous byte range of the arena —
 // and scans the range once with coalesced 16-byte loads; a byte to escape
@@ -172,12 +182,17 @@ __global__ void __launch_bounds__(kEscWarps * 32)
         }
     }
     __syncwarp();
-    if (lane < nc) extra[c0 + lane] = s_cnt[wid][lane];
+    if (lane < nc) {
+      // a cell whose extra may not fit 32 bits is summed by its reader instead
+      const bool big = s_off[wid][lane + 1] - s_off[wid][lane] > 0xFFFFFFFFull / 6;
+      extra[c0 + lane] = big ? kExtraBig : s_cnt[wid][lane];
+    }
     __syncwarp();
   }
 }
 
-__global__ void k_prompt_len_cells(const uint64_t* __restrict__ offsets,
+__global__ void k_prompt_len_cells(const uint8_t* __restrict__ arena,
+                                   const uint64_t* __restrict__ offsets,
                                    const uint32_t* __restrict__ extra, uint64_t n_rows, uint32_t m,
                                    Sched sc, uint64_t n_entries,
                                    const uint64_t* __restrict__ name_esc_len, uint64_t prefix_len,
@@ -194,7 +209,10 @@ __global__ void k_prompt_len_cells(const uint64_t* __restrict__ offsets,
         break;
       }
       const uint64_t c = r * m + f;
-      tot += (p > a ? 2 : 0) + 1 + name_esc_len[f] + 4 + (offsets[c + 1] - offsets[c]) + extra[c] + 1;
+      const uint64_t o = offsets[c], len = offsets[c + 1] - o;
+      uint64_t x = extra[c];
+      if (x == kExtraBig) x = esc_extra_serial(arena, o, o + len);  // a cell of > 700 MB
+      tot += (p > a ? 2 : 0) + 1 + name_esc_len[f] + 4 + len + x + 1;
     }
     out_len[i] = prefix_len + 2 + tot;
   }
@@ -467,12 +485,13 @@ void render_prompts_device(const DeviceTable& t, uint64_t n_entries, const uint6
   DevBuf<int> err(1, s);
   err.zero();
   const uint64_t cells = t.n * uint64_t(m);
+  int herr = 0;
   if (cells && n_fields * 2 >= cells) {
     // dense schedule: escaped lengths of all cells in storage order
     DevBuf<uint32_t> extra(cells, s);
     PO_LAUNCH(k_cell_esc_extra, grid_for(cells, kEscWarps * 32), kEscWarps * 32, 0, s, t.arena,
               t.offsets, cells, extra.get());
-    PO_LAUNCH(k_prompt_len_cells, grid_for(n_entries, 256), 256, 0, s, t.offsets, extra.get(),
+    PO_LAUNCH(k_prompt_len_cells, grid_for(n_entries, 256), 256, 0, s, t.arena, t.offsets, extra.get(),
               t.n, m, sc, n_entries, d_name_len.get(), uint64_t(prefix.size()), lens.get(),
               err.get());
   } else {
@@ -484,7 +503,6 @@ void render_prompts_device(const DeviceTable& t, uint64_t n_entries, const uint6
   PO_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, lens.get(), out_off.get(), int64_t(n_entries + 1), s));
   DevBuf<uint8_t> tmp(tb, s);
   PO_CUDA(cub::DeviceScan::ExclusiveSum(tmp.get(), tb, lens.get(), out_off.get(), int64_t(n_entries + 1), s));
-  int herr = 0;
   err.download(&herr, 1);
   PO_CUDA(cudaMemcpyAsync(&total, out_off.get() + n_entries, 8, cudaMemcpyDeviceToHost, s));
   sync(s);
