@@ -177,8 +177,11 @@ int po_fd_compare(const po_table* t, uint32_t n_pairs, const int32_t* pair_a,
  * prompt i = out_bytes[out_offsets[i] .. out_offsets[i+1]). Call with
  * out_bytes == NULL to get the total size in *out_total (out_offsets is
  * filled either way, n_entries + 1 values); then again with a buffer of at
- * least that many bytes (else PO_ERR_SIZE). Outputs at out_location. A row or
- * field outside the table -> PO_ERR_OUT_OF_RANGE (Table::cell). */
+ * least that many bytes (else PO_ERR_SIZE, checked before any byte is
+ * written). Outputs at out_location; a device out_bytes is written in place
+ * (any alignment; bytes past out_total are untouched), a size query only
+ * computes lengths. A row or field outside the table -> PO_ERR_OUT_OF_RANGE
+ * (Table::cell). */
 int po_render_prompts(const po_table* t, uint64_t n_entries, const uint64_t* row_ids,
                       const uint64_t* order_offsets, const int32_t* order_fields,
                       uint32_t sched_location, const uint8_t* system_prompt,
