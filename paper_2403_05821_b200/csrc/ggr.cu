@@ -808,20 +808,33 @@ __global__ void k_dbg_perm(const uint32_t* pos, uint64_t n, unsigned* seen, unsi
 
 
 // Root partner sums: psum[colbase[c]+vid(r,c)][k] += len(r, partner k of c).
+// A warp takes 32 consecutive rows of one column that has partners; lanes
+// holding the same value add their partner lengths first (labeled partition)
+// and one lane per value issues the atomic (a Zipf-hot value otherwise
+// serialises on one address: C3's movie_title).
 __global__ void k_root_psum(const uint32_t* vid, uint64_t n, uint32_t m, uint32_t K,
                             const int32_t* dpart, const uint32_t* npart, const uint64_t* vlen,
                             const uint64_t* colbase, unsigned long long* psum) {
-  const uint64_t total = n * m;
-  for (uint64_t t = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; t < total;
-       t += uint64_t(gridDim.x) * blockDim.x) {
-    const uint64_t r = t / m;
-    const uint32_t c = uint32_t(t - r * m);
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t ntiles = (n + 31) / 32;
+  const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  auto tile32 = cg::tiled_partition<32>(cg::this_thread_block());
+  for (uint64_t w = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5; w < ntiles * m;
+       w += nwarps) {
+    const uint32_t c = uint32_t(w % m);
     const uint32_t np = npart[c];
-    if (!np) continue;
-    const uint64_t e = colbase[c] + vid[t];
+    if (!np) continue;  // warp-uniform
+    const uint64_t r = (w / m) * 32 + lane;
+    const bool valid = r < n;
+    const uint32_t v = valid ? vid[r * m + c] : 0xFFFFFFFFu;
+    auto g = cg::labeled_partition(tile32, v);
+    const uint64_t e = colbase[c] + v;
     for (uint32_t k = 0; k < np; ++k) {
       const int32_t p = dpart[c * K + k];
-      atomicAdd(&psum[e * K + k], (unsigned long long)vlen[colbase[p] + vid[r * m + p]]);
+      const unsigned long long l =
+          valid ? (unsigned long long)vlen[colbase[p] + vid[r * m + p]] : 0ull;
+      const unsigned long long sum = cg::reduce(g, l, cg::plus<unsigned long long>());
+      if (valid && g.thread_rank() == 0) atomicAdd(&psum[e * K + k], sum);
     }
   }
 }
