@@ -24,7 +24,12 @@ __global__ void k_first_row(const uint32_t* __restrict__ vid, uint64_t n, uint32
        t += uint64_t(gridDim.x) * blockDim.x) {
     const uint32_t c = uint32_t(t % m);
     if (!used[c]) continue;
-    atomicMin(&first[colbase[c] + vid[t]], uint32_t(t / m));
+    // values only decrease: a row not below the (possibly stale, never
+    // smaller) value read skips the atomic — hot values (a two-valued column)
+    // otherwise serialise on one address
+    uint32_t* f = &first[colbase[c] + vid[t]];
+    const uint32_t r = uint32_t(t / m);
+    if (*f > r) atomicMin(f, r);
   }
 }
 

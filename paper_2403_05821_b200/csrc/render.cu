@@ -395,7 +395,7 @@ __global__ void __launch_bounds__(kRenderWarps * 32)
 __global__ void k_first_index(const uint32_t* vid, uint64_t n, uint32_t* first) {
   for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
        i += uint64_t(gridDim.x) * blockDim.x)
-    atomicMin(&first[vid[i]], uint32_t(i));
+    if (first[vid[i]] > uint32_t(i)) atomicMin(&first[vid[i]], uint32_t(i));  // see k_first_row (fd.cu)
 }
 
 __global__ void k_is_first(const uint32_t* vid, uint64_t n, const uint32_t* first, uint32_t* flag) {
