@@ -64,3 +64,34 @@ def test_csv_c2_scale():
     assert got.field_names == t.field_names and got.row_count() == t.row_count()
     assert np.array_equal(got.offsets, t.offsets) and np.array_equal(got.arena[: got.cell_bytes],
                                                                      t.arena[: t.cell_bytes])
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_csv_block_paths(seed):
+    # texts of 20-200 KB made mostly of quote-free 16-byte blocks with commas,
+    # LF / CRLF line ends, blank lines, runs of empty cells and rare quoted
+    # cells: the transition, count and emit passes take their 16-byte block
+    # paths (and fall back to bytes around quotes and CRs) across many 4 KB
+    # chunks; compared with the reference reader (table or error)
+    rng = random.Random(1000 + seed)
+    R = _ref()
+    width = rng.randint(1, 7)
+    eol = rng.choice([b"\n", b"\r\n"])
+    # seeds 0, 3: blank lines; 1, 4: wrong widths (errors); 2, 5: clean tables
+    p_blank = 0.03 if seed % 3 == 0 else 0.0
+    p_wide = 0.03 if seed % 3 == 1 else 0.0
+    lines = [b",".join(b"h%d" % i for i in range(width))]
+    for _ in range(rng.randint(100, 1500)):
+        if rng.random() < p_blank:
+            lines.append(b"")  # a blank line (an error unless it is the last)
+            continue
+        cells = []
+        for _ in range(width if rng.random() >= p_wide else rng.randint(1, width + 2)):
+            k = rng.choice([0, 0, 1, 5, 15, 16, 17, 40, 120])
+            v = bytes(rng.choice(b"abcdefghij klmnop") for _ in range(k))
+            if rng.random() < 0.02:
+                v = b'"' + v.replace(b'"', b'""') + b',"'
+            cells.append(v)
+        lines.append(b",".join(cells))
+    d = eol.join(lines) + (eol if rng.random() < 0.7 else b"")
+    assert outcome(po.load_csv, d) == outcome(R.load_csv, d)
