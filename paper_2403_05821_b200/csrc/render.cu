@@ -342,6 +342,56 @@ __device__ __forceinline__ void stage_append(Stage& st, const uint8_t* src, uint
   __syncwarp();
 }
 
+// Bytes [r, r + 4) of src[0, len) (r may be negative or past the end: those
+// bytes are garbage, masked by the caller); only aligned words holding a
+// byte of [0, len) are read.
+__device__ __forceinline__ uint32_t word_at(const uint8_t* src, int32_t r, int32_t len) {
+  const uintptr_t sa = reinterpret_cast<uintptr_t>(src) + intptr_t(r);
+  const uint32_t sh = uint32_t(sa & 3);
+  const int32_t ra = r - int32_t(sh);
+  const uint32_t* A = reinterpret_cast<const uint32_t*>(sa - sh);
+  const uint32_t lo = (ra > -4 && ra < len) ? __ldg(A) : 0u;
+  const uint32_t hi = (ra > -8 && ra + 4 < len) ? __ldg(A + 1) : 0u;
+  return __byte_perm(lo, hi, 0x3210u + 0x1111u * sh);
+}
+// byte mask of the word bytes whose offset (relative to the word start r)
+// falls in [lo, hi)
+__device__ __forceinline__ uint32_t range_keep(int32_t r, int32_t lo, int32_t hi) {
+  const int32_t b0 = max(lo - r, 0), b1 = min(hi - r, 4);
+  return b1 > b0 ? (0xFFFFFFFFu >> (8 * (4 - (b1 - b0)))) << (8 * b0) : 0u;
+}
+
+// A field's name template a[0, la) followed by its value b[0, lb), escaped:
+// one copy step when both fit one 32-word window and the value has nothing
+// to escape (most short cells), else the two appends.
+__device__ __forceinline__ void stage_append_pair(Stage& st, const uint8_t* a, uint64_t la,
+                                                  const uint8_t* b, uint64_t lb, uint32_t lane) {
+  if (la + lb + 4 <= 128) {
+    stage_ensure(st, 132, lane);
+    __syncwarp();
+    const uint32_t bp = st.bp;
+    const uint32_t head = bp & 3u;
+    const int32_t LA = int32_t(la), T = int32_t(la + lb);
+    if (uint32_t(T) <= 128u - head) {
+      const int32_t r0 = int32_t(4 * lane) - int32_t(head);  // word start, relative to a[0]
+      const uint32_t va = word_at(a, r0, LA), vb = word_at(b, r0 - LA, T - LA);
+      const uint32_t ka = range_keep(r0, 0, LA), kb = range_keep(r0, LA, T);
+      if (!__any_sync(kFullMask, (esc_flags32(vb) & kb) != 0)) {
+        uint32_t* buf32 = reinterpret_cast<uint32_t*>(st.buf);
+        const uint32_t val = (va & ka) | (vb & kb), keep = ka | kb;
+        const uint32_t w = (bp >> 2) + lane;
+        if (keep == ~0u) buf32[w] = val;
+        else if (keep) buf32[w] = (buf32[w] & ~keep) | (val & keep);
+        st.bp = bp + uint32_t(T);
+        __syncwarp();
+        return;
+      }
+    }
+  }
+  stage_append<false>(st, a, la, lane);
+  stage_append<true>(st, b, lb, lane);
+}
+
 __global__ void __launch_bounds__(kRenderWarps * 32)
     k_prompt_write(const uint8_t* __restrict__ arena, const uint64_t* __restrict__ offsets,
                    uint32_t m, Sched sc, uint64_t n_entries, uint64_t per_warp,
@@ -382,8 +432,7 @@ __global__ void __launch_bounds__(kRenderWarps * 32)
       for (uint32_t k = 0; k < cnt; ++k) {
         const uint64_t o = __shfl_sync(kFullMask, co, k), l = __shfl_sync(kFullMask, cl, k);
         const uint64_t tO = __shfl_sync(kFullMask, to, k), tL = __shfl_sync(kFullMask, tl, k);
-        stage_append<false>(st, tmpl + tO, tL, lane);  // [{ or ", ]"name": "
-        stage_append<true>(st, arena + o, l, lane);
+        stage_append_pair(st, tmpl + tO, tL, arena + o, l, lane);  // [{ or ", ]"name": "value
       }
     }
     if (a != b) stage_put(st, 0x7D22u, 2, lane);  // "}
