@@ -629,6 +629,14 @@ __global__ void __launch_bounds__(256, MINB) k_hash_probe(const uint8_t* __restr
                                          uint32_t(r0 + r), ncid, overflow);
         if (search && res != kSearching) {
           out = res == kClaimed ? id : (res == kFound ? (id | kPending) : kNoCid);
+          // a cell of at most 8 bytes is one masked word: for a fixed length
+          // the full 64-bit hash is a bijection of it (odd multiply,
+          // xor-shift, fmix64), so an equal hash and an equal length mean
+          // equal bytes — no byte compare (not for h == 1, the image of the
+          // remapped 0, nor under debug hash masks)
+          if (res == kFound && len <= 8 && h != 1 && hash_mask == ~0ull &&
+              ld_volatile_u32(&D.vlen[id]) == uint32_t(len))
+            out = id;
           search = false;
         }
       }
