@@ -137,7 +137,8 @@ def test_c1_tokenizers_sharded(tok, sc):
 
 
 @pytest.mark.parametrize("cfg_id,rows,world", [(1, 10_000, 4), (2, 30_000, 2), (2, 30_000, 4),
-                                               (3, 30_000, 3), (4, 20_000, 4), (5, 2_000, 2)])
+                                               (3, 30_000, 3), (4, 20_000, 4), (5, 2_000, 2),
+                                               (3, 40_000, 8), (4, 40_000, 8)])
 def test_config_prefix_sharded(cfg_id, rows, world):
     t = gen.generate(cfg_id, n_rows=rows)
     check(t, world, gen.fds(cfg_id))
